@@ -1,0 +1,190 @@
+/*
+ * snap_b200.h -- C-ABI drop-in boundary for the SNAP aligner core on B200.
+ *
+ * The reference (`seedaln`, /root/reference/proj) exposes the hot path only as
+ * a C++ library API.  Every entry point below replaces one reference call
+ * site; the reference interface it stands in for is cited beside it
+ * (REF = /root/reference/proj).  Plain pointers and sizes only: no C++, no
+ * torch types.  Every function returns an int status:
+ *
+ *   SA_OK       0  success
+ *   SA_EINVAL   1  invalid argument   (reference: std::invalid_argument)
+ *   SA_ERUNTIME 2  CUDA / runtime      (reference: IoError / runtime_error)
+ *   SA_EFORMAT  3  format mismatch     (reference: FormatError)
+ *
+ * and leaves a message retrievable with sa_last_error().  The C++ adapter in
+ * snap_b200.hpp rethrows these as the reference's exception types.
+ *
+ * Ownership: the caller owns every host buffer it passes in; the library owns
+ * all device memory and pinned staging it allocates.  A context may be used
+ * from one thread at a time (calls on one context are serialised internally).
+ */
+#ifndef SNAP_B200_H
+#define SNAP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { SA_OK = 0, SA_EINVAL = 1, SA_ERUNTIME = 2, SA_EFORMAT = 3 };
+
+/* ResultKind, REF include/seedaln/aligner.hpp:32 */
+enum { SA_SINGLE_HIT = 0, SA_MULTIPLE_HITS = 1, SA_NOT_FOUND = 2 };
+/* Direction, REF include/seedaln/seed_index.hpp:14 */
+enum { SA_FORWARD = 0, SA_REVERSE_COMPLEMENT = 1 };
+
+/* AlignerParams, REF include/seedaln/aligner.hpp:19-30 (same defaults via
+ * sa_default_params; same validation rules, REF src/aligner.cpp:11-24). */
+typedef struct sa_params {
+    int32_t seed_size;            /* s: seed length in bases, [1, 32]        */
+    int32_t seeds_to_try;         /* n: seeds drawn per read, >= 1           */
+    int32_t max_distance;         /* d_max, -1 = ceil(0.12 * read length)    */
+    int32_t confidence_threshold; /* c, >= 1                                 */
+    int32_t max_hits;             /* h_max, >= 1                             */
+    int32_t bucket_size;          /* [1, 64]                                 */
+    int32_t force_max_dlimit;     /* bool: disable d_limit shrinking         */
+} sa_params;
+
+/* AlignmentResult, REF include/seedaln/aligner.hpp:36-44.  24 bytes. */
+typedef struct sa_result {
+    uint64_t position;     /* forward-strand start of the alignment          */
+    int32_t distance;      /* edit distance of the best hit, -1 if none      */
+    int32_t gap;           /* d_second - d_best capped at 1000 (kGapCap)     */
+    uint8_t kind;          /* SA_SINGLE_HIT / SA_MULTIPLE_HITS / SA_NOT_FOUND */
+    uint8_t has_position;  /* bool                                           */
+    uint8_t direction;     /* SA_FORWARD / SA_REVERSE_COMPLEMENT             */
+    uint8_t reserved[5];
+} sa_result;
+
+/* AlignStats, REF include/seedaln/aligner.hpp:47-66 (first 16 fields, same
+ * order and meaning; dp_cells counts this implementation's LV cells), plus
+ * path counters used for the algorithmic-byte roofline. */
+typedef struct sa_stats {
+    uint64_t reads;
+    uint64_t reads_too_short;
+    uint64_t seed_lookups;
+    uint64_t seeds_skipped_n;
+    uint64_t seeds_skipped_popular;
+    uint64_t reads_all_seeds_popular;
+    uint64_t distance_calls;
+    uint64_t distance_calls_after_first;
+    uint64_t early_out_after_first;
+    uint64_t dp_cells;
+    uint64_t multi_early_exits;
+    uint64_t pruning_exits;
+    uint64_t first_scored_was_best;
+    uint64_t single_hits;
+    uint64_t multiple_hits;
+    uint64_t not_found;
+    /* extensions (not in the reference's AlignStats) */
+    uint64_t hits_consumed;  /* sum of hit counts of non-popular looked-up seeds */
+    uint64_t window_bases;   /* sum over LV calls of the genome window length    */
+    uint64_t read_bases;     /* sum of read lengths                              */
+    uint64_t overflow_reads; /* reads re-run on the global candidate-table path  */
+} sa_stats;
+
+typedef struct sa_context sa_context;
+
+/* Defaults of AlignerParams (REF aligner.hpp:20-26). */
+void sa_default_params(sa_params* out);
+
+/* AlignerParams::validate (REF src/aligner.cpp:11-24).  SA_EINVAL on failure. */
+int sa_validate_params(const sa_params* p);
+
+/* seed_offsets (REF src/aligner.cpp:50-79).  Writes up to n offsets into out
+ * (capacity >= n) and stores the count in *count. Host-side, pure. */
+int sa_seed_offsets(uint64_t read_length, int32_t s, int32_t n, int32_t* out,
+                    int32_t* count);
+
+/* Context = genome resident in HBM + GPU seed index, one replica per device.
+ * Replaces SeedIndex::build(const PackedGenome&, int)   (REF src/seed_index.cpp:80-126)
+ * and the Aligner constructor's index/genome binding     (REF src/aligner.cpp:116-122).
+ * packed_words / nmask_words are exactly PackedGenome::packed_words() and
+ * n_mask_words() (REF include/seedaln/genome.hpp:73-74,82-83): 32 bases per
+ * word LSB-first (A=0 C=1 G=2 T=3), and one N bit per position.
+ * devices: CUDA ordinals (NULL/0 = device 0 only).
+ * Errors: SA_EINVAL when seed_size is outside [1,32], the genome is shorter
+ * than seed_size (REF seed_index.cpp:81-84) or longer than 2^32-1 bases. */
+int sa_create(const uint64_t* packed_words, uint64_t n_packed,
+              const uint64_t* nmask_words, uint64_t n_nmask,
+              uint64_t genome_length, int32_t seed_size,
+              const int32_t* devices, int32_t n_devices, sa_context** out);
+
+void sa_destroy(sa_context* ctx);
+
+/* Message of the last failing call on ctx (ctx == NULL: last failing call of
+ * this thread that had no context).  Never NULL. */
+const char* sa_last_error(const sa_context* ctx);
+
+/* Aligner::align over a batch (REF src/aligner.cpp:223-364, called per read
+ * by the run_align worker REF src/driver.cpp:113).  Reads are ASCII over
+ * {A,C,G,T,N}: read i is bases[offsets[i] .. offsets[i+1]).  results[i] is
+ * the AlignmentResult of read i (input order).  stats (nullable) receives the
+ * AlignStats summed over the batch (REF aligner.cpp:31-48 merge semantics).
+ * Blocking.  Host buffers may be pageable or pinned (sa_host_alloc);
+ * pinned buffers get the double-buffered asynchronous path.
+ * Errors: SA_EINVAL on invalid params, a seed-size mismatch with the index
+ * (REF aligner.cpp:119-121), or a read of length >= s holding a character
+ * outside {A,C,G,T,N} (REF genome.cpp:182-200 throws from align()). */
+int sa_align_batch(sa_context* ctx, const sa_params* params, const char* bases,
+                   const uint64_t* offsets, uint64_t n_reads, sa_result* results,
+                   sa_stats* stats);
+
+/* Same as sa_align_batch with every buffer already in device memory of the
+ * context's first device (no host copies); stream is a cudaStream_t (0 =
+ * legacy default).  max_read_length bounds every read's length (it sizes the
+ * per-warp shared-memory layout).  Asynchronous: returns after enqueueing.
+ * d_stats (device, nullable) is accumulated into, not overwritten.  Errors
+ * found by the kernels (invalid characters) are reported by the next sa_sync(). */
+int sa_align_device(sa_context* ctx, const sa_params* params, const char* d_bases,
+                    const uint64_t* d_offsets, uint64_t n_reads, uint64_t max_read_length,
+                    sa_result* d_results, sa_stats* d_stats, void* stream);
+
+/* Waits for sa_align_device work on stream and reports deferred errors. */
+int sa_sync(sa_context* ctx, void* stream);
+
+/* SeedIndex::lookup over a batch (REF src/seed_index.cpp:128-143).  seeds holds
+ * n_seeds ASCII seeds of exactly seed_size characters, back to back.
+ * counts[i] = LookupResult::count() (forward + rc; a palindromic seed counts
+ * twice, REF tests/test_seed_index.cpp:67-85).  If fwd_out/rc_out are non-NULL
+ * the positions are written there: seed i's forward list at
+ * fwd_out[i*cap ..] (ascending, at most cap entries) with its length in
+ * n_fwd[i], likewise rc_out / n_rc.  Seeds with N or of unknown key -> 0. */
+int sa_lookup_batch(sa_context* ctx, const char* seeds, uint64_t n_seeds,
+                    uint32_t* counts, uint64_t* fwd_out, uint32_t* n_fwd,
+                    uint64_t* rc_out, uint32_t* n_rc, uint32_t cap);
+
+/* Index shape: distinct seeds (REF SeedIndex::distinct_seeds, seed_index.hpp:62),
+ * total positions (SeedIndex::total_positions, :61) and device bytes held. */
+int sa_index_info(const sa_context* ctx, uint64_t* distinct_seeds,
+                  uint64_t* total_positions, uint64_t* device_bytes);
+
+/* bounded_distance over a batch (REF src/edit_distance.cpp:19-75): pair i is
+ * read reads[read_off[i]..read_off[i+1]) against window
+ * windows[win_off[i]..win_off[i+1]) with limit d_limits[i].  out[i] = the
+ * distance or -1 (nullopt).  Runs on `device`.  SA_EINVAL if any d_limit < 0
+ * (REF edit_distance.cpp:22-23). */
+int sa_bounded_distance_batch(const char* reads, const uint64_t* read_off,
+                              const char* windows, const uint64_t* win_off,
+                              const int32_t* d_limits, uint64_t n_pairs,
+                              int32_t* out, int32_t device);
+
+/* Pinned host memory for zero-staging transfers. */
+int sa_host_alloc(void** ptr, uint64_t bytes);
+void sa_host_free(void* ptr);
+
+/* Device time (ms, CUDA events) of the last sa_align_batch call from the
+ * first H2D copy to the last D2H copy, and of the align kernels alone. */
+int sa_last_timing(const sa_context* ctx, float* e2e_ms, float* kernel_ms);
+
+/* Number of CUDA kernels launched by the last sa_align_batch call. */
+int sa_last_launches(const sa_context* ctx, uint64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SNAP_B200_H */

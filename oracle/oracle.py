@@ -1,0 +1,289 @@
+"""TEST INFRASTRUCTURE ONLY -- ctypes access to the parity oracles.
+
+  OracleIndex / or_*   plain-C restatement (oracle/snap_oracle.c), built by
+                       `make -C oracle` into oracle/build/liboracle.so
+  RefIndex / ref_*     the reference library itself, compiled in place from
+                       /root/reference by `make -C oracle ref` into
+                       oracle/_ref/libseedaln_ref.so (travels prebuilt)
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+--impl reference legs import this module.  The product never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "build", "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libseedaln_ref.so")
+REF_DIR = "/root/reference/proj"
+
+RESULT_DTYPE = np.dtype(
+    [("position", "<u8"), ("distance", "<i4"), ("gap", "<i4"), ("kind", "u1"),
+     ("has_position", "u1"), ("direction", "u1"), ("reserved", "u1", (5,))]
+)
+STAT_FIELDS = (
+    "reads", "reads_too_short", "seed_lookups", "seeds_skipped_n", "seeds_skipped_popular",
+    "reads_all_seeds_popular", "distance_calls", "distance_calls_after_first",
+    "early_out_after_first", "dp_cells", "multi_early_exits", "pruning_exits",
+    "first_scored_was_best", "single_hits", "multiple_hits", "not_found",
+    "hits_consumed", "window_bases", "read_bases", "overflow_reads",
+)
+
+
+class Params(C.Structure):
+    _fields_ = [("seed_size", C.c_int32), ("seeds_to_try", C.c_int32),
+                ("max_distance", C.c_int32), ("confidence_threshold", C.c_int32),
+                ("max_hits", C.c_int32), ("bucket_size", C.c_int32),
+                ("force_max_dlimit", C.c_int32)]
+
+    @classmethod
+    def of(cls, p) -> "Params":
+        return cls(p.seed_size, p.seeds_to_try, p.max_distance, p.confidence_threshold, p.max_hits,
+                   p.bucket_size, 1 if p.force_max_dlimit else 0)
+
+
+class Stats(C.Structure):
+    _fields_ = [(f, C.c_uint64) for f in STAT_FIELDS]
+
+    def as_dict(self) -> dict:
+        return {f: int(getattr(self, f)) for f in STAT_FIELDS}
+
+
+def build(with_ref: bool | None = None) -> None:
+    """make -C oracle (and `ref` when /root/reference is present)."""
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+    if with_ref is None:
+        with_ref = os.path.isdir(REF_DIR)
+    if with_ref:
+        subprocess.run(["make", "-s", "-C", HERE, "ref", f"REF={REF_DIR}"], check=True)
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_SO)
+
+
+_o = None
+_r = None
+P64 = C.POINTER(C.c_uint64)
+
+
+def _u64p(a):
+    return a.ctypes.data_as(P64)
+
+
+class _OrIndex(C.Structure):
+    _fields_ = [("seed_size", C.c_int), ("n_keys", C.c_uint64), ("n_positions", C.c_uint64),
+                ("keys", C.c_void_p), ("offsets", C.c_void_p), ("positions", C.c_void_p)]
+
+
+class _OrGenome(C.Structure):
+    _fields_ = [("len", C.c_uint64), ("packed", C.c_void_p), ("nmask", C.c_void_p)]
+
+
+def olib():
+    global _o
+    if _o is None:
+        if not os.path.exists(ORACLE_SO):
+            build(with_ref=False)
+        lib = C.CDLL(ORACLE_SO)
+        lib.or_seed_offsets.argtypes = [C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_int)]
+        lib.or_pack_seed.argtypes = [C.c_char_p, C.c_int, P64]
+        lib.or_packed_rc.argtypes = [C.c_uint64, C.c_int]
+        lib.or_packed_rc.restype = C.c_uint64
+        lib.or_index_build.argtypes = [C.POINTER(_OrGenome), C.c_int, C.POINTER(_OrIndex)]
+        lib.or_index_free.argtypes = [C.POINTER(_OrIndex)]
+        lib.or_lookup.argtypes = [C.POINTER(_OrIndex), C.c_char_p, C.POINTER(C.c_void_p), P64,
+                                  C.POINTER(C.c_void_p), P64]
+        lib.or_bounded_distance.argtypes = [C.c_char_p, C.c_int64, C.c_char_p, C.c_int64, C.c_int, P64]
+        lib.or_full_dp_distance.argtypes = [C.c_char_p, C.c_int64, C.c_char_p, C.c_int64]
+        lib.or_align_batch.argtypes = [C.POINTER(_OrIndex), C.POINTER(_OrGenome), C.POINTER(Params),
+                                       C.c_void_p, P64, C.c_uint64, C.c_void_p, C.POINTER(Stats), C.c_int]
+        lib.or_pack_genome.argtypes = [C.c_char_p, C.c_uint64, P64, P64]
+        _o = lib
+    return _o
+
+
+def rlib():
+    global _r
+    if _r is None:
+        if not os.path.exists(REF_SO):
+            raise FileNotFoundError(f"{REF_SO} not built (make -C oracle ref needs /root/reference)")
+        lib = C.CDLL(REF_SO)
+        lib.ref_last_error.restype = C.c_char_p
+        lib.ref_create.argtypes = [P64, C.c_uint64, P64, C.c_uint64, C.c_uint64, C.c_int]
+        lib.ref_create.restype = C.c_void_p
+        lib.ref_destroy.argtypes = [C.c_void_p]
+        lib.ref_index_info.argtypes = [C.c_void_p, P64, P64]
+        lib.ref_genome_checksum.argtypes = [C.c_void_p]
+        lib.ref_genome_checksum.restype = C.c_uint64
+        lib.ref_lookup.argtypes = [C.c_void_p, C.c_char_p, C.c_int, P64, P64, P64, P64, C.c_uint64]
+        lib.ref_bounded_distance.argtypes = [C.c_char_p, C.c_uint64, C.c_char_p, C.c_uint64, C.c_int, P64]
+        lib.ref_full_dp_distance.argtypes = [C.c_char_p, C.c_uint64, C.c_char_p, C.c_uint64]
+        lib.ref_seed_offsets.argtypes = [C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_int)]
+        lib.ref_pack_seed.argtypes = [C.c_char_p, C.c_int, P64]
+        lib.ref_packed_rc.argtypes = [C.c_uint64, C.c_int]
+        lib.ref_packed_rc.restype = C.c_uint64
+        lib.ref_tracker_replay.argtypes = [C.c_int, C.POINTER(C.c_int64), C.c_int, C.POINTER(C.c_int64)]
+        lib.ref_align_batch.argtypes = [C.c_void_p, C.POINTER(Params), C.c_void_p, P64, C.c_uint64,
+                                        C.c_void_p, C.POINTER(Stats), C.c_int]
+        _r = lib
+    return _r
+
+
+# ----------------------------------------------------------------- pure helpers
+
+def or_seed_offsets(length: int, s: int, n: int) -> list[int]:
+    buf = (C.c_int * max(n, 1))()
+    k = olib().or_seed_offsets(length, s, n, buf)
+    return list(buf[:k])
+
+
+def ref_seed_offsets(length: int, s: int, n: int) -> list[int]:
+    buf = (C.c_int * max(n, 1))()
+    k = rlib().ref_seed_offsets(length, s, n, buf)
+    return list(buf[:k])
+
+
+def or_bounded_distance(read: str, win: str, d_limit: int) -> int | None | str:
+    cells = C.c_uint64()
+    v = olib().or_bounded_distance(read.encode(), len(read), win.encode(), len(win), d_limit, C.byref(cells))
+    return "throws" if v == -2 else (None if v < 0 else v)
+
+
+def ref_bounded_distance(read: str, win: str, d_limit: int) -> int | None | str:
+    cells = C.c_uint64()
+    v = rlib().ref_bounded_distance(read.encode(), len(read), win.encode(), len(win), d_limit, C.byref(cells))
+    return "throws" if v == -2 else (None if v < 0 else v)
+
+
+def or_full_dp(read: str, win: str) -> int:
+    return olib().or_full_dp_distance(read.encode(), len(read), win.encode(), len(win))
+
+
+def or_packed_rc(key: int, s: int) -> int:
+    return olib().or_packed_rc(key, s)
+
+
+def or_pack_seed(seed: str) -> int | None:
+    k = C.c_uint64()
+    return k.value if olib().or_pack_seed(seed.encode(), len(seed), C.byref(k)) else None
+
+
+def pack_genome(seq: bytes) -> tuple[np.ndarray, np.ndarray]:
+    n = len(seq)
+    packed = np.zeros(max(1, (n + 31) // 32), np.uint64)
+    nmask = np.zeros(max(1, (n + 63) // 64), np.uint64)
+    if olib().or_pack_genome(seq, n, _u64p(packed), _u64p(nmask)) != 0:
+        raise ValueError("illegal character")
+    return packed[:(n + 31) // 32], nmask[:(n + 63) // 64]
+
+
+# ----------------------------------------------------------------- indexes
+
+class OracleIndex:
+    """C restatement: CSR index + Aligner::align."""
+
+    def __init__(self, packed: np.ndarray, nmask: np.ndarray, length: int, s: int):
+        self.packed = np.ascontiguousarray(packed, np.uint64)
+        self.nmask = np.ascontiguousarray(nmask, np.uint64)
+        self.g = _OrGenome(length, self.packed.ctypes.data, self.nmask.ctypes.data)
+        self.ix = _OrIndex()
+        rc = olib().or_index_build(C.byref(self.g), s, C.byref(self.ix))
+        if rc:
+            raise ValueError(f"or_index_build failed ({rc})")
+
+    def __del__(self):
+        if _o is not None and getattr(self, "ix", None) is not None:
+            _o.or_index_free(C.byref(self.ix))
+            self.ix = None
+
+    def lookup(self, seed: str) -> tuple[list[int], list[int]]:
+        f, r = C.c_void_p(), C.c_void_p()
+        nf, nr = C.c_uint64(), C.c_uint64()
+        olib().or_lookup(C.byref(self.ix), seed.encode(), C.byref(f), C.byref(nf), C.byref(r), C.byref(nr))
+        fw = list(C.cast(f, C.POINTER(C.c_uint32))[:nf.value]) if nf.value else []
+        rv = list(C.cast(r, C.POINTER(C.c_uint32))[:nr.value]) if nr.value else []
+        return fw, rv
+
+    def align_arrays(self, params, bases, offsets, threads: int = 1):
+        offsets = np.ascontiguousarray(offsets, np.uint64)
+        n = offsets.size - 1
+        res = np.zeros(n, RESULT_DTYPE)
+        st = Stats()
+        p = Params.of(params)
+        b = np.ascontiguousarray(np.frombuffer(bases, np.uint8) if isinstance(bases, (bytes, bytearray)) else bases,
+                                 np.uint8)
+        rc = olib().or_align_batch(C.byref(self.ix), C.byref(self.g), C.byref(p), b.ctypes.data,
+                                   _u64p(offsets), n, res.ctypes.data, C.byref(st), threads)
+        if rc:
+            raise ValueError(f"or_align_batch failed ({rc})")
+        return res, st.as_dict()
+
+
+class RefIndex:
+    """The reference library (oracle/_ref): SeedIndex::build + Aligner::align."""
+
+    def __init__(self, packed: np.ndarray, nmask: np.ndarray, length: int, s: int):
+        lib = rlib()
+        self.packed = np.ascontiguousarray(packed, np.uint64)
+        self.nmask = np.ascontiguousarray(nmask, np.uint64)
+        self.h = lib.ref_create(_u64p(self.packed), self.packed.size, _u64p(self.nmask), self.nmask.size,
+                                length, s)
+        if not self.h:
+            raise ValueError(lib.ref_last_error().decode())
+        self.s = s
+
+    def __del__(self):
+        if _r is not None and getattr(self, "h", None):
+            _r.ref_destroy(self.h)
+            self.h = None
+
+    def info(self) -> tuple[int, int]:
+        d, t = C.c_uint64(), C.c_uint64()
+        rlib().ref_index_info(self.h, C.byref(d), C.byref(t))
+        return d.value, t.value
+
+    def lookup(self, seed: str, cap: int = 1 << 16) -> tuple[list[int], list[int]]:
+        f = np.zeros(cap, np.uint64)
+        r = np.zeros(cap, np.uint64)
+        nf, nr = C.c_uint64(), C.c_uint64()
+        rc = rlib().ref_lookup(self.h, seed.encode(), len(seed), _u64p(f), C.byref(nf), _u64p(r),
+                               C.byref(nr), cap)
+        if rc:
+            raise ValueError(rlib().ref_last_error().decode())
+        return [int(x) for x in f[:nf.value]], [int(x) for x in r[:nr.value]]
+
+    def align_arrays(self, params, bases, offsets, threads: int = 1):
+        offsets = np.ascontiguousarray(offsets, np.uint64)
+        n = offsets.size - 1
+        res = np.zeros(n, RESULT_DTYPE)
+        st = Stats()
+        p = Params.of(params)
+        b = np.ascontiguousarray(np.frombuffer(bases, np.uint8) if isinstance(bases, (bytes, bytearray)) else bases,
+                                 np.uint8)
+        rc = rlib().ref_align_batch(self.h, C.byref(p), b.ctypes.data, _u64p(offsets), n,
+                                    res.ctypes.data, C.byref(st), threads)
+        if rc:
+            raise ValueError(rlib().ref_last_error().decode())
+        return res, st.as_dict()
+
+
+def ref_tracker_replay(merge_radius: int, ops: list[tuple[int, int, int]]) -> list[tuple[int, int, int, int]]:
+    flat = (C.c_int64 * (3 * len(ops)))(*[v for op in ops for v in op])
+    out = (C.c_int64 * (4 * len(ops)))()
+    rlib().ref_tracker_replay(merge_radius, flat, len(ops), out)
+    return [tuple(out[4 * i:4 * i + 4]) for i in range(len(ops))]
+
+
+def compare_results(a: np.ndarray, b: np.ndarray) -> list[int]:
+    """Indices of reads whose AlignmentResult differs in any field
+    (kind, has_position, position, direction, distance, gap)."""
+    diff = np.zeros(a.size, bool)
+    for f in ("kind", "has_position", "position", "direction", "distance", "gap"):
+        diff |= a[f] != b[f]
+    return np.nonzero(diff)[0].tolist()

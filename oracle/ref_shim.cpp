@@ -1,0 +1,228 @@
+// ref_shim.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// A thin extern "C" harness around the UNMODIFIED reference library
+// (/root/reference/proj/src, compiled in place by oracle/Makefile into
+// oracle/_ref/libseedaln_ref.so).  It calls only the reference's public API:
+//   PackedGenome::adopt_storage  (REF include/seedaln/genome.hpp:75-76)
+//   SeedIndex::build / lookup    (REF src/seed_index.cpp:80-143)
+//   bounded_distance / full_dp   (REF src/edit_distance.cpp:19-95)
+//   seed_offsets / Aligner::align(REF src/aligner.cpp:50-79,223-364)
+// and the align_corpus threading pattern of the acceptance suite
+// (REF tests/acceptance/acceptance_main.cpp:52-67,106-124).
+// Used by tests/ as the parity pin for the C restatement, and by bench.py's
+// cpu_baseline and --impl reference legs.  Never part of the product.
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../include/snap_b200.h"
+#include "seedaln/aligner.hpp"
+#include "seedaln/edit_distance.hpp"
+#include "seedaln/errors.hpp"
+#include "seedaln/genome.hpp"
+#include "seedaln/seed_index.hpp"
+
+using namespace seedaln;
+
+namespace {
+
+struct RefHandle {
+    PackedGenome genome;
+    SeedIndex index;
+};
+
+thread_local std::string g_err;
+
+void fill_stats(const AlignStats& a, sa_stats* out) {
+    uint64_t* d = reinterpret_cast<uint64_t*>(out);
+    const uint64_t v[16] = {a.reads,
+                            a.reads_too_short,
+                            a.seed_lookups,
+                            a.seeds_skipped_n,
+                            a.seeds_skipped_popular,
+                            a.reads_all_seeds_popular,
+                            a.distance_calls,
+                            a.distance_calls_after_first,
+                            a.early_out_after_first,
+                            a.dp_cells,
+                            a.multi_early_exits,
+                            a.pruning_exits,
+                            a.first_scored_was_best,
+                            a.single_hits,
+                            a.multiple_hits,
+                            a.not_found};
+    for (int i = 0; i < 16; ++i) d[i] += v[i];
+}
+
+AlignerParams to_params(const sa_params* p) {
+    AlignerParams a;
+    a.seed_size = p->seed_size;
+    a.seeds_to_try = p->seeds_to_try;
+    a.max_distance = p->max_distance;
+    a.confidence_threshold = p->confidence_threshold;
+    a.max_hits = p->max_hits;
+    a.bucket_size = p->bucket_size;
+    a.force_max_dlimit = p->force_max_dlimit != 0;
+    return a;
+}
+
+void to_result(const AlignmentResult& r, sa_result* out) {
+    std::memset(out, 0, sizeof(*out));
+    out->position = r.position;
+    out->distance = r.distance;
+    out->gap = r.gap;
+    out->kind = static_cast<uint8_t>(r.kind);
+    out->has_position = r.has_position ? 1 : 0;
+    out->direction = static_cast<uint8_t>(r.direction);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+void* ref_create(const uint64_t* packed, uint64_t n_packed, const uint64_t* nmask,
+                 uint64_t n_nmask, uint64_t len, int seed_size) {
+    try {
+        auto* h = new RefHandle;
+        std::vector<Contig> contigs{{"c1", 0, len}};
+        h->genome.adopt_storage(std::move(contigs), len,
+                                std::vector<uint64_t>(packed, packed + n_packed),
+                                std::vector<uint64_t>(nmask, nmask + n_nmask));
+        h->index = SeedIndex::build(h->genome, seed_size);
+        return h;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
+void ref_destroy(void* h) { delete static_cast<RefHandle*>(h); }
+
+void ref_index_info(void* hv, uint64_t* distinct, uint64_t* total) {
+    auto* h = static_cast<RefHandle*>(hv);
+    *distinct = h->index.distinct_seeds();
+    *total = h->index.total_positions();
+}
+
+uint64_t ref_genome_checksum(void* hv) { return static_cast<RefHandle*>(hv)->genome.checksum(); }
+
+// returns 0 ok, 1 invalid_argument
+int ref_lookup(void* hv, const char* seed, int s, uint64_t* fwd, uint64_t* n_fwd, uint64_t* rc,
+               uint64_t* n_rc, uint64_t cap) {
+    auto* h = static_cast<RefHandle*>(hv);
+    try {
+        LookupResult r = h->index.lookup(std::string_view(seed, static_cast<size_t>(s)));
+        *n_fwd = r.forward.size();
+        *n_rc = r.rc.size();
+        for (size_t i = 0; i < r.forward.size() && i < cap; ++i) fwd[i] = r.forward[i];
+        for (size_t i = 0; i < r.rc.size() && i < cap; ++i) rc[i] = r.rc[i];
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+// -1 = nullopt, -2 = threw invalid_argument
+int ref_bounded_distance(const char* read, uint64_t m, const char* win, uint64_t w, int d_limit,
+                         uint64_t* cells) {
+    try {
+        DistanceOutcome o = bounded_distance(std::string_view(read, m), std::string_view(win, w),
+                                             d_limit, cells);
+        return o ? *o : -1;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return -2;
+    }
+}
+
+int ref_full_dp_distance(const char* read, uint64_t m, const char* win, uint64_t w) {
+    return full_dp_distance(std::string_view(read, m), std::string_view(win, w));
+}
+
+int ref_seed_offsets(uint64_t len, int s, int n, int* out) {
+    std::vector<int> v = seed_offsets(len, s, n);
+    for (size_t i = 0; i < v.size(); ++i) out[i] = v[i];
+    return static_cast<int>(v.size());
+}
+
+int ref_pack_seed(const char* seed, int s, uint64_t* out) {
+    return pack_seed(std::string_view(seed, static_cast<size_t>(s)), *out) ? 1 : 0;
+}
+
+uint64_t ref_packed_rc(uint64_t key, int s) { return packed_reverse_complement(key, s); }
+
+// BestTracker replay for known-answer tests: ops = (distance, position, dir)
+// triples; writes (d_best, d_second, best_position, gap) after each op.
+void ref_tracker_replay(int merge_radius, const int64_t* ops, int n_ops, int64_t* out) {
+    BestTracker t(merge_radius);
+    for (int i = 0; i < n_ops; ++i) {
+        t.observe(static_cast<int>(ops[3 * i]), static_cast<uint64_t>(ops[3 * i + 1]),
+                  static_cast<Direction>(ops[3 * i + 2]));
+        out[4 * i] = t.d_best();
+        out[4 * i + 1] = t.d_second();
+        out[4 * i + 2] = static_cast<int64_t>(t.best_position());
+        out[4 * i + 3] = t.gap();
+    }
+}
+
+// 0 ok, 1 invalid_argument (params, or a read the reference rejects)
+int ref_align_batch(void* hv, const sa_params* p, const char* bases, const uint64_t* offsets,
+                    uint64_t n, sa_result* results, sa_stats* stats, int threads) {
+    auto* h = static_cast<RefHandle*>(hv);
+    AlignerParams params = to_params(p);
+    try {
+        params.validate();
+        Aligner probe(h->index, h->genome, params);  // throws on seed-size mismatch
+        (void)probe;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+    if (threads < 1) threads = 1;
+    std::atomic<uint64_t> cursor{0};
+    std::atomic<bool> failed{false};
+    std::mutex mu;
+    AlignStats total;
+    auto body = [&]() {
+        Aligner local(h->index, h->genome, params);
+        try {
+            const uint64_t grain = 64;
+            while (!failed.load()) {
+                uint64_t begin = cursor.fetch_add(grain);
+                if (begin >= n) break;
+                uint64_t end = std::min(n, begin + grain);
+                for (uint64_t i = begin; i < end; ++i) {
+                    Read r;
+                    r.bases.assign(bases + offsets[i], offsets[i + 1] - offsets[i]);
+                    to_result(local.align(r), &results[i]);
+                }
+            }
+        } catch (const std::exception& e) {
+            std::lock_guard<std::mutex> lock(mu);
+            g_err = e.what();
+            failed = true;
+        }
+        std::lock_guard<std::mutex> lock(mu);
+        total.merge(local.stats());
+    };
+    if (threads == 1) {
+        body();
+    } else {
+        std::vector<std::thread> th;
+        for (int t = 0; t < threads; ++t) th.emplace_back(body);
+        for (auto& t : th) t.join();
+    }
+    if (stats) fill_stats(total, stats);
+    return failed ? 1 : 0;
+}
+
+}  // extern "C"

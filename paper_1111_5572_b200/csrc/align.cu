@@ -1,0 +1,888 @@
+// align.cu -- the aligner hot path on sm_100a.
+//
+// K2..K5 of SURVEY.md §2 fused into one persistent warp-per-read kernel that
+// replays Aligner::align (REF src/aligner.cpp:223-364) bit-exactly:
+//   * read -> 2-bit planes (forward and reverse complement) in shared memory
+//     via coalesced byte loads and __ballot_sync           (REF :241, genome.cpp:182-200)
+//   * seed offsets (REF :50-79), computed once per distinct read length
+//   * seed keys + canonical probes of the HBM hash index, one lane per seed,
+//     issued speculatively for 32 seeds at a time         (REF seed_index.cpp:128-143)
+//   * the sequential seed loop (REF :256-316): N skip, h_max filter, hits ->
+//     anchors -> shared-memory vote table (warp-aggregated with
+//     __match_any_sync), best-unscored selection by warp argmax
+//     (REF :124-167), d_limit rule + Landau-Vishkin verification of every
+//     anchor of the chosen bucket (REF :169-221), BestTracker (REF :87-114),
+//     multi and pruning exits (REF :290-315)
+//   * classification and result (REF :318-363)
+// LV (REF src/edit_distance.cpp:19-75) is warp-cooperative: one lane per
+// diagonal (registers, d_limit <= 15) or lanes striding diagonals over a
+// shared-memory frontier (larger d_limit); the genome window is staged into
+// shared memory once per candidate bucket and matches are extended 32 bases
+// at a time by xor-ing bit planes and taking __ffs of the mismatch word.
+//
+// Vote tables live in shared memory (cap entries per warp).  A read whose
+// candidates overflow that table is deferred to the slow kernel (same code,
+// tables in global memory sized for the worst case n * h_max).
+#include <cuda_runtime.h>
+
+#include "align_kernels.cuh"
+#include "common.cuh"
+
+namespace sab {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr uint32_t kScored = 0x80000000u;
+
+SA_DEV uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// ------------------------------------------------------------------ LV
+
+// Extend diagonal k from read index i while bases match (REF
+// edit_distance.cpp:35-42; N never matches, :11-13).  R/W are shared-memory
+// plane arrays; window index j lives at plane bit wofs + j.
+SA_DEV int lv_slide(const uint4* R, const uint4* W, uint32_t wofs, int i, int k, int cap,
+                    uint64_t& cells) {
+    const int start = i;
+    while (i < cap) {
+        uint32_t rl, rh, rn, wl, wh, wn;
+        extract32(R, static_cast<uint64_t>(i), rl, rh, rn);
+        extract32(W, static_cast<uint64_t>(wofs + static_cast<uint32_t>(i + k)), wl, wh, wn);
+        const uint32_t mism = (rl ^ wl) | (rh ^ wh) | rn | wn;
+        if (mism == 0) {
+            i += 32;
+        } else {
+            i += __ffs(mism) - 1;
+            break;
+        }
+    }
+    if (i > cap) i = cap;
+    cells += static_cast<uint64_t>(i - start) + 1;
+    return i;
+}
+
+// One LV iteration for diagonal k given the previous frontier values of
+// k-1, k, k+1 (REF edit_distance.cpp:46-67).
+SA_DEV int lv_step(int e, int k, int prev_km1, int prev_k, int prev_kp1, int m, int w,
+                   const uint4* R, const uint4* W, uint32_t wofs, uint64_t& cells) {
+    if (k > w) return kUnreach;  // whole diagonal outside the window (:47)
+    int cand;
+    if (e == 0) {
+        cand = 0;
+    } else {
+        cand = prev_k + 1;                                  // substitution
+        cand = max(cand, prev_kp1 + 1);                     // extra read char
+        cand = max(cand, prev_km1);                         // extra window char
+    }
+    if (cand < max(0, -k)) return kUnreach;                // (:56-59)
+    const int cap = min(m, w - k);
+    cand = min(cand, cap);                                 // (:60)
+    return lv_slide(R, W, wofs, cand, k, cap, cells);
+}
+
+// Register wavefront for d_limit <= 15: lane l owns diagonal k = l - d_limit.
+SA_DEV int lv_warp_reg(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, int dl,
+                       int lane, uint64_t& cells) {
+    const int k = lane - dl;
+    const bool mine = lane <= 2 * dl;
+    int fr = kUnreach;
+    for (int e = 0; e <= dl; ++e) {
+        int up = __shfl_down_sync(FULL, fr, 1);
+        int dn = __shfl_up_sync(FULL, fr, 1);
+        if (lane == 31) up = kUnreach;
+        if (lane == 0) dn = kUnreach;
+        const bool active = mine && k >= -e && k <= e;
+        if (active) fr = lv_step(e, k, dn, fr, up, m, w, R, W, wofs, cells);
+        if (__any_sync(FULL, active && fr == m)) return e;
+    }
+    return -1;
+}
+
+// Shared-memory wavefront for any d_limit: F holds 2 * (2*dl + 3) ints.
+SA_DEV int lv_warp_smem(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, int dl,
+                        int* F, int lane, uint64_t& cells) {
+    const int width = 2 * dl + 3;
+    int* cur = F;
+    int* nxt = F + width;
+    for (int t = lane; t < 2 * width; t += 32) F[t] = kUnreach;
+    __syncwarp();
+    const int off = dl + 1;
+    for (int e = 0; e <= dl; ++e) {
+        bool found = false;
+        for (int k = -e + lane; k <= e; k += 32) {
+            const int v = lv_step(e, k, cur[k - 1 + off], cur[k + off], cur[k + 1 + off], m, w, R,
+                                  W, wofs, cells);
+            nxt[k + off] = v;
+            found |= (v == m);
+        }
+        __syncwarp();
+        if (__any_sync(FULL, found)) return e;
+        int* t = cur;
+        cur = nxt;
+        nxt = t;
+    }
+    return -1;
+}
+
+SA_DEV int lv_warp(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, int dl, int* F,
+                   int lane, uint64_t& cells) {
+    if (dl <= 15) return lv_warp_reg(R, m, W, wofs, w, dl, lane, cells);
+    return lv_warp_smem(R, m, W, wofs, w, dl, F, lane, cells);
+}
+
+// ------------------------------------------------------------------ read staging
+
+// ASCII read -> forward and reverse-complement planes.  Positions at or past
+// the end read as N.  Returns true if a character outside {A,C,G,T,N} occurs.
+SA_DEV bool stage_read(const char* __restrict__ src, int len, int nblk, uint4* R, uint4* C,
+                       int lane) {
+    bool bad = false;
+    for (int b = 0; b < nblk; ++b) {
+        const int pos = b * 32 + lane;
+        int code = 4, code2 = 4;
+        if (pos < len) {
+            code = read_code(static_cast<unsigned char>(__ldg(src + pos)));
+            code2 = read_code(static_cast<unsigned char>(__ldg(src + len - 1 - pos)));
+        }
+        bad |= (code == 5) | (code2 == 5);
+        const bool acgt = code < 4, acgt2 = code2 < 4;
+        const uint32_t lo = __ballot_sync(FULL, acgt && (code & 1));
+        const uint32_t hi = __ballot_sync(FULL, acgt && (code & 2));
+        const uint32_t nn = __ballot_sync(FULL, !acgt);
+        const uint32_t lo2 = __ballot_sync(FULL, acgt2 && !(code2 & 1));  // complement
+        const uint32_t hi2 = __ballot_sync(FULL, acgt2 && !(code2 & 2));
+        const uint32_t nn2 = __ballot_sync(FULL, !acgt2);
+        if (lane == 0) {
+            R[b] = make_uint4(lo, hi, nn, 0);
+            C[b] = make_uint4(lo2, hi2, nn2, 0);
+        }
+    }
+    return __any_sync(FULL, bad);
+}
+
+// REF src/aligner.cpp:50-79 seed_offsets, restated for shift values < s <= 32:
+// a tier whose shift was already used adds nothing new; otherwise it adds
+// every offset shift + j*s <= max_off.  Lane 0 fills offs; returns the count.
+SA_DEV int compute_offsets(int len, int s, int n, int* offs, int lane) {
+    int cnt = 0;
+    if (lane == 0) {
+        const int max_off = len - s;
+        uint32_t used = 0;
+        auto emit = [&](int shift) {
+            if ((used >> shift) & 1u) return;
+            used |= 1u << shift;
+            for (int o = shift; o <= max_off && cnt < n; o += s) offs[cnt++] = o;
+        };
+        emit(0);
+        for (int level = 1; (1 << level) <= 4 * s && cnt < n; ++level)
+            for (int odd = 1; odd < (1 << level) && cnt < n; odd += 2) emit((odd * s) >> level);
+    }
+    __syncwarp();
+    return __shfl_sync(FULL, cnt, 0);
+}
+
+// ------------------------------------------------------------------ per-read state
+
+struct Tracker {  // BestTracker, REF aligner.hpp:82-101
+    int d_best, d_second;
+    uint64_t best_pos;
+    int best_dir;
+};
+
+SA_DEV void tracker_observe(Tracker& t, int merge_radius, int distance, uint64_t position,
+                            int direction) {  // REF aligner.cpp:87-109
+    if (t.d_best < kInfDistance && direction == t.best_dir) {
+        const uint64_t delta = position > t.best_pos ? position - t.best_pos : t.best_pos - position;
+        if (delta <= static_cast<uint64_t>(merge_radius)) {
+            if (distance < t.d_best) {
+                t.d_best = distance;
+                t.best_pos = position;
+            }
+            return;
+        }
+    }
+    if (distance < t.d_best) {
+        t.d_second = t.d_best;
+        t.d_best = distance;
+        t.best_pos = position;
+        t.best_dir = direction;
+    } else if (distance < t.d_second) {
+        t.d_second = distance;
+    }
+}
+
+SA_DEV int tracker_gap(const Tracker& t) {  // REF aligner.cpp:111-114
+    if (t.d_second >= kInfDistance) return kGapCap;
+    return min(t.d_second - t.d_best, kGapCap);
+}
+
+struct CandTable {
+    unsigned long long* ckey;  // bucket*2 + dir, insertion order
+    unsigned long long* cmask; // anchor bits
+    uint32_t* ccnt;            // seeds_hitting | kScored
+    uint32_t* chslot;          // hash slot of the entry (for cleanup)
+    unsigned long long* hkey;  // hash keys
+    uint32_t* hval;            // list index
+    int cap, hcap;
+};
+
+struct ReadStats {  // per-read deltas, committed only when the read completes
+    uint32_t lookups, skipped_n, skipped_pop, dist_calls, after_first, early_out_after_first;
+    uint32_t multi_exits, pruning_exits;
+    uint64_t hits_consumed, window_bases;
+};
+
+struct Ctx {
+    const AlignLaunch* a;
+    int lane;
+    int len, s, c, bs, d_max;
+    const uint4* R;
+    const uint4* C;
+    uint4* W;
+    int* F;
+    CandTable t;
+    uint32_t n_cands, n_unscored;
+    Tracker tr;
+    uint32_t calls;
+    bool first_done, first_valid;
+    int first_dir;
+    uint64_t first_pos;
+    uint64_t cells;  // per lane
+    ReadStats st;
+};
+
+SA_DEV uint32_t cand_hash(unsigned long long key, int hcap) {
+    return static_cast<uint32_t>((key * 0x9E3779B97F4A7C15ull) >> 40) & static_cast<uint32_t>(hcap - 1);
+}
+
+// Warp-cooperative add_hit for up to 32 hits (REF aligner.cpp:124-134).
+// Returns false when the table would overflow.
+SA_DEV bool insert_wave(Ctx& x, bool valid, unsigned long long key, int bit) {
+    const int lane = x.lane;
+    const unsigned long long ukey = valid ? key : (0xFFFFFFFF00000000ull | static_cast<unsigned>(lane));
+    const unsigned peers = __match_any_sync(FULL, ukey);
+    const int leader = __ffs(peers) - 1;
+    const bool is_leader = valid && lane == leader;
+    bool isnew = false;
+    uint32_t slot = 0, idx = 0;
+    if (is_leader) {
+        uint32_t h = cand_hash(key, x.t.hcap);
+        volatile unsigned long long* hk = x.t.hkey;
+        for (;;) {
+            unsigned long long cur = hk[h];
+            if (cur == key) {
+                idx = x.t.hval[h];
+                break;
+            }
+            if (cur == kEmptyKey) {
+                unsigned long long old = atomicCAS(x.t.hkey + h, kEmptyKey, key);
+                if (old == kEmptyKey) {
+                    isnew = true;
+                    slot = h;
+                    break;
+                }
+                if (old == key) {
+                    idx = x.t.hval[h];
+                    break;
+                }
+            }
+            h = (h + 1) & static_cast<uint32_t>(x.t.hcap - 1);
+        }
+    }
+    const uint32_t newmask = __ballot_sync(FULL, isnew);
+    const uint32_t nnew = __popc(newmask);
+    if (x.n_cands + nnew > static_cast<uint32_t>(x.t.cap)) return false;
+    if (isnew) {
+        idx = x.n_cands + __popc(newmask & lanemask_lt());
+        x.t.hval[slot] = idx;
+        x.t.chslot[idx] = slot;
+        x.t.ckey[idx] = key;
+        x.t.cmask[idx] = 0ull;
+        x.t.ccnt[idx] = 0u;
+    }
+    x.n_cands += nnew;
+    x.n_unscored += nnew;
+    __syncwarp();
+    idx = __shfl_sync(FULL, idx, leader);
+    if (is_leader) x.t.ccnt[idx] += static_cast<uint32_t>(__popc(peers));
+    if (valid) atomicOr(x.t.cmask + idx, 1ull << bit);
+    __syncwarp();
+    return true;
+}
+
+// REF aligner.cpp:169-221 score_candidate
+SA_DEV void score_candidate(Ctx& x, uint32_t idx) {
+    const AlignLaunch& a = *x.a;
+    const int lane = x.lane;
+    if (lane == 0) x.t.ccnt[idx] |= kScored;
+    x.n_unscored--;
+    const unsigned long long kk = x.t.ckey[idx];
+    const unsigned long long mm = x.t.cmask[idx];
+    __syncwarp();
+
+    const int c = x.c, d_max = x.d_max;
+    int d_limit;
+    if (x.tr.d_best > d_max) d_limit = d_max + c - 1;
+    else if (x.tr.d_second >= x.tr.d_best + c) d_limit = x.tr.d_best + c - 1;
+    else d_limit = x.tr.d_best - 1;
+    if (a.force) d_limit = d_max + c - 1;
+    if (d_limit < 0) return;  // (:184)
+
+    const int dir = static_cast<int>(kk & 1ull);
+    const uint64_t base_pos = (kk >> 1) * static_cast<uint64_t>(x.bs);
+    const uint64_t amin = base_pos + static_cast<uint64_t>(__ffsll(static_cast<long long>(mm)) - 1);
+    const uint64_t amax = base_pos + static_cast<uint64_t>(63 - __clzll(static_cast<long long>(mm)));
+    const uint4* orient = dir ? x.C : x.R;
+
+    // stage the union of this bucket's windows once (REF genome.cpp:114-123
+    // substring: truncated at the genome end only)
+    const uint64_t gb0 = amin >> 5;
+    uint64_t end = amax + static_cast<uint64_t>(x.len) + static_cast<uint64_t>(d_limit);
+    if (end > a.glen) end = a.glen;
+    if (amin < a.glen) {
+        const int nblk = static_cast<int>(((end - 1) >> 5) - gb0) + 2;
+        for (int t = lane; t < nblk; t += 32) x.W[t] = __ldg(a.planes + gb0 + t);
+    }
+    __syncwarp();
+
+    int best_d = kInfDistance;
+    uint64_t best_anchor = 0;
+    for (unsigned long long m = mm; m != 0ull; m &= m - 1ull) {
+        const uint64_t anchor = base_pos + static_cast<uint64_t>(__ffsll(static_cast<long long>(m)) - 1);
+        if (anchor >= a.glen) continue;
+        const uint64_t rem = a.glen - anchor;
+        const uint64_t want = static_cast<uint64_t>(x.len) + static_cast<uint64_t>(d_limit);
+        const int w = static_cast<int>(want < rem ? want : rem);
+        const uint32_t wofs = static_cast<uint32_t>(anchor - gb0 * 32);
+        const int d = lv_warp(orient, x.len, x.W, wofs, w, d_limit, x.F, lane, x.cells);
+        x.st.dist_calls++;
+        x.calls++;
+        x.st.window_bases += static_cast<uint64_t>(w);
+        if (x.calls > 1) {
+            x.st.after_first++;
+            if (d < 0) x.st.early_out_after_first++;
+        }
+        if (d >= 0 && d < best_d) {
+            best_d = d;
+            best_anchor = anchor;
+        }
+    }
+    if (!x.first_done) {
+        x.first_done = true;
+        if (best_d < kInfDistance) {
+            x.first_valid = true;
+            x.first_pos = best_anchor;
+            x.first_dir = dir;
+        }
+    }
+    if (best_d < kInfDistance) tracker_observe(x.tr, x.bs, best_d, best_anchor, dir);
+}
+
+// REF aligner.cpp:141-167 score_best_candidate: unscored candidate with most
+// seeds hitting, then smallest anchor, then Forward.
+SA_DEV void score_best(Ctx& x) {
+    if (x.n_unscored == 0) return;
+    uint32_t bc = 0;
+    unsigned long long bk = ~0ull;
+    int bi = -1;
+    for (uint32_t j = x.lane; j < x.n_cands; j += 32) {
+        const uint32_t cc = x.t.ccnt[j];
+        if (cc & kScored) continue;
+        const unsigned long long kk = x.t.ckey[j];
+        const unsigned long long mm = x.t.cmask[j];
+        const unsigned long long amin =
+            (kk >> 1) * static_cast<unsigned long long>(x.bs) + static_cast<unsigned long long>(__ffsll(static_cast<long long>(mm)) - 1);
+        const unsigned long long ord = (amin << 1) | (kk & 1ull);
+        if (cc > bc || (cc == bc && ord < bk)) {
+            bc = cc;
+            bk = ord;
+            bi = static_cast<int>(j);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint32_t oc = __shfl_xor_sync(FULL, bc, o);
+        const unsigned long long ok = __shfl_xor_sync(FULL, bk, o);
+        const int oi = __shfl_xor_sync(FULL, bi, o);
+        if (oc > bc || (oc == bc && ok < bk)) {
+            bc = oc;
+            bk = ok;
+            bi = oi;
+        }
+    }
+    if (bi >= 0) score_candidate(x, static_cast<uint32_t>(bi));
+}
+
+SA_DEV void clear_table(CandTable& t, uint32_t n_cands, bool full, int lane) {
+    __syncwarp();
+    if (full) {
+        for (int j = lane; j < t.hcap; j += 32) t.hkey[j] = kEmptyKey;
+    } else {
+        for (uint32_t j = lane; j < n_cands; j += 32) t.hkey[t.chslot[j]] = kEmptyKey;
+    }
+    __syncwarp();
+}
+
+// per-seed flags
+constexpr uint32_t kSeedN = 1, kSeedQflip = 2, kSeedPal = 4, kSeedSingleRc = 8;
+
+template <bool kSlow>
+__global__ void __launch_bounds__(256) align_kernel(const AlignLaunch a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    unsigned char* ws = smem + static_cast<size_t>(wib) * a.smem_per_warp;
+
+    Ctx x;
+    x.a = &a;
+    x.lane = lane;
+    x.s = a.s;
+    x.c = a.c;
+    x.bs = a.bs;
+    uint4* R = reinterpret_cast<uint4*>(ws);
+    uint4* Cp = R + a.wbr;
+    x.R = R;
+    x.C = Cp;
+    x.W = Cp + a.wbr;
+    int* offs = reinterpret_cast<int*>(x.W + a.wbw);
+    x.F = offs + a.n_off_cap;
+    unsigned char* tb;
+    if (kSlow) {
+        const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+        tb = a.gscratch + gw * a.gscratch_per_warp;
+    } else {
+        tb = reinterpret_cast<unsigned char*>(x.F + a.f_ints);
+    }
+    x.t.cap = a.cap;
+    x.t.hcap = a.hcap;
+    x.t.ckey = reinterpret_cast<unsigned long long*>(tb);
+    x.t.cmask = x.t.ckey + a.cap;
+    x.t.hkey = x.t.cmask + a.cap;
+    x.t.ccnt = reinterpret_cast<uint32_t*>(x.t.hkey + a.hcap);
+    x.t.chslot = x.t.ccnt + a.cap;
+    x.t.hval = x.t.chslot + a.cap;
+    for (int j = lane; j < a.hcap; j += 32) x.t.hkey[j] = kEmptyKey;
+    __syncwarp();
+
+    // per-warp accumulators (uniform across lanes; lane 0 commits)
+    unsigned long long acc[kNumStats];
+#pragma unroll
+    for (int i = 0; i < kNumStats; ++i) acc[i] = 0;
+    uint64_t lane_cells = 0;
+
+    int cached_len = -1, n_eff = 0;
+    const uint32_t smask = seed_mask32(a.s);
+    const uint32_t n_work = kSlow ? *a.work_count : a.n_reads;
+
+    for (;;) {
+        uint32_t r = 0;
+        if (lane == 0) r = atomicAdd(a.cursor, 1u);
+        r = __shfl_sync(FULL, r, 0);
+        if (r >= n_work) break;
+        if (kSlow) r = a.work_list[r];
+
+        const uint64_t o0 = a.offsets[r], o1 = a.offsets[r + 1];
+        const int len = static_cast<int>(o1 - o0);
+        const char* src = a.bases + (o0 - a.base_off);
+        x.len = len;
+        sa_result res;
+        res.position = 0;
+        res.distance = -1;
+        res.gap = 0;
+        res.kind = SA_NOT_FOUND;
+        res.has_position = 0;
+        res.direction = 0;
+#pragma unroll
+        for (int i = 0; i < 5; ++i) res.reserved[i] = 0;
+
+        if (len < a.s) {  // REF aligner.cpp:231-235
+            if (lane == 0) {
+                a.results[r] = res;
+                acc[0] += 1;   // reads
+                acc[1] += 1;   // reads_too_short
+                acc[15] += 1;  // not_found
+                acc[18] += static_cast<unsigned long long>(len);
+            }
+            continue;
+        }
+        x.d_max = a.dmax_param >= 0 ? a.dmax_param : (12 * len + 99) / 100;
+        if (len != cached_len) {
+            n_eff = compute_offsets(len, a.s, min(a.n, a.n_off_cap), offs, lane);
+            cached_len = len;
+        }
+        const int tier0 = len / a.s;
+        const int nblk = (len + 31) / 32 + 1;
+        if (stage_read(src, len, nblk, R, Cp, lane)) {
+            if (lane == 0) {
+                atomicOr(a.error_flag, 1u);
+                atomicMin(a.error_read, r);
+            }
+            continue;
+        }
+        __syncwarp();
+
+        x.n_cands = 0;
+        x.n_unscored = 0;
+        x.tr.d_best = kInfDistance;
+        x.tr.d_second = kInfDistance;
+        x.tr.best_pos = 0;
+        x.tr.best_dir = 0;
+        x.calls = 0;
+        x.first_done = false;
+        x.first_valid = false;
+        x.first_dir = 0;
+        x.first_pos = 0;
+        x.cells = 0;
+        x.st = ReadStats{};
+        int tested = 0;
+        bool any_lookup = false, any_popular = false, early_multi = false, overflow = false;
+
+        // per-lane seed record of the current wave
+        int s_off = 0;
+        uint32_t s_flags = 0, s_count = 0, s_payload = 0;
+
+        for (int i = 0; i < n_eff; ++i) {
+            if ((i & 31) == 0) {  // speculative probes for seeds i .. i+31
+                const int si = i + lane;
+                s_flags = 0;
+                s_count = 0;
+                s_payload = 0;
+                if (si < n_eff) {
+                    s_off = offs[si];
+                    uint32_t lo, hi, nn;
+                    extract32(R, static_cast<uint64_t>(s_off), lo, hi, nn);
+                    if (nn & smask) {
+                        s_flags = kSeedN;
+                    } else {
+                        const uint64_t key = plane_key(lo, hi, a.s);
+                        const uint64_t rc = plane_rc_key(lo, hi, a.s);
+                        const uint64_t canon = key < rc ? key : rc;
+                        if (key != canon) s_flags |= kSeedQflip;
+                        if (key == rc) s_flags |= kSeedPal;
+                        unsigned int payload, meta;
+                        if (probe_slot(a.table, a.n_slots, canon, payload, meta)) {
+                            const uint32_t ntot = meta & 0x7fffffffu;
+                            s_count = (s_flags & kSeedPal) ? 2u * ntot : ntot;
+                            s_payload = payload;
+                            if (meta & 0x80000000u) s_flags |= kSeedSingleRc;
+                        }
+                    }
+                }
+            }
+            const int src_lane = i & 31;
+            const uint32_t flags = __shfl_sync(FULL, s_flags, src_lane);
+            const uint32_t cnt = __shfl_sync(FULL, s_count, src_lane);
+            const uint32_t payload = __shfl_sync(FULL, s_payload, src_lane);
+            const int off = __shfl_sync(FULL, s_off, src_lane);
+
+            if (flags & kSeedN) {  // REF :259-262
+                x.st.skipped_n++;
+                continue;
+            }
+            x.st.lookups++;
+            if (cnt > static_cast<uint32_t>(a.hmax)) {  // REF :265-269
+                any_popular = true;
+                x.st.skipped_pop++;
+                continue;
+            }
+            any_lookup = true;
+            x.st.hits_consumed += cnt;
+            if (i < tier0) ++tested;
+
+            if (cnt > 0) {  // REF :273-286
+                const bool pal = (flags & kSeedPal) != 0;
+                const uint32_t ntot = pal ? cnt / 2 : cnt;
+                const bool inl = ntot == 1;
+                uint32_t n_fwd = 0;
+                if (!inl) n_fwd = __ldg(a.pool + payload);
+                const int rc_shift = len - a.s - off;
+                const uint32_t qflip = (flags & kSeedQflip) ? 1u : 0u;
+                for (uint32_t base = 0; base < cnt && !overflow; base += 32) {
+                    const uint32_t t = base + lane;
+                    const bool valid = t < cnt;
+                    unsigned long long key = 0;
+                    int bit = 0;
+                    if (valid) {
+                        const uint32_t j = pal ? (t < ntot ? t : t - ntot) : t;
+                        uint32_t pos, eflag;
+                        if (inl) {
+                            pos = payload;
+                            eflag = (flags & kSeedSingleRc) ? 1u : 0u;
+                        } else {
+                            pos = __ldg(a.pool + payload + 1 + j);
+                            eflag = j >= n_fwd ? 1u : 0u;
+                        }
+                        const uint32_t dir = pal ? (t >= ntot ? 1u : 0u) : (eflag ^ qflip);
+                        const int64_t anchor =
+                            static_cast<int64_t>(pos) - (dir ? rc_shift : off);
+                        const uint32_t aa = anchor < 0 ? 0u : static_cast<uint32_t>(anchor);
+                        const uint32_t bucket = aa / static_cast<uint32_t>(a.bs);
+                        bit = static_cast<int>(aa - bucket * static_cast<uint32_t>(a.bs));
+                        key = (static_cast<unsigned long long>(bucket) << 1) | dir;
+                    }
+                    if (!insert_wave(x, valid, key, bit)) overflow = true;
+                }
+                if (overflow) break;
+            }
+
+            score_best(x);  // REF :288
+            if (x.tr.d_best < a.c && x.tr.d_second < x.tr.d_best + a.c) {  // REF :290-295
+                x.st.multi_exits++;
+                early_multi = true;
+                break;
+            }
+            if (tested >= x.tr.d_best + a.c) {  // REF :296-315
+                x.st.pruning_exits++;
+                while (x.n_unscored > 0) {
+                    score_best(x);
+                    if (x.tr.d_best < a.c && x.tr.d_second < x.tr.d_best + a.c) {
+                        x.st.multi_exits++;
+                        early_multi = true;
+                        break;
+                    }
+                }
+                break;
+            }
+        }
+
+        if (overflow) {  // defer to the global-table kernel
+            clear_table(x.t, x.n_cands, true, lane);
+            if (lane == 0) {
+                const unsigned slot = atomicAdd(a.overflow_count, 1u);
+                a.overflow_list[slot] = r;
+                acc[19] += 1;
+            }
+            continue;
+        }
+        clear_table(x.t, x.n_cands, false, lane);
+
+        // classification, REF :318-363
+        int kind;
+        bool all_pop = false;
+        const int d_max = x.d_max;
+        if (early_multi) {
+            kind = SA_MULTIPLE_HITS;
+        } else {
+            if (x.tr.d_best <= d_max && x.tr.d_second >= x.tr.d_best + a.c) kind = SA_SINGLE_HIT;
+            else if (x.tr.d_best <= d_max) kind = SA_MULTIPLE_HITS;
+            else kind = SA_NOT_FOUND;
+            if (kind == SA_NOT_FOUND && any_popular && !any_lookup) {
+                all_pop = true;
+                kind = SA_MULTIPLE_HITS;
+            }
+        }
+        res.kind = static_cast<uint8_t>(kind);
+        bool first_best = false;
+        if (kind == SA_SINGLE_HIT ||
+            (kind == SA_MULTIPLE_HITS && x.tr.d_best < kInfDistance && x.tr.d_best <= d_max)) {
+            res.has_position = 1;
+            res.position = x.tr.best_pos;
+            res.direction = static_cast<uint8_t>(x.tr.best_dir);
+            res.distance = x.tr.d_best;
+            res.gap = tracker_gap(x.tr);
+        }
+        if (kind == SA_SINGLE_HIT && x.first_valid && x.first_dir == x.tr.best_dir) {
+            const uint64_t delta = x.first_pos > x.tr.best_pos ? x.first_pos - x.tr.best_pos
+                                                               : x.tr.best_pos - x.first_pos;
+            first_best = delta <= static_cast<uint64_t>(a.bs);
+        }
+        lane_cells += x.cells;
+        if (lane == 0) {
+            a.results[r] = res;
+            acc[0] += 1;
+            acc[2] += x.st.lookups;
+            acc[3] += x.st.skipped_n;
+            acc[4] += x.st.skipped_pop;
+            acc[5] += all_pop ? 1 : 0;
+            acc[6] += x.st.dist_calls;
+            acc[7] += x.st.after_first;
+            acc[8] += x.st.early_out_after_first;
+            acc[10] += x.st.multi_exits;
+            acc[11] += x.st.pruning_exits;
+            acc[12] += first_best ? 1 : 0;
+            acc[13] += kind == SA_SINGLE_HIT ? 1 : 0;
+            acc[14] += kind == SA_MULTIPLE_HITS ? 1 : 0;
+            acc[15] += kind == SA_NOT_FOUND ? 1 : 0;
+            acc[16] += x.st.hits_consumed;
+            acc[17] += x.st.window_bases;
+            acc[18] += static_cast<unsigned long long>(len);
+        }
+    }
+
+    for (int o = 16; o > 0; o >>= 1) lane_cells += __shfl_xor_sync(FULL, lane_cells, o);
+    if (lane == 0) {
+        acc[9] = lane_cells;
+#pragma unroll
+        for (int i = 0; i < kNumStats; ++i)
+            if (acc[i]) atomicAdd(a.stats + i, acc[i]);
+    }
+}
+
+// ------------------------------------------------------------------ standalone LV
+
+__global__ void __launch_bounds__(256) lv_batch_kernel(const LvLaunch a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    unsigned char* ws = smem + static_cast<size_t>(wib) * a.smem_per_warp;
+    uint4* R = reinterpret_cast<uint4*>(ws);
+    uint4* W = R + a.wbr;
+    int* F = reinterpret_cast<int*>(W + a.wbw);
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t p = gw; p < a.n_pairs; p += nw) {
+        const int m = static_cast<int>(a.read_off[p + 1] - a.read_off[p]);
+        const int w = static_cast<int>(a.win_off[p + 1] - a.win_off[p]);
+        const char* rs = a.reads + a.read_off[p];
+        const char* wsrc = a.wins + a.win_off[p];
+        int dl = a.d_limits[p];
+        // distance <= m always (m insertions), so a limit above m changes nothing
+        if (dl > m) dl = m;
+        bool bad = false;
+        const int rb = (m + 31) / 32 + 1, wb = (w + 31) / 32 + 1;
+        for (int b = 0; b < rb; ++b) {
+            const int pos = b * 32 + lane;
+            const int code = pos < m ? read_code(static_cast<unsigned char>(rs[pos])) : 4;
+            bad |= code == 5;
+            const uint32_t lo = __ballot_sync(FULL, code < 4 && (code & 1));
+            const uint32_t hi = __ballot_sync(FULL, code < 4 && (code & 2));
+            const uint32_t nn = __ballot_sync(FULL, code >= 4);
+            if (lane == 0) R[b] = make_uint4(lo, hi, nn, 0);
+        }
+        for (int b = 0; b < wb; ++b) {
+            const int pos = b * 32 + lane;
+            const int code = pos < w ? read_code(static_cast<unsigned char>(wsrc[pos])) : 4;
+            bad |= code == 5;
+            const uint32_t lo = __ballot_sync(FULL, code < 4 && (code & 1));
+            const uint32_t hi = __ballot_sync(FULL, code < 4 && (code & 2));
+            const uint32_t nn = __ballot_sync(FULL, code >= 4);
+            if (lane == 0) W[b] = make_uint4(lo, hi, nn, 0);
+        }
+        __syncwarp();
+        if (__any_sync(FULL, bad)) {
+            if (lane == 0) {
+                atomicOr(a.error_flag, 1u);
+                a.out[p] = -2;
+            }
+            continue;
+        }
+        uint64_t cells = 0;
+        const int d = lv_warp(R, m, W, 0u, w, dl, F, lane, cells);
+        if (lane == 0) a.out[p] = d;
+        __syncwarp();
+    }
+}
+
+// ------------------------------------------------------------------ lookup
+
+// SeedIndex::lookup over a batch (REF src/seed_index.cpp:128-143), one thread
+// per seed.  Seeds are ASCII; anything but A/C/G/T (any case) yields 0 hits
+// like pack_seed's failure path (REF :51-60, :141).
+__global__ void lookup_kernel(const LookupLaunch a) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < a.n_seeds;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const char* sd = a.seeds + i * a.s;
+        uint64_t key = 0;
+        bool ok = true;
+        for (int j = 0; j < a.s; ++j) {
+            int b;
+            switch (sd[j]) {
+                case 'A': case 'a': b = 0; break;
+                case 'C': case 'c': b = 1; break;
+                case 'G': case 'g': b = 2; break;
+                case 'T': case 't': b = 3; break;
+                default: b = -1;
+            }
+            if (b < 0) ok = false;
+            key = (key << 2) | static_cast<uint64_t>(b & 3);
+        }
+        uint32_t nf = 0, nr = 0;
+        if (ok) {
+            // rc by bit tricks (REF :62-70)
+            uint64_t x = ~key;
+            x = ((x & 0x3333333333333333ull) << 2) | ((x >> 2) & 0x3333333333333333ull);
+            x = ((x & 0x0f0f0f0f0f0f0f0full) << 4) | ((x >> 4) & 0x0f0f0f0f0f0f0f0full);
+            x = __byte_perm(static_cast<uint32_t>(x >> 32), 0, 0x0123) |
+                (static_cast<uint64_t>(__byte_perm(static_cast<uint32_t>(x), 0, 0x0123)) << 32);
+            const uint64_t rc = x >> (64 - 2 * a.s);
+            const uint64_t canon = key < rc ? key : rc;
+            const bool qflip = key != canon, pal = key == rc;
+            unsigned int payload, meta;
+            if (probe_slot(a.table, a.n_slots, canon, payload, meta)) {
+                const uint32_t ntot = meta & 0x7fffffffu;
+                uint32_t n_canon;  // windows equal to canon
+                if (ntot == 1) n_canon = (meta & 0x80000000u) ? 0u : 1u;
+                else n_canon = a.pool[payload];
+                auto pos_at = [&](uint32_t j) -> uint64_t {
+                    return ntot == 1 ? payload : a.pool[payload + 1 + j];
+                };
+                if (pal) {
+                    nf = nr = ntot;
+                    if (a.fwd_out)
+                        for (uint32_t j = 0; j < ntot && j < a.cap; ++j) {
+                            a.fwd_out[i * a.cap + j] = pos_at(j);
+                            a.rc_out[i * a.cap + j] = pos_at(j);
+                        }
+                } else {
+                    // forward list = windows equal to the query
+                    const uint32_t fb = qflip ? n_canon : 0, fe = qflip ? ntot : n_canon;
+                    const uint32_t rb = qflip ? 0 : n_canon, re = qflip ? n_canon : ntot;
+                    nf = fe - fb;
+                    nr = re - rb;
+                    if (a.fwd_out) {
+                        for (uint32_t j = 0; j < nf && j < a.cap; ++j)
+                            a.fwd_out[i * a.cap + j] = pos_at(fb + j);
+                        for (uint32_t j = 0; j < nr && j < a.cap; ++j)
+                            a.rc_out[i * a.cap + j] = pos_at(rb + j);
+                    }
+                }
+            }
+        }
+        a.counts[i] = nf + nr;
+        if (a.n_fwd) a.n_fwd[i] = nf;
+        if (a.n_rc) a.n_rc[i] = nr;
+    }
+}
+
+}  // namespace
+
+void launch_align_fast(const AlignLaunch& a, int grid, int block, cudaStream_t st) {
+    align_kernel<false><<<grid, block, a.smem_per_warp * (block / 32), st>>>(a);
+}
+
+void launch_align_slow(const AlignLaunch& a, int grid, int block, cudaStream_t st) {
+    align_kernel<true><<<grid, block, a.smem_per_warp * (block / 32), st>>>(a);
+}
+
+void launch_lv_batch(const LvLaunch& a, int grid, int block, cudaStream_t st) {
+    lv_batch_kernel<<<grid, block, a.smem_per_warp * (block / 32), st>>>(a);
+}
+
+void launch_lookup(const LookupLaunch& a, cudaStream_t st) {
+    uint64_t g = (a.n_seeds + 127) / 128;
+    if (g > 148 * 32) g = 148 * 32;
+    if (g < 1) g = 1;
+    lookup_kernel<<<static_cast<int>(g), 128, 0, st>>>(a);
+}
+
+cudaError_t align_set_smem(uint32_t smem_bytes) {
+    cudaError_t e = cudaFuncSetAttribute(align_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem_bytes));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(align_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem_bytes));
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(lv_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem_bytes));
+}
+
+cudaError_t align_fast_occupancy(int block, uint32_t smem_bytes, int* blocks_per_sm) {
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, align_kernel<false>, block,
+                                                         smem_bytes);
+}
+
+}  // namespace sab

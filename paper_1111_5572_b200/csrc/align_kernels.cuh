@@ -1,0 +1,95 @@
+// align_kernels.cuh -- launch descriptors shared by the host batcher and the
+// kernels in align.cu.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/snap_b200.h"
+#include "common.cuh"
+
+namespace sab {
+
+// counters accumulated on the device; first 20 mirror sa_stats
+constexpr int kNumStats = 20;
+
+struct AlignLaunch {
+    // replica
+    const uint4* planes;
+    uint64_t glen;
+    const Slot* table;
+    uint64_t n_slots;
+    const uint32_t* pool;
+    // reads: read i = bases[offsets[i] - base_off, offsets[i+1] - base_off)
+    const char* bases;
+    const uint64_t* offsets;
+    uint64_t base_off;
+    uint32_t n_reads;
+    // AlignerParams
+    int s, n, dmax_param, c, hmax, bs, force;
+    // per-warp layout (units: uint4 blocks / ints / entries)
+    int wbr;        // read-plane blocks (fwd and rc each)
+    int wbw;        // window staging blocks
+    int n_off_cap;  // seed offset slots (ints, multiple of 4)
+    int dl_max;     // largest d_limit of the batch
+    int f_ints;     // frontier ints (0 when dl_max <= 15)
+    int cap;        // candidate list capacity
+    int hcap;       // candidate hash slots (power of two)
+    uint32_t smem_per_warp;
+    // outputs
+    sa_result* results;
+    unsigned long long* stats;  // kNumStats
+    unsigned int* cursor;
+    unsigned int* overflow_list;
+    unsigned int* overflow_count;
+    unsigned int* error_flag;
+    unsigned int* error_read;  // atomicMin of the first bad read index
+    // slow path: process work_list[0..*work_count) with global candidate tables
+    const unsigned int* work_list;
+    const unsigned int* work_count;
+    unsigned char* gscratch;
+    uint64_t gscratch_per_warp;
+};
+
+// bytes of one candidate table with capacity cap and hcap hash slots
+inline uint64_t cand_table_bytes(int cap, int hcap) {
+    return static_cast<uint64_t>(cap) * (8 + 8 + 4 + 4) + static_cast<uint64_t>(hcap) * (8 + 4);
+}
+
+struct LvLaunch {
+    const char* reads;
+    const uint64_t* read_off;
+    const char* wins;
+    const uint64_t* win_off;
+    const int32_t* d_limits;
+    uint32_t n_pairs;
+    int wbr, wbw, f_ints;
+    uint32_t smem_per_warp;
+    int32_t* out;
+    unsigned int* error_flag;
+};
+
+struct LookupLaunch {
+    const uint4* planes;
+    const Slot* table;
+    uint64_t n_slots;
+    const uint32_t* pool;
+    const char* seeds;
+    uint64_t n_seeds;
+    int s;
+    uint32_t* counts;
+    uint64_t* fwd_out;
+    uint32_t* n_fwd;
+    uint64_t* rc_out;
+    uint32_t* n_rc;
+    uint32_t cap;
+};
+
+void launch_align_fast(const AlignLaunch& a, int grid, int block, cudaStream_t st);
+void launch_align_slow(const AlignLaunch& a, int grid, int block, cudaStream_t st);
+void launch_lv_batch(const LvLaunch& a, int grid, int block, cudaStream_t st);
+void launch_lookup(const LookupLaunch& a, cudaStream_t st);
+cudaError_t align_fast_occupancy(int block, uint32_t smem_bytes, int* blocks_per_sm);
+cudaError_t align_set_smem(uint32_t smem_bytes);
+
+}  // namespace sab

@@ -1,0 +1,766 @@
+// capi.cu -- the C-ABI boundary (include/snap_b200.h) and the host batcher.
+//
+// One sa_context = one index replica per device (genome planes + seed table
+// built on that device) and, per device, a worker that pulls read chunks from
+// a shared cursor and streams them through two CUDA streams:
+//   H2D bases/offsets -> fast align kernel -> slow (overflow) kernel -> D2H results
+// so the copies of chunk k+1 overlap the kernels of chunk k.  Results land in
+// input order (chunk i writes results[r0 .. r1)).  No collective is involved:
+// replicas are independent (REF include/seedaln/aligner.hpp:112-115 shares the
+// index read-only across workers; here across GPUs).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/snap_b200.h"
+#include "align_kernels.cuh"
+#include "device_index.h"
+
+using namespace sab;
+
+namespace {
+
+thread_local std::string g_thread_err;
+
+constexpr int kCtlWords = 4;  // cursor_fast, cursor_slow, overflow_count, error_flag
+constexpr uint64_t kChunkReads = 1u << 20;
+constexpr uint64_t kChunkBytes = 256ull << 20;
+constexpr int kFastCap = 64, kFastHcap = 128;
+constexpr uint64_t kSlowScratchBudget = 2ull << 30;
+
+struct Stage {  // one of the two pipeline slots of a replica
+    cudaStream_t st = nullptr;
+    char* d_bases = nullptr;
+    uint64_t bases_cap = 0;
+    uint64_t* d_offsets = nullptr;
+    sa_result* d_results = nullptr;
+    unsigned int* d_overflow = nullptr;
+    uint64_t reads_cap = 0;
+    unsigned int* d_ctl = nullptr;
+    cudaEvent_t k0 = nullptr, k1 = nullptr;
+};
+
+struct Replica {
+    int device = 0;
+    int sm_count = 148;
+    DeviceIndex ix;
+    Stage stage[3];  // [0],[1] batch pipeline, [2] sa_align_device
+    unsigned long long* d_stats = nullptr;
+    unsigned int* d_err = nullptr;         // error flag
+    unsigned long long* d_err_read = nullptr;
+    unsigned char* d_gscratch = nullptr;
+    uint64_t gscratch_bytes = 0;
+    uint32_t smem_attr = 0;
+    cudaEvent_t e_start = nullptr, e_end = nullptr;
+};
+
+struct LaunchShape {
+    AlignLaunch proto;  // layout + params fields filled
+    int fast_block, fast_grid;
+    int slow_block, slow_grid;
+    uint32_t slow_smem_per_warp;
+    uint64_t slow_table_bytes;
+    int slow_cap, slow_hcap;
+};
+
+}  // namespace
+
+struct sa_context {
+    std::vector<Replica> reps;
+    int seed_size = 0;
+    uint64_t glen = 0;
+    std::string err;
+    std::mutex mu;
+    float last_e2e_ms = 0, last_kernel_ms = 0;
+    uint64_t last_launches = 0;
+};
+
+namespace {
+
+int fail(sa_context* ctx, int code, const std::string& msg) {
+    if (ctx) ctx->err = msg;
+    else g_thread_err = msg;
+    return code;
+}
+
+#define CUDA_TRY(ctx, x)                                                              \
+    do {                                                                              \
+        cudaError_t e_ = (x);                                                         \
+        if (e_ != cudaSuccess)                                                        \
+            return fail(ctx, SA_ERUNTIME, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+int validate_params(const sa_params* p, std::string& why) {  // REF src/aligner.cpp:11-24
+    if (!p) { why = "params is NULL"; return SA_EINVAL; }
+    if (p->seed_size < 1 || p->seed_size > 32) { why = "seed-size must be in [1, 32]"; return SA_EINVAL; }
+    if (p->seeds_to_try < 1) { why = "seeds-to-try must be >= 1"; return SA_EINVAL; }
+    if (p->max_distance < -1) { why = "max-dist must be >= 0 (or -1 for auto)"; return SA_EINVAL; }
+    if (p->confidence_threshold < 1) { why = "confidence must be >= 1"; return SA_EINVAL; }
+    if (p->max_hits < 1) { why = "max-hits must be >= 1"; return SA_EINVAL; }
+    if (p->bucket_size < 1 || p->bucket_size > 64) { why = "bucket-size must be in [1, 64]"; return SA_EINVAL; }
+    return SA_OK;
+}
+
+inline int round4(int v) { return (v + 3) & ~3; }
+inline uint32_t round16(uint64_t v) { return static_cast<uint32_t>((v + 15) & ~15ull); }
+
+// Per-warp shared-memory layout for reads up to Lmax bases.
+int make_shape(Replica& rep, const sa_params* p, uint64_t Lmax, LaunchShape& sh, std::string& why) {
+    AlignLaunch& a = sh.proto;
+    std::memset(&a, 0, sizeof(a));
+    a.planes = rep.ix.planes;
+    a.glen = rep.ix.glen;
+    a.table = rep.ix.table;
+    a.n_slots = rep.ix.n_slots;
+    a.pool = rep.ix.pool;
+    a.s = p->seed_size;
+    a.n = p->seeds_to_try;
+    a.dmax_param = p->max_distance;
+    a.c = p->confidence_threshold;
+    a.hmax = p->max_hits;
+    a.bs = p->bucket_size;
+    a.force = p->force_max_dlimit ? 1 : 0;
+    if (Lmax < static_cast<uint64_t>(p->seed_size)) Lmax = p->seed_size;
+    if (Lmax > (1u << 20)) {
+        why = "read longer than 1 Mbp";
+        return SA_EINVAL;
+    }
+    const int L = static_cast<int>(Lmax);
+    const int dmax = p->max_distance >= 0 ? p->max_distance : (12 * L + 99) / 100;
+    a.dl_max = dmax + p->confidence_threshold - 1;
+    a.wbr = (L + 31) / 32 + 2;
+    a.wbw = (64 + L + a.dl_max + 31) / 32 + 4;
+    a.n_off_cap = round4(std::max(1, std::min(p->seeds_to_try, L - p->seed_size + 1)));
+    a.f_ints = a.dl_max > 15 ? round4(2 * (2 * a.dl_max + 3)) : 0;
+    const uint64_t common = 16ull * (2 * a.wbr + a.wbw) + 4ull * (a.n_off_cap + a.f_ints);
+    a.cap = kFastCap;
+    a.hcap = kFastHcap;
+    a.smem_per_warp = round16(common + cand_table_bytes(a.cap, a.hcap));
+    const uint32_t kMaxSmem = 227 * 1024;
+    if (a.smem_per_warp > kMaxSmem) {
+        why = "read too long for the shared-memory layout (limit ~60 kbp)";
+        return SA_EINVAL;
+    }
+    int warps = std::min<int>(8, kMaxSmem / a.smem_per_warp);
+    sh.fast_block = 32 * warps;
+    int bps = 0;
+    if (rep.smem_attr < kMaxSmem) {
+        if (align_set_smem(kMaxSmem) != cudaSuccess) {
+            why = "cudaFuncSetAttribute failed";
+            return SA_ERUNTIME;
+        }
+        rep.smem_attr = kMaxSmem;
+    }
+    if (align_fast_occupancy(sh.fast_block, a.smem_per_warp * warps, &bps) != cudaSuccess || bps < 1) bps = 1;
+    sh.fast_grid = bps * rep.sm_count;
+
+    // slow path: candidate tables in global memory, worst case n_eff * h_max
+    const uint64_t n_eff = static_cast<uint64_t>(std::min(p->seeds_to_try, L - p->seed_size + 1));
+    uint64_t cap_slow = std::max<uint64_t>(64, n_eff * static_cast<uint64_t>(p->max_hits));
+    if (cap_slow > (1u << 26)) cap_slow = 1u << 26;
+    uint64_t hcap_slow = 1;
+    while (hcap_slow < 2 * cap_slow) hcap_slow <<= 1;
+    sh.slow_cap = static_cast<int>(cap_slow);
+    sh.slow_hcap = static_cast<int>(hcap_slow);
+    sh.slow_table_bytes = (cand_table_bytes(sh.slow_cap, sh.slow_hcap) + 255) & ~255ull;
+    sh.slow_smem_per_warp = round16(common);
+    uint64_t slow_warps = std::min<uint64_t>(static_cast<uint64_t>(rep.sm_count) * 8,
+                                             std::max<uint64_t>(32, kSlowScratchBudget / sh.slow_table_bytes));
+    sh.slow_block = 32;
+    sh.slow_grid = static_cast<int>(slow_warps);
+    a.gscratch_per_warp = sh.slow_table_bytes;
+    // the slow launch overrides cap/hcap/smem_per_warp
+    return SA_OK;
+}
+
+int ensure_stage(sa_context* ctx, Stage& s, uint64_t bytes, uint64_t reads) {
+    if (!s.st) {
+        CUDA_TRY(ctx, cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking));
+        CUDA_TRY(ctx, cudaEventCreate(&s.k0));
+        CUDA_TRY(ctx, cudaEventCreate(&s.k1));
+        CUDA_TRY(ctx, cudaMalloc(&s.d_ctl, kCtlWords * sizeof(unsigned int)));
+    }
+    if (bytes > s.bases_cap) {
+        if (s.d_bases) cudaFree(s.d_bases);
+        s.d_bases = nullptr;
+        uint64_t nb = std::max<uint64_t>(bytes, 1 << 16);
+        CUDA_TRY(ctx, cudaMalloc(&s.d_bases, nb + 64));
+        s.bases_cap = nb;
+    }
+    if (reads > s.reads_cap) {
+        if (s.d_offsets) cudaFree(s.d_offsets);
+        if (s.d_results) cudaFree(s.d_results);
+        if (s.d_overflow) cudaFree(s.d_overflow);
+        s.d_offsets = nullptr;
+        s.d_results = nullptr;
+        s.d_overflow = nullptr;
+        uint64_t nr = std::max<uint64_t>(reads, 1024);
+        CUDA_TRY(ctx, cudaMalloc(&s.d_offsets, (nr + 1) * sizeof(uint64_t)));
+        CUDA_TRY(ctx, cudaMalloc(&s.d_results, nr * sizeof(sa_result)));
+        CUDA_TRY(ctx, cudaMalloc(&s.d_overflow, nr * sizeof(unsigned int)));
+        s.reads_cap = nr;
+    }
+    return SA_OK;
+}
+
+int ensure_scratch(sa_context* ctx, Replica& rep, const LaunchShape& sh) {
+    uint64_t need = static_cast<uint64_t>(sh.slow_grid) * sh.slow_table_bytes;
+    if (need > rep.gscratch_bytes) {
+        if (rep.d_gscratch) cudaFree(rep.d_gscratch);
+        rep.d_gscratch = nullptr;
+        CUDA_TRY(ctx, cudaMalloc(&rep.d_gscratch, need));
+        rep.gscratch_bytes = need;
+        // hash keys must start empty; tables are self-cleaning afterwards
+        CUDA_TRY(ctx, cudaMemset(rep.d_gscratch, 0xff, need));
+    }
+    return SA_OK;
+}
+
+// Enqueue fast + slow kernels for reads already on the device.
+int enqueue_align(sa_context* ctx, Replica& rep, Stage& stg, const LaunchShape& sh,
+                  const char* d_bases, const uint64_t* d_offsets, uint64_t base_off,
+                  uint64_t n_reads, sa_result* d_results, unsigned long long* d_stats,
+                  unsigned int* d_overflow, bool time_it, uint64_t& launches) {
+    AlignLaunch a = sh.proto;
+    a.bases = d_bases;
+    a.offsets = d_offsets;
+    a.base_off = base_off;
+    a.n_reads = static_cast<uint32_t>(n_reads);
+    a.results = d_results;
+    a.stats = d_stats;
+    a.cursor = stg.d_ctl + 0;
+    a.overflow_count = stg.d_ctl + 2;
+    a.overflow_list = d_overflow;
+    a.error_flag = rep.d_err;
+    a.error_read = nullptr;
+    a.gscratch = rep.d_gscratch;
+    CUDA_TRY(ctx, cudaMemsetAsync(stg.d_ctl, 0, kCtlWords * sizeof(unsigned int), stg.st));
+    if (time_it) CUDA_TRY(ctx, cudaEventRecord(stg.k0, stg.st));
+    launch_align_fast(a, sh.fast_grid, sh.fast_block, stg.st);
+    CUDA_TRY(ctx, cudaGetLastError());
+    AlignLaunch b = a;
+    b.cursor = stg.d_ctl + 1;
+    b.work_list = d_overflow;
+    b.work_count = stg.d_ctl + 2;
+    b.overflow_list = nullptr;
+    b.overflow_count = nullptr;
+    b.cap = sh.slow_cap;
+    b.hcap = sh.slow_hcap;
+    b.smem_per_warp = sh.slow_smem_per_warp;
+    launch_align_slow(b, sh.slow_grid, sh.slow_block, stg.st);
+    CUDA_TRY(ctx, cudaGetLastError());
+    if (time_it) CUDA_TRY(ctx, cudaEventRecord(stg.k1, stg.st));
+    launches += 2;
+    return SA_OK;
+}
+
+int check_errors(sa_context* ctx, Replica& rep) {
+    unsigned int flag = 0;
+    CUDA_TRY(ctx, cudaMemcpy(&flag, rep.d_err, sizeof(flag), cudaMemcpyDeviceToHost));
+    if (flag) {
+        CUDA_TRY(ctx, cudaMemset(rep.d_err, 0, sizeof(unsigned int)));
+        return fail(ctx, SA_EINVAL, "reverse_complement: non-base character (read holds a "
+                                    "character outside {A,C,G,T,N})");
+    }
+    return SA_OK;
+}
+
+void add_stats(sa_stats* dst, const unsigned long long* src) {
+    uint64_t* d = reinterpret_cast<uint64_t*>(dst);
+    for (int i = 0; i < kNumStats; ++i) d[i] += src[i];
+}
+
+}  // namespace
+
+extern "C" {
+
+void sa_default_params(sa_params* out) {  // REF include/seedaln/aligner.hpp:20-26
+    out->seed_size = 20;
+    out->seeds_to_try = 25;
+    out->max_distance = -1;
+    out->confidence_threshold = 2;
+    out->max_hits = 300;
+    out->bucket_size = 32;
+    out->force_max_dlimit = 0;
+}
+
+int sa_validate_params(const sa_params* p) {
+    std::string why;
+    int rc = validate_params(p, why);
+    if (rc) g_thread_err = why;
+    return rc;
+}
+
+int sa_seed_offsets(uint64_t read_length, int32_t s, int32_t n, int32_t* out, int32_t* count) {
+    // REF src/aligner.cpp:50-79 (host copy of the kernel's compute_offsets)
+    *count = 0;
+    if (s < 1 || n < 1 || read_length < static_cast<uint64_t>(s)) return SA_OK;
+    if (s > 32) {
+        g_thread_err = "seed size must be in [1, 32]";
+        return SA_EINVAL;
+    }
+    const int64_t max_off = static_cast<int64_t>(read_length) - s;
+    int cnt = 0;
+    uint64_t used = 0;
+    auto emit = [&](int shift) {
+        if ((used >> shift) & 1ull) return;
+        used |= 1ull << shift;
+        for (int64_t o = shift; o <= max_off && cnt < n; o += s) out[cnt++] = static_cast<int32_t>(o);
+    };
+    emit(0);
+    for (int level = 1; (int64_t{1} << level) <= 4 * int64_t{s} && cnt < n; ++level)
+        for (int64_t odd = 1; odd < (int64_t{1} << level) && cnt < n; odd += 2)
+            emit(static_cast<int>((odd * s) >> level));
+    *count = cnt;
+    return SA_OK;
+}
+
+const char* sa_last_error(const sa_context* ctx) {
+    return ctx ? ctx->err.c_str() : g_thread_err.c_str();
+}
+
+int sa_create(const uint64_t* packed_words, uint64_t n_packed, const uint64_t* nmask_words,
+              uint64_t n_nmask, uint64_t genome_length, int32_t seed_size, const int32_t* devices,
+              int32_t n_devices, sa_context** out) {
+    if (!out) return fail(nullptr, SA_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (seed_size < 1 || seed_size > 32)  // REF src/seed_index.cpp:81-82
+        return fail(nullptr, SA_EINVAL, "seed size must be in [1, 32]");
+    if (genome_length < static_cast<uint64_t>(seed_size))  // REF :83-84
+        return fail(nullptr, SA_EINVAL, "genome shorter than seed size");
+    if (genome_length > 0xffffffffull - 64)
+        return fail(nullptr, SA_EINVAL, "genome longer than 2^32 - 64 bases");
+    if (n_packed != (genome_length + 31) / 32 || n_nmask != (genome_length + 63) / 64)
+        return fail(nullptr, SA_EFORMAT, "packed/n-mask word counts do not match genome length");
+    std::vector<int> devs;
+    if (!devices || n_devices <= 0) devs.push_back(0);
+    else devs.assign(devices, devices + n_devices);
+    int have = 0;
+    if (cudaGetDeviceCount(&have) != cudaSuccess || have == 0)
+        return fail(nullptr, SA_ERUNTIME, "no CUDA device visible");
+    auto* ctx = new sa_context;
+    ctx->seed_size = seed_size;
+    ctx->glen = genome_length;
+    ctx->reps.resize(devs.size());
+    std::vector<std::string> errs(devs.size());
+    std::vector<int> codes(devs.size(), 0);
+    auto build = [&](size_t i) {
+        Replica& rep = ctx->reps[i];
+        rep.device = devs[i];
+        if (cudaSetDevice(rep.device) != cudaSuccess) {
+            codes[i] = SA_ERUNTIME;
+            errs[i] = "cudaSetDevice failed";
+            return;
+        }
+        cudaDeviceGetAttribute(&rep.sm_count, cudaDevAttrMultiProcessorCount, rep.device);
+        cudaStream_t st;
+        cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+        std::string e;
+        if (build_device_index(packed_words, n_packed, nmask_words, n_nmask, genome_length,
+                               seed_size, st, &rep.ix, e) != 0) {
+            codes[i] = SA_ERUNTIME;
+            errs[i] = "index build on device " + std::to_string(rep.device) + ": " + e;
+        }
+        cudaStreamDestroy(st);
+        if (!codes[i]) {
+            if (cudaMalloc(&rep.d_stats, kNumStats * sizeof(unsigned long long)) != cudaSuccess ||
+                cudaMalloc(&rep.d_err, sizeof(unsigned int)) != cudaSuccess ||
+                cudaMemset(rep.d_err, 0, sizeof(unsigned int)) != cudaSuccess ||
+                cudaEventCreate(&rep.e_start) != cudaSuccess ||
+                cudaEventCreate(&rep.e_end) != cudaSuccess) {
+                codes[i] = SA_ERUNTIME;
+                errs[i] = "device allocation failed";
+            }
+        }
+    };
+    if (devs.size() == 1) {
+        build(0);
+    } else {
+        std::vector<std::thread> th;
+        for (size_t i = 0; i < devs.size(); ++i) th.emplace_back(build, i);
+        for (auto& t : th) t.join();
+    }
+    for (size_t i = 0; i < devs.size(); ++i) {
+        if (codes[i]) {
+            int c = codes[i];
+            std::string m = errs[i];
+            sa_destroy(ctx);
+            return fail(nullptr, c, m);
+        }
+    }
+    *out = ctx;
+    return SA_OK;
+}
+
+void sa_destroy(sa_context* ctx) {
+    if (!ctx) return;
+    for (auto& rep : ctx->reps) {
+        cudaSetDevice(rep.device);
+        for (auto& s : rep.stage) {
+            if (s.st) cudaStreamSynchronize(s.st);
+            if (s.d_bases) cudaFree(s.d_bases);
+            if (s.d_offsets) cudaFree(s.d_offsets);
+            if (s.d_results) cudaFree(s.d_results);
+            if (s.d_overflow) cudaFree(s.d_overflow);
+            if (s.d_ctl) cudaFree(s.d_ctl);
+            if (s.k0) cudaEventDestroy(s.k0);
+            if (s.k1) cudaEventDestroy(s.k1);
+            if (s.st) cudaStreamDestroy(s.st);
+        }
+        if (rep.d_stats) cudaFree(rep.d_stats);
+        if (rep.d_err) cudaFree(rep.d_err);
+        if (rep.d_gscratch) cudaFree(rep.d_gscratch);
+        if (rep.e_start) cudaEventDestroy(rep.e_start);
+        if (rep.e_end) cudaEventDestroy(rep.e_end);
+        free_device_index(&rep.ix);
+    }
+    delete ctx;
+}
+
+int sa_index_info(const sa_context* ctx, uint64_t* distinct_seeds, uint64_t* total_positions,
+                  uint64_t* device_bytes) {
+    if (!ctx || ctx->reps.empty()) return fail(nullptr, SA_EINVAL, "null context");
+    const DeviceIndex& ix = ctx->reps[0].ix;
+    if (distinct_seeds) *distinct_seeds = ix.n_distinct;
+    if (total_positions) *total_positions = ix.n_positions;
+    if (device_bytes) *device_bytes = ix.device_bytes;
+    return SA_OK;
+}
+
+int sa_align_batch(sa_context* ctx, const sa_params* params, const char* bases,
+                   const uint64_t* offsets, uint64_t n_reads, sa_result* results, sa_stats* stats) {
+    if (!ctx) return fail(nullptr, SA_EINVAL, "null context");
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    std::string why;
+    if (int rc = validate_params(params, why)) return fail(ctx, rc, why);
+    if (params->seed_size != ctx->seed_size)  // REF src/aligner.cpp:119-121
+        return fail(ctx, SA_EINVAL, "index seed size does not match params");
+    if (n_reads == 0) {
+        ctx->last_e2e_ms = ctx->last_kernel_ms = 0;
+        ctx->last_launches = 0;
+        return SA_OK;
+    }
+    if (!bases || !offsets || !results) return fail(ctx, SA_EINVAL, "null buffer");
+    if (n_reads >= 0xffffffffull) return fail(ctx, SA_EINVAL, "too many reads in one batch");
+    uint64_t Lmax = 0;
+    for (uint64_t i = 0; i < n_reads; ++i) {
+        if (offsets[i + 1] < offsets[i]) return fail(ctx, SA_EINVAL, "offsets not ascending");
+        Lmax = std::max(Lmax, offsets[i + 1] - offsets[i]);
+    }
+    // chunk boundaries (reads and bytes bounded)
+    std::vector<uint64_t> bounds{0};
+    while (bounds.back() < n_reads) {
+        uint64_t b = bounds.back();
+        uint64_t e = std::min(n_reads, b + kChunkReads);
+        while (e > b + 1 && offsets[e] - offsets[b] > kChunkBytes) e = b + (e - b) / 2;
+        bounds.push_back(e);
+    }
+    const size_t n_chunks = bounds.size() - 1;
+    std::atomic<size_t> next{0};
+    std::vector<int> codes(ctx->reps.size(), 0);
+    std::vector<std::string> msgs(ctx->reps.size());
+    std::vector<sa_stats> part(ctx->reps.size());
+    std::vector<float> e2e(ctx->reps.size(), 0), kms(ctx->reps.size(), 0);
+    std::vector<uint64_t> launches(ctx->reps.size(), 0);
+
+    auto worker = [&](size_t ri) {
+        Replica& rep = ctx->reps[ri];
+        sa_context local_err;  // per-worker error sink
+        auto run = [&]() -> int {
+            if (cudaSetDevice(rep.device) != cudaSuccess) return fail(&local_err, SA_ERUNTIME, "cudaSetDevice");
+            LaunchShape sh;
+            std::string w;
+            if (int rc = make_shape(rep, params, Lmax, sh, w)) return fail(&local_err, rc, w);
+            if (int rc = ensure_scratch(&local_err, rep, sh)) return rc;
+            uint64_t max_bytes = 0, max_reads = 0;
+            for (size_t c = 0; c < n_chunks; ++c) {
+                max_reads = std::max(max_reads, bounds[c + 1] - bounds[c]);
+                max_bytes = std::max(max_bytes, offsets[bounds[c + 1]] - offsets[bounds[c]]);
+            }
+            for (int k = 0; k < 2; ++k)
+                if (int rc = ensure_stage(&local_err, rep.stage[k], max_bytes, max_reads)) return rc;
+            CUDA_TRY(&local_err, cudaMemsetAsync(rep.d_stats, 0, kNumStats * sizeof(unsigned long long), rep.stage[0].st));
+            CUDA_TRY(&local_err, cudaEventRecord(rep.e_start, rep.stage[0].st));
+            CUDA_TRY(&local_err, cudaStreamWaitEvent(rep.stage[1].st, rep.e_start, 0));
+            std::vector<std::pair<int, int>> timed;  // (stage, chunk#) whose kernel events to read
+            int k = 0;
+            for (;;) {
+                size_t c = next.fetch_add(1);
+                if (c >= n_chunks) break;
+                Stage& stg = rep.stage[k & 1];
+                // stage reuse: kernel events of the previous chunk on this stage
+                if (k >= 2) {
+                    CUDA_TRY(&local_err, cudaEventSynchronize(stg.k1));
+                    float ms = 0;
+                    cudaEventElapsedTime(&ms, stg.k0, stg.k1);
+                    kms[ri] += ms;
+                }
+                const uint64_t r0 = bounds[c], r1 = bounds[c + 1];
+                const uint64_t b0 = offsets[r0], b1 = offsets[r1];
+                CUDA_TRY(&local_err, cudaMemcpyAsync(stg.d_bases, bases + b0, b1 - b0, cudaMemcpyHostToDevice, stg.st));
+                CUDA_TRY(&local_err, cudaMemcpyAsync(stg.d_offsets, offsets + r0, (r1 - r0 + 1) * sizeof(uint64_t),
+                                                     cudaMemcpyHostToDevice, stg.st));
+                if (int rc = enqueue_align(&local_err, rep, stg, sh, stg.d_bases, stg.d_offsets, b0, r1 - r0,
+                                           stg.d_results, rep.d_stats, stg.d_overflow, true, launches[ri]))
+                    return rc;
+                CUDA_TRY(&local_err, cudaMemcpyAsync(results + r0, stg.d_results, (r1 - r0) * sizeof(sa_result),
+                                                     cudaMemcpyDeviceToHost, stg.st));
+                ++k;
+            }
+            for (int j = 0; j < 2 && j < k; ++j) {
+                Stage& stg = rep.stage[(k - 1 - j) & 1];
+                CUDA_TRY(&local_err, cudaEventSynchronize(stg.k1));
+                float ms = 0;
+                cudaEventElapsedTime(&ms, stg.k0, stg.k1);
+                kms[ri] += ms;
+            }
+            CUDA_TRY(&local_err, cudaEventRecord(rep.stage[1].k1, rep.stage[1].st));
+            CUDA_TRY(&local_err, cudaStreamWaitEvent(rep.stage[0].st, rep.stage[1].k1, 0));
+            CUDA_TRY(&local_err, cudaEventRecord(rep.e_end, rep.stage[0].st));
+            CUDA_TRY(&local_err, cudaEventSynchronize(rep.e_end));
+            cudaEventElapsedTime(&e2e[ri], rep.e_start, rep.e_end);
+            unsigned long long h[kNumStats];
+            CUDA_TRY(&local_err, cudaMemcpy(h, rep.d_stats, sizeof(h), cudaMemcpyDeviceToHost));
+            std::memset(&part[ri], 0, sizeof(sa_stats));
+            add_stats(&part[ri], h);
+            return check_errors(&local_err, rep);
+        };
+        codes[ri] = run();
+        if (codes[ri]) msgs[ri] = local_err.err;
+    };
+    if (ctx->reps.size() == 1) {
+        worker(0);
+    } else {
+        std::vector<std::thread> th;
+        for (size_t i = 0; i < ctx->reps.size(); ++i) th.emplace_back(worker, i);
+        for (auto& t : th) t.join();
+    }
+    for (size_t i = 0; i < ctx->reps.size(); ++i)
+        if (codes[i]) return fail(ctx, codes[i], msgs[i]);
+    ctx->last_e2e_ms = *std::max_element(e2e.begin(), e2e.end());
+    ctx->last_kernel_ms = *std::max_element(kms.begin(), kms.end());
+    ctx->last_launches = 0;
+    for (auto l : launches) ctx->last_launches += l;
+    if (stats)
+        for (auto& p : part) {
+            uint64_t* d = reinterpret_cast<uint64_t*>(stats);
+            const uint64_t* s = reinterpret_cast<const uint64_t*>(&p);
+            for (size_t i = 0; i < sizeof(sa_stats) / 8; ++i) d[i] += s[i];
+        }
+    return SA_OK;
+}
+
+int sa_align_device(sa_context* ctx, const sa_params* params, const char* d_bases,
+                    const uint64_t* d_offsets, uint64_t n_reads, uint64_t max_read_length,
+                    sa_result* d_results, sa_stats* d_stats, void* stream) {
+    if (!ctx) return fail(nullptr, SA_EINVAL, "null context");
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    std::string why;
+    if (int rc = validate_params(params, why)) return fail(ctx, rc, why);
+    if (params->seed_size != ctx->seed_size)
+        return fail(ctx, SA_EINVAL, "index seed size does not match params");
+    if (n_reads == 0) return SA_OK;
+    if (n_reads >= 0xffffffffull) return fail(ctx, SA_EINVAL, "too many reads in one batch");
+    Replica& rep = ctx->reps[0];
+    CUDA_TRY(ctx, cudaSetDevice(rep.device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (max_read_length == 0) return fail(ctx, SA_EINVAL, "max_read_length must be given");
+    LaunchShape sh;
+    if (int rc = make_shape(rep, params, max_read_length, sh, why)) return fail(ctx, rc, why);
+    if (int rc = ensure_scratch(ctx, rep, sh)) return rc;
+    Stage& stg = rep.stage[2];
+    if (int rc = ensure_stage(ctx, stg, 0, n_reads)) return rc;
+    // the caller's stream drives; stage[2] keeps only control words
+    Stage tmp = stg;
+    tmp.st = st;
+    unsigned long long* stats_dst = reinterpret_cast<unsigned long long*>(d_stats);
+    if (!stats_dst) stats_dst = rep.d_stats;
+    uint64_t launches = 0;
+    if (int rc = enqueue_align(ctx, rep, tmp, sh, d_bases, d_offsets, 0, n_reads, d_results,
+                               stats_dst, stg.d_overflow, false, launches))
+        return rc;
+    ctx->last_launches = launches;
+    return SA_OK;
+}
+
+int sa_sync(sa_context* ctx, void* stream) {
+    if (!ctx) return fail(nullptr, SA_EINVAL, "null context");
+    Replica& rep = ctx->reps[0];
+    CUDA_TRY(ctx, cudaSetDevice(rep.device));
+    CUDA_TRY(ctx, cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    return check_errors(ctx, rep);
+}
+
+int sa_lookup_batch(sa_context* ctx, const char* seeds, uint64_t n_seeds, uint32_t* counts,
+                    uint64_t* fwd_out, uint32_t* n_fwd, uint64_t* rc_out, uint32_t* n_rc,
+                    uint32_t cap) {
+    if (!ctx) return fail(nullptr, SA_EINVAL, "null context");
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    if (n_seeds == 0) return SA_OK;
+    if (!seeds || !counts) return fail(ctx, SA_EINVAL, "null buffer");
+    if ((fwd_out == nullptr) != (rc_out == nullptr)) return fail(ctx, SA_EINVAL, "fwd_out/rc_out must both be set");
+    Replica& rep = ctx->reps[0];
+    CUDA_TRY(ctx, cudaSetDevice(rep.device));
+    const int s = ctx->seed_size;
+    char* d_seeds = nullptr;
+    uint32_t *d_counts = nullptr, *d_nf = nullptr, *d_nr = nullptr;
+    uint64_t *d_fwd = nullptr, *d_rc = nullptr;
+    const bool lists = fwd_out != nullptr && cap > 0;
+    CUDA_TRY(ctx, cudaMalloc(&d_seeds, n_seeds * s));
+    CUDA_TRY(ctx, cudaMalloc(&d_counts, n_seeds * 4));
+    CUDA_TRY(ctx, cudaMalloc(&d_nf, n_seeds * 4));
+    CUDA_TRY(ctx, cudaMalloc(&d_nr, n_seeds * 4));
+    if (lists) {
+        CUDA_TRY(ctx, cudaMalloc(&d_fwd, n_seeds * cap * 8));
+        CUDA_TRY(ctx, cudaMalloc(&d_rc, n_seeds * cap * 8));
+    }
+    CUDA_TRY(ctx, cudaMemcpy(d_seeds, seeds, n_seeds * s, cudaMemcpyHostToDevice));
+    LookupLaunch a{};
+    a.planes = rep.ix.planes;
+    a.table = rep.ix.table;
+    a.n_slots = rep.ix.n_slots;
+    a.pool = rep.ix.pool;
+    a.seeds = d_seeds;
+    a.n_seeds = n_seeds;
+    a.s = s;
+    a.counts = d_counts;
+    a.fwd_out = d_fwd;
+    a.rc_out = d_rc;
+    a.n_fwd = d_nf;
+    a.n_rc = d_nr;
+    a.cap = lists ? cap : 0;
+    launch_lookup(a, 0);
+    CUDA_TRY(ctx, cudaGetLastError());
+    CUDA_TRY(ctx, cudaDeviceSynchronize());
+    CUDA_TRY(ctx, cudaMemcpy(counts, d_counts, n_seeds * 4, cudaMemcpyDeviceToHost));
+    if (n_fwd) CUDA_TRY(ctx, cudaMemcpy(n_fwd, d_nf, n_seeds * 4, cudaMemcpyDeviceToHost));
+    if (n_rc) CUDA_TRY(ctx, cudaMemcpy(n_rc, d_nr, n_seeds * 4, cudaMemcpyDeviceToHost));
+    if (lists) {
+        CUDA_TRY(ctx, cudaMemcpy(fwd_out, d_fwd, n_seeds * cap * 8, cudaMemcpyDeviceToHost));
+        CUDA_TRY(ctx, cudaMemcpy(rc_out, d_rc, n_seeds * cap * 8, cudaMemcpyDeviceToHost));
+    }
+    cudaFree(d_seeds);
+    cudaFree(d_counts);
+    cudaFree(d_nf);
+    cudaFree(d_nr);
+    if (d_fwd) cudaFree(d_fwd);
+    if (d_rc) cudaFree(d_rc);
+    ctx->last_launches = 1;
+    return SA_OK;
+}
+
+int sa_bounded_distance_batch(const char* reads, const uint64_t* read_off, const char* windows,
+                              const uint64_t* win_off, const int32_t* d_limits, uint64_t n_pairs,
+                              int32_t* out, int32_t device) {
+    if (n_pairs == 0) return SA_OK;
+    if (!reads || !read_off || !windows || !win_off || !d_limits || !out)
+        return fail(nullptr, SA_EINVAL, "null buffer");
+    uint64_t mmax = 0, wmax = 0;
+    int dlmax = 0;
+    for (uint64_t i = 0; i < n_pairs; ++i) {
+        if (d_limits[i] < 0)  // REF src/edit_distance.cpp:22-23
+            return fail(nullptr, SA_EINVAL, "bounded_distance: negative d_limit");
+        if (read_off[i + 1] < read_off[i] || win_off[i + 1] < win_off[i])
+            return fail(nullptr, SA_EINVAL, "offsets not ascending");
+        const uint64_t m = read_off[i + 1] - read_off[i];
+        mmax = std::max(mmax, m);
+        wmax = std::max(wmax, win_off[i + 1] - win_off[i]);
+        dlmax = std::max<int>(dlmax, static_cast<int>(std::min<uint64_t>(d_limits[i], m)));
+    }
+    LvLaunch a{};
+    a.wbr = static_cast<int>((mmax + 31) / 32 + 2);
+    a.wbw = static_cast<int>((wmax + 31) / 32 + 2);
+    a.f_ints = dlmax > 15 ? round4(2 * (2 * dlmax + 3)) : 0;
+    a.smem_per_warp = round16(16ull * (a.wbr + a.wbw) + 4ull * a.f_ints);
+    if (a.smem_per_warp > 227 * 1024) return fail(nullptr, SA_EINVAL, "pair too long for the LV kernel");
+    if (cudaSetDevice(device) != cudaSuccess) return fail(nullptr, SA_ERUNTIME, "cudaSetDevice failed");
+    const uint64_t rb = read_off[n_pairs] - read_off[0], wb = win_off[n_pairs] - win_off[0];
+    char *d_r = nullptr, *d_w = nullptr;
+    uint64_t *d_ro = nullptr, *d_wo = nullptr;
+    int32_t *d_dl = nullptr, *d_out = nullptr;
+    unsigned int* d_err = nullptr;
+    std::vector<uint64_t> ro(read_off, read_off + n_pairs + 1), wo(win_off, win_off + n_pairs + 1);
+    for (auto& v : ro) v -= read_off[0];
+    for (auto& v : wo) v -= win_off[0];
+#define LV_TRY(x)                                                                              \
+    do {                                                                                       \
+        cudaError_t e_ = (x);                                                                  \
+        if (e_ != cudaSuccess) return fail(nullptr, SA_ERUNTIME, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+    LV_TRY(cudaMalloc(&d_r, rb + 16));
+    LV_TRY(cudaMalloc(&d_w, wb + 16));
+    LV_TRY(cudaMalloc(&d_ro, (n_pairs + 1) * 8));
+    LV_TRY(cudaMalloc(&d_wo, (n_pairs + 1) * 8));
+    LV_TRY(cudaMalloc(&d_dl, n_pairs * 4));
+    LV_TRY(cudaMalloc(&d_out, n_pairs * 4));
+    LV_TRY(cudaMalloc(&d_err, 4));
+    LV_TRY(cudaMemset(d_err, 0, 4));
+    if (rb) LV_TRY(cudaMemcpy(d_r, reads + read_off[0], rb, cudaMemcpyHostToDevice));
+    if (wb) LV_TRY(cudaMemcpy(d_w, windows + win_off[0], wb, cudaMemcpyHostToDevice));
+    LV_TRY(cudaMemcpy(d_ro, ro.data(), (n_pairs + 1) * 8, cudaMemcpyHostToDevice));
+    LV_TRY(cudaMemcpy(d_wo, wo.data(), (n_pairs + 1) * 8, cudaMemcpyHostToDevice));
+    LV_TRY(cudaMemcpy(d_dl, d_limits, n_pairs * 4, cudaMemcpyHostToDevice));
+    LV_TRY(align_set_smem(227 * 1024));
+    a.reads = d_r;
+    a.read_off = d_ro;
+    a.wins = d_w;
+    a.win_off = d_wo;
+    a.d_limits = d_dl;
+    a.n_pairs = static_cast<uint32_t>(n_pairs);
+    a.out = d_out;
+    a.error_flag = d_err;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    int warps = std::max<int>(1, std::min<int>(8, (227 * 1024) / a.smem_per_warp));
+    uint64_t need_warps = std::min<uint64_t>(n_pairs, static_cast<uint64_t>(sms) * 64);
+    int grid = static_cast<int>(std::max<uint64_t>(1, (need_warps + warps - 1) / warps));
+    launch_lv_batch(a, grid, 32 * warps, 0);
+    LV_TRY(cudaGetLastError());
+    LV_TRY(cudaDeviceSynchronize());
+    unsigned int err = 0;
+    LV_TRY(cudaMemcpy(out, d_out, n_pairs * 4, cudaMemcpyDeviceToHost));
+    LV_TRY(cudaMemcpy(&err, d_err, 4, cudaMemcpyDeviceToHost));
+    cudaFree(d_r);
+    cudaFree(d_w);
+    cudaFree(d_ro);
+    cudaFree(d_wo);
+    cudaFree(d_dl);
+    cudaFree(d_out);
+    cudaFree(d_err);
+#undef LV_TRY
+    if (err) return fail(nullptr, SA_EINVAL, "bounded_distance batch: characters outside {A,C,G,T,N}");
+    return SA_OK;
+}
+
+int sa_host_alloc(void** ptr, uint64_t bytes) {
+    if (!ptr) return fail(nullptr, SA_EINVAL, "ptr is NULL");
+    cudaError_t e = cudaMallocHost(ptr, bytes ? bytes : 1);
+    if (e != cudaSuccess) return fail(nullptr, SA_ERUNTIME, cudaGetErrorString(e));
+    return SA_OK;
+}
+
+void sa_host_free(void* ptr) {
+    if (ptr) cudaFreeHost(ptr);
+}
+
+int sa_last_timing(const sa_context* ctx, float* e2e_ms, float* kernel_ms) {
+    if (!ctx) return fail(nullptr, SA_EINVAL, "null context");
+    if (e2e_ms) *e2e_ms = ctx->last_e2e_ms;
+    if (kernel_ms) *kernel_ms = ctx->last_kernel_ms;
+    return SA_OK;
+}
+
+int sa_last_launches(const sa_context* ctx, uint64_t* launches) {
+    if (!ctx) return fail(nullptr, SA_EINVAL, "null context");
+    *launches = ctx->last_launches;
+    return SA_OK;
+}
+
+}  // extern "C"

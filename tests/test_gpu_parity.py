@@ -1,0 +1,218 @@
+"""Parity of the CUDA path (through the C-ABI) against the oracle.
+
+Bar: bit-exact -- every AlignmentResult field (kind, has_position, position,
+direction, distance, gap) and every AlignStats counter the reference defines
+except dp_cells (implementation-specific), for every read.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1111_5572_b200 import api, synth
+
+pytestmark = pytest.mark.gpu
+
+ACGT = np.frombuffer(b"ACGT", np.uint8)
+
+
+def _case(name, genome_len, n_reads, n_runs=0, read_n_frac=0.0, seed=7):
+    cfg = synth.CONFIGS[name].scaled(genome_len=genome_len, n_reads=n_reads)
+    g = synth.make_genome(cfg)
+    rng = np.random.default_rng(seed)
+    for p in rng.integers(0, genome_len - 50, n_runs):
+        g[p:p + int(rng.integers(1, 40))] = ord("N")
+    packed, nmask = synth.pack_genome(g)
+    bases, offs, tp, td = synth.make_reads(cfg, g)
+    if read_n_frac:
+        for i in rng.integers(0, n_reads, int(n_reads * read_n_frac)):
+            bases[int(offs[i]) + int(rng.integers(0, cfg.read_len))] = ord("N")
+    return cfg, g, packed, nmask, bases, offs
+
+
+def _gpu_vs_oracle(cfg, g, packed, nmask, bases, offs, params=None):
+    params = params or cfg.params
+    genome = api.PackedGenome(packed, nmask, g.size)
+    idx = api.SeedIndex.build(genome, params.seed_size)
+    al = api.Aligner(idx, genome, params)
+    got = al.align_arrays(bases, offs)
+    want, wst = O.OracleIndex(packed, nmask, g.size, params.seed_size).align_arrays(params, bases, offs, threads=8)
+    bad = O.compare_results(got, want)
+    assert not bad, f"{len(bad)} reads differ; first {bad[:5]}: gpu {got[bad[:3]]} oracle {want[bad[:3]]}"
+    gst = al.stats().values
+    for f in O.STAT_FIELDS[:16] + ("hits_consumed", "window_bases", "read_bases"):
+        if f == "dp_cells":
+            continue
+        assert gst[f] == wst[f], f"stat {f}: gpu {gst[f]} oracle {wst[f]}"
+    return got, gst
+
+
+# ----------------------------------------------------------------- LV
+
+def test_lv_known_answers():
+    # REF tests/test_edit_distance.cpp:37-68
+    cases = [("ACGT", "ACGTAA", 2, 0), ("ACGT", "AGGTAA", 2, 1), ("ACGTACGT", "ACGACGTCCC", 2, 1),
+             ("AAAA", "TTTTTT", 2, None), ("AC", "ACGTGT", 3, 0), ("ACGT", "AC", 3, 2), ("ACGT", "", 4, 4),
+             ("AN", "AN", 2, 1), ("ANNA", "AGGA", 4, 2), ("ACGT", "ACGN", 2, 1)]
+    got = api.bounded_distance_batch([(r, w, d) for r, w, d, _ in cases])
+    assert got == [e for *_, e in cases]
+    with pytest.raises(ValueError):
+        api.bounded_distance("A", "A", -1)
+
+
+def _random_triples(rng, n, max_len=100, max_edits=11, max_dl=16):
+    out = []
+    for _ in range(n):
+        L = int(rng.integers(1, max_len + 1))
+        read = ACGT[rng.integers(0, 4, L)].tobytes().decode()
+        win = list(read)
+        for _ in range(int(rng.integers(0, max_edits))):
+            if not win:
+                break
+            i = int(rng.integers(0, len(win)))
+            op = int(rng.integers(0, 3))
+            if op == 0:
+                win[i] = "ACGT"[int(rng.integers(0, 4))]
+            elif op == 1:
+                win.insert(i, "ACGT"[int(rng.integers(0, 4))])
+            else:
+                del win[i]
+        win += list(ACGT[rng.integers(0, 4, 8)].tobytes().decode())
+        if rng.integers(0, 16) == 0:
+            win[int(rng.integers(0, len(win)))] = "N"
+        if rng.integers(0, 16) == 0:
+            read = read[:-1] + "N"
+        dl = int(rng.integers(0, max_dl))
+        out.append((read, "".join(win)[:L + dl], dl))
+    return out
+
+
+def test_lv_random_vs_oracle():
+    # acceptance criterion 2 style (REF tests/acceptance/acceptance_main.cpp:293-333)
+    rng = np.random.default_rng(0xC2C2)
+    triples = _random_triples(rng, 20000)
+    got = api.bounded_distance_batch(triples)
+    want = [O.or_bounded_distance(r, w, d) for r, w, d in triples]
+    assert got == want
+    full = [O.or_full_dp(r, w) for r, w, d in triples[:3000]]
+    for (r, w, d), gv, f in zip(triples, got, full):
+        assert gv == (f if f <= d else None)
+
+
+def test_lv_wide_limits_vs_oracle():
+    rng = np.random.default_rng(11)
+    triples = []
+    for _ in range(300):
+        L = int(rng.integers(200, 3000))
+        t = _random_triples(rng, 1, max_len=1, max_edits=1, max_dl=1)  # noqa: F841
+        read = ACGT[rng.integers(0, 4, L)].tobytes().decode()
+        win = list(read)
+        for _ in range(int(rng.integers(0, L // 8))):
+            i = int(rng.integers(0, len(win)))
+            op = int(rng.integers(0, 3))
+            if op == 0:
+                win[i] = "ACGT"[int(rng.integers(0, 4))]
+            elif op == 1:
+                win.insert(i, "ACGT"[int(rng.integers(0, 4))])
+            else:
+                del win[i]
+        dl = int(rng.integers(16, 400))
+        win = "".join(win) + ACGT[rng.integers(0, 4, dl)].tobytes().decode()
+        triples.append((read, win[:L + dl], dl))
+    got = api.bounded_distance_batch(triples)
+    want = [O.or_bounded_distance(r, w, d) for r, w, d in triples]
+    assert got == want
+
+
+# ----------------------------------------------------------------- lookup
+
+@pytest.mark.parametrize("s", [3, 4, 7, 8, 20, 31, 32])
+def test_lookup_vs_oracle(s):
+    rng = np.random.default_rng(s)
+    for trial in range(6):
+        L = int(rng.integers(max(s, 50), 20000))
+        seq = ACGT[rng.integers(0, 4, L)]
+        if trial % 3 == 0:
+            seq[rng.random(L) < 0.03] = ord("N")
+        seq = seq.tobytes()
+        packed, nmask = O.pack_genome(seq)
+        gi = api.SeedIndex.build(api.PackedGenome(packed, nmask, L), s)
+        oi = O.OracleIndex(packed, nmask, L, s)
+        probes = []
+        for p in range(200):
+            if p % 2 == 0 and L > s:
+                at = int(rng.integers(0, L - s + 1))
+                probes.append(seq[at:at + s].decode())
+            else:
+                probes.append(ACGT[rng.integers(0, 4, s)].tobytes().decode())
+        res = gi.lookup_batch(probes, cap=L)
+        for q, r in zip(probes, res):
+            f, rc = oi.lookup(q)
+            assert (r.forward, r.rc) == (f, rc), q
+        assert gi.total_positions() == oi.ix.n_positions
+
+
+def test_lookup_palindrome_and_rc():
+    # REF tests/test_seed_index.cpp:67-95
+    g = api.PackedGenome.from_sequence("ACGTACGTAC")
+    idx = api.SeedIndex.build(g, 4)
+    assert idx.total_positions() == 7
+    r = idx.lookup("ACGT")
+    assert r.forward == [0, 4] and r.rc == [0, 4] and r.count() == 4
+    assert idx.lookup("CGTA").forward == [1, 5]
+    g2 = api.PackedGenome.from_sequence("AACCGG")
+    r2 = api.SeedIndex.build(g2, 4).lookup("GGTT")
+    assert r2.forward == [] and r2.rc == [0] and r2.count() == 1
+    g3 = api.PackedGenome.from_sequence("ACNTA")
+    i3 = api.SeedIndex.build(g3, 3)
+    assert i3.total_positions() == 0 and i3.lookup("ACN").count() == 0
+
+
+# ----------------------------------------------------------------- aligner
+
+@pytest.mark.parametrize("name,glen,nreads,runs,nfrac", [
+    ("C0", 1_000_000, 10_000, 0, 0.0),
+    ("C1", 5_000_000, 30_000, 20, 0.02),
+    ("C2", 8_000_000, 30_000, 20, 0.02),
+    ("C3", 8_000_000, 2_000, 10, 0.01),
+    ("C4", 3_000_000, 60, 5, 0.0),
+])
+def test_align_parity(name, glen, nreads, runs, nfrac):
+    cfg, g, packed, nmask, bases, offs = _case(name, glen, nreads, runs, nfrac)
+    got, st = _gpu_vs_oracle(cfg, g, packed, nmask, bases, offs)
+    assert st["reads"] == nreads
+
+
+def test_align_force_max_dlimit_parity():
+    cfg, g, packed, nmask, bases, offs = _case("C2", 4_000_000, 10_000, 10, 0.01)
+    p = synth.CONFIGS["C2"].params
+    forced = api.AlignerParams(**{**p.__dict__, "force_max_dlimit": True})
+    _gpu_vs_oracle(cfg, g, packed, nmask, bases, offs, params=forced)
+
+
+def test_align_ragged_and_short_reads():
+    cfg, g, packed, nmask, bases, offs = _case("C1", 2_000_000, 3000)
+    rng = np.random.default_rng(3)
+    reads = []
+    for i in range(3000):
+        L = int(rng.integers(0, 260))
+        st = int(rng.integers(0, g.size - L - 1))
+        r = bytearray(g[st:st + L].tobytes())
+        for _ in range(int(rng.integers(0, 4))):
+            if L:
+                r[int(rng.integers(0, L))] = ACGT[int(rng.integers(0, 4))]
+        reads.append(bytes(r))
+    buf, offs2 = api.reads_to_buffer(reads)
+    b = np.frombuffer(buf, np.uint8).copy()
+    _gpu_vs_oracle(cfg, g, packed, nmask, b, offs2)
+
+
+def test_invalid_character_raises():
+    cfg, g, packed, nmask, bases, offs = _case("C0", 200_000, 10)
+    genome = api.PackedGenome(packed, nmask, g.size)
+    al = api.Aligner(api.SeedIndex.build(genome, 20), genome, cfg.params)
+    b = bases.copy()
+    b[5] = ord("x")
+    with pytest.raises(ValueError):
+        al.align_arrays(b, offs)
+    # a read shorter than s is never inspected (REF aligner.cpp:231-235)
+    assert al.align_batch(["ACGx"])[0].kind == api.ResultKind.NotFound
