@@ -1,0 +1,360 @@
+#!/usr/bin/env python
+"""Benchmark: reads aligned/s on BASELINE.json config C1 (configs[1]: 100 Mbp
+i.i.d. genome, 1,000,000 x 100 bp reads per GPU, 1.5% substitutions + 0.1%
+geometric indels; s=20, n=10, h_max=300, d_max=10, c=2).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU)
+
+One step = one pass of the aligner hot path over the rank's batch of reads.
+`value`: reads already resident in HBM (sa_align_device), CUDA events on the
+launching stream, L2 flushed (256 MiB write) before every timed step, max over
+ranks.  `e2e`: the same batch through the public C-ABI call sa_align_batch from
+pinned host buffers (H2D reads+offsets, kernels, D2H results inside the
+CUDA-event-timed region).  Weak scaling: each rank aligns its own 1M reads
+against its own index replica; no collective on the data path.
+`--impl reference`: the reference's own CPU Aligner (oracle/_ref, compiled from
+/root/reference) on all host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "reads aligned/sec (whole box, 1/2/4/8 B200) and achieved HBM GB/s vs roofline"
+UNIT = "reads/s"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def _baseline_metric() -> str:
+    try:
+        with open(os.path.join(ROOT, "BASELINE.json")) as f:
+            return json.load(f).get("metric", METRIC)
+    except Exception:
+        return METRIC
+
+
+def _peaks() -> tuple[float, str]:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def _workload(cfg, reads_per_gpu: int) -> dict:
+    p = cfg.params
+    return {"workload": f"{cfg.name}: {cfg.genome_len // 1_000_000} Mbp i.i.d. genome (seed {cfg.genome_seed}), "
+                        f"{reads_per_gpu} x {cfg.read_len} bp reads per GPU, {cfg.sub_rate:.3%} subs + "
+                        f"{cfg.indel_rate:.2%} indels (geometric p={cfg.geom_p}, max {cfg.max_indel})",
+            "reads_per_gpu": reads_per_gpu, "read_len": cfg.read_len, "genome_bp": cfg.genome_len,
+            "params": {"seed_size": p.seed_size, "seeds_to_try": p.seeds_to_try, "max_hits": p.max_hits,
+                       "max_distance": p.max_distance, "confidence_threshold": p.confidence_threshold,
+                       "bucket_size": p.bucket_size},
+            "l2": "flushed by a 256 MiB device write before every timed step",
+            "parallelism": "replicas (full index per GPU, reads sharded, no collective)"}
+
+
+def run_reference(args) -> None:
+    rank, world, _ = _env_rank()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    from paper_1111_5572_b200 import synth
+
+    cfg = synth.CONFIGS[args.config]
+    g = synth.make_genome(cfg)
+    packed, nmask = synth.pack_genome(g)
+    n = args.reads_per_gpu or cfg.n_reads
+    sample = min(n, args.ref_sample)
+    bases, offs, _, _ = synth.make_reads(cfg, g, n_reads=sample, seed=cfg.read_seed)
+    cores = os.cpu_count() or 1
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libseedaln_ref.so not built"}))
+        return
+    t0 = time.perf_counter()
+    ri = O.RefIndex(packed, nmask, g.size, cfg.params.seed_size)
+    build_s = time.perf_counter() - t0
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        ri.align_arrays(cfg.params, bases, offs, threads=cores)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    v = sample / statistics.mean(times)
+    line = {"impl": "reference", "metric": _baseline_metric(), "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.mean(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic", "config": _workload(cfg, sample),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
+                             "sample": f"{sample} reads of {cfg.name} per step, reference Aligner (oracle/_ref, "
+                                       f"-O2) one per thread, atomic cursor grain 64; index build {build_s:.1f}s excluded"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args) -> None:
+    import torch
+
+    rank, world, local_rank = _env_rank()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    else:
+        torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+
+    from paper_1111_5572_b200 import api, synth
+
+    cfg = synth.CONFIGS[args.config]
+    R = args.reads_per_gpu or cfg.n_reads
+    t0 = time.perf_counter()
+    g = synth.make_genome(cfg)
+    packed, nmask = synth.pack_genome(g)
+    bases, offs, _, _ = synth.make_reads(cfg, g, n_reads=R, seed=cfg.read_seed + 7919 * rank)
+    gen_s = time.perf_counter() - t0
+    genome = api.PackedGenome(packed, nmask, g.size)
+    t0 = time.perf_counter()
+    idx = api.SeedIndex.build(genome, cfg.params.seed_size, devices=[local_rank])
+    build_s = time.perf_counter() - t0
+    al = api.Aligner(idx, genome, cfg.params)
+    L = cfg.read_len
+
+    # ---------------- device-resident (value)
+    d_bases = torch.from_numpy(bases).to(dev)
+    d_offs = torch.from_numpy(offs.view(np.int64)).to(dev)
+    d_res = torch.empty(R * 24, dtype=torch.uint8, device=dev)
+    d_stats = torch.zeros(20, dtype=torch.int64, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sptr = stream.cuda_stream
+
+    def step():
+        al.align_device(d_bases.data_ptr(), d_offs.data_ptr(), R, L, d_res.data_ptr(), d_stats.data_ptr(), sptr)
+
+    for _ in range(args.warmup):
+        step()
+    al.sync(sptr)
+    d_stats.zero_()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    step_ms, fast_ms, slow_ms = [], [], []
+    for _ in range(args.steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        f, s = al.last_kernel_times()
+        fast_ms.append(f)
+        slow_ms.append(s)
+    al.sync(sptr)
+    torch.cuda.synchronize(dev)
+    clocks = sampler.stop()
+    launches_per_step = al.last_launches()
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = world * R * args.steps / (total_ms / 1000.0)
+
+    st = dict(zip(api.STAT_FIELDS, [int(v) // args.steps for v in d_stats.cpu().tolist()]))
+    res_dev = d_res.cpu().numpy().view(api.RESULT_DTYPE)
+
+    # ---------------- end to end through the C-ABI (e2e)
+    pin_b = api.PinnedBuffer(bases.nbytes)
+    pin_o = api.PinnedBuffer(offs.nbytes)
+    pin_r = api.PinnedBuffer(R * 24)
+    hb = pin_b.array(np.uint8, bases.size)
+    ho = pin_o.array(np.uint64, offs.size)
+    hr = pin_r.array(api.RESULT_DTYPE, R)
+    hb[:] = bases
+    ho[:] = offs
+    for _ in range(args.warmup):
+        al.align_arrays(hb, ho, hr)
+    e2e_ms = []
+    if world > 1:
+        torch.distributed.barrier()
+    for _ in range(args.steps):
+        al.align_arrays(hb, ho, hr)
+        e2e_ms.append(al.last_timing()[0])
+    e2e_total = sum(e2e_ms)
+    if world > 1:
+        t = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    e2e_value = world * R * args.steps / (e2e_total / 1000.0)
+    e2e_launches = al.last_launches()
+    assert (hr["kind"] == res_dev["kind"]).all() and (hr["position"] == res_dev["position"]).all(), \
+        "e2e and device-resident results differ"
+
+    # ---------------- roofline of the dominant (fused) kernel
+    peak, peak_src = _peaks()
+    alg_bytes = (st["reads"] * (math.ceil(L / 4) + 24) + 32 * st["seed_lookups"] + 4 * st["hits_consumed"]
+                 + st["window_bases"] / 4.0)
+    fast_mean = statistics.mean(fast_ms)
+    achieved = alg_bytes / (fast_mean / 1000.0) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as f:
+                traffic = json.load(f).get(cfg.name, {}).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    line = {
+        "metric": _baseline_metric(), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": _workload(cfg, R),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "align_kernel<false> (fused seed/probe/vote/LV/classify)",
+                     "kernel_ms": fast_mean, "overflow_kernel_ms": statistics.mean(slow_ms),
+                     "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(bases.nbytes + offs.nbytes),
+                "d2h_bytes_per_step": int(R * 24 + 160), "ms_per_step": e2e_total / args.steps,
+                "gpu_launches_per_step": e2e_launches},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clocks,
+        "stats_per_step": {k: st[k] for k in ("reads", "seed_lookups", "hits_consumed", "distance_calls",
+                                               "window_bases", "single_hits", "multiple_hits", "not_found",
+                                               "overflow_reads")},
+        "setup_s": {"generate": round(gen_s, 2), "gpu_index_build": round(build_s, 2)},
+    }
+
+    # ---------------- CPU baseline: the reference, rank 0, N=1 only
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, g, packed, nmask, bases, offs, res_dev, args)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def cpu_baseline(cfg, g, packed, nmask, bases, offs, res_dev, args) -> dict:
+    from oracle import oracle as O
+
+    cores = os.cpu_count() or 1
+    sample = min(args.cpu_sample, offs.size - 1)
+    sb = bases[:int(offs[sample])]
+    so = offs[:sample + 1]
+    if O.ref_available():
+        kind = "reference"
+        t0 = time.perf_counter()
+        ix = O.RefIndex(packed, nmask, g.size, cfg.params.seed_size)
+    else:
+        kind = "port"
+        t0 = time.perf_counter()
+        ix = O.OracleIndex(packed, nmask, g.size, cfg.params.seed_size)
+    build_s = time.perf_counter() - t0
+    best = None
+    for _ in range(2):
+        t0 = time.perf_counter()
+        res, _ = ix.align_arrays(cfg.params, sb, so, threads=cores)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    mism = len(O.compare_results(res, res_dev[:sample]))
+    return {"value": sample / best, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"first {sample} reads of the GPU batch, {cores} threads (one reference Aligner per "
+                      f"thread, atomic cursor grain 64), best of 2; index build {build_s:.1f}s excluded",
+            "parity_mismatches_vs_gpu": mism}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C1")
+    ap.add_argument("--reads-per-gpu", type=int, default=0)
+    ap.add_argument("--cpu-sample", type=int, default=400_000)
+    ap.add_argument("--ref-sample", type=int, default=400_000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -180,6 +180,11 @@ void sa_host_free(void* ptr);
  * first H2D copy to the last D2H copy, and of the align kernels alone. */
 int sa_last_timing(const sa_context* ctx, float* e2e_ms, float* kernel_ms);
 
+/* Device time (ms, CUDA events) of the last align call's kernels: the fused
+ * shared-memory-table kernel and the overflow (global-table) kernel, summed
+ * over chunks.  After sa_align_device this waits for those events. */
+int sa_last_kernel_times(sa_context* ctx, float* fast_ms, float* slow_ms);
+
 /* Number of CUDA kernels launched by the last sa_align_batch call. */
 int sa_last_launches(const sa_context* ctx, uint64_t* launches);
 

@@ -112,6 +112,7 @@ def _load():
         "sa_host_free": (None, [C.c_void_p]),
         "sa_last_timing": (C.c_int, [C.c_void_p, P(C.c_float), P(C.c_float)]),
         "sa_last_launches": (C.c_int, [C.c_void_p, P(C.c_uint64)]),
+        "sa_last_kernel_times": (C.c_int, [C.c_void_p, P(C.c_float), P(C.c_float)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -443,6 +444,30 @@ class Aligner:
         v = C.c_uint64()
         _load().sa_last_launches(self._idx._ctx, C.byref(v))
         return v.value
+
+    def last_kernel_times(self) -> tuple[float, float]:
+        """(fused kernel ms, overflow kernel ms) of the last call (CUDA events)."""
+        f, s = C.c_float(), C.c_float()
+        rc = _load().sa_last_kernel_times(self._idx._ctx, C.byref(f), C.byref(s))
+        if rc:
+            _raise(rc, self._idx._ctx)
+        return f.value, s.value
+
+    def align_device(self, d_bases: int, d_offsets: int, n_reads: int, max_read_length: int,
+                     d_results: int, d_stats: int = 0, stream: int = 0) -> None:
+        """Device-resident batch (raw CUDA pointers, e.g. torch data_ptr()); async on stream."""
+        p = self._params._c()
+        rc = _load().sa_align_device(self._idx._ctx, C.byref(p), C.c_void_p(d_bases), C.c_void_p(d_offsets),
+                                     n_reads, max_read_length, C.c_void_p(d_results),
+                                     C.c_void_p(d_stats) if d_stats else None,
+                                     C.c_void_p(stream) if stream else None)
+        if rc:
+            _raise(rc, self._idx._ctx)
+
+    def sync(self, stream: int = 0) -> None:
+        rc = _load().sa_sync(self._idx._ctx, C.c_void_p(stream) if stream else None)
+        if rc:
+            _raise(rc, self._idx._ctx)
 
 
 def align_read(read, idx: SeedIndex, g: PackedGenome, params: AlignerParams,

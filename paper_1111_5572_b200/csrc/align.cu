@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(256) align_kernel(const AlignLaunch a) {
         if (stage_read(src, len, nblk, R, Cp, lane)) {
             if (lane == 0) {
                 atomicOr(a.error_flag, 1u);
-                atomicMin(a.error_read, r);
+                atomicMin(a.error_read, a.read_base + r);
             }
             continue;
         }
@@ -651,6 +651,10 @@ __global__ void __launch_bounds__(256) align_kernel(const AlignLaunch a) {
 
         if (overflow) {  // defer to the global-table kernel
             clear_table(x.t, x.n_cands, true, lane);
+            if (kSlow) {  // table sized n_eff * h_max cannot overflow unless clamped
+                if (lane == 0) atomicOr(a.error_flag, 2u);
+                continue;
+            }
             if (lane == 0) {
                 const unsigned slot = atomicAdd(a.overflow_count, 1u);
                 a.overflow_list[slot] = r;

@@ -43,7 +43,8 @@ struct AlignLaunch {
     unsigned int* overflow_list;
     unsigned int* overflow_count;
     unsigned int* error_flag;
-    unsigned int* error_read;  // atomicMin of the first bad read index
+    unsigned long long* error_read;  // atomicMin of the first bad read (absolute index)
+    unsigned long long read_base;    // absolute index of read 0 of this launch
     // slow path: process work_list[0..*work_count) with global candidate tables
     const unsigned int* work_list;
     const unsigned int* work_count;

@@ -30,7 +30,7 @@ namespace {
 thread_local std::string g_thread_err;
 
 constexpr int kCtlWords = 4;  // cursor_fast, cursor_slow, overflow_count, error_flag
-constexpr uint64_t kChunkReads = 1u << 20;
+constexpr uint64_t kChunkReads = 1u << 18;
 constexpr uint64_t kChunkBytes = 256ull << 20;
 constexpr int kFastCap = 64, kFastHcap = 128;
 constexpr uint64_t kSlowScratchBudget = 2ull << 30;
@@ -44,8 +44,19 @@ struct Stage {  // one of the two pipeline slots of a replica
     unsigned int* d_overflow = nullptr;
     uint64_t reads_cap = 0;
     unsigned int* d_ctl = nullptr;
-    cudaEvent_t k0 = nullptr, k1 = nullptr;
+    cudaEvent_t k0 = nullptr, km = nullptr, k1 = nullptr;  // fast kernel [k0,km), slow [km,k1)
 };
+
+cudaError_t stage_times(Stage& s, float& fast_ms, float& slow_ms) {
+    cudaError_t e = cudaEventSynchronize(s.k1);
+    if (e != cudaSuccess) return e;
+    float a = 0, b = 0;
+    cudaEventElapsedTime(&a, s.k0, s.km);
+    cudaEventElapsedTime(&b, s.km, s.k1);
+    fast_ms += a;
+    slow_ms += b;
+    return cudaSuccess;
+}
 
 struct Replica {
     int device = 0;
@@ -58,7 +69,7 @@ struct Replica {
     unsigned char* d_gscratch = nullptr;
     uint64_t gscratch_bytes = 0;
     uint32_t smem_attr = 0;
-    cudaEvent_t e_start = nullptr, e_end = nullptr;
+    cudaEvent_t e_start = nullptr, e_end = nullptr, e_join = nullptr;
 };
 
 struct LaunchShape {
@@ -78,7 +89,8 @@ struct sa_context {
     uint64_t glen = 0;
     std::string err;
     std::mutex mu;
-    float last_e2e_ms = 0, last_kernel_ms = 0;
+    float last_e2e_ms = 0, last_kernel_ms = 0, last_slow_ms = 0;
+    bool device_timing_pending = false;  // sa_align_device events not yet read
     uint64_t last_launches = 0;
 };
 
@@ -184,6 +196,7 @@ int ensure_stage(sa_context* ctx, Stage& s, uint64_t bytes, uint64_t reads) {
     if (!s.st) {
         CUDA_TRY(ctx, cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking));
         CUDA_TRY(ctx, cudaEventCreate(&s.k0));
+        CUDA_TRY(ctx, cudaEventCreate(&s.km));
         CUDA_TRY(ctx, cudaEventCreate(&s.k1));
         CUDA_TRY(ctx, cudaMalloc(&s.d_ctl, kCtlWords * sizeof(unsigned int)));
     }
@@ -226,8 +239,9 @@ int ensure_scratch(sa_context* ctx, Replica& rep, const LaunchShape& sh) {
 // Enqueue fast + slow kernels for reads already on the device.
 int enqueue_align(sa_context* ctx, Replica& rep, Stage& stg, const LaunchShape& sh,
                   const char* d_bases, const uint64_t* d_offsets, uint64_t base_off,
-                  uint64_t n_reads, sa_result* d_results, unsigned long long* d_stats,
-                  unsigned int* d_overflow, bool time_it, uint64_t& launches) {
+                  uint64_t n_reads, uint64_t read_base, sa_result* d_results,
+                  unsigned long long* d_stats, unsigned int* d_overflow, bool time_it,
+                  uint64_t& launches) {
     AlignLaunch a = sh.proto;
     a.bases = d_bases;
     a.offsets = d_offsets;
@@ -239,12 +253,14 @@ int enqueue_align(sa_context* ctx, Replica& rep, Stage& stg, const LaunchShape& 
     a.overflow_count = stg.d_ctl + 2;
     a.overflow_list = d_overflow;
     a.error_flag = rep.d_err;
-    a.error_read = nullptr;
+    a.error_read = rep.d_err_read;
+    a.read_base = read_base;
     a.gscratch = rep.d_gscratch;
     CUDA_TRY(ctx, cudaMemsetAsync(stg.d_ctl, 0, kCtlWords * sizeof(unsigned int), stg.st));
     if (time_it) CUDA_TRY(ctx, cudaEventRecord(stg.k0, stg.st));
     launch_align_fast(a, sh.fast_grid, sh.fast_block, stg.st);
     CUDA_TRY(ctx, cudaGetLastError());
+    if (time_it) CUDA_TRY(ctx, cudaEventRecord(stg.km, stg.st));
     AlignLaunch b = a;
     b.cursor = stg.d_ctl + 1;
     b.work_list = d_overflow;
@@ -263,11 +279,20 @@ int enqueue_align(sa_context* ctx, Replica& rep, Stage& stg, const LaunchShape& 
 
 int check_errors(sa_context* ctx, Replica& rep) {
     unsigned int flag = 0;
+    unsigned long long first = 0;
     CUDA_TRY(ctx, cudaMemcpy(&flag, rep.d_err, sizeof(flag), cudaMemcpyDeviceToHost));
-    if (flag) {
+    if (flag & 2u) {
         CUDA_TRY(ctx, cudaMemset(rep.d_err, 0, sizeof(unsigned int)));
-        return fail(ctx, SA_EINVAL, "reverse_complement: non-base character (read holds a "
-                                    "character outside {A,C,G,T,N})");
+        return fail(ctx, SA_ERUNTIME, "candidate table overflow on the global-table path "
+                                      "(seeds_to_try * max_hits above 2^26)");
+    }
+    if (flag) {
+        CUDA_TRY(ctx, cudaMemcpy(&first, rep.d_err_read, sizeof(first), cudaMemcpyDeviceToHost));
+        CUDA_TRY(ctx, cudaMemset(rep.d_err, 0, sizeof(unsigned int)));
+        CUDA_TRY(ctx, cudaMemset(rep.d_err_read, 0xff, sizeof(unsigned long long)));
+        return fail(ctx, SA_EINVAL, "reverse_complement: non-base character (read " +
+                                        std::to_string(first) +
+                                        " holds a character outside {A,C,G,T,N})");
     }
     return SA_OK;
 }
@@ -373,8 +398,11 @@ int sa_create(const uint64_t* packed_words, uint64_t n_packed, const uint64_t* n
             if (cudaMalloc(&rep.d_stats, kNumStats * sizeof(unsigned long long)) != cudaSuccess ||
                 cudaMalloc(&rep.d_err, sizeof(unsigned int)) != cudaSuccess ||
                 cudaMemset(rep.d_err, 0, sizeof(unsigned int)) != cudaSuccess ||
+                cudaMalloc(&rep.d_err_read, sizeof(unsigned long long)) != cudaSuccess ||
+                cudaMemset(rep.d_err_read, 0xff, sizeof(unsigned long long)) != cudaSuccess ||
                 cudaEventCreate(&rep.e_start) != cudaSuccess ||
-                cudaEventCreate(&rep.e_end) != cudaSuccess) {
+                cudaEventCreate(&rep.e_end) != cudaSuccess ||
+                cudaEventCreate(&rep.e_join) != cudaSuccess) {
                 codes[i] = SA_ERUNTIME;
                 errs[i] = "device allocation failed";
             }
@@ -411,14 +439,17 @@ void sa_destroy(sa_context* ctx) {
             if (s.d_overflow) cudaFree(s.d_overflow);
             if (s.d_ctl) cudaFree(s.d_ctl);
             if (s.k0) cudaEventDestroy(s.k0);
+            if (s.km) cudaEventDestroy(s.km);
             if (s.k1) cudaEventDestroy(s.k1);
             if (s.st) cudaStreamDestroy(s.st);
         }
         if (rep.d_stats) cudaFree(rep.d_stats);
         if (rep.d_err) cudaFree(rep.d_err);
+        if (rep.d_err_read) cudaFree(rep.d_err_read);
         if (rep.d_gscratch) cudaFree(rep.d_gscratch);
         if (rep.e_start) cudaEventDestroy(rep.e_start);
         if (rep.e_end) cudaEventDestroy(rep.e_end);
+        if (rep.e_join) cudaEventDestroy(rep.e_join);
         free_device_index(&rep.ix);
     }
     delete ctx;
@@ -467,7 +498,7 @@ int sa_align_batch(sa_context* ctx, const sa_params* params, const char* bases,
     std::vector<int> codes(ctx->reps.size(), 0);
     std::vector<std::string> msgs(ctx->reps.size());
     std::vector<sa_stats> part(ctx->reps.size());
-    std::vector<float> e2e(ctx->reps.size(), 0), kms(ctx->reps.size(), 0);
+    std::vector<float> e2e(ctx->reps.size(), 0), kms(ctx->reps.size(), 0), kslow(ctx->reps.size(), 0);
     std::vector<uint64_t> launches(ctx->reps.size(), 0);
 
     auto worker = [&](size_t ri) {
@@ -489,40 +520,29 @@ int sa_align_batch(sa_context* ctx, const sa_params* params, const char* bases,
             CUDA_TRY(&local_err, cudaMemsetAsync(rep.d_stats, 0, kNumStats * sizeof(unsigned long long), rep.stage[0].st));
             CUDA_TRY(&local_err, cudaEventRecord(rep.e_start, rep.stage[0].st));
             CUDA_TRY(&local_err, cudaStreamWaitEvent(rep.stage[1].st, rep.e_start, 0));
-            std::vector<std::pair<int, int>> timed;  // (stage, chunk#) whose kernel events to read
             int k = 0;
             for (;;) {
                 size_t c = next.fetch_add(1);
                 if (c >= n_chunks) break;
                 Stage& stg = rep.stage[k & 1];
-                // stage reuse: kernel events of the previous chunk on this stage
-                if (k >= 2) {
-                    CUDA_TRY(&local_err, cudaEventSynchronize(stg.k1));
-                    float ms = 0;
-                    cudaEventElapsedTime(&ms, stg.k0, stg.k1);
-                    kms[ri] += ms;
-                }
+                // stage reuse: collect the kernel events of its previous chunk
+                if (k >= 2) CUDA_TRY(&local_err, stage_times(stg, kms[ri], kslow[ri]));
                 const uint64_t r0 = bounds[c], r1 = bounds[c + 1];
                 const uint64_t b0 = offsets[r0], b1 = offsets[r1];
                 CUDA_TRY(&local_err, cudaMemcpyAsync(stg.d_bases, bases + b0, b1 - b0, cudaMemcpyHostToDevice, stg.st));
                 CUDA_TRY(&local_err, cudaMemcpyAsync(stg.d_offsets, offsets + r0, (r1 - r0 + 1) * sizeof(uint64_t),
                                                      cudaMemcpyHostToDevice, stg.st));
                 if (int rc = enqueue_align(&local_err, rep, stg, sh, stg.d_bases, stg.d_offsets, b0, r1 - r0,
-                                           stg.d_results, rep.d_stats, stg.d_overflow, true, launches[ri]))
+                                           r0, stg.d_results, rep.d_stats, stg.d_overflow, true, launches[ri]))
                     return rc;
                 CUDA_TRY(&local_err, cudaMemcpyAsync(results + r0, stg.d_results, (r1 - r0) * sizeof(sa_result),
                                                      cudaMemcpyDeviceToHost, stg.st));
                 ++k;
             }
-            for (int j = 0; j < 2 && j < k; ++j) {
-                Stage& stg = rep.stage[(k - 1 - j) & 1];
-                CUDA_TRY(&local_err, cudaEventSynchronize(stg.k1));
-                float ms = 0;
-                cudaEventElapsedTime(&ms, stg.k0, stg.k1);
-                kms[ri] += ms;
-            }
-            CUDA_TRY(&local_err, cudaEventRecord(rep.stage[1].k1, rep.stage[1].st));
-            CUDA_TRY(&local_err, cudaStreamWaitEvent(rep.stage[0].st, rep.stage[1].k1, 0));
+            for (int j = 0; j < 2 && j < k; ++j)
+                CUDA_TRY(&local_err, stage_times(rep.stage[(k - 1 - j) & 1], kms[ri], kslow[ri]));
+            CUDA_TRY(&local_err, cudaEventRecord(rep.e_join, rep.stage[1].st));
+            CUDA_TRY(&local_err, cudaStreamWaitEvent(rep.stage[0].st, rep.e_join, 0));
             CUDA_TRY(&local_err, cudaEventRecord(rep.e_end, rep.stage[0].st));
             CUDA_TRY(&local_err, cudaEventSynchronize(rep.e_end));
             cudaEventElapsedTime(&e2e[ri], rep.e_start, rep.e_end);
@@ -546,6 +566,8 @@ int sa_align_batch(sa_context* ctx, const sa_params* params, const char* bases,
         if (codes[i]) return fail(ctx, codes[i], msgs[i]);
     ctx->last_e2e_ms = *std::max_element(e2e.begin(), e2e.end());
     ctx->last_kernel_ms = *std::max_element(kms.begin(), kms.end());
+    ctx->last_slow_ms = *std::max_element(kslow.begin(), kslow.end());
+    ctx->device_timing_pending = false;
     ctx->last_launches = 0;
     for (auto l : launches) ctx->last_launches += l;
     if (stats)
@@ -583,10 +605,27 @@ int sa_align_device(sa_context* ctx, const sa_params* params, const char* d_base
     unsigned long long* stats_dst = reinterpret_cast<unsigned long long*>(d_stats);
     if (!stats_dst) stats_dst = rep.d_stats;
     uint64_t launches = 0;
-    if (int rc = enqueue_align(ctx, rep, tmp, sh, d_bases, d_offsets, 0, n_reads, d_results,
-                               stats_dst, stg.d_overflow, false, launches))
+    if (int rc = enqueue_align(ctx, rep, tmp, sh, d_bases, d_offsets, 0, n_reads, 0, d_results,
+                               stats_dst, stg.d_overflow, true, launches))
         return rc;
     ctx->last_launches = launches;
+    ctx->device_timing_pending = true;
+    return SA_OK;
+}
+
+int sa_last_kernel_times(sa_context* ctx, float* fast_ms, float* slow_ms) {
+    if (!ctx) return fail(nullptr, SA_EINVAL, "null context");
+    if (ctx->device_timing_pending) {  // events of the last sa_align_device call
+        Replica& rep = ctx->reps[0];
+        CUDA_TRY(ctx, cudaSetDevice(rep.device));
+        float f = 0, s = 0;
+        CUDA_TRY(ctx, stage_times(rep.stage[2], f, s));
+        ctx->last_kernel_ms = f;
+        ctx->last_slow_ms = s;
+        ctx->device_timing_pending = false;
+    }
+    if (fast_ms) *fast_ms = ctx->last_kernel_ms;
+    if (slow_ms) *slow_ms = ctx->last_slow_ms;
     return SA_OK;
 }
 
