@@ -216,3 +216,53 @@ def test_invalid_character_raises():
         al.align_arrays(b, offs)
     # a read shorter than s is never inspected (REF aligner.cpp:231-235)
     assert al.align_batch(["ACGx"])[0].kind == api.ResultKind.NotFound
+
+
+# ----------------------------------------------------------------- golden fixtures (reference outputs)
+
+import json  # noqa: E402
+import os  # noqa: E402
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def test_lv_golden_gpu():
+    d = np.load(os.path.join(GOLD, "lv_golden.npz"))
+    rb, ro, wb, wo = d["reads"].tobytes(), d["read_off"], d["wins"].tobytes(), d["win_off"]
+    triples = [(rb[ro[i]:ro[i + 1]].decode(), wb[wo[i]:wo[i + 1]].decode(), int(d["d_limits"][i]))
+               for i in range(d["d_limits"].size)]
+    got = api.bounded_distance_batch(triples)
+    assert [-1 if v is None else v for v in got] == d["expected"].tolist()
+
+
+def test_lookup_golden_gpu():
+    with open(os.path.join(GOLD, "lookup_golden.json")) as f:
+        data = json.load(f)
+    for s, dd in data.items():
+        g = api.PackedGenome.from_sequence(dd["genome"])
+        idx = api.SeedIndex.build(g, int(s))
+        assert idx.total_positions() == dd["total"]
+        assert idx.distinct_seeds() == dd["distinct"]
+        res = idx.lookup_batch(dd["queries"], cap=len(dd["genome"]))
+        for q, r, f, rc in zip(dd["queries"], res, dd["fwd"], dd["rc"]):
+            assert (r.forward, r.rc) == (f, rc), (s, q)
+
+
+@pytest.mark.parametrize("case", ["C1", "C2", "C2_force", "C3", "C4", "REP"])
+def test_align_golden_gpu(case):
+    d = np.load(os.path.join(GOLD, "align_golden.npz"))
+    g = d[f"{case}__genome"]
+    pa = [int(v) for v in d[f"{case}__params"]]
+    p = api.AlignerParams(seed_size=pa[0], seeds_to_try=pa[1], max_distance=pa[2], confidence_threshold=pa[3],
+                          max_hits=pa[4], bucket_size=pa[5], force_max_dlimit=bool(pa[6]))
+    packed, nmask = synth.pack_genome(g)
+    genome = api.PackedGenome(packed, nmask, g.size)
+    al = api.Aligner(api.SeedIndex.build(genome, p.seed_size), genome, p)
+    got = al.align_arrays(d[f"{case}__bases"], d[f"{case}__offsets"])
+    want = d[f"{case}__results"].view(api.RESULT_DTYPE)
+    assert O.compare_results(got, want) == []
+    st = al.stats().values
+    exp = d[f"{case}__stats"].tolist()
+    for i, f in enumerate(api.REFERENCE_STAT_FIELDS):
+        if f != "dp_cells":
+            assert st[f] == exp[i], f
