@@ -65,10 +65,16 @@ class ClockSampler:
         self.proc = None
 
     def start(self):
+        """Launch nvidia-smi and block until its first sample arrives, so the
+        timed region that follows is covered."""
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
                  "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            import select
+
+            r, _, _ = select.select([self.proc.stdout], [], [], 5.0)
+            self.first = self.proc.stdout.readline() if r else ""
         except Exception:
             self.proc = None
 
@@ -81,6 +87,7 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
             out = ""
+        out = getattr(self, "first", "") + out
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in out.strip().splitlines():
@@ -223,7 +230,6 @@ def run_ours(args) -> None:
         slow_ms.append(s)
     al.sync(sptr)
     torch.cuda.synchronize(dev)
-    clocks = sampler.stop()
     launches_per_step = al.last_launches()
     total_ms = sum(step_ms)
     if world > 1:
@@ -259,6 +265,7 @@ def run_ours(args) -> None:
         e2e_total = float(t.item())
     e2e_value = world * R * args.steps / (e2e_total / 1000.0)
     e2e_launches = al.last_launches()
+    clocks = sampler.stop()  # covers both timed regions (device-resident and e2e)
     assert (hr["kind"] == res_dev["kind"]).all() and (hr["position"] == res_dev["position"]).all(), \
         "e2e and device-resident results differ"
 
@@ -339,7 +346,7 @@ def cpu_baseline(cfg, g, packed, nmask, bases, offs, res_dev, args) -> dict:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="C1")

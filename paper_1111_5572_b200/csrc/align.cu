@@ -2,17 +2,22 @@
 //
 // K2..K5 of SURVEY.md §2 fused into one persistent warp-per-read kernel that
 // replays Aligner::align (REF src/aligner.cpp:223-364) bit-exactly:
-//   * read -> 2-bit planes (forward and reverse complement) in shared memory
-//     via coalesced byte loads and __ballot_sync           (REF :241, genome.cpp:182-200)
+//   * reads are software-pipelined per warp: offsets two reads ahead in
+//     registers, the next read's bytes streamed into shared memory with
+//     cp.async while the current read is processed
+//   * read -> 2-bit planes: SWAR decode of 4 ASCII bases per lane
+//     (__vcmpeq4), 32-base plane words assembled with shuffles; the
+//     reverse complement (REF :241, genome.cpp:182-200) by __brev of planes
 //   * seed offsets (REF :50-79), computed once per distinct read length
 //   * seed keys + canonical probes of the HBM hash index, one lane per seed,
-//     issued speculatively for 32 seeds at a time         (REF seed_index.cpp:128-143)
+//     issued speculatively for 32 seeds at a time         (REF seed_index.cpp:128-143);
+//     an inline (singleton) hit immediately prefetches its genome window to L2
 //   * the sequential seed loop (REF :256-316): N skip, h_max filter, hits ->
-//     anchors -> shared-memory vote table (warp-aggregated with
-//     __match_any_sync), best-unscored selection by warp argmax
-//     (REF :124-167), d_limit rule + Landau-Vishkin verification of every
-//     anchor of the chosen bucket (REF :169-221), BestTracker (REF :87-114),
-//     multi and pruning exits (REF :290-315)
+//     anchors -> shared-memory vote table (single-hit fast path, otherwise
+//     warp-aggregated with __match_any_sync), best-unscored selection by warp
+//     argmax (REF :124-167), d_limit rule + Landau-Vishkin verification of
+//     every anchor of the chosen bucket (REF :169-221), BestTracker
+//     (REF :87-114), multi and pruning exits (REF :290-315)
 //   * classification and result (REF :318-363)
 // LV (REF src/edit_distance.cpp:19-75) is warp-cooperative: one lane per
 // diagonal (registers, d_limit <= 15) or lanes striding diagonals over a
@@ -41,13 +46,22 @@ SA_DEV uint32_t lanemask_lt() {
     return m;
 }
 
+SA_DEV void cp_async4(void* smem_dst, const void* gsrc) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gsrc) : "memory");
+}
+SA_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+SA_DEV void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+SA_DEV void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 // ------------------------------------------------------------------ LV
 
 // Extend diagonal k from read index i while bases match (REF
 // edit_distance.cpp:35-42; N never matches, :11-13).  R/W are shared-memory
 // plane arrays; window index j lives at plane bit wofs + j.
 SA_DEV int lv_slide(const uint4* R, const uint4* W, uint32_t wofs, int i, int k, int cap,
-                    uint64_t& cells) {
+                    uint32_t& cells) {
     const int start = i;
     while (i < cap) {
         uint32_t rl, rh, rn, wl, wh, wn;
@@ -62,32 +76,32 @@ SA_DEV int lv_slide(const uint4* R, const uint4* W, uint32_t wofs, int i, int k,
         }
     }
     if (i > cap) i = cap;
-    cells += static_cast<uint64_t>(i - start) + 1;
+    cells += static_cast<uint32_t>(i - start) + 1;
     return i;
 }
 
 // One LV iteration for diagonal k given the previous frontier values of
 // k-1, k, k+1 (REF edit_distance.cpp:46-67).
 SA_DEV int lv_step(int e, int k, int prev_km1, int prev_k, int prev_kp1, int m, int w,
-                   const uint4* R, const uint4* W, uint32_t wofs, uint64_t& cells) {
+                   const uint4* R, const uint4* W, uint32_t wofs, uint32_t& cells) {
     if (k > w) return kUnreach;  // whole diagonal outside the window (:47)
     int cand;
     if (e == 0) {
         cand = 0;
     } else {
-        cand = prev_k + 1;                                  // substitution
-        cand = max(cand, prev_kp1 + 1);                     // extra read char
-        cand = max(cand, prev_km1);                         // extra window char
+        cand = prev_k + 1;                // substitution
+        cand = max(cand, prev_kp1 + 1);   // extra read char
+        cand = max(cand, prev_km1);       // extra window char
     }
-    if (cand < max(0, -k)) return kUnreach;                // (:56-59)
+    if (cand < max(0, -k)) return kUnreach;  // (:56-59)
     const int cap = min(m, w - k);
-    cand = min(cand, cap);                                 // (:60)
+    cand = min(cand, cap);  // (:60)
     return lv_slide(R, W, wofs, cand, k, cap, cells);
 }
 
 // Register wavefront for d_limit <= 15: lane l owns diagonal k = l - d_limit.
 SA_DEV int lv_warp_reg(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, int dl,
-                       int lane, uint64_t& cells) {
+                       int lane, uint32_t& cells) {
     const int k = lane - dl;
     const bool mine = lane <= 2 * dl;
     int fr = kUnreach;
@@ -105,7 +119,7 @@ SA_DEV int lv_warp_reg(const uint4* R, int m, const uint4* W, uint32_t wofs, int
 
 // Shared-memory wavefront for any d_limit: F holds 2 * (2*dl + 3) ints.
 SA_DEV int lv_warp_smem(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, int dl,
-                        int* F, int lane, uint64_t& cells) {
+                        int* F, int lane, uint32_t& cells) {
     const int width = 2 * dl + 3;
     int* cur = F;
     int* nxt = F + width;
@@ -130,39 +144,89 @@ SA_DEV int lv_warp_smem(const uint4* R, int m, const uint4* W, uint32_t wofs, in
 }
 
 SA_DEV int lv_warp(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, int dl, int* F,
-                   int lane, uint64_t& cells) {
+                   int lane, uint32_t& cells) {
     if (dl <= 15) return lv_warp_reg(R, m, W, wofs, w, dl, lane, cells);
     return lv_warp_smem(R, m, W, wofs, w, dl, F, lane, cells);
 }
 
 // ------------------------------------------------------------------ read staging
 
-// ASCII read -> forward and reverse-complement planes.  Positions at or past
-// the end read as N.  Returns true if a character outside {A,C,G,T,N} occurs.
-SA_DEV bool stage_read(const char* __restrict__ src, int len, int nblk, uint4* R, uint4* C,
-                       int lane) {
+// Gather bit 0 of each byte into a nibble.
+SA_DEV uint32_t byte_bits(uint32_t x) { return (x | (x >> 7) | (x >> 14) | (x >> 21)) & 0xFu; }
+
+// Decode a read of `len` ASCII bases whose first byte is byte `shift` of the
+// 4-byte-aligned word array Wd (nwords words; generic address space: shared
+// staging buffer or global) into forward planes R and reverse-complement
+// planes C (REF genome.cpp:182-200), both followed by an all-N block.
+// Returns true when a character outside {A,C,G,T,N} occurs (the reference
+// throws from reverse_complement).
+SA_DEV bool decode_read(const uint32_t* Wd, int shift, int nwords, int len, uint4* R, uint4* C,
+                        int lane) {
     bool bad = false;
-    for (int b = 0; b < nblk; ++b) {
-        const int pos = b * 32 + lane;
-        int code = 4, code2 = 4;
-        if (pos < len) {
-            code = read_code(static_cast<unsigned char>(__ldg(src + pos)));
-            code2 = read_code(static_cast<unsigned char>(__ldg(src + len - 1 - pos)));
+    const int nb = (len + 31) >> 5;
+    const int rounds = (len + 127) >> 7;
+    for (int rd = 0; rd < rounds; ++rd) {
+        const int pos0 = rd * 128 + 4 * lane;
+        uint32_t v = 0x4E4E4E4Eu;  // "NNNN"
+        if (pos0 < len) {
+            const int k = rd * 32 + lane;
+            const uint32_t w0 = Wd[k];
+            const uint32_t w1 = k + 1 < nwords ? Wd[k + 1] : 0u;
+            v = __funnelshift_r(w0, w1, 8 * shift);
+            const int valid = len - pos0;
+            if (valid < 4) {
+                const uint32_t keep = (1u << (8 * valid)) - 1u;
+                v = (v & keep) | (0x4E4E4E4Eu & ~keep);
+            }
         }
-        bad |= (code == 5) | (code2 == 5);
-        const bool acgt = code < 4, acgt2 = code2 < 4;
-        const uint32_t lo = __ballot_sync(FULL, acgt && (code & 1));
-        const uint32_t hi = __ballot_sync(FULL, acgt && (code & 2));
-        const uint32_t nn = __ballot_sync(FULL, !acgt);
-        const uint32_t lo2 = __ballot_sync(FULL, acgt2 && !(code2 & 1));  // complement
-        const uint32_t hi2 = __ballot_sync(FULL, acgt2 && !(code2 & 2));
-        const uint32_t nn2 = __ballot_sync(FULL, !acgt2);
-        if (lane == 0) {
-            R[b] = make_uint4(lo, hi, nn, 0);
-            C[b] = make_uint4(lo2, hi2, nn2, 0);
+        const uint32_t isC = __vcmpeq4(v, 0x43434343u), isG = __vcmpeq4(v, 0x47474747u);
+        const uint32_t isT = __vcmpeq4(v, 0x54545454u), isN = __vcmpeq4(v, 0x4E4E4E4Eu);
+        const uint32_t isA = __vcmpeq4(v, 0x41414141u);
+        bad |= (isA | isC | isG | isT | isN) != 0xFFFFFFFFu;
+        const int sh = 4 * (lane & 7);
+        uint32_t lo = byte_bits((isC | isT) & 0x01010101u) << sh;
+        uint32_t hi = byte_bits((isG | isT) & 0x01010101u) << sh;
+        uint32_t nn = byte_bits(isN & 0x01010101u) << sh;
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            lo |= __shfl_xor_sync(FULL, lo, o);
+            hi |= __shfl_xor_sync(FULL, hi, o);
+            nn |= __shfl_xor_sync(FULL, nn, o);
         }
+        const int blk = rd * 4 + (lane >> 3);
+        if ((lane & 7) == 0 && blk < nb) R[blk] = make_uint4(lo, hi, nn, 0);
     }
+    if (lane == 0) R[nb] = make_uint4(0, 0, 0xFFFFFFFFu, 0);
+    __syncwarp();
+    // rc word q, bit b = complement of forward base len-1-32q-b
+    for (int q = lane; q < nb; q += 32) {
+        const int p_lo = len - 32 * (q + 1);
+        uint32_t l, h, n;
+        if (p_lo >= 0) {
+            extract32(R, static_cast<uint64_t>(p_lo), l, h, n);
+        } else {
+            extract32(R, 0ull, l, h, n);
+            const int s = -p_lo;
+            l <<= s;
+            h <<= s;
+            n = (n << s) | ((1u << s) - 1u);
+        }
+        C[q] = make_uint4(__brev(~l), __brev(~h), __brev(n), 0);
+    }
+    if (lane == 0) C[nb] = make_uint4(0, 0, 0xFFFFFFFFu, 0);
+    __syncwarp();
     return __any_sync(FULL, bad);
+}
+
+// Start copying a read's aligned words into a shared staging buffer.
+SA_DEV void issue_read_copy(const char* src, int len, uint32_t* stage, int lane, int& shift,
+                            int& nwords) {
+    const uintptr_t addr = reinterpret_cast<uintptr_t>(src);
+    const uintptr_t abase = addr & ~static_cast<uintptr_t>(3);
+    shift = static_cast<int>(addr & 3);
+    nwords = static_cast<int>((addr + static_cast<uintptr_t>(len) - abase + 3) >> 2);
+    for (int w = lane; w < nwords; w += 32)
+        cp_async4(stage + w, reinterpret_cast<const void*>(abase + 4ull * w));
 }
 
 // REF src/aligner.cpp:50-79 seed_offsets, restated for shift values < s <= 32:
@@ -222,25 +286,25 @@ SA_DEV int tracker_gap(const Tracker& t) {  // REF aligner.cpp:111-114
 }
 
 struct CandTable {
-    unsigned long long* ckey;  // bucket*2 + dir, insertion order
-    unsigned long long* cmask; // anchor bits
-    uint32_t* ccnt;            // seeds_hitting | kScored
-    uint32_t* chslot;          // hash slot of the entry (for cleanup)
-    unsigned long long* hkey;  // hash keys
-    uint32_t* hval;            // list index
+    unsigned long long* ckey;   // bucket*2 + dir, insertion order
+    unsigned long long* cmask;  // anchor bits
+    uint32_t* ccnt;             // seeds_hitting | kScored
+    uint32_t* chslot;           // hash slot of the entry (for cleanup)
+    unsigned long long* hkey;   // hash keys
+    uint32_t* hval;             // list index
     int cap, hcap;
 };
 
 struct ReadStats {  // per-read deltas, committed only when the read completes
     uint32_t lookups, skipped_n, skipped_pop, dist_calls, after_first, early_out_after_first;
     uint32_t multi_exits, pruning_exits;
-    uint64_t hits_consumed, window_bases;
+    uint32_t hits_consumed, window_bases;
 };
 
 struct Ctx {
     const AlignLaunch* a;
     int lane;
-    int len, s, c, bs, d_max;
+    int len, d_max;
     const uint4* R;
     const uint4* C;
     uint4* W;
@@ -252,7 +316,7 @@ struct Ctx {
     bool first_done, first_valid;
     int first_dir;
     uint64_t first_pos;
-    uint64_t cells;  // per lane
+    uint32_t cells;  // per lane
     ReadStats st;
 };
 
@@ -264,6 +328,43 @@ SA_DEV uint32_t cand_hash(unsigned long long key, int hcap) {
 // Returns false when the table would overflow.
 SA_DEV bool insert_wave(Ctx& x, bool valid, unsigned long long key, int bit) {
     const int lane = x.lane;
+    const uint32_t vmask = __ballot_sync(FULL, valid);
+    if (vmask == 0) return true;
+    if ((vmask & (vmask - 1)) == 0) {  // one hit: uniform probe, no atomics
+        const int src = __ffs(vmask) - 1;
+        key = __shfl_sync(FULL, key, src);
+        bit = __shfl_sync(FULL, bit, src);
+        uint32_t h = cand_hash(key, x.t.hcap);
+        for (;;) {
+            const unsigned long long cur = x.t.hkey[h];
+            if (cur == key) {
+                const uint32_t idx = x.t.hval[h];
+                if (lane == 0) {
+                    x.t.ccnt[idx] += 1u;
+                    x.t.cmask[idx] |= 1ull << bit;
+                }
+                break;
+            }
+            if (cur == kEmptyKey) {
+                if (x.n_cands + 1 > static_cast<uint32_t>(x.t.cap)) return false;
+                const uint32_t idx = x.n_cands;
+                if (lane == 0) {
+                    x.t.hkey[h] = key;
+                    x.t.hval[h] = idx;
+                    x.t.chslot[idx] = h;
+                    x.t.ckey[idx] = key;
+                    x.t.cmask[idx] = 1ull << bit;
+                    x.t.ccnt[idx] = 1u;
+                }
+                x.n_cands += 1;
+                x.n_unscored += 1;
+                break;
+            }
+            h = (h + 1) & static_cast<uint32_t>(x.t.hcap - 1);
+        }
+        __syncwarp();
+        return true;
+    }
     const unsigned long long ukey = valid ? key : (0xFFFFFFFF00000000ull | static_cast<unsigned>(lane));
     const unsigned peers = __match_any_sync(FULL, ukey);
     const int leader = __ffs(peers) - 1;
@@ -310,7 +411,10 @@ SA_DEV bool insert_wave(Ctx& x, bool valid, unsigned long long key, int bit) {
     __syncwarp();
     idx = __shfl_sync(FULL, idx, leader);
     if (is_leader) x.t.ccnt[idx] += static_cast<uint32_t>(__popc(peers));
-    if (valid) atomicOr(x.t.cmask + idx, 1ull << bit);
+    if (valid) {
+        if (peers == (1u << lane)) x.t.cmask[idx] |= 1ull << bit;
+        else atomicOr(x.t.cmask + idx, 1ull << bit);
+    }
     __syncwarp();
     return true;
 }
@@ -319,13 +423,13 @@ SA_DEV bool insert_wave(Ctx& x, bool valid, unsigned long long key, int bit) {
 SA_DEV void score_candidate(Ctx& x, uint32_t idx) {
     const AlignLaunch& a = *x.a;
     const int lane = x.lane;
-    if (lane == 0) x.t.ccnt[idx] |= kScored;
-    x.n_unscored--;
     const unsigned long long kk = x.t.ckey[idx];
     const unsigned long long mm = x.t.cmask[idx];
     __syncwarp();
+    if (lane == 0) x.t.ccnt[idx] |= kScored;
+    x.n_unscored--;
 
-    const int c = x.c, d_max = x.d_max;
+    const int c = a.c, d_max = x.d_max;
     int d_limit;
     if (x.tr.d_best > d_max) d_limit = d_max + c - 1;
     else if (x.tr.d_second >= x.tr.d_best + c) d_limit = x.tr.d_best + c - 1;
@@ -334,7 +438,7 @@ SA_DEV void score_candidate(Ctx& x, uint32_t idx) {
     if (d_limit < 0) return;  // (:184)
 
     const int dir = static_cast<int>(kk & 1ull);
-    const uint64_t base_pos = (kk >> 1) * static_cast<uint64_t>(x.bs);
+    const uint64_t base_pos = (kk >> 1) * static_cast<uint64_t>(a.bs);
     const uint64_t amin = base_pos + static_cast<uint64_t>(__ffsll(static_cast<long long>(mm)) - 1);
     const uint64_t amax = base_pos + static_cast<uint64_t>(63 - __clzll(static_cast<long long>(mm)));
     const uint4* orient = dir ? x.C : x.R;
@@ -362,7 +466,7 @@ SA_DEV void score_candidate(Ctx& x, uint32_t idx) {
         const int d = lv_warp(orient, x.len, x.W, wofs, w, d_limit, x.F, lane, x.cells);
         x.st.dist_calls++;
         x.calls++;
-        x.st.window_bases += static_cast<uint64_t>(w);
+        x.st.window_bases += static_cast<uint32_t>(w);
         if (x.calls > 1) {
             x.st.after_first++;
             if (d < 0) x.st.early_out_after_first++;
@@ -380,13 +484,18 @@ SA_DEV void score_candidate(Ctx& x, uint32_t idx) {
             x.first_dir = dir;
         }
     }
-    if (best_d < kInfDistance) tracker_observe(x.tr, x.bs, best_d, best_anchor, dir);
+    if (best_d < kInfDistance) tracker_observe(x.tr, a.bs, best_d, best_anchor, dir);
 }
 
 // REF aligner.cpp:141-167 score_best_candidate: unscored candidate with most
 // seeds hitting, then smallest anchor, then Forward.
 SA_DEV void score_best(Ctx& x) {
     if (x.n_unscored == 0) return;
+    if (x.n_cands == 1) {  // the only candidate is the unscored one
+        score_candidate(x, 0);
+        return;
+    }
+    const AlignLaunch& a = *x.a;
     uint32_t bc = 0;
     unsigned long long bk = ~0ull;
     int bi = -1;
@@ -395,8 +504,8 @@ SA_DEV void score_best(Ctx& x) {
         if (cc & kScored) continue;
         const unsigned long long kk = x.t.ckey[j];
         const unsigned long long mm = x.t.cmask[j];
-        const unsigned long long amin =
-            (kk >> 1) * static_cast<unsigned long long>(x.bs) + static_cast<unsigned long long>(__ffsll(static_cast<long long>(mm)) - 1);
+        const unsigned long long amin = (kk >> 1) * static_cast<unsigned long long>(a.bs) +
+                                        static_cast<unsigned long long>(__ffsll(static_cast<long long>(mm)) - 1);
         const unsigned long long ord = (amin << 1) | (kk & 1ull);
         if (cc > bc || (cc == bc && ord < bk)) {
             bc = cc;
@@ -430,8 +539,234 @@ SA_DEV void clear_table(CandTable& t, uint32_t n_cands, bool full, int lane) {
 // per-seed flags
 constexpr uint32_t kSeedN = 1, kSeedQflip = 2, kSeedPal = 4, kSeedSingleRc = 8;
 
+// stats slots (sa_stats order)
+enum {
+    S_READS, S_TOO_SHORT, S_LOOKUPS, S_SKIP_N, S_SKIP_POP, S_ALL_POP, S_DIST, S_DIST_AFTER,
+    S_EARLY_OUT, S_CELLS, S_MULTI, S_PRUNE, S_FIRST_BEST, S_SINGLE, S_MULTIPLE, S_NOT_FOUND,
+    S_HITS, S_WINDOW, S_READ_BASES, S_OVERFLOW
+};
+
+// Align one read whose planes are already in R/C.  Returns false when the
+// candidate table overflowed (nothing committed).
 template <bool kSlow>
-__global__ void __launch_bounds__(256) align_kernel(const AlignLaunch a) {
+SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
+                      unsigned long long* wst) {
+    const AlignLaunch& a = *x.a;
+    const int lane = x.lane;
+    const int len = x.len;
+    const uint32_t smask = seed_mask32(a.s);
+    const bool bs_pow2 = (a.bs & (a.bs - 1)) == 0;
+    const int bs_shift = __ffs(a.bs) - 1;
+
+    x.n_cands = 0;
+    x.n_unscored = 0;
+    x.tr.d_best = kInfDistance;
+    x.tr.d_second = kInfDistance;
+    x.tr.best_pos = 0;
+    x.tr.best_dir = 0;
+    x.calls = 0;
+    x.first_done = false;
+    x.first_valid = false;
+    x.first_dir = 0;
+    x.first_pos = 0;
+    x.cells = 0;
+    x.st = ReadStats{};
+    int tested = 0;
+    bool any_lookup = false, any_popular = false, early_multi = false, overflow = false;
+
+    int s_off = 0;
+    uint32_t s_flags = 0, s_count = 0, s_payload = 0;
+
+    for (int i = 0; i < n_eff; ++i) {
+        if ((i & 31) == 0) {  // speculative probes for seeds i .. i+31
+            const int si = i + lane;
+            s_flags = 0;
+            s_count = 0;
+            s_payload = 0;
+            if (si < n_eff) {
+                s_off = offs[si];
+                uint32_t lo, hi, nn;
+                extract32(x.R, static_cast<uint64_t>(s_off), lo, hi, nn);
+                if (nn & smask) {
+                    s_flags = kSeedN;
+                } else {
+                    const uint64_t key = planar_key(lo, hi, a.s);
+                    const uint64_t rc = planar_rc_key(lo, hi, a.s);
+                    const uint64_t canon = key < rc ? key : rc;
+                    if (key != canon) s_flags |= kSeedQflip;
+                    if (key == rc) s_flags |= kSeedPal;
+                    unsigned int payload, meta;
+                    if (probe_slot(a.table, a.n_slots, canon, payload, meta)) {
+                        const uint32_t ntot = meta & 0x7fffffffu;
+                        s_count = (s_flags & kSeedPal) ? 2u * ntot : ntot;
+                        s_payload = payload;
+                        if (meta & 0x80000000u) s_flags |= kSeedSingleRc;
+                        if (ntot == 1 && !(s_flags & kSeedPal)) {
+                            // the likely candidate: pull its genome window into L2 now
+                            const uint32_t dir = ((meta >> 31) & 1u) ^ ((s_flags & kSeedQflip) ? 1u : 0u);
+                            const int64_t anc = static_cast<int64_t>(payload) -
+                                                (dir ? (len - a.s - s_off) : s_off);
+                            const uint64_t b = anc < 0 ? 0 : (static_cast<uint64_t>(anc) >> 5);
+                            prefetch_l2(a.planes + b);
+                            prefetch_l2(a.planes + b + ((len + a.dl_max + 32) >> 5));
+                        }
+                    }
+                }
+            }
+        }
+        const int src_lane = i & 31;
+        const uint32_t flags = __shfl_sync(FULL, s_flags, src_lane);
+        const uint32_t cnt = __shfl_sync(FULL, s_count, src_lane);
+        if (flags & kSeedN) {  // REF :259-262
+            x.st.skipped_n++;
+            continue;
+        }
+        x.st.lookups++;
+        if (cnt > static_cast<uint32_t>(a.hmax)) {  // REF :265-269
+            any_popular = true;
+            x.st.skipped_pop++;
+            continue;
+        }
+        any_lookup = true;
+        x.st.hits_consumed += cnt;
+        if (i < tier0) ++tested;
+
+        if (cnt > 0) {  // REF :273-286
+            const uint32_t payload = __shfl_sync(FULL, s_payload, src_lane);
+            const int off = __shfl_sync(FULL, s_off, src_lane);
+            const bool pal = (flags & kSeedPal) != 0;
+            const uint32_t ntot = pal ? cnt / 2 : cnt;
+            const bool inl = ntot == 1;
+            uint32_t n_fwd = 0;
+            if (!inl) n_fwd = __ldg(a.pool + payload);
+            const int rc_shift = len - a.s - off;
+            const uint32_t qflip = (flags & kSeedQflip) ? 1u : 0u;
+            for (uint32_t base = 0; base < cnt; base += 32) {
+                const uint32_t t = base + lane;
+                const bool valid = t < cnt;
+                unsigned long long key = 0;
+                int bit = 0;
+                if (valid) {
+                    const uint32_t j = pal ? (t < ntot ? t : t - ntot) : t;
+                    uint32_t pos, eflag;
+                    if (inl) {
+                        pos = payload;
+                        eflag = (flags & kSeedSingleRc) ? 1u : 0u;
+                    } else {
+                        pos = __ldg(a.pool + payload + 1 + j);
+                        eflag = j >= n_fwd ? 1u : 0u;
+                    }
+                    const uint32_t dir = pal ? (t >= ntot ? 1u : 0u) : (eflag ^ qflip);
+                    const int64_t anchor = static_cast<int64_t>(pos) - (dir ? rc_shift : off);
+                    const uint32_t aa = anchor < 0 ? 0u : static_cast<uint32_t>(anchor);
+                    uint32_t bucket;
+                    if (bs_pow2) {
+                        bucket = aa >> bs_shift;
+                        bit = static_cast<int>(aa & static_cast<uint32_t>(a.bs - 1));
+                    } else {
+                        bucket = aa / static_cast<uint32_t>(a.bs);
+                        bit = static_cast<int>(aa - bucket * static_cast<uint32_t>(a.bs));
+                    }
+                    key = (static_cast<unsigned long long>(bucket) << 1) | dir;
+                }
+                if (!insert_wave(x, valid, key, bit)) {
+                    overflow = true;
+                    break;
+                }
+            }
+            if (overflow) break;
+        }
+
+        score_best(x);  // REF :288
+        if (x.tr.d_best < a.c && x.tr.d_second < x.tr.d_best + a.c) {  // REF :290-295
+            x.st.multi_exits++;
+            early_multi = true;
+            break;
+        }
+        if (tested >= x.tr.d_best + a.c) {  // REF :296-315
+            x.st.pruning_exits++;
+            while (x.n_unscored > 0) {
+                score_best(x);
+                if (x.tr.d_best < a.c && x.tr.d_second < x.tr.d_best + a.c) {
+                    x.st.multi_exits++;
+                    early_multi = true;
+                    break;
+                }
+            }
+            break;
+        }
+    }
+
+    if (overflow) {
+        clear_table(x.t, x.n_cands, true, lane);
+        return false;
+    }
+    clear_table(x.t, x.n_cands, false, lane);
+
+    // classification, REF :318-363
+    int kind;
+    bool all_pop = false;
+    const int d_max = x.d_max;
+    if (early_multi) {
+        kind = SA_MULTIPLE_HITS;
+    } else {
+        if (x.tr.d_best <= d_max && x.tr.d_second >= x.tr.d_best + a.c) kind = SA_SINGLE_HIT;
+        else if (x.tr.d_best <= d_max) kind = SA_MULTIPLE_HITS;
+        else kind = SA_NOT_FOUND;
+        if (kind == SA_NOT_FOUND && any_popular && !any_lookup) {
+            all_pop = true;
+            kind = SA_MULTIPLE_HITS;
+        }
+    }
+    sa_result res;
+    res.position = 0;
+    res.distance = -1;
+    res.gap = 0;
+    res.kind = static_cast<uint8_t>(kind);
+    res.has_position = 0;
+    res.direction = 0;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) res.reserved[i] = 0;
+    bool first_best = false;
+    if (kind == SA_SINGLE_HIT ||
+        (kind == SA_MULTIPLE_HITS && x.tr.d_best < kInfDistance && x.tr.d_best <= d_max)) {
+        res.has_position = 1;
+        res.position = x.tr.best_pos;
+        res.direction = static_cast<uint8_t>(x.tr.best_dir);
+        res.distance = x.tr.d_best;
+        res.gap = tracker_gap(x.tr);
+    }
+    if (kind == SA_SINGLE_HIT && x.first_valid && x.first_dir == x.tr.best_dir) {
+        const uint64_t delta = x.first_pos > x.tr.best_pos ? x.first_pos - x.tr.best_pos
+                                                           : x.tr.best_pos - x.first_pos;
+        first_best = delta <= static_cast<uint64_t>(a.bs);
+    }
+    uint32_t cells = x.cells;
+    for (int o = 16; o > 0; o >>= 1) cells += __shfl_xor_sync(FULL, cells, o);
+    if (lane == 0) {
+        a.results[r] = res;
+        wst[S_READS] += 1;
+        wst[S_LOOKUPS] += x.st.lookups;
+        wst[S_SKIP_N] += x.st.skipped_n;
+        wst[S_SKIP_POP] += x.st.skipped_pop;
+        wst[S_ALL_POP] += all_pop ? 1 : 0;
+        wst[S_DIST] += x.st.dist_calls;
+        wst[S_DIST_AFTER] += x.st.after_first;
+        wst[S_EARLY_OUT] += x.st.early_out_after_first;
+        wst[S_CELLS] += cells;
+        wst[S_MULTI] += x.st.multi_exits;
+        wst[S_PRUNE] += x.st.pruning_exits;
+        wst[S_FIRST_BEST] += first_best ? 1 : 0;
+        wst[S_SINGLE + (kind - SA_SINGLE_HIT)] += 1;
+        wst[S_HITS] += x.st.hits_consumed;
+        wst[S_WINDOW] += x.st.window_bases;
+        wst[S_READ_BASES] += static_cast<unsigned long long>(len);
+    }
+    return true;
+}
+
+template <bool kSlow>
+__global__ void __launch_bounds__(256, 3) align_kernel(const AlignLaunch a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
@@ -440,9 +775,6 @@ __global__ void __launch_bounds__(256) align_kernel(const AlignLaunch a) {
     Ctx x;
     x.a = &a;
     x.lane = lane;
-    x.s = a.s;
-    x.c = a.c;
-    x.bs = a.bs;
     uint4* R = reinterpret_cast<uint4*>(ws);
     uint4* Cp = R + a.wbr;
     x.R = R;
@@ -450,12 +782,14 @@ __global__ void __launch_bounds__(256) align_kernel(const AlignLaunch a) {
     x.W = Cp + a.wbr;
     int* offs = reinterpret_cast<int*>(x.W + a.wbw);
     x.F = offs + a.n_off_cap;
+    uint32_t* stage = reinterpret_cast<uint32_t*>(x.F + a.f_ints);  // 2 * sbw words
+    unsigned long long* wst = reinterpret_cast<unsigned long long*>(stage + 2 * a.sbw);
     unsigned char* tb;
     if (kSlow) {
         const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
         tb = a.gscratch + gw * a.gscratch_per_warp;
     } else {
-        tb = reinterpret_cast<unsigned char*>(x.F + a.f_ints);
+        tb = reinterpret_cast<unsigned char*>(wst + kNumStats);
     }
     x.t.cap = a.cap;
     x.t.hcap = a.hcap;
@@ -466,264 +800,138 @@ __global__ void __launch_bounds__(256) align_kernel(const AlignLaunch a) {
     x.t.chslot = x.t.ccnt + a.cap;
     x.t.hval = x.t.chslot + a.cap;
     for (int j = lane; j < a.hcap; j += 32) x.t.hkey[j] = kEmptyKey;
+    if (lane < kNumStats) wst[lane] = 0;
     __syncwarp();
 
-    // per-warp accumulators (uniform across lanes; lane 0 commits)
-    unsigned long long acc[kNumStats];
-#pragma unroll
-    for (int i = 0; i < kNumStats; ++i) acc[i] = 0;
-    uint64_t lane_cells = 0;
-
-    int cached_len = -1, n_eff = 0;
-    const uint32_t smask = seed_mask32(a.s);
-    const uint32_t n_work = kSlow ? *a.work_count : a.n_reads;
-
-    for (;;) {
-        uint32_t r = 0;
-        if (lane == 0) r = atomicAdd(a.cursor, 1u);
-        r = __shfl_sync(FULL, r, 0);
-        if (r >= n_work) break;
-        if (kSlow) r = a.work_list[r];
-
-        const uint64_t o0 = a.offsets[r], o1 = a.offsets[r + 1];
-        const int len = static_cast<int>(o1 - o0);
-        const char* src = a.bases + (o0 - a.base_off);
+    int cached_len = -1, n_eff = 0, tier0 = 0;
+    auto prepare = [&](int len) {
         x.len = len;
-        sa_result res;
-        res.position = 0;
-        res.distance = -1;
-        res.gap = 0;
-        res.kind = SA_NOT_FOUND;
-        res.has_position = 0;
-        res.direction = 0;
-#pragma unroll
-        for (int i = 0; i < 5; ++i) res.reserved[i] = 0;
-
-        if (len < a.s) {  // REF aligner.cpp:231-235
-            if (lane == 0) {
-                a.results[r] = res;
-                acc[0] += 1;   // reads
-                acc[1] += 1;   // reads_too_short
-                acc[15] += 1;  // not_found
-                acc[18] += static_cast<unsigned long long>(len);
-            }
-            continue;
-        }
         x.d_max = a.dmax_param >= 0 ? a.dmax_param : (12 * len + 99) / 100;
         if (len != cached_len) {
             n_eff = compute_offsets(len, a.s, min(a.n, a.n_off_cap), offs, lane);
+            tier0 = len / a.s;
             cached_len = len;
         }
-        const int tier0 = len / a.s;
-        const int nblk = (len + 31) / 32 + 1;
-        if (stage_read(src, len, nblk, R, Cp, lane)) {
-            if (lane == 0) {
-                atomicOr(a.error_flag, 1u);
-                atomicMin(a.error_read, a.read_base + r);
-            }
-            continue;
-        }
-        __syncwarp();
-
-        x.n_cands = 0;
-        x.n_unscored = 0;
-        x.tr.d_best = kInfDistance;
-        x.tr.d_second = kInfDistance;
-        x.tr.best_pos = 0;
-        x.tr.best_dir = 0;
-        x.calls = 0;
-        x.first_done = false;
-        x.first_valid = false;
-        x.first_dir = 0;
-        x.first_pos = 0;
-        x.cells = 0;
-        x.st = ReadStats{};
-        int tested = 0;
-        bool any_lookup = false, any_popular = false, early_multi = false, overflow = false;
-
-        // per-lane seed record of the current wave
-        int s_off = 0;
-        uint32_t s_flags = 0, s_count = 0, s_payload = 0;
-
-        for (int i = 0; i < n_eff; ++i) {
-            if ((i & 31) == 0) {  // speculative probes for seeds i .. i+31
-                const int si = i + lane;
-                s_flags = 0;
-                s_count = 0;
-                s_payload = 0;
-                if (si < n_eff) {
-                    s_off = offs[si];
-                    uint32_t lo, hi, nn;
-                    extract32(R, static_cast<uint64_t>(s_off), lo, hi, nn);
-                    if (nn & smask) {
-                        s_flags = kSeedN;
-                    } else {
-                        const uint64_t key = plane_key(lo, hi, a.s);
-                        const uint64_t rc = plane_rc_key(lo, hi, a.s);
-                        const uint64_t canon = key < rc ? key : rc;
-                        if (key != canon) s_flags |= kSeedQflip;
-                        if (key == rc) s_flags |= kSeedPal;
-                        unsigned int payload, meta;
-                        if (probe_slot(a.table, a.n_slots, canon, payload, meta)) {
-                            const uint32_t ntot = meta & 0x7fffffffu;
-                            s_count = (s_flags & kSeedPal) ? 2u * ntot : ntot;
-                            s_payload = payload;
-                            if (meta & 0x80000000u) s_flags |= kSeedSingleRc;
-                        }
-                    }
-                }
-            }
-            const int src_lane = i & 31;
-            const uint32_t flags = __shfl_sync(FULL, s_flags, src_lane);
-            const uint32_t cnt = __shfl_sync(FULL, s_count, src_lane);
-            const uint32_t payload = __shfl_sync(FULL, s_payload, src_lane);
-            const int off = __shfl_sync(FULL, s_off, src_lane);
-
-            if (flags & kSeedN) {  // REF :259-262
-                x.st.skipped_n++;
-                continue;
-            }
-            x.st.lookups++;
-            if (cnt > static_cast<uint32_t>(a.hmax)) {  // REF :265-269
-                any_popular = true;
-                x.st.skipped_pop++;
-                continue;
-            }
-            any_lookup = true;
-            x.st.hits_consumed += cnt;
-            if (i < tier0) ++tested;
-
-            if (cnt > 0) {  // REF :273-286
-                const bool pal = (flags & kSeedPal) != 0;
-                const uint32_t ntot = pal ? cnt / 2 : cnt;
-                const bool inl = ntot == 1;
-                uint32_t n_fwd = 0;
-                if (!inl) n_fwd = __ldg(a.pool + payload);
-                const int rc_shift = len - a.s - off;
-                const uint32_t qflip = (flags & kSeedQflip) ? 1u : 0u;
-                for (uint32_t base = 0; base < cnt && !overflow; base += 32) {
-                    const uint32_t t = base + lane;
-                    const bool valid = t < cnt;
-                    unsigned long long key = 0;
-                    int bit = 0;
-                    if (valid) {
-                        const uint32_t j = pal ? (t < ntot ? t : t - ntot) : t;
-                        uint32_t pos, eflag;
-                        if (inl) {
-                            pos = payload;
-                            eflag = (flags & kSeedSingleRc) ? 1u : 0u;
-                        } else {
-                            pos = __ldg(a.pool + payload + 1 + j);
-                            eflag = j >= n_fwd ? 1u : 0u;
-                        }
-                        const uint32_t dir = pal ? (t >= ntot ? 1u : 0u) : (eflag ^ qflip);
-                        const int64_t anchor =
-                            static_cast<int64_t>(pos) - (dir ? rc_shift : off);
-                        const uint32_t aa = anchor < 0 ? 0u : static_cast<uint32_t>(anchor);
-                        const uint32_t bucket = aa / static_cast<uint32_t>(a.bs);
-                        bit = static_cast<int>(aa - bucket * static_cast<uint32_t>(a.bs));
-                        key = (static_cast<unsigned long long>(bucket) << 1) | dir;
-                    }
-                    if (!insert_wave(x, valid, key, bit)) overflow = true;
-                }
-                if (overflow) break;
-            }
-
-            score_best(x);  // REF :288
-            if (x.tr.d_best < a.c && x.tr.d_second < x.tr.d_best + a.c) {  // REF :290-295
-                x.st.multi_exits++;
-                early_multi = true;
-                break;
-            }
-            if (tested >= x.tr.d_best + a.c) {  // REF :296-315
-                x.st.pruning_exits++;
-                while (x.n_unscored > 0) {
-                    score_best(x);
-                    if (x.tr.d_best < a.c && x.tr.d_second < x.tr.d_best + a.c) {
-                        x.st.multi_exits++;
-                        early_multi = true;
-                        break;
-                    }
-                }
-                break;
-            }
-        }
-
-        if (overflow) {  // defer to the global-table kernel
-            clear_table(x.t, x.n_cands, true, lane);
-            if (kSlow) {  // table sized n_eff * h_max cannot overflow unless clamped
-                if (lane == 0) atomicOr(a.error_flag, 2u);
-                continue;
-            }
-            if (lane == 0) {
-                const unsigned slot = atomicAdd(a.overflow_count, 1u);
-                a.overflow_list[slot] = r;
-                acc[19] += 1;
-            }
-            continue;
-        }
-        clear_table(x.t, x.n_cands, false, lane);
-
-        // classification, REF :318-363
-        int kind;
-        bool all_pop = false;
-        const int d_max = x.d_max;
-        if (early_multi) {
-            kind = SA_MULTIPLE_HITS;
-        } else {
-            if (x.tr.d_best <= d_max && x.tr.d_second >= x.tr.d_best + a.c) kind = SA_SINGLE_HIT;
-            else if (x.tr.d_best <= d_max) kind = SA_MULTIPLE_HITS;
-            else kind = SA_NOT_FOUND;
-            if (kind == SA_NOT_FOUND && any_popular && !any_lookup) {
-                all_pop = true;
-                kind = SA_MULTIPLE_HITS;
-            }
-        }
-        res.kind = static_cast<uint8_t>(kind);
-        bool first_best = false;
-        if (kind == SA_SINGLE_HIT ||
-            (kind == SA_MULTIPLE_HITS && x.tr.d_best < kInfDistance && x.tr.d_best <= d_max)) {
-            res.has_position = 1;
-            res.position = x.tr.best_pos;
-            res.direction = static_cast<uint8_t>(x.tr.best_dir);
-            res.distance = x.tr.d_best;
-            res.gap = tracker_gap(x.tr);
-        }
-        if (kind == SA_SINGLE_HIT && x.first_valid && x.first_dir == x.tr.best_dir) {
-            const uint64_t delta = x.first_pos > x.tr.best_pos ? x.first_pos - x.tr.best_pos
-                                                               : x.tr.best_pos - x.first_pos;
-            first_best = delta <= static_cast<uint64_t>(a.bs);
-        }
-        lane_cells += x.cells;
+    };
+    auto bad_read = [&](uint32_t r) {
         if (lane == 0) {
+            atomicOr(a.error_flag, 1u);
+            atomicMin(a.error_read, a.read_base + r);
+        }
+    };
+    auto short_read = [&](uint32_t r, int len) {  // REF aligner.cpp:231-235
+        if (lane == 0) {
+            sa_result res;
+            res.position = 0;
+            res.distance = -1;
+            res.gap = 0;
+            res.kind = SA_NOT_FOUND;
+            res.has_position = 0;
+            res.direction = 0;
+#pragma unroll
+            for (int i = 0; i < 5; ++i) res.reserved[i] = 0;
             a.results[r] = res;
-            acc[0] += 1;
-            acc[2] += x.st.lookups;
-            acc[3] += x.st.skipped_n;
-            acc[4] += x.st.skipped_pop;
-            acc[5] += all_pop ? 1 : 0;
-            acc[6] += x.st.dist_calls;
-            acc[7] += x.st.after_first;
-            acc[8] += x.st.early_out_after_first;
-            acc[10] += x.st.multi_exits;
-            acc[11] += x.st.pruning_exits;
-            acc[12] += first_best ? 1 : 0;
-            acc[13] += kind == SA_SINGLE_HIT ? 1 : 0;
-            acc[14] += kind == SA_MULTIPLE_HITS ? 1 : 0;
-            acc[15] += kind == SA_NOT_FOUND ? 1 : 0;
-            acc[16] += x.st.hits_consumed;
-            acc[17] += x.st.window_bases;
-            acc[18] += static_cast<unsigned long long>(len);
+            wst[S_READS] += 1;
+            wst[S_TOO_SHORT] += 1;
+            wst[S_NOT_FOUND] += 1;
+            wst[S_READ_BASES] += static_cast<unsigned long long>(len);
+        }
+    };
+
+    if (!kSlow && a.prefetch) {
+        // static striding with a two-deep software pipeline
+        const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+        uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+        const uint32_t N = a.n_reads;
+        uint64_t c0 = 0, c1 = 0, n0 = 0, n1 = 0;
+        if (r < N) {
+            c0 = a.offsets[r];
+            c1 = a.offsets[r + 1];
+        }
+        if (r + nw < N) {
+            n0 = a.offsets[r + nw];
+            n1 = a.offsets[r + nw + 1];
+        }
+        int cur = 0, sh_cur = 0, nw_cur = 0;
+        if (r < N)
+            issue_read_copy(a.bases + (c0 - a.base_off), static_cast<int>(c1 - c0), stage, lane, sh_cur,
+                            nw_cur);
+        cp_async_commit();
+        for (; r < N; r += nw) {
+            uint64_t f0 = 0, f1 = 0;
+            const uint32_t r2 = r + 2 * nw;
+            if (r2 < N) {
+                f0 = a.offsets[r2];
+                f1 = a.offsets[r2 + 1];
+            }
+            int sh_nxt = 0, nw_nxt = 0;
+            if (r + nw < N)
+                issue_read_copy(a.bases + (n0 - a.base_off), static_cast<int>(n1 - n0),
+                                stage + (cur ^ 1) * a.sbw, lane, sh_nxt, nw_nxt);
+            cp_async_commit();
+            cp_async_wait1();
+            __syncwarp();
+            const int len = static_cast<int>(c1 - c0);
+            if (len < a.s) {
+                short_read(r, len);
+            } else {
+                prepare(len);
+                if (decode_read(stage + cur * a.sbw, sh_cur, nw_cur, len, R, Cp, lane)) {
+                    bad_read(r);
+                } else if (!align_one<kSlow>(x, r, n_eff, offs, tier0, wst)) {
+                    if (lane == 0) {
+                        const unsigned slot = atomicAdd(a.overflow_count, 1u);
+                        a.overflow_list[slot] = r;
+                        wst[S_OVERFLOW] += 1;
+                    }
+                }
+            }
+            __syncwarp();
+            c0 = n0;
+            c1 = n1;
+            n0 = f0;
+            n1 = f1;
+            sh_cur = sh_nxt;
+            nw_cur = nw_nxt;
+            cur ^= 1;
+        }
+    } else {
+        // dynamic fetch (work list for the slow kernel), reads decoded from global
+        const uint32_t n_work = kSlow ? *a.work_count : a.n_reads;
+        for (;;) {
+            uint32_t r = 0;
+            if (lane == 0) r = atomicAdd(a.cursor, 1u);
+            r = __shfl_sync(FULL, r, 0);
+            if (r >= n_work) break;
+            if (kSlow) r = a.work_list[r];
+            const uint64_t o0 = a.offsets[r], o1 = a.offsets[r + 1];
+            const int len = static_cast<int>(o1 - o0);
+            if (len < a.s) {
+                short_read(r, len);
+                continue;
+            }
+            prepare(len);
+            const uintptr_t addr = reinterpret_cast<uintptr_t>(a.bases + (o0 - a.base_off));
+            const uint32_t* wd = reinterpret_cast<const uint32_t*>(addr & ~static_cast<uintptr_t>(3));
+            const int nwords = static_cast<int>((addr + len - (addr & ~static_cast<uintptr_t>(3)) + 3) >> 2);
+            if (decode_read(wd, static_cast<int>(addr & 3), nwords, len, R, Cp, lane)) {
+                bad_read(r);
+                continue;
+            }
+            if (!align_one<kSlow>(x, r, n_eff, offs, tier0, wst)) {
+                if (kSlow) {  // table sized n_eff * h_max cannot overflow unless clamped
+                    if (lane == 0) atomicOr(a.error_flag, 2u);
+                } else if (lane == 0) {
+                    const unsigned slot = atomicAdd(a.overflow_count, 1u);
+                    a.overflow_list[slot] = r;
+                    wst[S_OVERFLOW] += 1;
+                }
+            }
         }
     }
 
-    for (int o = 16; o > 0; o >>= 1) lane_cells += __shfl_xor_sync(FULL, lane_cells, o);
-    if (lane == 0) {
-        acc[9] = lane_cells;
-#pragma unroll
-        for (int i = 0; i < kNumStats; ++i)
-            if (acc[i]) atomicAdd(a.stats + i, acc[i]);
-    }
+    __syncwarp();
+    if (lane < kNumStats && wst[lane]) atomicAdd(a.stats + lane, wst[lane]);
 }
 
 // ------------------------------------------------------------------ standalone LV
@@ -774,7 +982,7 @@ __global__ void __launch_bounds__(256) lv_batch_kernel(const LvLaunch a) {
             }
             continue;
         }
-        uint64_t cells = 0;
+        uint32_t cells = 0;
         const int d = lv_warp(R, m, W, 0u, w, dl, F, lane, cells);
         if (lane == 0) a.out[p] = d;
         __syncwarp();
@@ -790,7 +998,7 @@ __global__ void lookup_kernel(const LookupLaunch a) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < a.n_seeds;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const char* sd = a.seeds + i * a.s;
-        uint64_t key = 0;
+        uint32_t lo = 0, hi = 0;
         bool ok = true;
         for (int j = 0; j < a.s; ++j) {
             int b;
@@ -802,17 +1010,13 @@ __global__ void lookup_kernel(const LookupLaunch a) {
                 default: b = -1;
             }
             if (b < 0) ok = false;
-            key = (key << 2) | static_cast<uint64_t>(b & 3);
+            lo |= static_cast<uint32_t>(b & 1) << j;
+            hi |= static_cast<uint32_t>((b >> 1) & 1) << j;
         }
         uint32_t nf = 0, nr = 0;
         if (ok) {
-            // rc by bit tricks (REF :62-70)
-            uint64_t x = ~key;
-            x = ((x & 0x3333333333333333ull) << 2) | ((x >> 2) & 0x3333333333333333ull);
-            x = ((x & 0x0f0f0f0f0f0f0f0full) << 4) | ((x >> 4) & 0x0f0f0f0f0f0f0f0full);
-            x = __byte_perm(static_cast<uint32_t>(x >> 32), 0, 0x0123) |
-                (static_cast<uint64_t>(__byte_perm(static_cast<uint32_t>(x), 0, 0x0123)) << 32);
-            const uint64_t rc = x >> (64 - 2 * a.s);
+            const uint64_t key = planar_key(lo, hi, a.s);
+            const uint64_t rc = planar_rc_key(lo, hi, a.s);
             const uint64_t canon = key < rc ? key : rc;
             const bool qflip = key != canon, pal = key == rc;
             unsigned int payload, meta;

@@ -35,6 +35,9 @@ struct AlignLaunch {
     int f_ints;     // frontier ints (0 when dl_max <= 15)
     int cap;        // candidate list capacity
     int hcap;       // candidate hash slots (power of two)
+    int sbw;        // words per read staging buffer (two per warp; 0 = no prefetch)
+    int prefetch;   // fast kernel: static striding + cp.async read pipeline
+    int dl_prefetch;  // (unused by kernels) reserved
     uint32_t smem_per_warp;
     // outputs
     sa_result* results;

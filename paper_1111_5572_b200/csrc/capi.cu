@@ -151,10 +151,13 @@ int make_shape(Replica& rep, const sa_params* p, uint64_t Lmax, LaunchShape& sh,
     a.wbw = (64 + L + a.dl_max + 31) / 32 + 4;
     a.n_off_cap = round4(std::max(1, std::min(p->seeds_to_try, L - p->seed_size + 1)));
     a.f_ints = a.dl_max > 15 ? round4(2 * (2 * a.dl_max + 3)) : 0;
-    const uint64_t common = 16ull * (2 * a.wbr + a.wbw) + 4ull * (a.n_off_cap + a.f_ints);
+    const uint64_t common = 16ull * (2 * a.wbr + a.wbw) + 4ull * (a.n_off_cap + a.f_ints) +
+                            8ull * kNumStats;
     a.cap = kFastCap;
     a.hcap = kFastHcap;
-    a.smem_per_warp = round16(common + cand_table_bytes(a.cap, a.hcap));
+    a.prefetch = L <= 1024 ? 1 : 0;
+    a.sbw = a.prefetch ? round4((L + 3) / 4 + 2) : 0;
+    a.smem_per_warp = round16(common + 8ull * a.sbw + cand_table_bytes(a.cap, a.hcap));
     const uint32_t kMaxSmem = 227 * 1024;
     if (a.smem_per_warp > kMaxSmem) {
         why = "read too long for the shared-memory layout (limit ~60 kbp)";
@@ -270,6 +273,8 @@ int enqueue_align(sa_context* ctx, Replica& rep, Stage& stg, const LaunchShape& 
     b.cap = sh.slow_cap;
     b.hcap = sh.slow_hcap;
     b.smem_per_warp = sh.slow_smem_per_warp;
+    b.sbw = 0;
+    b.prefetch = 0;
     launch_align_slow(b, sh.slow_grid, sh.slow_block, stg.st);
     CUDA_TRY(ctx, cudaGetLastError());
     if (time_it) CUDA_TRY(ctx, cudaEventRecord(stg.k1, stg.st));

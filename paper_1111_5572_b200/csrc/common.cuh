@@ -51,19 +51,29 @@ SA_DEV uint64_t spread32(uint32_t v) {
 
 SA_DEV uint32_t seed_mask32(int s) { return s >= 32 ? 0xffffffffu : ((1u << s) - 1u); }
 
-// Key of the s-base string whose planes (bit j = base j) are lo/hi: first base
-// in the high bits, 2 bits per base (REF src/seed_index.cpp:51-60 pack_seed).
-SA_DEV uint64_t plane_key(uint32_t lo, uint32_t hi, int s) {
-    uint64_t f = spread32(__brev(lo)) | (spread32(__brev(hi)) << 1);
-    return f >> (64 - 2 * s);
+// Seed keys in "planar" form: key = (hi bits << s) | lo bits of the s-base
+// string (bit j = base j).  This is a bijection of the reference's packed key
+// (REF src/seed_index.cpp:51-60, first base in the high bits), so equality,
+// palindromes and the canonical pair {q, rc(q)} are the same; only the choice
+// of representative (the smaller planar key) differs, and build and probe use
+// the same rule.  It costs a few ALU ops instead of 2-bit interleaving.
+SA_DEV uint64_t planar_key(uint32_t lo, uint32_t hi, int s) {
+    const uint32_t m = seed_mask32(s);
+    return (static_cast<uint64_t>(hi & m) << s) | (lo & m);
 }
 
-// Key of the reverse complement of the same string
-// (REF src/seed_index.cpp:62-70 packed_reverse_complement).
-SA_DEV uint64_t plane_rc_key(uint32_t lo, uint32_t hi, int s) {
-    const uint32_t m = seed_mask32(s);
-    uint64_t f = spread32(~lo & m) | (spread32(~hi & m) << 1);
-    return f;
+// Planar key of the reverse complement (REF src/seed_index.cpp:62-70): the
+// complement flips both code bits (A<->T, C<->G); reversal is __brev.
+SA_DEV uint64_t planar_rc_key(uint32_t lo, uint32_t hi, int s) {
+    const uint32_t rl = __brev(~lo) >> (32 - s);
+    const uint32_t rh = __brev(~hi) >> (32 - s);
+    return (static_cast<uint64_t>(rh) << s) | rl;
+}
+
+// Reference packed key (first base high) of the same string, for tests.
+SA_DEV uint64_t packed_key(uint32_t lo, uint32_t hi, int s) {
+    uint64_t f = spread32(__brev(lo)) | (spread32(__brev(hi)) << 1);
+    return f >> (64 - 2 * s);
 }
 
 SA_DEV uint64_t mix64(uint64_t x) {

@@ -76,8 +76,8 @@ __global__ void emit_kernel(const uint4* __restrict__ planes, uint64_t n_windows
         if (n & smask) {
             k = sentinel;
         } else {
-            const uint64_t key = plane_key(lo, hi, s);
-            const uint64_t rc = plane_rc_key(lo, hi, s);
+            const uint64_t key = planar_key(lo, hi, s);
+            const uint64_t rc = planar_rc_key(lo, hi, s);
             const uint64_t canon = key < rc ? key : rc;
             k = s <= 31 ? ((canon << 1) | (key != canon ? 1ull : 0ull)) : canon;
             ++valid_here;
@@ -119,8 +119,8 @@ __global__ void pool_need_kernel(const uint32_t* __restrict__ run_start, uint64_
 SA_DEV bool window_is_rc(const uint4* planes, uint32_t pos, int s) {
     uint32_t lo, hi, n;
     extract32_ldg(planes, pos, lo, hi, n);
-    const uint64_t key = plane_key(lo, hi, s);
-    const uint64_t rc = plane_rc_key(lo, hi, s);
+    const uint64_t key = planar_key(lo, hi, s);
+    const uint64_t rc = planar_rc_key(lo, hi, s);
     return rc < key;
 }
 
