@@ -27,7 +27,7 @@ from typing import Iterable, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libsnapb200.so")
+LIB_PATH = os.environ.get("SNAP_B200_LIB") or os.path.join(_HERE, "lib", "libsnapb200.so")
 SYNTH_PATH = os.path.join(_HERE, "lib", "libsnap_synth.so")
 
 SA_OK, SA_EINVAL, SA_ERUNTIME, SA_EFORMAT = 0, 1, 2, 3

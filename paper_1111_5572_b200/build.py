@@ -70,6 +70,26 @@ def build(verbose: bool = False) -> dict[str, str]:
     return {"cuda": so, "synth": synth_so}
 
 
+def build_variant(name: str, defines: list[str]) -> str:
+    """Experimental build with extra -D flags into lib/variants/ (select at
+    run time with SNAP_B200_LIB=<path>); the default library is untouched."""
+    vdir = os.path.join(LIB, "variants")
+    vobj = os.path.join(OBJ, name)
+    os.makedirs(vdir, exist_ok=True)
+    os.makedirs(vobj, exist_ok=True)
+    objs, jobs = [], []
+    for src in CUDA_SOURCES:
+        o = os.path.join(vobj, src.replace(".cu", ".o"))
+        objs.append(o)
+        jobs.append([NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", o])
+    with ThreadPoolExecutor(max_workers=len(jobs)) as ex:
+        for _ in ex.map(_run, jobs):
+            pass
+    so = os.path.join(vdir, f"libsnapb200_{name}.so")
+    _run([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static", "-o", so, *objs])
+    return so
+
+
 if __name__ == "__main__":
     build(verbose=True)
     sys.exit(0)

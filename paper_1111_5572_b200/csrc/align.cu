@@ -546,15 +546,120 @@ enum {
     S_HITS, S_WINDOW, S_READ_BASES, S_OVERFLOW
 };
 
-// Align one read whose planes are already in R/C.  Returns false when the
-// candidate table overflowed (nothing committed).
+// Seed at read offset `off` (planes R): flags (N / query-is-rc-of-canon /
+// palindrome) and its canonical planar key.
+SA_DEV uint32_t seed_key(const AlignLaunch& a, const uint4* R, int off, uint64_t& canon) {
+    uint32_t lo, hi, nn;
+    extract32(R, static_cast<uint64_t>(off), lo, hi, nn);
+    canon = 0;
+    if (nn & seed_mask32(a.s)) return kSeedN;  // REF aligner.cpp:259-262
+    const uint64_t key = planar_key(lo, hi, a.s);
+    const uint64_t rc = planar_rc_key(lo, hi, a.s);
+    canon = key < rc ? key : rc;
+    uint32_t f = 0;
+    if (key != canon) f |= kSeedQflip;
+    if (key == rc) f |= kSeedPal;
+    return f;
+}
+
+// Seed record {flags, hit count (REF LookupResult::count), payload, offset}
+// from a resolved probe.  A singleton hit is the likely candidate: its genome
+// window is prefetched into L2 right away.
+SA_DEV uint4 seed_record(const AlignLaunch& a, uint32_t flags, bool found, unsigned payload,
+                         unsigned meta, int off, int len) {
+    uint32_t cnt = 0;
+    if (found) {
+        const uint32_t ntot = meta & 0x7fffffffu;
+        cnt = (flags & kSeedPal) ? 2u * ntot : ntot;
+        if (meta & 0x80000000u) flags |= kSeedSingleRc;
+        if (ntot == 1 && !(flags & kSeedPal)) {
+            const uint32_t dir = ((meta >> 31) & 1u) ^ ((flags & kSeedQflip) ? 1u : 0u);
+            const int64_t anc = static_cast<int64_t>(payload) - (dir ? (len - a.s - off) : off);
+            const uint64_t b = anc < 0 ? 0 : (static_cast<uint64_t>(anc) >> 5);
+            prefetch_l2(a.planes + b);
+            prefetch_l2(a.planes + b + ((len + a.dl_max + 32) >> 5));
+        }
+    }
+    return make_uint4(flags, cnt, found ? payload : 0u, static_cast<uint32_t>(off));
+}
+
+// Probe seeds i .. i+31 synchronously (one lane each) into recs[0..31].
+SA_DEV void compute_wave_sync(const AlignLaunch& a, const uint4* R, const int* offs, int i,
+                              int n_eff, int len, uint4* recs, int lane) {
+    const int si = i + lane;
+    if (si < n_eff) {
+        const int off = offs[si];
+        uint64_t canon;
+        const uint32_t f = seed_key(a, R, off, canon);
+        uint4 rec = make_uint4(f, 0, 0, static_cast<uint32_t>(off));
+        if (!(f & kSeedN)) {
+            unsigned p = 0, m = 0;
+            const bool found = probe_slot(a.table, a.n_slots, canon, p, m);
+            rec = seed_record(a, f, found, p, m, off, len);
+        }
+        recs[lane] = rec;
+    }
+    __syncwarp();
+}
+
+SA_DEV void cp_async16(void* smem_dst, const void* gsrc) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc) : "memory");
+}
+SA_DEV void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// Pipelined wave 0 of the NEXT read: keys now, home slots fetched by cp.async
+// into shared memory while the current read runs; resolve_wave0 finishes.
+SA_DEV void issue_wave0(const AlignLaunch& a, const uint4* R, const int* offs, int n_eff,
+                        uint4* recs, uint4* pslot, unsigned long long* pcanon, int lane) {
+    if (lane < n_eff) {
+        const int off = offs[lane];
+        uint64_t canon;
+        const uint32_t f = seed_key(a, R, off, canon);
+        recs[lane] = make_uint4(f, 0, 0, static_cast<uint32_t>(off));
+        pcanon[lane] = canon;
+        if (!(f & kSeedN)) cp_async16(pslot + lane, a.table + home_slot(canon, a.n_slots));
+    }
+    cp_async_commit();
+}
+
+SA_DEV void resolve_wave0(const AlignLaunch& a, int n_eff, int len, uint4* recs, const uint4* pslot,
+                          const unsigned long long* pcanon, int lane) {
+    cp_async_wait0();
+    if (lane < n_eff) {
+        const uint4 rec = recs[lane];
+        if (!(rec.x & kSeedN)) {
+            const uint64_t canon = pcanon[lane];
+            const uint4 v = pslot[lane];
+            const uint64_t k = (static_cast<uint64_t>(v.y) << 32) | v.x;
+            unsigned p = 0, m = 0;
+            bool found;
+            if (k == canon) {
+                found = true;
+                p = v.z;
+                m = v.w;
+            } else if (k == kEmptyKey) {
+                found = false;
+            } else {
+                uint64_t h = home_slot(canon, a.n_slots) + 1;
+                if (h == a.n_slots) h = 0;
+                found = probe_from(a.table, a.n_slots, canon, h, p, m);
+            }
+            recs[lane] = seed_record(a, rec.x, found, p, m, static_cast<int>(rec.w), len);
+        }
+    }
+    __syncwarp();
+}
+
+// Align one read whose planes are already in x.R / x.C.  recs holds the seed
+// records of wave 0 when wave0_ready.  Returns false when the candidate
+// table overflowed (nothing committed).
 template <bool kSlow>
 SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
-                      unsigned long long* wst) {
+                      unsigned long long* wst, uint4* recs, bool wave0_ready) {
     const AlignLaunch& a = *x.a;
     const int lane = x.lane;
     const int len = x.len;
-    const uint32_t smask = seed_mask32(a.s);
     const bool bs_pow2 = (a.bs & (a.bs - 1)) == 0;
     const int bs_shift = __ffs(a.bs) - 1;
 
@@ -574,49 +679,12 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
     int tested = 0;
     bool any_lookup = false, any_popular = false, early_multi = false, overflow = false;
 
-    int s_off = 0;
-    uint32_t s_flags = 0, s_count = 0, s_payload = 0;
-
     for (int i = 0; i < n_eff; ++i) {
-        if ((i & 31) == 0) {  // speculative probes for seeds i .. i+31
-            const int si = i + lane;
-            s_flags = 0;
-            s_count = 0;
-            s_payload = 0;
-            if (si < n_eff) {
-                s_off = offs[si];
-                uint32_t lo, hi, nn;
-                extract32(x.R, static_cast<uint64_t>(s_off), lo, hi, nn);
-                if (nn & smask) {
-                    s_flags = kSeedN;
-                } else {
-                    const uint64_t key = planar_key(lo, hi, a.s);
-                    const uint64_t rc = planar_rc_key(lo, hi, a.s);
-                    const uint64_t canon = key < rc ? key : rc;
-                    if (key != canon) s_flags |= kSeedQflip;
-                    if (key == rc) s_flags |= kSeedPal;
-                    unsigned int payload, meta;
-                    if (probe_slot(a.table, a.n_slots, canon, payload, meta)) {
-                        const uint32_t ntot = meta & 0x7fffffffu;
-                        s_count = (s_flags & kSeedPal) ? 2u * ntot : ntot;
-                        s_payload = payload;
-                        if (meta & 0x80000000u) s_flags |= kSeedSingleRc;
-                        if (ntot == 1 && !(s_flags & kSeedPal)) {
-                            // the likely candidate: pull its genome window into L2 now
-                            const uint32_t dir = ((meta >> 31) & 1u) ^ ((s_flags & kSeedQflip) ? 1u : 0u);
-                            const int64_t anc = static_cast<int64_t>(payload) -
-                                                (dir ? (len - a.s - s_off) : s_off);
-                            const uint64_t b = anc < 0 ? 0 : (static_cast<uint64_t>(anc) >> 5);
-                            prefetch_l2(a.planes + b);
-                            prefetch_l2(a.planes + b + ((len + a.dl_max + 32) >> 5));
-                        }
-                    }
-                }
-            }
-        }
-        const int src_lane = i & 31;
-        const uint32_t flags = __shfl_sync(FULL, s_flags, src_lane);
-        const uint32_t cnt = __shfl_sync(FULL, s_count, src_lane);
+        if ((i & 31) == 0 && (i > 0 || !wave0_ready))  // speculative probes, seeds i .. i+31
+            compute_wave_sync(a, x.R, offs, i, n_eff, len, recs, lane);
+        const uint4 rec = recs[i & 31];
+        const uint32_t flags = rec.x;
+        const uint32_t cnt = rec.y;
         if (flags & kSeedN) {  // REF :259-262
             x.st.skipped_n++;
             continue;
@@ -632,8 +700,8 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
         if (i < tier0) ++tested;
 
         if (cnt > 0) {  // REF :273-286
-            const uint32_t payload = __shfl_sync(FULL, s_payload, src_lane);
-            const int off = __shfl_sync(FULL, s_off, src_lane);
+            const uint32_t payload = rec.z;
+            const int off = static_cast<int>(rec.w);
             const bool pal = (flags & kSeedPal) != 0;
             const uint32_t ntot = pal ? cnt / 2 : cnt;
             const bool inl = ntot == 1;
@@ -765,24 +833,31 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
     return true;
 }
 
+#ifndef SA_MIN_BLOCKS
+#define SA_MIN_BLOCKS 3  // 256-thread blocks per SM the register budget must allow
+#endif
+
 template <bool kSlow>
-__global__ void __launch_bounds__(256, 3) align_kernel(const AlignLaunch a) {
+__global__ void __launch_bounds__(256, SA_MIN_BLOCKS) align_kernel(const AlignLaunch a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     unsigned char* ws = smem + static_cast<size_t>(wib) * a.smem_per_warp;
 
+    // per-warp layout (capi.cu make_shape): planes[2] {R, C}, window, seed
+    // records[2], probe landing zone, offsets[2], LV frontier, read staging[2],
+    // stats, candidate table (global memory for the slow kernel)
     Ctx x;
     x.a = &a;
     x.lane = lane;
-    uint4* R = reinterpret_cast<uint4*>(ws);
-    uint4* Cp = R + a.wbr;
-    x.R = R;
-    x.C = Cp;
-    x.W = Cp + a.wbr;
-    int* offs = reinterpret_cast<int*>(x.W + a.wbw);
-    x.F = offs + a.n_off_cap;
-    uint32_t* stage = reinterpret_cast<uint32_t*>(x.F + a.f_ints);  // 2 * sbw words
+    uint4* planes = reinterpret_cast<uint4*>(ws);  // buffer q: R = planes + 2q*wbr, C = R + wbr
+    x.W = planes + 4 * a.wbr;
+    uint4* recs = x.W + a.wbw;                      // 2 x 32
+    uint4* pslot = recs + 64;                       // 32
+    unsigned long long* pcanon = reinterpret_cast<unsigned long long*>(pslot + 32);  // 32
+    int* offs = reinterpret_cast<int*>(pcanon + 32);  // 2 x n_off_cap
+    x.F = offs + 2 * a.n_off_cap;
+    uint32_t* stage = reinterpret_cast<uint32_t*>(x.F + a.f_ints);  // 2 x sbw words
     unsigned long long* wst = reinterpret_cast<unsigned long long*>(stage + 2 * a.sbw);
     unsigned char* tb;
     if (kSlow) {
@@ -803,15 +878,16 @@ __global__ void __launch_bounds__(256, 3) align_kernel(const AlignLaunch a) {
     if (lane < kNumStats) wst[lane] = 0;
     __syncwarp();
 
-    int cached_len = -1, n_eff = 0, tier0 = 0;
-    auto prepare = [&](int len) {
-        x.len = len;
-        x.d_max = a.dmax_param >= 0 ? a.dmax_param : (12 * len + 99) / 100;
-        if (len != cached_len) {
-            n_eff = compute_offsets(len, a.s, min(a.n, a.n_off_cap), offs, lane);
-            tier0 = len / a.s;
-            cached_len = len;
+    int cached_len0 = -1, cached_len1 = -1, n_eff0 = 0, n_eff1 = 0;
+    // offsets for read length len into buffer q (cached per buffer)
+    auto offsets_for = [&](int q, int len) -> int {
+        int& cl = q ? cached_len1 : cached_len0;
+        int& ne = q ? n_eff1 : n_eff0;
+        if (len != cl) {
+            ne = compute_offsets(len, a.s, min(a.n, a.n_off_cap), offs + q * a.n_off_cap, lane);
+            cl = len;
         }
+        return ne;
     };
     auto bad_read = [&](uint32_t r) {
         if (lane == 0) {
@@ -837,63 +913,103 @@ __global__ void __launch_bounds__(256, 3) align_kernel(const AlignLaunch a) {
             wst[S_READ_BASES] += static_cast<unsigned long long>(len);
         }
     };
+    auto overflowed = [&](uint32_t r) {
+        if (kSlow) {  // table sized n_eff * h_max cannot overflow unless clamped
+            if (lane == 0) atomicOr(a.error_flag, 2u);
+        } else if (lane == 0) {  // defer to the global-table kernel
+            const unsigned slot = atomicAdd(a.overflow_count, 1u);
+            a.overflow_list[slot] = r;
+            wst[S_OVERFLOW] += 1;
+        }
+    };
+    // status of a staged read: 0 = decoded, 1 = shorter than s, 2 = bad character
+    auto prep = [&](int q, int len, const uint32_t* words, int sh, int nwd) -> int {
+        if (len < a.s) return 1;
+        offsets_for(q, len);
+        uint4* R = planes + 2 * q * a.wbr;
+        return decode_read(words, sh, nwd, len, R, R + a.wbr, lane) ? 2 : 0;
+    };
+    auto process = [&](uint32_t r, int q, int len, int st, bool wave0_ready) {
+        if (st == 1) {
+            short_read(r, len);
+        } else if (st == 2) {
+            bad_read(r);
+        } else {
+            x.R = planes + 2 * q * a.wbr;
+            x.C = x.R + a.wbr;
+            x.len = len;
+            x.d_max = a.dmax_param >= 0 ? a.dmax_param : (12 * len + 99) / 100;
+            const int ne = q ? n_eff1 : n_eff0;
+            if (!align_one<kSlow>(x, r, ne, offs + q * a.n_off_cap, len / a.s, wst, recs + 32 * q, wave0_ready))
+                overflowed(r);
+        }
+    };
 
     if (!kSlow && a.prefetch) {
-        // static striding with a two-deep software pipeline
+        // Static striding, software-pipelined one read ahead: while read r is
+        // aligned, read r+nw is already decoded and its wave-0 index probes are
+        // in flight (cp.async), and read r+2nw's bytes are being copied.
         const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-        uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
         const uint32_t N = a.n_reads;
-        uint64_t c0 = 0, c1 = 0, n0 = 0, n1 = 0;
+        uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
         if (r < N) {
-            c0 = a.offsets[r];
-            c1 = a.offsets[r + 1];
-        }
-        if (r + nw < N) {
-            n0 = a.offsets[r + nw];
-            n1 = a.offsets[r + nw + 1];
-        }
-        int cur = 0, sh_cur = 0, nw_cur = 0;
-        if (r < N)
-            issue_read_copy(a.bases + (c0 - a.base_off), static_cast<int>(c1 - c0), stage, lane, sh_cur,
-                            nw_cur);
-        cp_async_commit();
-        for (; r < N; r += nw) {
-            uint64_t f0 = 0, f1 = 0;
-            const uint32_t r2 = r + 2 * nw;
-            if (r2 < N) {
-                f0 = a.offsets[r2];
-                f1 = a.offsets[r2 + 1];
+            const uint64_t c0 = a.offsets[r], c1 = a.offsets[r + 1];
+            uint64_t n0 = 0, n1 = 0;
+            if (r + nw < N) {
+                n0 = a.offsets[r + nw];
+                n1 = a.offsets[r + nw + 1];
             }
-            int sh_nxt = 0, nw_nxt = 0;
-            if (r + nw < N)
-                issue_read_copy(a.bases + (n0 - a.base_off), static_cast<int>(n1 - n0),
-                                stage + (cur ^ 1) * a.sbw, lane, sh_nxt, nw_nxt);
+            int sh = 0, nwd = 0;
+            issue_read_copy(a.bases + (c0 - a.base_off), static_cast<int>(c1 - c0), stage, lane, sh, nwd);
             cp_async_commit();
-            cp_async_wait1();
+            cp_async_wait0();
             __syncwarp();
-            const int len = static_cast<int>(c1 - c0);
-            if (len < a.s) {
-                short_read(r, len);
-            } else {
-                prepare(len);
-                if (decode_read(stage + cur * a.sbw, sh_cur, nw_cur, len, R, Cp, lane)) {
-                    bad_read(r);
-                } else if (!align_one<kSlow>(x, r, n_eff, offs, tier0, wst)) {
-                    if (lane == 0) {
-                        const unsigned slot = atomicAdd(a.overflow_count, 1u);
-                        a.overflow_list[slot] = r;
-                        wst[S_OVERFLOW] += 1;
-                    }
-                }
+            int len_cur = static_cast<int>(c1 - c0);
+            int st_cur = prep(0, len_cur, stage, sh, nwd);
+            if (st_cur == 0) {
+                issue_wave0(a, planes, offs, n_eff0, recs, pslot, pcanon, lane);
+                resolve_wave0(a, n_eff0, len_cur, recs, pslot, pcanon, lane);
             }
-            __syncwarp();
-            c0 = n0;
-            c1 = n1;
-            n0 = f0;
-            n1 = f1;
-            sh_cur = sh_nxt;
-            nw_cur = nw_nxt;
-            cur ^= 1;
+            int sh_n = 0, nw_n = 0;
+            if (r + nw < N)
+                issue_read_copy(a.bases + (n0 - a.base_off), static_cast<int>(n1 - n0), stage + a.sbw, lane,
+                                sh_n, nw_n);
+            cp_async_commit();
+            int p = 0;
+            for (; r < N; r += nw) {
+                const bool has_next = r + nw < N;
+                const bool has_next2 = r + 2 * nw < N;
+                cp_async_wait0();
+                __syncwarp();
+                const int len_n = static_cast<int>(n1 - n0);
+                int st_n = 1;
+                if (has_next) {
+                    st_n = prep(p ^ 1, len_n, stage + (p ^ 1) * a.sbw, sh_n, nw_n);
+                    if (st_n == 0)
+                        issue_wave0(a, planes + 2 * (p ^ 1) * a.wbr, offs + (p ^ 1) * a.n_off_cap,
+                                    p ? n_eff0 : n_eff1, recs + 32 * (p ^ 1), pslot, pcanon, lane);
+                }
+                uint64_t f0 = 0, f1 = 0;
+                if (has_next2) {
+                    f0 = a.offsets[r + 2 * nw];
+                    f1 = a.offsets[r + 2 * nw + 1];
+                }
+                process(r, p, len_cur, st_cur, true);
+                if (has_next && st_n == 0)
+                    resolve_wave0(a, p ? n_eff0 : n_eff1, len_n, recs + 32 * (p ^ 1), pslot, pcanon, lane);
+                sh_n = 0;
+                nw_n = 0;
+                if (has_next2)
+                    issue_read_copy(a.bases + (f0 - a.base_off), static_cast<int>(f1 - f0), stage + p * a.sbw,
+                                    lane, sh_n, nw_n);
+                cp_async_commit();
+                n0 = f0;
+                n1 = f1;
+                len_cur = len_n;
+                st_cur = st_n;
+                p ^= 1;
+            }
+            cp_async_wait0();
         }
     } else {
         // dynamic fetch (work list for the slow kernel), reads decoded from global
@@ -906,27 +1022,11 @@ __global__ void __launch_bounds__(256, 3) align_kernel(const AlignLaunch a) {
             if (kSlow) r = a.work_list[r];
             const uint64_t o0 = a.offsets[r], o1 = a.offsets[r + 1];
             const int len = static_cast<int>(o1 - o0);
-            if (len < a.s) {
-                short_read(r, len);
-                continue;
-            }
-            prepare(len);
             const uintptr_t addr = reinterpret_cast<uintptr_t>(a.bases + (o0 - a.base_off));
-            const uint32_t* wd = reinterpret_cast<const uint32_t*>(addr & ~static_cast<uintptr_t>(3));
-            const int nwords = static_cast<int>((addr + len - (addr & ~static_cast<uintptr_t>(3)) + 3) >> 2);
-            if (decode_read(wd, static_cast<int>(addr & 3), nwords, len, R, Cp, lane)) {
-                bad_read(r);
-                continue;
-            }
-            if (!align_one<kSlow>(x, r, n_eff, offs, tier0, wst)) {
-                if (kSlow) {  // table sized n_eff * h_max cannot overflow unless clamped
-                    if (lane == 0) atomicOr(a.error_flag, 2u);
-                } else if (lane == 0) {
-                    const unsigned slot = atomicAdd(a.overflow_count, 1u);
-                    a.overflow_list[slot] = r;
-                    wst[S_OVERFLOW] += 1;
-                }
-            }
+            const uintptr_t abase = addr & ~static_cast<uintptr_t>(3);
+            const int nwords = static_cast<int>((addr + len - abase + 3) >> 2);
+            const int st = prep(0, len, reinterpret_cast<const uint32_t*>(abase), static_cast<int>(addr & 3), nwords);
+            process(r, 0, len, st, false);
         }
     }
 

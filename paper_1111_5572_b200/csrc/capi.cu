@@ -151,8 +151,10 @@ int make_shape(Replica& rep, const sa_params* p, uint64_t Lmax, LaunchShape& sh,
     a.wbw = (64 + L + a.dl_max + 31) / 32 + 4;
     a.n_off_cap = round4(std::max(1, std::min(p->seeds_to_try, L - p->seed_size + 1)));
     a.f_ints = a.dl_max > 15 ? round4(2 * (2 * a.dl_max + 3)) : 0;
-    const uint64_t common = 16ull * (2 * a.wbr + a.wbw) + 4ull * (a.n_off_cap + a.f_ints) +
-                            8ull * kNumStats;
+    // per warp: planes[2]{R,C}, window, seed records[2][32], probe landing
+    // zone[32] + keys[32], offsets[2], LV frontier, stats (align.cu kernel)
+    const uint64_t common = 16ull * (4 * a.wbr + a.wbw + 64 + 32) + 8ull * 32 +
+                            4ull * (2 * a.n_off_cap + a.f_ints) + 8ull * kNumStats;
     a.cap = kFastCap;
     a.hcap = kFastHcap;
     a.prefetch = L <= 1024 ? 1 : 0;

@@ -124,9 +124,8 @@ SA_DEV int read_code(unsigned char ch) {
 }
 
 // Probe the table for a canonical key.  Returns false on a miss.
-SA_DEV bool probe_slot(const Slot* __restrict__ table, uint64_t n_slots, uint64_t canon,
+SA_DEV bool probe_from(const Slot* __restrict__ table, uint64_t n_slots, uint64_t canon, uint64_t h,
                        unsigned int& payload, unsigned int& meta) {
-    uint64_t h = home_slot(canon, n_slots);
     const ulonglong2* t = reinterpret_cast<const ulonglong2*>(table);
     for (;;) {
         ulonglong2 v = __ldg(t + h);
@@ -138,6 +137,11 @@ SA_DEV bool probe_slot(const Slot* __restrict__ table, uint64_t n_slots, uint64_
         if (v.x == kEmptyKey) return false;
         h = (h + 1 == n_slots) ? 0 : h + 1;
     }
+}
+
+SA_DEV bool probe_slot(const Slot* __restrict__ table, uint64_t n_slots, uint64_t canon,
+                       unsigned int& payload, unsigned int& meta) {
+    return probe_from(table, n_slots, canon, home_slot(canon, n_slots), payload, meta);
 }
 
 }  // namespace sab

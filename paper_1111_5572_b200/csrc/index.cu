@@ -319,7 +319,10 @@ int build_device_index(const uint64_t* h_packed, uint64_t n_packed, const uint64
             goto fail;
         }
         ix.pool_len = pool_total;
-        ix.n_slots = n_runs + n_runs / 2 + n_runs / 6 + 64;  // load ~0.6
+#ifndef SA_TABLE_LOAD_PCT
+#define SA_TABLE_LOAD_PCT 60  // target fill of the open-addressing table
+#endif
+        ix.n_slots = n_runs * 100 / SA_TABLE_LOAD_PCT + 64;
         CK(cudaMalloc(&ix.table, ix.n_slots * sizeof(Slot)));
         CK(cudaMemsetAsync(ix.table, 0xff, ix.n_slots * sizeof(Slot), st));
         CK(cudaMalloc(&ix.pool, (pool_total + 1) * sizeof(uint32_t)));
