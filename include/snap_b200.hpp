@@ -1,0 +1,128 @@
+// snap_b200.hpp -- header-only C++ adapter over the C ABI (snap_b200.h) that
+// restores the reference's C++ shape and exception contract:
+//
+//   seedaln::SeedIndex::build(genome, s)        -> snap_b200::SeedIndex(packed, nmask, len, s)
+//   seedaln::Aligner(idx, genome, params)       -> snap_b200::Aligner(idx, params)
+//   Aligner::align(const Read&)                 -> Aligner::align(std::string_view)   (batch of 1; tests)
+//                                               -> Aligner::align_batch(...)          (production)
+//   std::invalid_argument / FormatError / IoError are rethrown from the status
+//   codes (REF include/seedaln/errors.hpp:10-30).
+//
+// Link with paper_1111_5572_b200/lib/libsnapb200.so.  See INTEGRATION.md.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <vector>
+
+#include "snap_b200.h"
+
+namespace snap_b200 {
+
+class FormatError : public std::runtime_error {
+public:
+    using std::runtime_error::runtime_error;
+};
+
+inline void check(int rc, const sa_context* ctx) {
+    if (rc == SA_OK) return;
+    std::string msg = sa_last_error(ctx);
+    if (rc == SA_EINVAL) throw std::invalid_argument(msg);
+    if (rc == SA_EFORMAT) throw FormatError(msg);
+    throw std::runtime_error(msg);
+}
+
+inline sa_params default_params() {
+    sa_params p;
+    sa_default_params(&p);
+    return p;
+}
+
+// Seed index + genome replica(s) resident in HBM (replaces SeedIndex::build,
+// REF src/seed_index.cpp:80-126).  Non-copyable, movable.
+class SeedIndex {
+public:
+    SeedIndex(const std::vector<uint64_t>& packed_words, const std::vector<uint64_t>& n_mask_words,
+              uint64_t genome_length, int seed_size, const std::vector<int32_t>& devices = {0}) {
+        check(sa_create(packed_words.data(), packed_words.size(), n_mask_words.data(),
+                        n_mask_words.size(), genome_length, seed_size, devices.data(),
+                        static_cast<int32_t>(devices.size()), &ctx_),
+              nullptr);
+        seed_size_ = seed_size;
+    }
+    SeedIndex(const SeedIndex&) = delete;
+    SeedIndex& operator=(const SeedIndex&) = delete;
+    SeedIndex(SeedIndex&& o) noexcept : ctx_(o.ctx_), seed_size_(o.seed_size_) { o.ctx_ = nullptr; }
+    ~SeedIndex() { sa_destroy(ctx_); }
+
+    int seed_size() const { return seed_size_; }
+    uint64_t distinct_seeds() const {
+        uint64_t d = 0;
+        check(sa_index_info(ctx_, &d, nullptr, nullptr), ctx_);
+        return d;
+    }
+    uint64_t total_positions() const {
+        uint64_t t = 0;
+        check(sa_index_info(ctx_, nullptr, &t, nullptr), ctx_);
+        return t;
+    }
+    sa_context* context() const { return ctx_; }
+
+private:
+    sa_context* ctx_ = nullptr;
+    int seed_size_ = 0;
+};
+
+// Replaces seedaln::Aligner (REF include/seedaln/aligner.hpp:116-158).
+class Aligner {
+public:
+    Aligner(const SeedIndex& idx, const sa_params& params) : idx_(&idx), params_(params) {
+        check(sa_validate_params(&params_), nullptr);  // REF aligner.cpp:119
+        if (idx.seed_size() != params_.seed_size)      // REF aligner.cpp:120-121
+            throw std::invalid_argument("index seed size does not match params");
+    }
+
+    // reads: bases[offsets[i] .. offsets[i+1]); results in input order
+    void align_batch(const char* bases, const uint64_t* offsets, uint64_t n, sa_result* results) {
+        sa_stats st{};
+        check(sa_align_batch(idx_->context(), &params_, bases, offsets, n, results, &st),
+              idx_->context());
+        merge(st);
+    }
+
+    std::vector<sa_result> align_batch(const std::vector<std::string>& reads) {
+        std::string buf;
+        std::vector<uint64_t> offs{0};
+        for (const auto& r : reads) {
+            buf += r;
+            offs.push_back(buf.size());
+        }
+        std::vector<sa_result> out(reads.size());
+        align_batch(buf.data(), offs.data(), reads.size(), out.data());
+        return out;
+    }
+
+    sa_result align(std::string_view bases) {  // REF aligner.cpp:223 (batch of one)
+        uint64_t offs[2] = {0, bases.size()};
+        sa_result r{};
+        align_batch(bases.data(), offs, 1, &r);
+        return r;
+    }
+
+    const sa_stats& stats() const { return stats_; }
+
+private:
+    void merge(const sa_stats& s) {  // REF aligner.cpp:31-48
+        auto* d = reinterpret_cast<uint64_t*>(&stats_);
+        const auto* v = reinterpret_cast<const uint64_t*>(&s);
+        for (size_t i = 0; i < sizeof(sa_stats) / sizeof(uint64_t); ++i) d[i] += v[i];
+    }
+
+    const SeedIndex* idx_;
+    sa_params params_;
+    sa_stats stats_{};
+};
+
+}  // namespace snap_b200

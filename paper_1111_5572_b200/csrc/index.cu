@@ -319,10 +319,15 @@ int build_device_index(const uint64_t* h_packed, uint64_t n_packed, const uint64
             goto fail;
         }
         ix.pool_len = pool_total;
-#ifndef SA_TABLE_LOAD_PCT
-#define SA_TABLE_LOAD_PCT 60  // target fill of the open-addressing table
-#endif
-        ix.n_slots = n_runs * 100 / SA_TABLE_LOAD_PCT + 64;
+        {
+            // Target fill of the open-addressing table: 35% keeps probe chains
+            // at ~1.3 slots; fall back to 60% when that would take more than a
+            // third of the free HBM (3.1 Gbp genomes).
+            size_t free_b = 0, total_b = 0;
+            cudaMemGetInfo(&free_b, &total_b);
+            const uint64_t sparse = n_runs * 100 / 35 + 64;
+            ix.n_slots = sparse * sizeof(Slot) <= free_b / 3 ? sparse : n_runs * 100 / 60 + 64;
+        }
         CK(cudaMalloc(&ix.table, ix.n_slots * sizeof(Slot)));
         CK(cudaMemsetAsync(ix.table, 0xff, ix.n_slots * sizeof(Slot), st));
         CK(cudaMalloc(&ix.pool, (pool_total + 1) * sizeof(uint32_t)));

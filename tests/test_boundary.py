@@ -128,3 +128,22 @@ def test_product_never_touches_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(from|import)\s+oracle|liboracle|seedaln_ref|snap_oracle", txt, re.M), f
+
+
+def test_cpp_adapter_compiles_and_links(tmp_path):
+    """include/snap_b200.hpp (the C++ drop-in shape) compiles against the C ABI
+    and links against libsnapb200.so (no GPU call is made)."""
+    src = tmp_path / "use.cpp"
+    src.write_text(
+        '#include "snap_b200.hpp"\n'
+        "int main(int argc, char**) {\n"
+        "  if (argc > 5) { snap_b200::SeedIndex idx({0}, {0}, 20, 20);\n"
+        "    snap_b200::Aligner al(idx, snap_b200::default_params());\n"
+        "    auto r = al.align(\"ACGT\"); return r.kind; }\n"
+        "  return 0; }\n")
+    exe = tmp_path / "use"
+    r = subprocess.run(["g++", "-std=c++17", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe),
+                        api.LIB_PATH, f"-Wl,-rpath,{os.path.dirname(api.LIB_PATH)}"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert subprocess.run([str(exe)]).returncode == 0
