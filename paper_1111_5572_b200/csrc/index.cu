@@ -3,16 +3,26 @@
 // Replaces SeedIndex::build (REF src/seed_index.cpp:80-126), which rolls a
 // 2s-bit key over every N-free window, std::sorts (key, pos) pairs and lays
 // out a CSR of u64 keys/offsets/positions.  Here:
-//   K0 planes_kernel     PackedGenome words -> bit planes (common.cuh)
-//   K1a emit_kernel      one thread per window: canonical key + strand flag
-//   K1b CUB radix sort   (canon<<1|flag, pos), stable -> positions ascending
-//   K1c head/scan        run boundaries of equal canonical keys
-//   K1d insert_kernel    one thread per distinct canonical key: position
-//                        list into the pool (canon-strand windows first),
-//                        open-addressing insert with atomicCAS on the key
+//   K0 planes_kernel      PackedGenome words -> bit planes (common.cuh)
+//   per key-hash partition p of P (P = 1 up to a few hundred Mbp; more for
+//   3.1 Gbp genomes, so build temporaries stay bounded):
+//     K1a count/write     ordered compaction of the N-free windows whose
+//                         canonical key falls in p: (canon<<1|strand, pos),
+//                         positions ascending (block scan, deterministic)
+//     K1b CUB radix sort  stable -> positions stay ascending per key
+//     K1c head/scan       run boundaries of equal canonical keys
+//     K1d insert_kernel   one thread per distinct key: position list into the
+//                         pool (canon-strand windows first), open-addressing
+//                         insert with atomicCAS on the key
+// The table is sized from the window count (an upper bound on distinct keys)
+// before the first partition; the pool grows between partitions if needed.
 // The index answers exactly the reference's lookup(): see common.cuh.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <string>
@@ -23,6 +33,10 @@
 namespace sab {
 
 namespace {
+
+constexpr int kEmitThreads = 256;
+constexpr int kEmitPerThread = 16;  // consecutive windows per thread
+constexpr uint64_t kEmitPerBlock = static_cast<uint64_t>(kEmitThreads) * kEmitPerThread;
 
 SA_DEV uint32_t compact_even(uint64_t x) {
     x &= 0x5555555555555555ull;
@@ -61,33 +75,70 @@ __global__ void planes_kernel(const uint64_t* __restrict__ packed, uint64_t n_pa
     }
 }
 
-// K1a: sort key per window (REF seed_index.cpp:96-110 rolling key; windows
-// holding N are skipped, here given the sentinel so they sort last).
-__global__ void emit_kernel(const uint4* __restrict__ planes, uint64_t n_windows, int s,
-                            unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals,
-                            unsigned long long sentinel, unsigned long long* n_valid) {
-    const uint32_t smask = seed_mask32(s);
-    uint32_t valid_here = 0;
-    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n_windows;
-         p += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t lo, hi, n;
-        extract32_ldg(planes, p, lo, hi, n);
-        unsigned long long k;
-        if (n & smask) {
-            k = sentinel;
-        } else {
-            const uint64_t key = planar_key(lo, hi, s);
-            const uint64_t rc = planar_rc_key(lo, hi, s);
-            const uint64_t canon = key < rc ? key : rc;
-            k = s <= 31 ? ((canon << 1) | (key != canon ? 1ull : 0ull)) : canon;
-            ++valid_here;
-        }
-        keys[p] = k;
-        vals[p] = static_cast<uint32_t>(p);
+// Window p's sort key, or false when the window holds N (REF
+// seed_index.cpp:96-110 skips those) or its key is outside partition `part`.
+SA_DEV bool window_key(const uint4* planes, uint64_t p, int s, uint32_t part, uint32_t n_parts,
+                       unsigned long long& sk) {
+    uint32_t lo, hi, n;
+    extract32_ldg(planes, p, lo, hi, n);
+    if (n & seed_mask32(s)) return false;
+    const uint64_t key = planar_key(lo, hi, s);
+    const uint64_t rc = planar_rc_key(lo, hi, s);
+    const uint64_t canon = key < rc ? key : rc;
+    if (n_parts > 1 && static_cast<uint32_t>(((mix64(canon) >> 32) * n_parts) >> 32) != part) return false;
+    sk = s <= 31 ? ((canon << 1) | (key != canon ? 1ull : 0ull)) : canon;
+    return true;
+}
+
+// K1a (count): windows of partition `part` per block of kEmitPerBlock windows.
+__global__ void __launch_bounds__(kEmitThreads) count_part_kernel(const uint4* __restrict__ planes,
+                                                                  uint64_t n_windows, int s, uint32_t part,
+                                                                  uint32_t n_parts,
+                                                                  unsigned long long* block_counts) {
+    typedef cub::BlockReduce<unsigned int, kEmitThreads> Reduce;
+    __shared__ typename Reduce::TempStorage tmp;
+    const uint64_t base = blockIdx.x * kEmitPerBlock + static_cast<uint64_t>(threadIdx.x) * kEmitPerThread;
+    unsigned int c = 0;
+    for (int j = 0; j < kEmitPerThread; ++j) {
+        const uint64_t p = base + j;
+        unsigned long long sk;
+        if (p < n_windows && window_key(planes, p, s, part, n_parts, sk)) ++c;
     }
-    // warp-aggregated count
-    for (int o = 16; o > 0; o >>= 1) valid_here += __shfl_xor_sync(0xffffffffu, valid_here, o);
-    if ((threadIdx.x & 31) == 0 && valid_here) atomicAdd(n_valid, (unsigned long long)valid_here);
+    const unsigned int tot = Reduce(tmp).Sum(c);
+    if (threadIdx.x == 0) block_counts[blockIdx.x] = tot;
+}
+
+// K1a (write): same walk; each thread writes its matches at its block offset
+// plus its exclusive prefix, so output keeps genome position order.
+__global__ void __launch_bounds__(kEmitThreads) write_part_kernel(const uint4* __restrict__ planes,
+                                                                  uint64_t n_windows, int s, uint32_t part,
+                                                                  uint32_t n_parts,
+                                                                  const unsigned long long* block_offs,
+                                                                  unsigned long long* __restrict__ keys,
+                                                                  uint32_t* __restrict__ vals) {
+    typedef cub::BlockScan<unsigned int, kEmitThreads> Scan;
+    __shared__ typename Scan::TempStorage tmp;
+    const uint64_t base = blockIdx.x * kEmitPerBlock + static_cast<uint64_t>(threadIdx.x) * kEmitPerThread;
+    unsigned long long sk[kEmitPerThread];
+    unsigned int c = 0, m = 0;
+    for (int j = 0; j < kEmitPerThread; ++j) {
+        const uint64_t p = base + j;
+        if (p < n_windows && window_key(planes, p, s, part, n_parts, sk[c])) {
+            m |= 1u << j;
+            ++c;
+        }
+    }
+    unsigned int pre;
+    Scan(tmp).ExclusiveSum(c, pre);
+    uint64_t o = block_offs[blockIdx.x] + pre;
+    unsigned int k = 0;
+    for (int j = 0; j < kEmitPerThread; ++j) {
+        if (m & (1u << j)) {
+            keys[o] = sk[k++];
+            vals[o] = static_cast<uint32_t>(base + j);
+            ++o;
+        }
+    }
 }
 
 SA_DEV uint64_t canon_of(unsigned long long sk, int s) { return s <= 31 ? (sk >> 1) : sk; }
@@ -128,7 +179,7 @@ SA_DEV bool window_is_rc(const uint4* planes, uint32_t pos, int s) {
 __global__ void insert_kernel(const unsigned long long* __restrict__ keys,
                               const uint32_t* __restrict__ vals,
                               const uint32_t* __restrict__ run_start, uint64_t n_runs,
-                              const unsigned long long* __restrict__ pool_off,
+                              const unsigned long long* __restrict__ pool_off, uint64_t pool_base,
                               const uint4* __restrict__ planes, int s, Slot* table,
                               uint64_t n_slots, uint32_t* __restrict__ pool,
                               unsigned long long* n_distinct) {
@@ -146,7 +197,7 @@ __global__ void insert_kernel(const unsigned long long* __restrict__ keys,
             meta = 1u | (flag ? 0x80000000u : 0u);
             distinct += 1;
         } else {
-            const uint64_t off = pool_off[r];
+            const uint64_t off = pool_base + pool_off[r];
             uint32_t n_fwd = 0;
             if (s <= 31) {  // sorted by flag within the run: canon strand first
                 uint32_t lo = b, hi = e;
@@ -193,12 +244,31 @@ int grid_for(uint64_t n, int threads) {
     return static_cast<int>(g);
 }
 
+struct Scratch {  // build temporaries, freed at the end
+    void* p[12] = {};
+    int n = 0;
+    template <typename T>
+    cudaError_t alloc(T** out, uint64_t count) {
+        void* q = nullptr;
+        cudaError_t e = cudaMalloc(&q, std::max<uint64_t>(count, 1) * sizeof(T));
+        if (e == cudaSuccess) {
+            p[n++] = q;
+            *out = static_cast<T*>(q);
+        }
+        return e;
+    }
+    ~Scratch() {
+        for (int i = 0; i < n; ++i) cudaFree(p[i]);
+    }
+};
+
 #define CK(x)                                                                  \
     do {                                                                       \
         cudaError_t e_ = (x);                                                  \
         if (e_ != cudaSuccess) {                                               \
             err = std::string(#x) + ": " + cudaGetErrorString(e_);             \
-            goto fail;                                                         \
+            free_device_index(&ix);                                            \
+            return 2;                                                          \
         }                                                                      \
     } while (0)
 
@@ -219,159 +289,156 @@ int build_device_index(const uint64_t* h_packed, uint64_t n_packed, const uint64
     ix.seed_size = s;
     ix.n_blocks = (glen + 31) / 32 + 2;
     const uint64_t n_windows = glen - s + 1;
-    const unsigned long long sentinel = s <= 31 ? ((1ull << (2 * s + 1)) - 1) : ~0ull;
     const int end_bit = s <= 31 ? 2 * s + 1 : 64;
 
-    uint64_t* d_packed = nullptr;
-    uint64_t* d_nmask = nullptr;
-    unsigned long long *k0 = nullptr, *k1 = nullptr, *d_count = nullptr, *pool_off = nullptr;
-    uint32_t *v0 = nullptr, *v1 = nullptr, *head = nullptr, *rid = nullptr, *run_start = nullptr;
-    void* temp = nullptr;
-    size_t temp_bytes = 0, need = 0;
-    unsigned long long n_valid = 0, pool_total = 0, last_need = 0;
-    uint32_t last_head = 0, last_rid = 0;
-    uint64_t n_runs = 0;
-    cub::DoubleBuffer<unsigned long long> kb;
-    cub::DoubleBuffer<uint32_t> vb;
-
+    // ---- genome planes
     CK(cudaMalloc(&ix.planes, ix.n_blocks * sizeof(uint4)));
-    CK(cudaMalloc(&d_packed, n_packed * sizeof(uint64_t) + 8));
-    CK(cudaMalloc(&d_nmask, n_nmask * sizeof(uint64_t) + 8));
-    CK(cudaMemcpyAsync(d_packed, h_packed, n_packed * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(d_nmask, h_nmask, n_nmask * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
-    planes_kernel<<<grid_for(ix.n_blocks, 256), 256, 0, st>>>(d_packed, n_packed, d_nmask, glen,
-                                                               ix.planes, ix.n_blocks);
-    CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(st));
-    cudaFree(d_packed);
-    d_packed = nullptr;
-    cudaFree(d_nmask);
-    d_nmask = nullptr;
-
-    CK(cudaMalloc(&k0, n_windows * sizeof(unsigned long long)));
-    CK(cudaMalloc(&k1, n_windows * sizeof(unsigned long long)));
-    CK(cudaMalloc(&v0, n_windows * sizeof(uint32_t)));
-    CK(cudaMalloc(&v1, n_windows * sizeof(uint32_t)));
-    CK(cudaMalloc(&d_count, sizeof(unsigned long long)));
-    CK(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), st));
-    emit_kernel<<<grid_for(n_windows, 256), 256, 0, st>>>(ix.planes, n_windows, s, k0, v0,
-                                                           sentinel, d_count);
-    CK(cudaGetLastError());
-
-    kb = cub::DoubleBuffer<unsigned long long>(k0, k1);
-    vb = cub::DoubleBuffer<uint32_t>(v0, v1);
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, kb, vb, (int64_t)n_windows, 0, end_bit, st));
-    CK(cudaMalloc(&temp, temp_bytes));
-    CK(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, kb, vb, (int64_t)n_windows, 0, end_bit, st));
-    CK(cudaMemcpyAsync(&n_valid, d_count, sizeof(n_valid), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    cudaFree(temp);
-    temp = nullptr;
-    ix.n_positions = n_valid;
-
-    if (n_valid > 0) {
-        // k/v of the sorted pairs live in kb.Current()/vb.Current(); reuse the
-        // other buffers as scratch for the head flags and run ids.
-        head = reinterpret_cast<uint32_t*>(kb.Alternate());
-        rid = vb.Alternate();
-        head_kernel<<<grid_for(n_valid, 256), 256, 0, st>>>(kb.Current(), n_valid, s, head);
+    {
+        Scratch up;
+        uint64_t *d_packed = nullptr, *d_nmask = nullptr;
+        CK(up.alloc(&d_packed, n_packed + 1));
+        CK(up.alloc(&d_nmask, n_nmask + 1));
+        CK(cudaMemcpyAsync(d_packed, h_packed, n_packed * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d_nmask, h_nmask, n_nmask * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+        planes_kernel<<<grid_for(ix.n_blocks, 256), 256, 0, st>>>(d_packed, n_packed, d_nmask, glen,
+                                                                   ix.planes, ix.n_blocks);
         CK(cudaGetLastError());
-        temp_bytes = 0;
-        CK(cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, head, rid, (int64_t)n_valid, st));
-        CK(cudaMalloc(&temp, temp_bytes));
-        CK(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, head, rid, (int64_t)n_valid, st));
-        CK(cudaMemcpyAsync(&last_head, head + n_valid - 1, 4, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(&last_rid, rid + n_valid - 1, 4, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        cudaFree(temp);
-        temp = nullptr;
-        n_runs = static_cast<uint64_t>(last_rid) + last_head;
-        ix.n_keys = n_runs;
-
-        CK(cudaMalloc(&run_start, (n_runs + 1) * sizeof(uint32_t)));
-        starts_kernel<<<grid_for(n_valid, 256), 256, 0, st>>>(head, rid, n_valid, run_start);
-        CK(cudaGetLastError());
-        {
-            uint32_t nv = static_cast<uint32_t>(n_valid);
-            CK(cudaMemcpyAsync(run_start + n_runs, &nv, 4, cudaMemcpyHostToDevice, st));
-            CK(cudaStreamSynchronize(st));
-        }
-        // pool offsets: exclusive sum of per-run needs (head/rid no longer used)
-        CK(cudaMalloc(&pool_off, (n_runs + 1) * sizeof(unsigned long long)));
-        {
-            unsigned long long* needv = reinterpret_cast<unsigned long long*>(kb.Alternate());
-            // Alternate holds n_windows u64 >= n_runs entries
-            pool_need_kernel<<<grid_for(n_runs, 256), 256, 0, st>>>(run_start, n_runs, needv);
-            CK(cudaGetLastError());
-            temp_bytes = 0;
-            CK(cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, needv, pool_off, (int64_t)n_runs, st));
-            CK(cudaMalloc(&temp, temp_bytes));
-            CK(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, needv, pool_off, (int64_t)n_runs, st));
-            CK(cudaMemcpyAsync(&pool_total, pool_off + n_runs - 1, 8, cudaMemcpyDeviceToHost, st));
-            CK(cudaMemcpyAsync(&last_need, needv + n_runs - 1, 8, cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
-            cudaFree(temp);
-            temp = nullptr;
-            pool_total += last_need;
-        }
-        if (pool_total >= 0xffffffffull) {
-            err = "position pool exceeds 2^32 entries";
-            goto fail;
-        }
-        ix.pool_len = pool_total;
-        {
-            // Target fill of the open-addressing table: 35% keeps probe chains
-            // at ~1.3 slots; fall back to 60% when that would take more than a
-            // third of the free HBM (3.1 Gbp genomes).
-            size_t free_b = 0, total_b = 0;
-            cudaMemGetInfo(&free_b, &total_b);
-            const uint64_t sparse = n_runs * 100 / 35 + 64;
-            ix.n_slots = sparse * sizeof(Slot) <= free_b / 3 ? sparse : n_runs * 100 / 60 + 64;
-        }
-        CK(cudaMalloc(&ix.table, ix.n_slots * sizeof(Slot)));
-        CK(cudaMemsetAsync(ix.table, 0xff, ix.n_slots * sizeof(Slot), st));
-        CK(cudaMalloc(&ix.pool, (pool_total + 1) * sizeof(uint32_t)));
-        CK(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), st));
-        insert_kernel<<<grid_for(n_runs, 128), 128, 0, st>>>(kb.Current(), vb.Current(), run_start,
-                                                              n_runs, pool_off, ix.planes, s,
-                                                              ix.table, ix.n_slots, ix.pool,
-                                                              d_count);
-        CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(&ix.n_distinct, d_count, 8, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-    } else {
-        ix.n_slots = 64;
-        CK(cudaMalloc(&ix.table, ix.n_slots * sizeof(Slot)));
-        CK(cudaMemsetAsync(ix.table, 0xff, ix.n_slots * sizeof(Slot), st));
-        CK(cudaMalloc(&ix.pool, sizeof(uint32_t)));
         CK(cudaStreamSynchronize(st));
     }
-    cudaFree(k0);
-    cudaFree(k1);
-    cudaFree(v0);
-    cudaFree(v1);
-    cudaFree(d_count);
-    if (run_start) cudaFree(run_start);
-    if (pool_off) cudaFree(pool_off);
-    ix.device_bytes = ix.n_blocks * sizeof(uint4) + ix.n_slots * sizeof(Slot) +
-                      (ix.pool_len + 1) * sizeof(uint32_t);
-    *out = ix;
-    (void)need;
-    return 0;
 
-fail:
-    if (d_packed) cudaFree(d_packed);
-    if (d_nmask) cudaFree(d_nmask);
-    if (k0) cudaFree(k0);
-    if (k1) cudaFree(k1);
-    if (v0) cudaFree(v0);
-    if (v1) cudaFree(v1);
-    if (d_count) cudaFree(d_count);
-    if (run_start) cudaFree(run_start);
-    if (pool_off) cudaFree(pool_off);
-    if (temp) cudaFree(temp);
-    free_device_index(&ix);
-    return 2;
+    // ---- table sized from the window count (upper bound on distinct keys):
+    // 35% target load keeps probe chains ~1.3 slots; 60% when that would take
+    // more than a third of the free HBM (3.1 Gbp genomes)
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    {
+        const uint64_t sparse = n_windows * 100 / 35 + 64;
+        ix.n_slots = sparse * sizeof(Slot) <= free_b / 3 ? sparse : n_windows * 100 / 60 + 64;
+    }
+    CK(cudaMalloc(&ix.table, ix.n_slots * sizeof(Slot)));
+    CK(cudaMemsetAsync(ix.table, 0xff, ix.n_slots * sizeof(Slot), st));
+
+    // ---- partitions: ~40 B of temporaries per window of a partition
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    const uint64_t budget = free_b / 2;
+    uint32_t n_parts = static_cast<uint32_t>((n_windows * 48 + budget - 1) / budget);
+    if (n_parts < 1) n_parts = 1;
+    if (const char* e = getenv("SA_INDEX_PARTS")) {  // test hook: force a partitioned build
+        const long f = strtol(e, nullptr, 10);
+        if (f > static_cast<long>(n_parts) && f < 65536) n_parts = static_cast<uint32_t>(f);
+    }
+    const uint64_t cap = n_windows / n_parts + n_windows / (8 * n_parts) + 4096;  // hash imbalance slack
+    uint64_t pool_cap = std::max<uint64_t>(1 << 20, n_windows / 8);
+    CK(cudaMalloc(&ix.pool, pool_cap * sizeof(uint32_t)));
+    uint64_t pool_used = 0;
+
+    Scratch tmp;
+    const uint64_t n_eblocks = (n_windows + kEmitPerBlock - 1) / kEmitPerBlock;
+    unsigned long long *bcount = nullptr, *boff = nullptr, *k0 = nullptr, *k1 = nullptr, *pool_off = nullptr,
+                       *d_count = nullptr;
+    uint32_t *v0 = nullptr, *v1 = nullptr, *run_start = nullptr;
+    CK(tmp.alloc(&bcount, n_eblocks + 1));
+    CK(tmp.alloc(&boff, n_eblocks + 1));
+    CK(tmp.alloc(&k0, cap + 1));  // +1: the run-need vector (aliased on k0/k1) has n_runs+1 entries
+    CK(tmp.alloc(&k1, cap + 1));
+    CK(tmp.alloc(&v0, cap));
+    CK(tmp.alloc(&v1, cap));
+    CK(tmp.alloc(&run_start, cap + 1));
+    CK(tmp.alloc(&pool_off, cap + 1));
+    CK(tmp.alloc(&d_count, 2));
+    CK(cudaMemsetAsync(d_count, 0, 2 * sizeof(unsigned long long), st));
+    void* temp = nullptr;
+    size_t temp_bytes = 0;
+    {
+        size_t a = 0, b = 0, c = 0;
+        cub::DoubleBuffer<unsigned long long> kb(k0, k1);
+        cub::DoubleBuffer<uint32_t> vb(v0, v1);
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, a, kb, vb, (int64_t)cap, 0, end_bit, st));
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, b, v0, v1, (int64_t)cap, st));
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, c, k0, k1, (int64_t)std::max(cap, n_eblocks) + 1, st));
+        temp_bytes = std::max(a, std::max(b, c));
+        CK(tmp.alloc(reinterpret_cast<unsigned char**>(&temp), temp_bytes));
+    }
+
+    for (uint32_t part = 0; part < n_parts; ++part) {
+        // K1a: ordered compaction of this partition's windows
+        count_part_kernel<<<static_cast<int>(n_eblocks), kEmitThreads, 0, st>>>(ix.planes, n_windows, s, part,
+                                                                                 n_parts, bcount);
+        CK(cudaGetLastError());
+        CK(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, bcount, boff, (int64_t)n_eblocks + 1, st));
+        unsigned long long n_p = 0;
+        CK(cudaMemsetAsync(bcount + n_eblocks, 0, sizeof(unsigned long long), st));
+        CK(cudaMemcpyAsync(&n_p, boff + n_eblocks, sizeof(n_p), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (n_p > cap) {
+            err = "index build: partition larger than its buffer";
+            free_device_index(&ix);
+            return 2;
+        }
+        ix.n_positions += n_p;
+        if (n_p == 0) continue;
+        write_part_kernel<<<static_cast<int>(n_eblocks), kEmitThreads, 0, st>>>(ix.planes, n_windows, s, part,
+                                                                                 n_parts, boff, k0, v0);
+        CK(cudaGetLastError());
+        // K1b: stable radix sort by (canon, strand)
+        cub::DoubleBuffer<unsigned long long> kb(k0, k1);
+        cub::DoubleBuffer<uint32_t> vb(v0, v1);
+        CK(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, kb, vb, (int64_t)n_p, 0, end_bit, st));
+        // K1c: runs of equal canonical keys (head flags / run ids in the spare buffers)
+        uint32_t* head = reinterpret_cast<uint32_t*>(kb.Alternate());
+        uint32_t* rid = vb.Alternate();
+        head_kernel<<<grid_for(n_p, 256), 256, 0, st>>>(kb.Current(), n_p, s, head);
+        CK(cudaGetLastError());
+        CK(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, head, rid, (int64_t)n_p, st));
+        uint32_t last_head = 0, last_rid = 0;
+        CK(cudaMemcpyAsync(&last_head, head + n_p - 1, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&last_rid, rid + n_p - 1, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        const uint64_t n_runs = static_cast<uint64_t>(last_rid) + last_head;
+        ix.n_keys += n_runs;
+        starts_kernel<<<grid_for(n_p, 256), 256, 0, st>>>(head, rid, n_p, run_start);
+        CK(cudaGetLastError());
+        {
+            const uint32_t nv = static_cast<uint32_t>(n_p);
+            CK(cudaMemcpyAsync(run_start + n_runs, &nv, 4, cudaMemcpyHostToDevice, st));
+        }
+        // pool offsets of this partition (head no longer needed: reuse as `need`)
+        unsigned long long* need = kb.Alternate();
+        pool_need_kernel<<<grid_for(n_runs, 256), 256, 0, st>>>(run_start, n_runs, need);
+        CK(cudaGetLastError());
+        CK(cudaMemsetAsync(need + n_runs, 0, sizeof(unsigned long long), st));
+        CK(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, need, pool_off, (int64_t)n_runs + 1, st));
+        unsigned long long part_pool = 0;
+        CK(cudaMemcpyAsync(&part_pool, pool_off + n_runs, 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (pool_used + part_pool >= 0xffffffffull) {
+            err = "position pool exceeds 2^32 entries";
+            free_device_index(&ix);
+            return 2;
+        }
+        if (pool_used + part_pool + 1 > pool_cap) {  // grow the pool
+            uint64_t ncap = std::max<uint64_t>(pool_cap * 2, pool_used + part_pool + (1 << 20));
+            uint32_t* np = nullptr;
+            CK(cudaMalloc(&np, ncap * sizeof(uint32_t)));
+            CK(cudaMemcpyAsync(np, ix.pool, pool_used * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+            CK(cudaStreamSynchronize(st));
+            cudaFree(ix.pool);
+            ix.pool = np;
+            pool_cap = ncap;
+        }
+        // K1d
+        insert_kernel<<<grid_for(n_runs, 128), 128, 0, st>>>(kb.Current(), vb.Current(), run_start, n_runs,
+                                                              pool_off, pool_used, ix.planes, s, ix.table,
+                                                              ix.n_slots, ix.pool, d_count);
+        CK(cudaGetLastError());
+        pool_used += part_pool;
+    }
+    CK(cudaMemcpyAsync(&ix.n_distinct, d_count, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    ix.pool_len = pool_used;
+    ix.device_bytes = ix.n_blocks * sizeof(uint4) + ix.n_slots * sizeof(Slot) + pool_cap * sizeof(uint32_t);
+    *out = ix;
+    return 0;
 }
 
 }  // namespace sab

@@ -266,3 +266,23 @@ def test_align_golden_gpu(case):
     for i, f in enumerate(api.REFERENCE_STAT_FIELDS):
         if f != "dp_cells":
             assert st[f] == exp[i], f
+
+
+@pytest.mark.parametrize("parts", [3, 17])
+def test_partitioned_index_build_identical(parts, monkeypatch):
+    """The key-hash-partitioned build (used automatically for 3.1 Gbp genomes)
+    yields the same index as the one-pass build: same lookups, same alignments."""
+    cfg, g, packed, nmask, bases, offs = _case("C2", 4_000_000, 8_000, 10, 0.01)
+    genome = api.PackedGenome(packed, nmask, g.size)
+    one = api.SeedIndex.build(genome, 20)
+    monkeypatch.setenv("SA_INDEX_PARTS", str(parts))
+    many = api.SeedIndex.build(genome, 20)
+    monkeypatch.delenv("SA_INDEX_PARTS")
+    assert (one.distinct_seeds(), one.total_positions()) == (many.distinct_seeds(), many.total_positions())
+    rng = np.random.default_rng(parts)
+    probes = [g[p:p + 20].tobytes().decode() for p in rng.integers(0, g.size - 20, 3000)]
+    a, b = one.lookup_batch(probes, cap=4096), many.lookup_batch(probes, cap=4096)
+    assert [(r.forward, r.rc) for r in a] == [(r.forward, r.rc) for r in b]
+    ra = api.Aligner(one, genome, cfg.params).align_arrays(bases, offs)
+    rb = api.Aligner(many, genome, cfg.params).align_arrays(bases, offs)
+    assert not O.compare_results(ra, rb)
