@@ -78,7 +78,8 @@ def _u64p(a):
 
 class _OrIndex(C.Structure):
     _fields_ = [("seed_size", C.c_int), ("n_keys", C.c_uint64), ("n_positions", C.c_uint64),
-                ("keys", C.c_void_p), ("offsets", C.c_void_p), ("positions", C.c_void_p)]
+                ("keys", C.c_void_p), ("offsets", C.c_void_p), ("positions", C.c_void_p),
+                ("n_queries", C.c_uint64), ("queries", C.c_void_p), ("misses", C.c_uint64)]
 
 
 class _OrGenome(C.Structure):
@@ -96,6 +97,8 @@ def olib():
         lib.or_packed_rc.argtypes = [C.c_uint64, C.c_int]
         lib.or_packed_rc.restype = C.c_uint64
         lib.or_index_build.argtypes = [C.POINTER(_OrGenome), C.c_int, C.POINTER(_OrIndex)]
+        lib.or_index_build_for_reads.argtypes = [C.POINTER(_OrGenome), C.c_int, C.c_int, C.c_void_p, P64,
+                                                 C.c_uint64, C.c_int, C.POINTER(_OrIndex)]
         lib.or_index_free.argtypes = [C.POINTER(_OrIndex)]
         lib.or_lookup.argtypes = [C.POINTER(_OrIndex), C.c_char_p, C.POINTER(C.c_void_p), P64,
                                   C.POINTER(C.c_void_p), P64]
@@ -186,16 +189,33 @@ def pack_genome(seq: bytes) -> tuple[np.ndarray, np.ndarray]:
 # ----------------------------------------------------------------- indexes
 
 class OracleIndex:
-    """C restatement: CSR index + Aligner::align."""
+    """C restatement: CSR index + Aligner::align.
 
-    def __init__(self, packed: np.ndarray, nmask: np.ndarray, length: int, s: int):
+    With `for_reads=(n_seeds, bases, offsets)` the index is restricted to the
+    keys those reads can probe (or_index_build_for_reads): the oracle for
+    3.1 Gbp genomes, where the full CSR would not fit this container.  Any
+    probe of another key is counted in `misses()`; align_arrays asserts 0.
+    """
+
+    def __init__(self, packed: np.ndarray, nmask: np.ndarray, length: int, s: int, for_reads=None,
+                 threads: int = 8):
         self.packed = np.ascontiguousarray(packed, np.uint64)
         self.nmask = np.ascontiguousarray(nmask, np.uint64)
         self.g = _OrGenome(length, self.packed.ctypes.data, self.nmask.ctypes.data)
         self.ix = _OrIndex()
-        rc = olib().or_index_build(C.byref(self.g), s, C.byref(self.ix))
+        if for_reads is None:
+            rc = olib().or_index_build(C.byref(self.g), s, C.byref(self.ix))
+        else:
+            n_seeds, bases, offsets = for_reads
+            offsets = np.ascontiguousarray(offsets, np.uint64)
+            b = np.ascontiguousarray(bases, np.uint8)
+            rc = olib().or_index_build_for_reads(C.byref(self.g), s, n_seeds, b.ctypes.data, _u64p(offsets),
+                                                 offsets.size - 1, threads, C.byref(self.ix))
         if rc:
-            raise ValueError(f"or_index_build failed ({rc})")
+            raise ValueError(f"oracle index build failed ({rc})")
+
+    def misses(self) -> int:
+        return int(self.ix.misses)
 
     def __del__(self):
         if _o is not None and getattr(self, "ix", None) is not None:
@@ -222,6 +242,8 @@ class OracleIndex:
                                    _u64p(offsets), n, res.ctypes.data, C.byref(st), threads)
         if rc:
             raise ValueError(f"or_align_batch failed ({rc})")
+        if self.ix.queries and self.ix.misses:
+            raise AssertionError(f"restricted oracle index probed {self.ix.misses} keys it was not built for")
         return res, st.as_dict()
 
 

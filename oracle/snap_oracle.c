@@ -234,7 +234,216 @@ int or_index_build(const or_genome* g, int seed_size, or_index* idx) {
     return 0;
 }
 
+/* ---- query-restricted build (test infrastructure for 3.1 Gbp configs) */
+
+static inline uint64_t mix_key(uint64_t x) {
+    x ^= x >> 33;
+    x *= 0xff51afd7ed558ccdull;
+    x ^= x >> 33;
+    x *= 0xc4ceb9fe1a85ec53ull;
+    return x ^ (x >> 33);
+}
+
+typedef struct {
+    const or_genome* g;
+    uint64_t s, mask, begin, end; /* windows [begin, end) */
+    const uint64_t* set;          /* open addressing, ~0 = empty */
+    uint64_t set_mask;
+    const uint64_t* filter;       /* 1 bit per hash bucket */
+    uint64_t filter_mask;
+    uint64_t* keys;               /* matches, grown as needed */
+    uint32_t* pos;
+    uint64_t n, cap;
+    int failed;
+} scan_job;
+
+static int set_contains(const uint64_t* set, uint64_t set_mask, uint64_t key) {
+    for (uint64_t h = mix_key(key) & set_mask;; h = (h + 1) & set_mask) {
+        if (set[h] == key) return 1;
+        if (set[h] == ~(uint64_t)0) return 0;
+    }
+}
+
+/* REF seed_index.cpp:96-110 rolling key, over windows [begin, end) only. */
+static void* scan_windows(void* arg) {
+    scan_job* j = (scan_job*)arg;
+    uint64_t key = 0;
+    int64_t last_n = -1;
+    const uint64_t from = j->begin;
+    const uint64_t to = j->end + j->s - 1; /* last base of the last window */
+    for (uint64_t p = from; p < to && p < j->g->len; ++p) {
+        int b = or_genome_at(j->g, p);
+        if (b == 4) {
+            last_n = (int64_t)p;
+            key = (key << 2) & j->mask;
+            continue;
+        }
+        key = ((key << 2) | (uint64_t)b) & j->mask;
+        if (p + 1 < from + j->s) continue;
+        uint64_t start = p + 1 - j->s;
+        if ((int64_t)start <= last_n) continue;
+        const uint64_t h = mix_key(key);
+        if (!((j->filter[(h >> 6) & j->filter_mask] >> (h & 63)) & 1)) continue;
+        if (!set_contains(j->set, j->set_mask, key)) continue;
+        if (j->n == j->cap) {
+            uint64_t nc = j->cap ? 2 * j->cap : 1 << 16;
+            uint64_t* nk = (uint64_t*)realloc(j->keys, nc * sizeof(uint64_t));
+            if (nk) j->keys = nk;
+            uint32_t* np = (uint32_t*)realloc(j->pos, nc * sizeof(uint32_t));
+            if (np) j->pos = np;
+            if (!nk || !np) {
+                j->failed = 1;
+                return NULL;
+            }
+            j->cap = nc;
+        }
+        j->keys[j->n] = key;
+        j->pos[j->n] = (uint32_t)start;
+        j->n++;
+    }
+    return NULL;
+}
+
+static int cmp_u64(const void* a, const void* b) {
+    uint64_t x = *(const uint64_t*)a, y = *(const uint64_t*)b;
+    return x < y ? -1 : x > y;
+}
+
+int or_index_build_for_reads(const or_genome* g, int seed_size, int n_seeds, const char* bases,
+                             const uint64_t* offsets, uint64_t n_reads, int threads, or_index* idx) {
+    memset(idx, 0, sizeof(*idx));
+    if (seed_size < 1 || seed_size > 32 || n_seeds < 1) return SA_EINVAL;
+    if (g->len < (uint64_t)seed_size || g->len > 0xffffffffull) return SA_EINVAL;
+    if (threads < 1) threads = 1;
+    idx->seed_size = seed_size;
+    const uint64_t s = (uint64_t)seed_size;
+
+    /* every key align() can probe (REF aligner.cpp:256-265, seed_index.cpp:128-143) */
+    uint64_t nq = 0, qcap = 1 << 12;
+    uint64_t* q = (uint64_t*)malloc(qcap * sizeof(uint64_t));
+    int* offs = (int*)malloc((size_t)n_seeds * sizeof(int));
+    if (!q || !offs) {
+        free(q); free(offs);
+        return SA_ERUNTIME;
+    }
+    for (uint64_t r = 0; r < n_reads; ++r) {
+        const uint64_t len = offsets[r + 1] - offsets[r];
+        const int k = or_seed_offsets(len, seed_size, n_seeds, offs);
+        for (int i = 0; i < k; ++i) {
+            uint64_t key;
+            if (!or_pack_seed(bases + offsets[r] + offs[i], seed_size, &key)) continue;
+            if (nq + 2 > qcap) {
+                qcap *= 2;
+                uint64_t* nq2 = (uint64_t*)realloc(q, qcap * sizeof(uint64_t));
+                if (!nq2) {
+                    free(q); free(offs);
+                    return SA_ERUNTIME;
+                }
+                q = nq2;
+            }
+            q[nq++] = key;
+            q[nq++] = or_packed_rc(key, seed_size);
+        }
+    }
+    free(offs);
+    qsort(q, nq, sizeof(uint64_t), cmp_u64);
+    uint64_t u = 0;
+    for (uint64_t i = 0; i < nq; ++i)
+        if (u == 0 || q[i] != q[u - 1]) q[u++] = q[i];
+    idx->queries = q;
+    idx->n_queries = u;
+
+    uint64_t set_size = 64;
+    while (set_size < 4 * u) set_size <<= 1;
+    uint64_t filter_words = 1024;
+    while (filter_words * 64 < 16 * u) filter_words <<= 1;
+    uint64_t* set = (uint64_t*)malloc(set_size * sizeof(uint64_t));
+    uint64_t* filter = (uint64_t*)calloc(filter_words, sizeof(uint64_t));
+    scan_job* jobs = (scan_job*)calloc((size_t)threads, sizeof(scan_job));
+    pthread_t* th = (pthread_t*)calloc((size_t)threads, sizeof(pthread_t));
+    if (!set || !filter || !jobs || !th) {
+        free(set); free(filter); free(jobs); free(th);
+        or_index_free(idx);
+        return SA_ERUNTIME;
+    }
+    memset(set, 0xff, set_size * sizeof(uint64_t));
+    for (uint64_t i = 0; i < u; ++i) {
+        const uint64_t h = mix_key(q[i]);
+        filter[(h >> 6) & (filter_words - 1)] |= (uint64_t)1 << (h & 63);
+        uint64_t at = h & (set_size - 1);
+        while (set[at] != ~(uint64_t)0) at = (at + 1) & (set_size - 1);
+        set[at] = q[i];
+    }
+
+    const uint64_t n_windows = g->len - s + 1;
+    for (int t = 0; t < threads; ++t) {
+        scan_job* j = &jobs[t];
+        j->g = g;
+        j->s = s;
+        j->mask = s == 32 ? ~(uint64_t)0 : (((uint64_t)1 << (2 * s)) - 1);
+        j->begin = n_windows * (uint64_t)t / (uint64_t)threads;
+        j->end = n_windows * (uint64_t)(t + 1) / (uint64_t)threads;
+        j->set = set;
+        j->set_mask = set_size - 1;
+        j->filter = filter;
+        j->filter_mask = filter_words - 1;
+        pthread_create(&th[t], NULL, scan_windows, j);
+    }
+    int failed = 0;
+    uint64_t n = 0;
+    for (int t = 0; t < threads; ++t) {
+        pthread_join(th[t], NULL);
+        failed |= jobs[t].failed;
+        n += jobs[t].n;
+    }
+    free(set); free(filter); free(th);
+    /* concatenated in chunk order = genome position order, then the same
+     * stable sort and CSR as or_index_build (REF seed_index.cpp:112-124) */
+    uint64_t* keys = (uint64_t*)malloc((n ? n : 1) * sizeof(uint64_t));
+    uint32_t* pos = (uint32_t*)malloc((n ? n : 1) * sizeof(uint32_t));
+    if (!failed && keys && pos) {
+        uint64_t at = 0;
+        for (int t = 0; t < threads; ++t) {
+            if (jobs[t].n) {
+                memcpy(keys + at, jobs[t].keys, jobs[t].n * sizeof(uint64_t));
+                memcpy(pos + at, jobs[t].pos, jobs[t].n * sizeof(uint32_t));
+            }
+            at += jobs[t].n;
+        }
+    }
+    for (int t = 0; t < threads; ++t) {
+        free(jobs[t].keys);
+        free(jobs[t].pos);
+    }
+    free(jobs);
+    if (failed || !keys || !pos || radix_sort_pairs(keys, pos, n, (int)(2 * s)) != 0) {
+        free(keys); free(pos);
+        or_index_free(idx);
+        return SA_ERUNTIME;
+    }
+    uint64_t nk = 0;
+    for (uint64_t i = 0; i < n; ++i)
+        if (i == 0 || keys[i] != keys[i - 1]) nk++;
+    idx->keys = (uint64_t*)malloc((nk ? nk : 1) * sizeof(uint64_t));
+    idx->offsets = (uint64_t*)malloc((nk + 1) * sizeof(uint64_t));
+    uint64_t j = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        if (i == 0 || keys[i] != keys[i - 1]) {
+            idx->keys[j] = keys[i];
+            idx->offsets[j] = i;
+            j++;
+        }
+    }
+    idx->offsets[nk] = n;
+    free(keys);
+    idx->positions = pos;
+    idx->n_keys = nk;
+    idx->n_positions = n;
+    return 0;
+}
+
 void or_index_free(or_index* idx) {
+    free(idx->queries);
     free(idx->keys);
     free(idx->offsets);
     free(idx->positions);
@@ -243,6 +452,16 @@ void or_index_free(or_index* idx) {
 
 /* std::lower_bound probe, REF seed_index.cpp:131-138. */
 static void probe(const or_index* idx, uint64_t key, const uint32_t** span, uint64_t* len) {
+    if (idx->queries) { /* restricted index: the key must be one it was built for */
+        uint64_t a = 0, b = idx->n_queries;
+        while (a < b) {
+            uint64_t mid = a + (b - a) / 2;
+            if (idx->queries[mid] < key) a = mid + 1;
+            else b = mid;
+        }
+        if (a == idx->n_queries || idx->queries[a] != key)
+            __atomic_fetch_add(&((or_index*)idx)->misses, 1, __ATOMIC_RELAXED);
+    }
     uint64_t lo = 0, hi = idx->n_keys;
     while (lo < hi) {
         uint64_t mid = lo + (hi - lo) / 2;

@@ -42,6 +42,12 @@ typedef struct or_index {
     uint64_t* keys;
     uint64_t* offsets;
     uint32_t* positions;
+    /* query-restricted index (or_index_build_for_reads): only the keys in
+     * `queries` (sorted) are indexed; probing any other key counts a miss,
+     * so a test can prove it never asked the restricted index an unknown key */
+    uint64_t n_queries;
+    uint64_t* queries;
+    uint64_t misses;
 } or_index;
 
 int or_char_to_code(char c); /* 0..3 for ACGT (any case), 4 for IUPAC N-class, -1 illegal */
@@ -57,6 +63,13 @@ uint64_t or_packed_rc(uint64_t key, int s);
 
 int or_index_build(const or_genome* g, int seed_size, or_index* out); /* 0 ok */
 void or_index_free(or_index* idx);
+/* The same CSR restricted to every key a batch of reads can probe: the
+ * packed key and packed RC of each N-free seed at seed_offsets(len, s,
+ * n_seeds) of each read.  One threaded scan of the genome's windows collects
+ * their positions, so 3.1 Gbp genomes index in seconds and little memory;
+ * for those keys, lookup() answers exactly what or_index_build's would. */
+int or_index_build_for_reads(const or_genome* g, int seed_size, int n_seeds, const char* bases,
+                             const uint64_t* offsets, uint64_t n_reads, int threads, or_index* out);
 /* REF seed_index.cpp:128-143: forward span and rc span into idx->positions. */
 int or_lookup(const or_index* idx, const char* seed, const uint32_t** fwd, uint64_t* n_fwd,
               const uint32_t** rc, uint64_t* n_rc);

@@ -5,6 +5,11 @@ in full (1,000,000 reads, 100 Mbp).  C4 uses its full 500 Mbp genome with a
 sample of its 10 kbp reads.  Size-independent properties (determinism, batch
 chunking invariance, device-resident == host path, strand symmetry,
 force_max_dlimit invariance, multi-replica dealing) run at full C1 size.
+C2 builds its full 3.1 Gbp repeat genome index on the GPU (partitioned build)
+and aligns all 10 M reads; the first 1 M are checked read-for-read against the
+oracle, which at this size indexes only the keys those reads probe
+(OracleIndex(for_reads=...), itself proven equal to the full CSR in
+tests/test_oracle.py).  C3 reuses that genome with a 50 k-read sample.
 """
 import numpy as np
 import pytest
@@ -139,6 +144,66 @@ def test_c4_full_genome_sampled_reads():
     al = api.Aligner(api.SeedIndex.build(genome, 22), genome, cfg.params)
     got = al.align_arrays(bases, offs)
     oi = O.OracleIndex(packed, nmask, g.size, 22)
+    want, wst = oi.align_arrays(cfg.params, bases, offs, threads=16)
+    assert O.compare_results(got, want) == []
+    for f in api.REFERENCE_STAT_FIELDS:
+        if f != "dp_cells":
+            assert al.stats().values[f] == wst[f], f
+
+
+# ---------------------------------------------------------------- C2 / C3: the 3.1 Gbp repeat genome
+
+@pytest.fixture(scope="module")
+def c2_genome():
+    cfg = synth.CONFIGS["C2"]
+    g = synth.make_genome(cfg)
+    packed, nmask = synth.pack_genome(g)
+    genome = api.PackedGenome(packed, nmask, g.size)
+    idx = api.SeedIndex.build(genome, 20)  # key-hash-partitioned GPU build
+    yield dict(g=g, packed=packed, nmask=nmask, genome=genome, idx=idx)
+    del idx
+
+
+def test_c2_index_shape(c2_genome):
+    idx = c2_genome["idx"]
+    assert idx.total_positions() == c2_genome["g"].size - 20 + 1  # N-free genome: every window
+    assert 0 < idx.distinct_seeds() < idx.total_positions()
+
+
+def test_c2_full_reads_vs_oracle(c2_genome):
+    """All 10,000,000 C2 reads on the GPU; the first 1,000,000 checked
+    read-for-read against the oracle (restricted to the keys they probe)."""
+    cfg = synth.CONFIGS["C2"]
+    bases, offs, tpos, tdir = synth.make_reads(cfg, c2_genome["g"])
+    al = api.Aligner(c2_genome["idx"], c2_genome["genome"], cfg.params)
+    got = al.align_arrays(bases, offs)
+    assert got.size == 10_000_000
+    n = 1_000_000
+    sb, so = bases[:int(offs[n])], offs[:n + 1]
+    oi = O.OracleIndex(c2_genome["packed"], c2_genome["nmask"], c2_genome["g"].size, 20,
+                       for_reads=(cfg.params.seeds_to_try, sb, so), threads=16)
+    want, wst = oi.align_arrays(cfg.params, sb, so, threads=16)
+    assert O.compare_results(got[:n], want) == []
+    al1 = api.Aligner(c2_genome["idx"], c2_genome["genome"], cfg.params)
+    again = al1.align_arrays(sb, so)
+    assert O.compare_results(again, want) == []
+    for f in api.REFERENCE_STAT_FIELDS:
+        if f != "dp_cells":
+            assert al1.stats().values[f] == wst[f], f
+    # size-independent: accuracy against the simulator's truth on unique hits
+    single = got["kind"] == api.ResultKind.SingleHit
+    assert single.mean() > 0.95
+    near = np.abs(got["position"][single].astype(np.int64) - tpos[single].astype(np.int64)) <= 32
+    assert near.mean() > 0.99
+
+
+def test_c3_sampled_reads_vs_oracle(c2_genome):
+    cfg = synth.CONFIGS["C3"].scaled(n_reads=50_000)
+    bases, offs, _, _ = synth.make_reads(cfg, c2_genome["g"])
+    al = api.Aligner(c2_genome["idx"], c2_genome["genome"], cfg.params)
+    got = al.align_arrays(bases, offs)
+    oi = O.OracleIndex(c2_genome["packed"], c2_genome["nmask"], c2_genome["g"].size, 20,
+                       for_reads=(cfg.params.seeds_to_try, bases, offs), threads=16)
     want, wst = oi.align_arrays(cfg.params, bases, offs, threads=16)
     assert O.compare_results(got, want) == []
     for f in api.REFERENCE_STAT_FIELDS:
