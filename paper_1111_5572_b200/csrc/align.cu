@@ -918,7 +918,7 @@ __global__ void __launch_bounds__(256, SA_MIN_BLOCKS) align_kernel(const AlignLa
             if (lane == 0) atomicOr(a.error_flag, 2u);
         } else if (lane == 0) {  // defer to the global-table kernel
             const unsigned slot = atomicAdd(a.overflow_count, 1u);
-            a.overflow_list[slot] = r;
+            a.overflow_list[slot] = static_cast<unsigned>(a.read_base) + r;  // batch-absolute id
             wst[S_OVERFLOW] += 1;
         }
     };
@@ -1019,7 +1019,7 @@ __global__ void __launch_bounds__(256, SA_MIN_BLOCKS) align_kernel(const AlignLa
             if (lane == 0) r = atomicAdd(a.cursor, 1u);
             r = __shfl_sync(FULL, r, 0);
             if (r >= n_work) break;
-            if (kSlow) r = a.work_list[r];
+            if (kSlow && a.work_list) r = a.work_list[r];  // no list: every read of the launch
             const uint64_t o0 = a.offsets[r], o1 = a.offsets[r + 1];
             const int len = static_cast<int>(o1 - o0);
             const uintptr_t addr = reinterpret_cast<uintptr_t>(a.bases + (o0 - a.base_off));

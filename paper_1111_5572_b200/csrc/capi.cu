@@ -30,7 +30,16 @@ namespace {
 thread_local std::string g_thread_err;
 
 constexpr int kCtlWords = 4;  // cursor_fast, cursor_slow, overflow_count, error_flag
-constexpr uint64_t kChunkReads = 1u << 18;
+constexpr uint64_t kChunkReads = 1u << 17;  // default; SA_CHUNK_READS overrides (tuning)
+
+uint64_t chunk_reads_setting() {
+    static const uint64_t v = [] {
+        const char* e = getenv("SA_CHUNK_READS");
+        const long long x = e ? atoll(e) : 0;
+        return x >= 1024 ? static_cast<uint64_t>(x) : kChunkReads;
+    }();
+    return v;
+}
 constexpr uint64_t kChunkBytes = 256ull << 20;
 constexpr int kFastCap = 64, kFastHcap = 128;
 constexpr uint64_t kSlowScratchBudget = 2ull << 30;
@@ -58,6 +67,16 @@ cudaError_t stage_times(Stage& s, float& fast_ms, float& slow_ms) {
     return cudaSuccess;
 }
 
+struct LaunchShape {
+    AlignLaunch proto;  // layout + params fields filled
+    int fast_block, fast_grid;
+    int slow_block, slow_grid;
+    uint32_t slow_smem_per_warp;
+    uint64_t slow_table_bytes;
+    uint64_t scratch_bytes;  // global candidate tables of the overflow path
+    int slow_cap, slow_hcap;
+};
+
 struct Replica {
     int device = 0;
     int sm_count = 148;
@@ -70,16 +89,21 @@ struct Replica {
     uint64_t gscratch_bytes = 0;
     uint32_t smem_attr = 0;
     cudaEvent_t e_start = nullptr, e_end = nullptr, e_join = nullptr;
+    // batch-wide list of reads that overflowed the fast kernel's shared table
+    // (absolute read ids), redone by one global-table pass at the end
+    unsigned int* d_defer = nullptr;
+    unsigned int* d_defer_count = nullptr;
+    uint64_t defer_cap = 0;
+    // launch layouts already derived for (params, longest read): make_shape
+    // queries occupancy and free memory, too slow to repeat per call
+    struct ShapeEntry {
+        sa_params p;
+        uint64_t L;
+        LaunchShape sh;
+    };
+    std::vector<ShapeEntry> shapes;
 };
 
-struct LaunchShape {
-    AlignLaunch proto;  // layout + params fields filled
-    int fast_block, fast_grid;
-    int slow_block, slow_grid;
-    uint32_t slow_smem_per_warp;
-    uint64_t slow_table_bytes;
-    int slow_cap, slow_hcap;
-};
 
 }  // namespace
 
@@ -193,7 +217,20 @@ int make_shape(Replica& rep, const sa_params* p, uint64_t Lmax, LaunchShape& sh,
     sh.slow_block = 32;
     sh.slow_grid = static_cast<int>(slow_warps);
     a.gscratch_per_warp = sh.slow_table_bytes;
+    sh.scratch_bytes = slow_warps * sh.slow_table_bytes;
     // the slow launch overrides cap/hcap/smem_per_warp
+    return SA_OK;
+}
+
+int cached_shape(Replica& rep, const sa_params* p, uint64_t Lmax, LaunchShape& sh, std::string& why) {
+    for (const auto& e : rep.shapes)
+        if (e.L == Lmax && std::memcmp(&e.p, p, sizeof(sa_params)) == 0) {
+            sh = e.sh;
+            return SA_OK;
+        }
+    if (int rc = make_shape(rep, p, Lmax, sh, why)) return rc;
+    if (rep.shapes.size() >= 32) rep.shapes.erase(rep.shapes.begin());
+    rep.shapes.push_back({*p, Lmax, sh});
     return SA_OK;
 }
 
@@ -229,7 +266,7 @@ int ensure_stage(sa_context* ctx, Stage& s, uint64_t bytes, uint64_t reads) {
 }
 
 int ensure_scratch(sa_context* ctx, Replica& rep, const LaunchShape& sh) {
-    uint64_t need = static_cast<uint64_t>(sh.slow_grid) * sh.slow_table_bytes;
+    const uint64_t need = sh.scratch_bytes;
     if (need > rep.gscratch_bytes) {
         if (rep.d_gscratch) cudaFree(rep.d_gscratch);
         rep.d_gscratch = nullptr;
@@ -246,7 +283,7 @@ int enqueue_align(sa_context* ctx, Replica& rep, Stage& stg, const LaunchShape& 
                   const char* d_bases, const uint64_t* d_offsets, uint64_t base_off,
                   uint64_t n_reads, uint64_t read_base, sa_result* d_results,
                   unsigned long long* d_stats, unsigned int* d_overflow, bool time_it,
-                  uint64_t& launches) {
+                  uint64_t& launches, unsigned int* d_defer_count = nullptr) {
     AlignLaunch a = sh.proto;
     a.bases = d_bases;
     a.offsets = d_offsets;
@@ -257,6 +294,7 @@ int enqueue_align(sa_context* ctx, Replica& rep, Stage& stg, const LaunchShape& 
     a.cursor = stg.d_ctl + 0;
     a.overflow_count = stg.d_ctl + 2;
     a.overflow_list = d_overflow;
+    if (d_defer_count) a.overflow_count = d_defer_count;  // batch-wide list, drained at the end
     a.error_flag = rep.d_err;
     a.error_read = rep.d_err_read;
     a.read_base = read_base;
@@ -266,6 +304,11 @@ int enqueue_align(sa_context* ctx, Replica& rep, Stage& stg, const LaunchShape& 
     launch_align_fast(a, sh.fast_grid, sh.fast_block, stg.st);
     CUDA_TRY(ctx, cudaGetLastError());
     if (time_it) CUDA_TRY(ctx, cudaEventRecord(stg.km, stg.st));
+    launches += 1;
+    if (d_defer_count) {  // overflowing reads handled by the end-of-batch pass
+        if (time_it) CUDA_TRY(ctx, cudaEventRecord(stg.k1, stg.st));
+        return SA_OK;
+    }
     AlignLaunch b = a;
     b.cursor = stg.d_ctl + 1;
     b.work_list = d_overflow;
@@ -280,7 +323,7 @@ int enqueue_align(sa_context* ctx, Replica& rep, Stage& stg, const LaunchShape& 
     launch_align_slow(b, sh.slow_grid, sh.slow_block, stg.st);
     CUDA_TRY(ctx, cudaGetLastError());
     if (time_it) CUDA_TRY(ctx, cudaEventRecord(stg.k1, stg.st));
-    launches += 2;
+    launches += 1;
     return SA_OK;
 }
 
@@ -301,6 +344,75 @@ int check_errors(sa_context* ctx, Replica& rep) {
                                         std::to_string(first) +
                                         " holds a character outside {A,C,G,T,N})");
     }
+    return SA_OK;
+}
+
+int ensure_defer(sa_context* ctx, Replica& rep, uint64_t n) {
+    if (!rep.d_defer_count) CUDA_TRY(ctx, cudaMalloc(&rep.d_defer_count, sizeof(unsigned int)));
+    if (n > rep.defer_cap) {
+        if (rep.d_defer) cudaFree(rep.d_defer);
+        rep.d_defer = nullptr;
+        const uint64_t c = std::max<uint64_t>(n, 1 << 16);
+        CUDA_TRY(ctx, cudaMalloc(&rep.d_defer, c * sizeof(unsigned int)));
+        rep.defer_cap = c;
+    }
+    return SA_OK;
+}
+
+// End-of-batch overflow pass: the reads whose candidates overflowed the fast
+// kernel's shared table (their ids collected batch-wide, nothing committed for
+// them) are gathered on the host, copied once, aligned by the global-table
+// kernel and scattered into results.  Keeping this out of the chunk pipeline
+// means no kernel ever queues behind the persistent fast kernel of the next
+// chunk.  Returns the number of reads redone.
+int overflow_pass(sa_context* ctx, Replica& rep, Stage& stg, const LaunchShape& sh, const char* bases,
+                  const uint64_t* offsets, sa_result* results, uint64_t& launches, uint64_t& n_done) {
+    unsigned int n = 0;
+    n_done = 0;
+    CUDA_TRY(ctx, cudaMemcpyAsync(&n, rep.d_defer_count, sizeof(n), cudaMemcpyDeviceToHost, stg.st));
+    CUDA_TRY(ctx, cudaStreamSynchronize(stg.st));
+    if (n == 0) return SA_OK;
+    std::vector<unsigned int> ids(n);
+    CUDA_TRY(ctx, cudaMemcpy(ids.data(), rep.d_defer, n * sizeof(unsigned int), cudaMemcpyDeviceToHost));
+    std::vector<uint64_t> offs(n + 1, 0);
+    for (unsigned i = 0; i < n; ++i) offs[i + 1] = offs[i] + (offsets[ids[i] + 1] - offsets[ids[i]]);
+    std::vector<char> buf(offs[n]);
+    for (unsigned i = 0; i < n; ++i)
+        std::memcpy(buf.data() + offs[i], bases + offsets[ids[i]], offs[i + 1] - offs[i]);
+    if (int rc = ensure_stage(ctx, stg, offs[n], n)) return rc;
+    CUDA_TRY(ctx, cudaMemcpyAsync(stg.d_bases, buf.data(), offs[n], cudaMemcpyHostToDevice, stg.st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(stg.d_offsets, offs.data(), (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                                  stg.st));
+    CUDA_TRY(ctx, cudaMemsetAsync(stg.d_ctl, 0, kCtlWords * sizeof(unsigned int), stg.st));
+    AlignLaunch b = sh.proto;
+    b.bases = stg.d_bases;
+    b.offsets = stg.d_offsets;
+    b.base_off = 0;
+    b.n_reads = n;
+    b.results = stg.d_results;
+    b.stats = rep.d_stats;
+    b.cursor = stg.d_ctl + 1;
+    b.work_list = nullptr;  // every read of this launch
+    b.work_count = rep.d_defer_count;  // == n
+    b.overflow_list = nullptr;
+    b.overflow_count = nullptr;
+    b.error_flag = rep.d_err;
+    b.error_read = rep.d_err_read;
+    b.read_base = 0;
+    b.gscratch = rep.d_gscratch;
+    b.cap = sh.slow_cap;
+    b.hcap = sh.slow_hcap;
+    b.smem_per_warp = sh.slow_smem_per_warp;
+    b.sbw = 0;
+    b.prefetch = 0;
+    launch_align_slow(b, sh.slow_grid, sh.slow_block, stg.st);
+    CUDA_TRY(ctx, cudaGetLastError());
+    ++launches;
+    std::vector<sa_result> out(n);
+    CUDA_TRY(ctx, cudaMemcpyAsync(out.data(), stg.d_results, n * sizeof(sa_result), cudaMemcpyDeviceToHost, stg.st));
+    CUDA_TRY(ctx, cudaStreamSynchronize(stg.st));
+    for (unsigned i = 0; i < n; ++i) results[ids[i]] = out[i];
+    n_done = n;
     return SA_OK;
 }
 
@@ -454,6 +566,8 @@ void sa_destroy(sa_context* ctx) {
         if (rep.d_err) cudaFree(rep.d_err);
         if (rep.d_err_read) cudaFree(rep.d_err_read);
         if (rep.d_gscratch) cudaFree(rep.d_gscratch);
+        if (rep.d_defer) cudaFree(rep.d_defer);
+        if (rep.d_defer_count) cudaFree(rep.d_defer_count);
         if (rep.e_start) cudaEventDestroy(rep.e_start);
         if (rep.e_end) cudaEventDestroy(rep.e_end);
         if (rep.e_join) cudaEventDestroy(rep.e_join);
@@ -487,16 +601,18 @@ int sa_align_batch(sa_context* ctx, const sa_params* params, const char* bases,
     }
     if (!bases || !offsets || !results) return fail(ctx, SA_EINVAL, "null buffer");
     if (n_reads >= 0xffffffffull) return fail(ctx, SA_EINVAL, "too many reads in one batch");
-    uint64_t Lmax = 0;
-    for (uint64_t i = 0; i < n_reads; ++i) {
-        if (offsets[i + 1] < offsets[i]) return fail(ctx, SA_EINVAL, "offsets not ascending");
-        Lmax = std::max(Lmax, offsets[i + 1] - offsets[i]);
-    }
-    // chunk boundaries (reads and bytes bounded)
+    // chunk boundaries (reads and bytes bounded).  Offsets are validated per
+    // chunk inside the pipeline, so the host scan overlaps the GPU's work on
+    // the previous chunk; a bad chunk stops the batch before it is enqueued.
+    // Chunk sizes ramp up (16 k, 32 k, ... reads) so the first kernel starts
+    // after a short copy; the GPU is busy with chunk k while chunk k+1 copies.
+    const uint64_t chunk_reads = chunk_reads_setting();
     std::vector<uint64_t> bounds{0};
+    uint64_t step = std::min<uint64_t>(chunk_reads, 1u << 14);
     while (bounds.back() < n_reads) {
         uint64_t b = bounds.back();
-        uint64_t e = std::min(n_reads, b + kChunkReads);
+        uint64_t e = std::min(n_reads, b + step);
+        step = std::min(chunk_reads, 2 * step);
         while (e > b + 1 && offsets[e] - offsets[b] > kChunkBytes) e = b + (e - b) / 2;
         bounds.push_back(e);
     }
@@ -514,42 +630,80 @@ int sa_align_batch(sa_context* ctx, const sa_params* params, const char* bases,
         auto run = [&]() -> int {
             if (cudaSetDevice(rep.device) != cudaSuccess) return fail(&local_err, SA_ERUNTIME, "cudaSetDevice");
             LaunchShape sh;
-            std::string w;
-            if (int rc = make_shape(rep, params, Lmax, sh, w)) return fail(&local_err, rc, w);
-            if (int rc = ensure_scratch(&local_err, rep, sh)) return rc;
-            uint64_t max_bytes = 0, max_reads = 0;
-            for (size_t c = 0; c < n_chunks; ++c) {
-                max_reads = std::max(max_reads, bounds[c + 1] - bounds[c]);
-                max_bytes = std::max(max_bytes, offsets[bounds[c + 1]] - offsets[bounds[c]]);
-            }
-            for (int k = 0; k < 2; ++k)
-                if (int rc = ensure_stage(&local_err, rep.stage[k], max_bytes, max_reads)) return rc;
-            CUDA_TRY(&local_err, cudaMemsetAsync(rep.d_stats, 0, kNumStats * sizeof(unsigned long long), rep.stage[0].st));
-            CUDA_TRY(&local_err, cudaEventRecord(rep.e_start, rep.stage[0].st));
-            CUDA_TRY(&local_err, cudaStreamWaitEvent(rep.stage[1].st, rep.e_start, 0));
-            int k = 0;
+            uint64_t shape_L = 0;
+            int k = 0, bad = SA_OK;
+            // SA_OVERFLOW_KERNEL (test hook): overflow kernel after every chunk
+            const bool defer = getenv("SA_OVERFLOW_KERNEL") == nullptr;
             for (;;) {
                 size_t c = next.fetch_add(1);
                 if (c >= n_chunks) break;
+                const uint64_t r0 = bounds[c], r1 = bounds[c + 1];
+                uint64_t Lc = 0;
+                for (uint64_t i = r0; i < r1; ++i) {
+                    if (offsets[i + 1] < offsets[i]) {
+                        bad = fail(&local_err, SA_EINVAL, "offsets not ascending");
+                        break;
+                    }
+                    Lc = std::max(Lc, offsets[i + 1] - offsets[i]);
+                }
+                if (bad) break;
+                if (k == 0 || Lc > shape_L) {  // launch layout for the longest read so far
+                    std::string w;
+                    if ((bad = cached_shape(rep, params, std::max(Lc, shape_L), sh, w))) {
+                        fail(&local_err, bad, w);
+                        break;
+                    }
+                    shape_L = std::max(Lc, shape_L);
+                    if ((bad = ensure_scratch(&local_err, rep, sh))) break;
+                }
+                const uint64_t b0 = offsets[r0], b1 = offsets[r1];
                 Stage& stg = rep.stage[k & 1];
+                if ((bad = ensure_stage(&local_err, stg, b1 - b0, r1 - r0))) break;
+                if (k < 2) {
+                    if (k == 0) {
+                        if (defer && (bad = ensure_defer(&local_err, rep, n_reads))) break;
+                        if (defer)
+                            CUDA_TRY(&local_err, cudaMemsetAsync(rep.d_defer_count, 0, sizeof(unsigned int),
+                                                                 rep.stage[0].st));
+                        CUDA_TRY(&local_err, cudaMemsetAsync(rep.d_stats, 0, kNumStats * sizeof(unsigned long long),
+                                                             rep.stage[0].st));
+                        CUDA_TRY(&local_err, cudaEventRecord(rep.e_start, rep.stage[0].st));
+                    } else {
+                        CUDA_TRY(&local_err, cudaStreamWaitEvent(stg.st, rep.e_start, 0));
+                    }
+                }
                 // stage reuse: collect the kernel events of its previous chunk
                 if (k >= 2) CUDA_TRY(&local_err, stage_times(stg, kms[ri], kslow[ri]));
-                const uint64_t r0 = bounds[c], r1 = bounds[c + 1];
-                const uint64_t b0 = offsets[r0], b1 = offsets[r1];
                 CUDA_TRY(&local_err, cudaMemcpyAsync(stg.d_bases, bases + b0, b1 - b0, cudaMemcpyHostToDevice, stg.st));
                 CUDA_TRY(&local_err, cudaMemcpyAsync(stg.d_offsets, offsets + r0, (r1 - r0 + 1) * sizeof(uint64_t),
                                                      cudaMemcpyHostToDevice, stg.st));
-                if (int rc = enqueue_align(&local_err, rep, stg, sh, stg.d_bases, stg.d_offsets, b0, r1 - r0,
-                                           r0, stg.d_results, rep.d_stats, stg.d_overflow, true, launches[ri]))
+                if (int rc = enqueue_align(&local_err, rep, stg, sh, stg.d_bases, stg.d_offsets, b0, r1 - r0, r0,
+                                           stg.d_results, rep.d_stats, defer ? rep.d_defer : stg.d_overflow, true,
+                                           launches[ri], defer ? rep.d_defer_count : nullptr))
                     return rc;
                 CUDA_TRY(&local_err, cudaMemcpyAsync(results + r0, stg.d_results, (r1 - r0) * sizeof(sa_result),
                                                      cudaMemcpyDeviceToHost, stg.st));
                 ++k;
             }
+            if (bad || k == 0) {  // drain whatever was enqueued before returning
+                for (int j = 0; j < 2; ++j)
+                    if (rep.stage[j].st) cudaStreamSynchronize(rep.stage[j].st);
+                std::memset(&part[ri], 0, sizeof(sa_stats));
+                return bad;
+            }
+            if (k == 1) {  // stage[1] never joined: let the end event cover stage[0] only
+                CUDA_TRY(&local_err, cudaEventRecord(rep.e_join, rep.stage[0].st));
+            }
             for (int j = 0; j < 2 && j < k; ++j)
                 CUDA_TRY(&local_err, stage_times(rep.stage[(k - 1 - j) & 1], kms[ri], kslow[ri]));
-            CUDA_TRY(&local_err, cudaEventRecord(rep.e_join, rep.stage[1].st));
+            if (k >= 2) CUDA_TRY(&local_err, cudaEventRecord(rep.e_join, rep.stage[1].st));
             CUDA_TRY(&local_err, cudaStreamWaitEvent(rep.stage[0].st, rep.e_join, 0));
+            if (defer) {
+                uint64_t redone = 0;
+                if (int rc = overflow_pass(&local_err, rep, rep.stage[0], sh, bases, offsets, results, launches[ri],
+                                           redone))
+                    return rc;
+            }
             CUDA_TRY(&local_err, cudaEventRecord(rep.e_end, rep.stage[0].st));
             CUDA_TRY(&local_err, cudaEventSynchronize(rep.e_end));
             cudaEventElapsedTime(&e2e[ri], rep.e_start, rep.e_end);
@@ -602,7 +756,7 @@ int sa_align_device(sa_context* ctx, const sa_params* params, const char* d_base
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (max_read_length == 0) return fail(ctx, SA_EINVAL, "max_read_length must be given");
     LaunchShape sh;
-    if (int rc = make_shape(rep, params, max_read_length, sh, why)) return fail(ctx, rc, why);
+    if (int rc = cached_shape(rep, params, max_read_length, sh, why)) return fail(ctx, rc, why);
     if (int rc = ensure_scratch(ctx, rep, sh)) return rc;
     Stage& stg = rep.stage[2];
     if (int rc = ensure_stage(ctx, stg, 0, n_reads)) return rc;

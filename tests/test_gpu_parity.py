@@ -286,3 +286,20 @@ def test_partitioned_index_build_identical(parts, monkeypatch):
     ra = api.Aligner(one, genome, cfg.params).align_arrays(bases, offs)
     rb = api.Aligner(many, genome, cfg.params).align_arrays(bases, offs)
     assert not O.compare_results(ra, rb)
+
+
+@pytest.mark.parametrize("mode", ["deferred", "kernel"])
+def test_overflow_paths_parity(mode, monkeypatch):
+    """Reads with more candidates than the 64-entry shared table: collected
+    batch-wide and redone by one global-table pass at the end of the batch
+    (default), or by a global-table kernel after every chunk
+    (SA_OVERFLOW_KERNEL) -- same results, same stats."""
+    if mode == "kernel":
+        monkeypatch.setenv("SA_OVERFLOW_KERNEL", "1")
+    g = synth.make_repeat_genome(5, 2_000_000, 60, min_len=200, max_len=1500, min_copies=20, max_copies=150,
+                                 min_div=0.0, max_div=0.04)
+    packed, nmask = synth.pack_genome(g)
+    cfg = synth.CONFIGS["C3"].scaled(genome_len=g.size, n_reads=1500)
+    bases, offs, _, _ = synth.make_reads(cfg, g)
+    _, st = _gpu_vs_oracle(cfg, g, packed, nmask, bases, offs)
+    assert st["overflow_reads"] > 0
