@@ -143,8 +143,19 @@ SA_DEV int lv_warp_smem(const uint4* R, int m, const uint4* W, uint32_t wofs, in
     return -1;
 }
 
+// kRegLV: every d_limit of the launch is <= 15 (register wavefront only);
+// otherwise the shared-memory wavefront serves every limit.  One variant per
+// kernel keeps the inlined code small.
+template <bool kRegLV>
 SA_DEV int lv_warp(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, int dl, int* F,
                    int lane, uint32_t& cells) {
+    if (kRegLV) return lv_warp_reg(R, m, W, wofs, w, dl, lane, cells);
+    return lv_warp_smem(R, m, W, wofs, w, dl, F, lane, cells);
+}
+
+// standalone LV (lv_batch_kernel): any limit
+SA_DEV int lv_warp_any(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, int dl, int* F,
+                       int lane, uint32_t& cells) {
     if (dl <= 15) return lv_warp_reg(R, m, W, wofs, w, dl, lane, cells);
     return lv_warp_smem(R, m, W, wofs, w, dl, F, lane, cells);
 }
@@ -420,6 +431,7 @@ SA_DEV bool insert_wave(Ctx& x, bool valid, unsigned long long key, int bit) {
 }
 
 // REF aligner.cpp:169-221 score_candidate
+template <bool kRegLV>
 SA_DEV void score_candidate(Ctx& x, uint32_t idx) {
     const AlignLaunch& a = *x.a;
     const int lane = x.lane;
@@ -463,7 +475,7 @@ SA_DEV void score_candidate(Ctx& x, uint32_t idx) {
         const uint64_t want = static_cast<uint64_t>(x.len) + static_cast<uint64_t>(d_limit);
         const int w = static_cast<int>(want < rem ? want : rem);
         const uint32_t wofs = static_cast<uint32_t>(anchor - gb0 * 32);
-        const int d = lv_warp(orient, x.len, x.W, wofs, w, d_limit, x.F, lane, x.cells);
+        const int d = lv_warp<kRegLV>(orient, x.len, x.W, wofs, w, d_limit, x.F, lane, x.cells);
         x.st.dist_calls++;
         x.calls++;
         x.st.window_bases += static_cast<uint32_t>(w);
@@ -489,41 +501,42 @@ SA_DEV void score_candidate(Ctx& x, uint32_t idx) {
 
 // REF aligner.cpp:141-167 score_best_candidate: unscored candidate with most
 // seeds hitting, then smallest anchor, then Forward.
+template <bool kRegLV>
 SA_DEV void score_best(Ctx& x) {
     if (x.n_unscored == 0) return;
-    if (x.n_cands == 1) {  // the only candidate is the unscored one
-        score_candidate(x, 0);
-        return;
-    }
-    const AlignLaunch& a = *x.a;
-    uint32_t bc = 0;
-    unsigned long long bk = ~0ull;
-    int bi = -1;
-    for (uint32_t j = x.lane; j < x.n_cands; j += 32) {
-        const uint32_t cc = x.t.ccnt[j];
-        if (cc & kScored) continue;
-        const unsigned long long kk = x.t.ckey[j];
-        const unsigned long long mm = x.t.cmask[j];
-        const unsigned long long amin = (kk >> 1) * static_cast<unsigned long long>(a.bs) +
-                                        static_cast<unsigned long long>(__ffsll(static_cast<long long>(mm)) - 1);
-        const unsigned long long ord = (amin << 1) | (kk & 1ull);
-        if (cc > bc || (cc == bc && ord < bk)) {
-            bc = cc;
-            bk = ord;
-            bi = static_cast<int>(j);
+    int bi = 0;
+    if (x.n_cands > 1) {  // otherwise the only candidate is the unscored one
+        const AlignLaunch& a = *x.a;
+        uint32_t bc = 0;
+        unsigned long long bk = ~0ull;
+        bi = -1;
+        for (uint32_t j = x.lane; j < x.n_cands; j += 32) {
+            const uint32_t cc = x.t.ccnt[j];
+            if (cc & kScored) continue;
+            const unsigned long long kk = x.t.ckey[j];
+            const unsigned long long mm = x.t.cmask[j];
+            const unsigned long long amin = (kk >> 1) * static_cast<unsigned long long>(a.bs) +
+                                            static_cast<unsigned long long>(__ffsll(static_cast<long long>(mm)) - 1);
+            const unsigned long long ord = (amin << 1) | (kk & 1ull);
+            if (cc > bc || (cc == bc && ord < bk)) {
+                bc = cc;
+                bk = ord;
+                bi = static_cast<int>(j);
+            }
         }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        const uint32_t oc = __shfl_xor_sync(FULL, bc, o);
-        const unsigned long long ok = __shfl_xor_sync(FULL, bk, o);
-        const int oi = __shfl_xor_sync(FULL, bi, o);
-        if (oc > bc || (oc == bc && ok < bk)) {
-            bc = oc;
-            bk = ok;
-            bi = oi;
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint32_t oc = __shfl_xor_sync(FULL, bc, o);
+            const unsigned long long ok = __shfl_xor_sync(FULL, bk, o);
+            const int oi = __shfl_xor_sync(FULL, bi, o);
+            if (oc > bc || (oc == bc && ok < bk)) {
+                bc = oc;
+                bk = ok;
+                bi = oi;
+            }
         }
+        if (bi < 0) return;
     }
-    if (bi >= 0) score_candidate(x, static_cast<uint32_t>(bi));
+    score_candidate<kRegLV>(x, static_cast<uint32_t>(bi));
 }
 
 SA_DEV void clear_table(CandTable& t, uint32_t n_cands, bool full, int lane) {
@@ -654,7 +667,7 @@ SA_DEV void resolve_wave0(const AlignLaunch& a, int n_eff, int len, uint4* recs,
 // Align one read whose planes are already in x.R / x.C.  recs holds the seed
 // records of wave 0 when wave0_ready.  Returns false when the candidate
 // table overflowed (nothing committed).
-template <bool kSlow>
+template <bool kRegLV>
 SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
                       unsigned long long* wst, uint4* recs, bool wave0_ready) {
     const AlignLaunch& a = *x.a;
@@ -679,89 +692,95 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
     int tested = 0;
     bool any_lookup = false, any_popular = false, early_multi = false, overflow = false;
 
-    for (int i = 0; i < n_eff; ++i) {
-        if ((i & 31) == 0 && (i > 0 || !wave0_ready))  // speculative probes, seeds i .. i+31
-            compute_wave_sync(a, x.R, offs, i, n_eff, len, recs, lane);
-        const uint4 rec = recs[i & 31];
-        const uint32_t flags = rec.x;
-        const uint32_t cnt = rec.y;
-        if (flags & kSeedN) {  // REF :259-262
-            x.st.skipped_n++;
-            continue;
-        }
-        x.st.lookups++;
-        if (cnt > static_cast<uint32_t>(a.hmax)) {  // REF :265-269
-            any_popular = true;
-            x.st.skipped_pop++;
-            continue;
-        }
-        any_lookup = true;
-        x.st.hits_consumed += cnt;
-        if (i < tier0) ++tested;
-
-        if (cnt > 0) {  // REF :273-286
-            const uint32_t payload = rec.z;
-            const int off = static_cast<int>(rec.w);
-            const bool pal = (flags & kSeedPal) != 0;
-            const uint32_t ntot = pal ? cnt / 2 : cnt;
-            const bool inl = ntot == 1;
-            uint32_t n_fwd = 0;
-            if (!inl) n_fwd = __ldg(a.pool + payload);
-            const int rc_shift = len - a.s - off;
-            const uint32_t qflip = (flags & kSeedQflip) ? 1u : 0u;
-            for (uint32_t base = 0; base < cnt; base += 32) {
-                const uint32_t t = base + lane;
-                const bool valid = t < cnt;
-                unsigned long long key = 0;
-                int bit = 0;
-                if (valid) {
-                    const uint32_t j = pal ? (t < ntot ? t : t - ntot) : t;
-                    uint32_t pos, eflag;
-                    if (inl) {
-                        pos = payload;
-                        eflag = (flags & kSeedSingleRc) ? 1u : 0u;
-                    } else {
-                        pos = __ldg(a.pool + payload + 1 + j);
-                        eflag = j >= n_fwd ? 1u : 0u;
-                    }
-                    const uint32_t dir = pal ? (t >= ntot ? 1u : 0u) : (eflag ^ qflip);
-                    const int64_t anchor = static_cast<int64_t>(pos) - (dir ? rc_shift : off);
-                    const uint32_t aa = anchor < 0 ? 0u : static_cast<uint32_t>(anchor);
-                    uint32_t bucket;
-                    if (bs_pow2) {
-                        bucket = aa >> bs_shift;
-                        bit = static_cast<int>(aa & static_cast<uint32_t>(a.bs - 1));
-                    } else {
-                        bucket = aa / static_cast<uint32_t>(a.bs);
-                        bit = static_cast<int>(aa - bucket * static_cast<uint32_t>(a.bs));
-                    }
-                    key = (static_cast<unsigned long long>(bucket) << 1) | dir;
-                }
-                if (!insert_wave(x, valid, key, bit)) {
-                    overflow = true;
-                    break;
-                }
+    // The seed loop (REF :256-316) with the pruning loop (REF :296-315) folded
+    // in, so score_best -- and the LV under it -- is inlined once.
+    bool pruning = false;
+    int i = 0;
+    for (;;) {
+        if (!pruning) {
+            if (i >= n_eff) break;
+            if ((i & 31) == 0 && (i > 0 || !wave0_ready))  // speculative probes, seeds i .. i+31
+                compute_wave_sync(a, x.R, offs, i, n_eff, len, recs, lane);
+            const uint4 rec = recs[i & 31];
+            const uint32_t flags = rec.x;
+            const uint32_t cnt = rec.y;
+            if (flags & kSeedN) {  // REF :259-262
+                x.st.skipped_n++;
+                ++i;
+                continue;
             }
-            if (overflow) break;
-        }
+            x.st.lookups++;
+            if (cnt > static_cast<uint32_t>(a.hmax)) {  // REF :265-269
+                any_popular = true;
+                x.st.skipped_pop++;
+                ++i;
+                continue;
+            }
+            any_lookup = true;
+            x.st.hits_consumed += cnt;
+            if (i < tier0) ++tested;
 
-        score_best(x);  // REF :288
-        if (x.tr.d_best < a.c && x.tr.d_second < x.tr.d_best + a.c) {  // REF :290-295
+            if (cnt > 0) {  // REF :273-286
+                const uint32_t payload = rec.z;
+                const int off = static_cast<int>(rec.w);
+                const bool pal = (flags & kSeedPal) != 0;
+                const uint32_t ntot = pal ? cnt / 2 : cnt;
+                const bool inl = ntot == 1;
+                uint32_t n_fwd = 0;
+                if (!inl) n_fwd = __ldg(a.pool + payload);
+                const int rc_shift = len - a.s - off;
+                const uint32_t qflip = (flags & kSeedQflip) ? 1u : 0u;
+                for (uint32_t base = 0; base < cnt; base += 32) {
+                    const uint32_t t = base + lane;
+                    const bool valid = t < cnt;
+                    unsigned long long key = 0;
+                    int bit = 0;
+                    if (valid) {
+                        const uint32_t j = pal ? (t < ntot ? t : t - ntot) : t;
+                        uint32_t pos, eflag;
+                        if (inl) {
+                            pos = payload;
+                            eflag = (flags & kSeedSingleRc) ? 1u : 0u;
+                        } else {
+                            pos = __ldg(a.pool + payload + 1 + j);
+                            eflag = j >= n_fwd ? 1u : 0u;
+                        }
+                        const uint32_t dir = pal ? (t >= ntot ? 1u : 0u) : (eflag ^ qflip);
+                        const int64_t anchor = static_cast<int64_t>(pos) - (dir ? rc_shift : off);
+                        const uint32_t aa = anchor < 0 ? 0u : static_cast<uint32_t>(anchor);
+                        uint32_t bucket;
+                        if (bs_pow2) {
+                            bucket = aa >> bs_shift;
+                            bit = static_cast<int>(aa & static_cast<uint32_t>(a.bs - 1));
+                        } else {
+                            bucket = aa / static_cast<uint32_t>(a.bs);
+                            bit = static_cast<int>(aa - bucket * static_cast<uint32_t>(a.bs));
+                        }
+                        key = (static_cast<unsigned long long>(bucket) << 1) | dir;
+                    }
+                    if (!insert_wave(x, valid, key, bit)) {
+                        overflow = true;
+                        break;
+                    }
+                }
+                if (overflow) break;
+            }
+
+        } else if (x.n_unscored == 0) {
+            break;
+        }
+        score_best<kRegLV>(x);  // REF :288 (and :306 inside the pruning loop)
+        if (x.tr.d_best < a.c && x.tr.d_second < x.tr.d_best + a.c) {  // REF :290-295 / :307-312
             x.st.multi_exits++;
             early_multi = true;
             break;
         }
-        if (tested >= x.tr.d_best + a.c) {  // REF :296-315
-            x.st.pruning_exits++;
-            while (x.n_unscored > 0) {
-                score_best(x);
-                if (x.tr.d_best < a.c && x.tr.d_second < x.tr.d_best + a.c) {
-                    x.st.multi_exits++;
-                    early_multi = true;
-                    break;
-                }
+        if (!pruning) {
+            if (tested >= x.tr.d_best + a.c) {  // REF :296-315
+                x.st.pruning_exits++;
+                pruning = true;
             }
-            break;
+            ++i;
         }
     }
 
@@ -837,7 +856,9 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
 #define SA_MIN_BLOCKS 3  // 256-thread blocks per SM the register budget must allow
 #endif
 
-template <bool kSlow>
+// kSlow: global candidate tables over a work list; kPipe: static striding with
+// the cp.async read pipeline (short reads); kRegLV: register LV only.
+template <bool kSlow, bool kPipe, bool kRegLV>
 __global__ void __launch_bounds__(256, SA_MIN_BLOCKS) align_kernel(const AlignLaunch a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
@@ -940,12 +961,12 @@ __global__ void __launch_bounds__(256, SA_MIN_BLOCKS) align_kernel(const AlignLa
             x.len = len;
             x.d_max = a.dmax_param >= 0 ? a.dmax_param : (12 * len + 99) / 100;
             const int ne = q ? n_eff1 : n_eff0;
-            if (!align_one<kSlow>(x, r, ne, offs + q * a.n_off_cap, len / a.s, wst, recs + 32 * q, wave0_ready))
+            if (!align_one<kRegLV>(x, r, ne, offs + q * a.n_off_cap, len / a.s, wst, recs + 32 * q, wave0_ready))
                 overflowed(r);
         }
     };
 
-    if (!kSlow && a.prefetch) {
+    if (kPipe) {
         // Static striding, software-pipelined one read ahead: while read r is
         // aligned, read r+nw is already decoded and its wave-0 index probes are
         // in flight (cp.async), and read r+2nw's bytes are being copied.
@@ -1083,7 +1104,7 @@ __global__ void __launch_bounds__(256) lv_batch_kernel(const LvLaunch a) {
             continue;
         }
         uint32_t cells = 0;
-        const int d = lv_warp(R, m, W, 0u, w, dl, F, lane, cells);
+        const int d = lv_warp_any(R, m, W, 0u, w, dl, F, lane, cells);
         if (lane == 0) a.out[p] = d;
         __syncwarp();
     }
@@ -1158,12 +1179,32 @@ __global__ void lookup_kernel(const LookupLaunch a) {
 
 }  // namespace
 
+template <bool kSlow, bool kPipe, bool kRegLV>
+void launch_variant(const AlignLaunch& a, int grid, int block, cudaStream_t st) {
+    align_kernel<kSlow, kPipe, kRegLV><<<grid, block, a.smem_per_warp * (block / 32), st>>>(a);
+}
+
+// kernel variants: fast {pipelined, dynamic} x {register LV, shared LV}; slow {register, shared}
+template <bool kSlow, bool kPipe, bool kRegLV>
+cudaError_t set_smem_variant(int bytes) {
+    return cudaFuncSetAttribute(align_kernel<kSlow, kPipe, kRegLV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                bytes);
+}
+
 void launch_align_fast(const AlignLaunch& a, int grid, int block, cudaStream_t st) {
-    align_kernel<false><<<grid, block, a.smem_per_warp * (block / 32), st>>>(a);
+    const bool reg = a.dl_max <= 15;
+    if (a.prefetch) {
+        if (reg) launch_variant<false, true, true>(a, grid, block, st);
+        else launch_variant<false, true, false>(a, grid, block, st);
+    } else {
+        if (reg) launch_variant<false, false, true>(a, grid, block, st);
+        else launch_variant<false, false, false>(a, grid, block, st);
+    }
 }
 
 void launch_align_slow(const AlignLaunch& a, int grid, int block, cudaStream_t st) {
-    align_kernel<true><<<grid, block, a.smem_per_warp * (block / 32), st>>>(a);
+    if (a.dl_max <= 15) launch_variant<true, false, true>(a, grid, block, st);
+    else launch_variant<true, false, false>(a, grid, block, st);
 }
 
 void launch_lv_batch(const LvLaunch& a, int grid, int block, cudaStream_t st) {
@@ -1178,19 +1219,28 @@ void launch_lookup(const LookupLaunch& a, cudaStream_t st) {
 }
 
 cudaError_t align_set_smem(uint32_t smem_bytes) {
-    cudaError_t e = cudaFuncSetAttribute(align_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem_bytes));
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(align_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem_bytes));
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(lv_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(smem_bytes));
+    const int b = static_cast<int>(smem_bytes);
+    cudaError_t e;
+    if ((e = set_smem_variant<false, true, true>(b)) != cudaSuccess) return e;
+    if ((e = set_smem_variant<false, true, false>(b)) != cudaSuccess) return e;
+    if ((e = set_smem_variant<false, false, true>(b)) != cudaSuccess) return e;
+    if ((e = set_smem_variant<false, false, false>(b)) != cudaSuccess) return e;
+    if ((e = set_smem_variant<true, false, true>(b)) != cudaSuccess) return e;
+    if ((e = set_smem_variant<true, false, false>(b)) != cudaSuccess) return e;
+    return cudaFuncSetAttribute(lv_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
 }
 
-cudaError_t align_fast_occupancy(int block, uint32_t smem_bytes, int* blocks_per_sm) {
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, align_kernel<false>, block,
-                                                         smem_bytes);
+cudaError_t align_fast_occupancy(const AlignLaunch& a, int block, uint32_t smem_bytes, int* blocks_per_sm) {
+    const bool reg = a.dl_max <= 15;
+    if (a.prefetch)
+        return reg ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, align_kernel<false, true, true>,
+                                                                   block, smem_bytes)
+                   : cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, align_kernel<false, true, false>,
+                                                                   block, smem_bytes);
+    return reg ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, align_kernel<false, false, true>, block,
+                                                               smem_bytes)
+               : cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, align_kernel<false, false, false>, block,
+                                                               smem_bytes);
 }
 
 }  // namespace sab

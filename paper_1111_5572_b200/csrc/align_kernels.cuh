@@ -93,7 +93,7 @@ void launch_align_fast(const AlignLaunch& a, int grid, int block, cudaStream_t s
 void launch_align_slow(const AlignLaunch& a, int grid, int block, cudaStream_t st);
 void launch_lv_batch(const LvLaunch& a, int grid, int block, cudaStream_t st);
 void launch_lookup(const LookupLaunch& a, cudaStream_t st);
-cudaError_t align_fast_occupancy(int block, uint32_t smem_bytes, int* blocks_per_sm);
+cudaError_t align_fast_occupancy(const AlignLaunch& a, int block, uint32_t smem_bytes, int* blocks_per_sm);
 cudaError_t align_set_smem(uint32_t smem_bytes);
 
 }  // namespace sab

@@ -199,7 +199,7 @@ int make_shape(Replica& rep, const sa_params* p, uint64_t Lmax, LaunchShape& sh,
         }
         rep.smem_attr = kMaxSmem;
     }
-    if (align_fast_occupancy(sh.fast_block, a.smem_per_warp * warps, &bps) != cudaSuccess || bps < 1) bps = 1;
+    if (align_fast_occupancy(a, sh.fast_block, a.smem_per_warp * warps, &bps) != cudaSuccess || bps < 1) bps = 1;
     sh.fast_grid = bps * rep.sm_count;
 
     // slow path: candidate tables in global memory, worst case n_eff * h_max
