@@ -701,6 +701,73 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
             if (i >= n_eff) break;
             if ((i & 31) == 0 && (i > 0 || !wave0_ready))  // speculative probes, seeds i .. i+31
                 compute_wave_sync(a, x.R, offs, i, n_eff, len, recs, lane);
+            if (x.n_unscored == 0) {
+                // Fast-forward over a run of seeds that cannot change the
+                // candidate choice: N seeds, popular seeds, and lookups whose
+                // hits (none, or one) land in existing candidates -- all
+                // scored, as nothing is unscored.  Such a seed only moves
+                // counters, and score_best / the multi exit are no-ops for it;
+                // the pruning exit fires at the lookup where `tested` reaches
+                // d_best + c.  Exactly the sequential loop's effect, evaluated
+                // for the whole wave at once.
+                const int wb = i & ~31;
+                const int j = wb + lane;
+                const bool in = j >= i && j < n_eff && j < wb + 32;
+                const uint4 rr = recs[lane];
+                const bool isN = in && (rr.x & kSeedN);
+                const bool isPop = in && !isN && rr.y > static_cast<uint32_t>(a.hmax);
+                const bool lk = in && !isN && !isPop;
+                bool triv = lk && rr.y == 0u;
+                if (lk && rr.y == 1u) {  // a single (non-palindromic) hit
+                    const uint32_t dir = ((rr.x & kSeedSingleRc) ? 1u : 0u) ^ ((rr.x & kSeedQflip) ? 1u : 0u);
+                    const int o = static_cast<int>(rr.w);
+                    const int64_t anchor = static_cast<int64_t>(rr.z) - (dir ? (len - a.s - o) : o);
+                    const uint32_t aa = anchor < 0 ? 0u : static_cast<uint32_t>(anchor);
+                    const uint32_t bucket = bs_pow2 ? (aa >> bs_shift) : aa / static_cast<uint32_t>(a.bs);
+                    const unsigned long long key = (static_cast<unsigned long long>(bucket) << 1) | dir;
+                    for (uint32_t h = cand_hash(key, x.t.hcap);; h = (h + 1) & static_cast<uint32_t>(x.t.hcap - 1)) {
+                        const unsigned long long cur = x.t.hkey[h];
+                        if (cur == key) {
+                            triv = true;
+                            break;
+                        }
+                        if (cur == kEmptyKey) break;
+                    }
+                }
+                const uint32_t m_in = __ballot_sync(FULL, in);
+                const uint32_t m_n = __ballot_sync(FULL, isN);
+                const uint32_t m_p = __ballot_sync(FULL, isPop);
+                const uint32_t m_t = __ballot_sync(FULL, triv);
+                const uint32_t m_1 = __ballot_sync(FULL, triv && rr.y == 1u);
+                const uint32_t stop = m_in & ~(m_n | m_p | m_t);  // first seed needing the full path
+                uint32_t run = m_in & (stop ? ((stop & (0u - stop)) - 1u) : ~0u);
+                if (run != 0u) {
+                    const int t0 = tier0 - wb;
+                    const uint32_t below = t0 >= 32 ? ~0u : (t0 <= 0 ? 0u : ((1u << t0) - 1u));
+                    const uint32_t inc = run & m_t & below;
+                    const int need = x.tr.d_best + a.c - tested;  // > 0 here
+                    bool prune = false;
+                    if (__popc(inc) >= need) {  // exit at the need-th increment
+                        uint32_t m = inc;
+                        for (int k = 1; k < need; ++k) m &= m - 1u;
+                        run &= (m & (0u - m)) | ((m & (0u - m)) - 1u);
+                        prune = true;
+                    }
+                    x.st.skipped_n += __popc(run & m_n);
+                    x.st.lookups += __popc(run & ~m_n);
+                    x.st.skipped_pop += __popc(run & m_p);
+                    x.st.hits_consumed += __popc(run & m_1);
+                    tested += __popc(run & inc);
+                    any_popular |= (run & m_p) != 0u;
+                    any_lookup |= (run & m_t) != 0u;
+                    if (prune) {  // REF :296-315 with nothing unscored
+                        x.st.pruning_exits++;
+                        break;
+                    }
+                    i = wb + 32 - __clz(run);  // one past the run's last seed
+                    continue;
+                }
+            }
             const uint4 rec = recs[i & 31];
             const uint32_t flags = rec.x;
             const uint32_t cnt = rec.y;
