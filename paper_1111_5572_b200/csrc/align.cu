@@ -306,10 +306,12 @@ struct CandTable {
     int cap, hcap;
 };
 
-struct ReadStats {  // per-read deltas, committed only when the read completes
-    uint32_t lookups, skipped_n, skipped_pop, dist_calls, after_first, early_out_after_first;
-    uint32_t multi_exits, pruning_exits;
-    uint32_t hits_consumed, window_bases;
+
+// stats slots (sa_stats order)
+enum {
+    S_READS, S_TOO_SHORT, S_LOOKUPS, S_SKIP_N, S_SKIP_POP, S_ALL_POP, S_DIST, S_DIST_AFTER,
+    S_EARLY_OUT, S_CELLS, S_MULTI, S_PRUNE, S_FIRST_BEST, S_SINGLE, S_MULTIPLE, S_NOT_FOUND,
+    S_HITS, S_WINDOW, S_READ_BASES, S_OVERFLOW
 };
 
 struct Ctx {
@@ -327,9 +329,14 @@ struct Ctx {
     bool first_done, first_valid;
     int first_dir;
     uint64_t first_pos;
-    uint32_t cells;  // per lane
-    ReadStats st;
+    uint32_t cells;  // per lane, LV cells of the launch (dp_cells)
+    // Per-read counters, lane-distributed: lane k holds stats slot k (sa_stats
+    // order) for the read in flight -- one register for all of them.  Added to
+    // the warp totals when the read completes, dropped if it overflows.
+    uint32_t rs;
 };
+
+SA_DEV void stat_add(Ctx& x, int slot, uint32_t v) { x.rs += x.lane == slot ? v : 0u; }
 
 SA_DEV uint32_t cand_hash(unsigned long long key, int hcap) {
     return static_cast<uint32_t>((key * 0x9E3779B97F4A7C15ull) >> 40) & static_cast<uint32_t>(hcap - 1);
@@ -476,12 +483,12 @@ SA_DEV void score_candidate(Ctx& x, uint32_t idx) {
         const int w = static_cast<int>(want < rem ? want : rem);
         const uint32_t wofs = static_cast<uint32_t>(anchor - gb0 * 32);
         const int d = lv_warp<kRegLV>(orient, x.len, x.W, wofs, w, d_limit, x.F, lane, x.cells);
-        x.st.dist_calls++;
+        stat_add(x, S_DIST, 1u);
         x.calls++;
-        x.st.window_bases += static_cast<uint32_t>(w);
+        stat_add(x, S_WINDOW, static_cast<uint32_t>(w));
         if (x.calls > 1) {
-            x.st.after_first++;
-            if (d < 0) x.st.early_out_after_first++;
+            stat_add(x, S_DIST_AFTER, 1u);
+            if (d < 0) stat_add(x, S_EARLY_OUT, 1u);
         }
         if (d >= 0 && d < best_d) {
             best_d = d;
@@ -552,12 +559,6 @@ SA_DEV void clear_table(CandTable& t, uint32_t n_cands, bool full, int lane) {
 // per-seed flags
 constexpr uint32_t kSeedN = 1, kSeedQflip = 2, kSeedPal = 4, kSeedSingleRc = 8;
 
-// stats slots (sa_stats order)
-enum {
-    S_READS, S_TOO_SHORT, S_LOOKUPS, S_SKIP_N, S_SKIP_POP, S_ALL_POP, S_DIST, S_DIST_AFTER,
-    S_EARLY_OUT, S_CELLS, S_MULTI, S_PRUNE, S_FIRST_BEST, S_SINGLE, S_MULTIPLE, S_NOT_FOUND,
-    S_HITS, S_WINDOW, S_READ_BASES, S_OVERFLOW
-};
 
 // Seed at read offset `off` (planes R): flags (N / query-is-rc-of-canon /
 // palindrome) and its canonical planar key.
@@ -669,7 +670,7 @@ SA_DEV void resolve_wave0(const AlignLaunch& a, int n_eff, int len, uint4* recs,
 // table overflowed (nothing committed).
 template <bool kRegLV>
 SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
-                      unsigned long long* wst, uint4* recs, bool wave0_ready) {
+                      unsigned long long& acc, uint4* recs, bool wave0_ready) {
     const AlignLaunch& a = *x.a;
     const int lane = x.lane;
     const int len = x.len;
@@ -687,8 +688,7 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
     x.first_valid = false;
     x.first_dir = 0;
     x.first_pos = 0;
-    x.cells = 0;
-    x.st = ReadStats{};
+    x.rs = 0;
     int tested = 0;
     bool any_lookup = false, any_popular = false, early_multi = false, overflow = false;
 
@@ -753,15 +753,15 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
                         run &= (m & (0u - m)) | ((m & (0u - m)) - 1u);
                         prune = true;
                     }
-                    x.st.skipped_n += __popc(run & m_n);
-                    x.st.lookups += __popc(run & ~m_n);
-                    x.st.skipped_pop += __popc(run & m_p);
-                    x.st.hits_consumed += __popc(run & m_1);
+                    stat_add(x, S_SKIP_N, __popc(run & m_n));
+                    stat_add(x, S_LOOKUPS, __popc(run & ~m_n));
+                    stat_add(x, S_SKIP_POP, __popc(run & m_p));
+                    stat_add(x, S_HITS, __popc(run & m_1));
                     tested += __popc(run & inc);
                     any_popular |= (run & m_p) != 0u;
                     any_lookup |= (run & m_t) != 0u;
                     if (prune) {  // REF :296-315 with nothing unscored
-                        x.st.pruning_exits++;
+                        stat_add(x, S_PRUNE, 1u);
                         break;
                     }
                     i = wb + 32 - __clz(run);  // one past the run's last seed
@@ -772,19 +772,19 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
             const uint32_t flags = rec.x;
             const uint32_t cnt = rec.y;
             if (flags & kSeedN) {  // REF :259-262
-                x.st.skipped_n++;
+                stat_add(x, S_SKIP_N, 1u);
                 ++i;
                 continue;
             }
-            x.st.lookups++;
+            stat_add(x, S_LOOKUPS, 1u);
             if (cnt > static_cast<uint32_t>(a.hmax)) {  // REF :265-269
                 any_popular = true;
-                x.st.skipped_pop++;
+                stat_add(x, S_SKIP_POP, 1u);
                 ++i;
                 continue;
             }
             any_lookup = true;
-            x.st.hits_consumed += cnt;
+            stat_add(x, S_HITS, cnt);
             if (i < tier0) ++tested;
 
             if (cnt > 0) {  // REF :273-286
@@ -838,13 +838,13 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
         }
         score_best<kRegLV>(x);  // REF :288 (and :306 inside the pruning loop)
         if (x.tr.d_best < a.c && x.tr.d_second < x.tr.d_best + a.c) {  // REF :290-295 / :307-312
-            x.st.multi_exits++;
+            stat_add(x, S_MULTI, 1u);
             early_multi = true;
             break;
         }
         if (!pruning) {
             if (tested >= x.tr.d_best + a.c) {  // REF :296-315
-                x.st.pruning_exits++;
+                stat_add(x, S_PRUNE, 1u);
                 pruning = true;
             }
             ++i;
@@ -895,38 +895,24 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
                                                            : x.tr.best_pos - x.first_pos;
         first_best = delta <= static_cast<uint64_t>(a.bs);
     }
-    uint32_t cells = x.cells;
-    for (int o = 16; o > 0; o >>= 1) cells += __shfl_xor_sync(FULL, cells, o);
-    if (lane == 0) {
-        a.results[r] = res;
-        wst[S_READS] += 1;
-        wst[S_LOOKUPS] += x.st.lookups;
-        wst[S_SKIP_N] += x.st.skipped_n;
-        wst[S_SKIP_POP] += x.st.skipped_pop;
-        wst[S_ALL_POP] += all_pop ? 1 : 0;
-        wst[S_DIST] += x.st.dist_calls;
-        wst[S_DIST_AFTER] += x.st.after_first;
-        wst[S_EARLY_OUT] += x.st.early_out_after_first;
-        wst[S_CELLS] += cells;
-        wst[S_MULTI] += x.st.multi_exits;
-        wst[S_PRUNE] += x.st.pruning_exits;
-        wst[S_FIRST_BEST] += first_best ? 1 : 0;
-        wst[S_SINGLE + (kind - SA_SINGLE_HIT)] += 1;
-        wst[S_HITS] += x.st.hits_consumed;
-        wst[S_WINDOW] += x.st.window_bases;
-        wst[S_READ_BASES] += static_cast<unsigned long long>(len);
-    }
+    if (lane == 0) a.results[r] = res;
+    stat_add(x, S_READS, 1u);
+    stat_add(x, S_ALL_POP, all_pop ? 1u : 0u);
+    stat_add(x, S_FIRST_BEST, first_best ? 1u : 0u);
+    stat_add(x, S_SINGLE + (kind - SA_SINGLE_HIT), 1u);
+    stat_add(x, S_READ_BASES, static_cast<uint32_t>(len));
+    acc += x.rs;
     return true;
 }
 
 #ifndef SA_MIN_BLOCKS
-#define SA_MIN_BLOCKS 3  // 256-thread blocks per SM the register budget must allow
+#define SA_MIN_BLOCKS 3  // blocks of SA_FAST_WARPS warps per SM the register budget must allow
 #endif
 
 // kSlow: global candidate tables over a work list; kPipe: static striding with
 // the cp.async read pipeline (short reads); kRegLV: register LV only.
 template <bool kSlow, bool kPipe, bool kRegLV>
-__global__ void __launch_bounds__(256, SA_MIN_BLOCKS) align_kernel(const AlignLaunch a) {
+__global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kernel(const AlignLaunch a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
@@ -946,13 +932,15 @@ __global__ void __launch_bounds__(256, SA_MIN_BLOCKS) align_kernel(const AlignLa
     int* offs = reinterpret_cast<int*>(pcanon + 32);  // 2 x n_off_cap
     x.F = offs + 2 * a.n_off_cap;
     uint32_t* stage = reinterpret_cast<uint32_t*>(x.F + a.f_ints);  // 2 x sbw words
-    unsigned long long* wst = reinterpret_cast<unsigned long long*>(stage + 2 * a.sbw);
+    // warp totals, lane-distributed (lane k: sa_stats slot k); LV cells per lane
+    unsigned long long acc = 0;
+    x.cells = 0;
     unsigned char* tb;
     if (kSlow) {
         const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
         tb = a.gscratch + gw * a.gscratch_per_warp;
     } else {
-        tb = reinterpret_cast<unsigned char*>(wst + kNumStats);
+        tb = reinterpret_cast<unsigned char*>(reinterpret_cast<unsigned long long*>(stage + 2 * a.sbw) + kNumStats);
     }
     x.t.cap = a.cap;
     x.t.hcap = a.hcap;
@@ -963,7 +951,6 @@ __global__ void __launch_bounds__(256, SA_MIN_BLOCKS) align_kernel(const AlignLa
     x.t.chslot = x.t.ccnt + a.cap;
     x.t.hval = x.t.chslot + a.cap;
     for (int j = lane; j < a.hcap; j += 32) x.t.hkey[j] = kEmptyKey;
-    if (lane < kNumStats) wst[lane] = 0;
     __syncwarp();
 
     int cached_len0 = -1, cached_len1 = -1, n_eff0 = 0, n_eff1 = 0;
@@ -995,11 +982,9 @@ __global__ void __launch_bounds__(256, SA_MIN_BLOCKS) align_kernel(const AlignLa
 #pragma unroll
             for (int i = 0; i < 5; ++i) res.reserved[i] = 0;
             a.results[r] = res;
-            wst[S_READS] += 1;
-            wst[S_TOO_SHORT] += 1;
-            wst[S_NOT_FOUND] += 1;
-            wst[S_READ_BASES] += static_cast<unsigned long long>(len);
         }
+        acc += (lane == S_READS || lane == S_TOO_SHORT || lane == S_NOT_FOUND) ? 1u
+               : (lane == S_READ_BASES ? static_cast<uint32_t>(len) : 0u);
     };
     auto overflowed = [&](uint32_t r) {
         if (kSlow) {  // table sized n_eff * h_max cannot overflow unless clamped
@@ -1007,8 +992,8 @@ __global__ void __launch_bounds__(256, SA_MIN_BLOCKS) align_kernel(const AlignLa
         } else if (lane == 0) {  // defer to the global-table kernel
             const unsigned slot = atomicAdd(a.overflow_count, 1u);
             a.overflow_list[slot] = static_cast<unsigned>(a.read_base) + r;  // batch-absolute id
-            wst[S_OVERFLOW] += 1;
         }
+        if (!kSlow && lane == S_OVERFLOW) acc += 1u;
     };
     // status of a staged read: 0 = decoded, 1 = shorter than s, 2 = bad character
     auto prep = [&](int q, int len, const uint32_t* words, int sh, int nwd) -> int {
@@ -1028,7 +1013,7 @@ __global__ void __launch_bounds__(256, SA_MIN_BLOCKS) align_kernel(const AlignLa
             x.len = len;
             x.d_max = a.dmax_param >= 0 ? a.dmax_param : (12 * len + 99) / 100;
             const int ne = q ? n_eff1 : n_eff0;
-            if (!align_one<kRegLV>(x, r, ne, offs + q * a.n_off_cap, len / a.s, wst, recs + 32 * q, wave0_ready))
+            if (!align_one<kRegLV>(x, r, ne, offs + q * a.n_off_cap, len / a.s, acc, recs + 32 * q, wave0_ready))
                 overflowed(r);
         }
     };
@@ -1119,7 +1104,10 @@ __global__ void __launch_bounds__(256, SA_MIN_BLOCKS) align_kernel(const AlignLa
     }
 
     __syncwarp();
-    if (lane < kNumStats && wst[lane]) atomicAdd(a.stats + lane, wst[lane]);
+    unsigned long long cells = x.cells;
+    for (int o = 16; o > 0; o >>= 1) cells += __shfl_xor_sync(FULL, cells, o);
+    if (lane == S_CELLS) acc += cells;
+    if (lane < kNumStats && acc) atomicAdd(a.stats + lane, acc);
 }
 
 // ------------------------------------------------------------------ standalone LV

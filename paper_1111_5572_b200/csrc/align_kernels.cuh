@@ -55,6 +55,10 @@ struct AlignLaunch {
     uint64_t gscratch_per_warp;
 };
 
+#ifndef SA_FAST_WARPS
+#define SA_FAST_WARPS 8  // warps per block of the align kernels (compile-time: launch bounds)
+#endif
+
 // bytes of one candidate table with capacity cap and hcap hash slots
 inline uint64_t cand_table_bytes(int cap, int hcap) {
     return static_cast<uint64_t>(cap) * (8 + 8 + 4 + 4) + static_cast<uint64_t>(hcap) * (8 + 4);

@@ -189,7 +189,7 @@ int make_shape(Replica& rep, const sa_params* p, uint64_t Lmax, LaunchShape& sh,
         why = "read too long for the shared-memory layout (limit ~60 kbp)";
         return SA_EINVAL;
     }
-    int warps = std::min<int>(8, kMaxSmem / a.smem_per_warp);
+    int warps = std::min<int>(SA_FAST_WARPS, kMaxSmem / a.smem_per_warp);
     sh.fast_block = 32 * warps;
     int bps = 0;
     if (rep.smem_attr < kMaxSmem) {
