@@ -29,6 +29,7 @@ namespace {
 
 thread_local std::string g_thread_err;
 
+constexpr int kPipeStages = 3;  // chunk buffers in flight per replica (copy / kernel / copy-back)
 constexpr int kCtlWords = 4;  // cursor_fast, cursor_slow, overflow_count, error_flag
 constexpr uint64_t kChunkReads = 1u << 17;  // default; SA_CHUNK_READS overrides (tuning)
 
@@ -54,6 +55,7 @@ struct Stage {  // one of the two pipeline slots of a replica
     uint64_t reads_cap = 0;
     unsigned int* d_ctl = nullptr;
     cudaEvent_t k0 = nullptr, km = nullptr, k1 = nullptr;  // fast kernel [k0,km), slow [km,k1)
+    cudaEvent_t done = nullptr;                             // after the stage's last D2H
 };
 
 cudaError_t stage_times(Stage& s, float& fast_ms, float& slow_ms) {
@@ -81,7 +83,7 @@ struct Replica {
     int device = 0;
     int sm_count = 148;
     DeviceIndex ix;
-    Stage stage[3];  // [0],[1] batch pipeline, [2] sa_align_device
+    Stage stage[kPipeStages + 1];  // [0, kPipeStages) batch pipeline, [kPipeStages] sa_align_device
     unsigned long long* d_stats = nullptr;
     unsigned int* d_err = nullptr;         // error flag
     unsigned long long* d_err_read = nullptr;
@@ -240,6 +242,7 @@ int ensure_stage(sa_context* ctx, Stage& s, uint64_t bytes, uint64_t reads) {
         CUDA_TRY(ctx, cudaEventCreate(&s.k0));
         CUDA_TRY(ctx, cudaEventCreate(&s.km));
         CUDA_TRY(ctx, cudaEventCreate(&s.k1));
+        CUDA_TRY(ctx, cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
         CUDA_TRY(ctx, cudaMalloc(&s.d_ctl, kCtlWords * sizeof(unsigned int)));
     }
     if (bytes > s.bases_cap) {
@@ -560,6 +563,7 @@ void sa_destroy(sa_context* ctx) {
             if (s.k0) cudaEventDestroy(s.k0);
             if (s.km) cudaEventDestroy(s.km);
             if (s.k1) cudaEventDestroy(s.k1);
+            if (s.done) cudaEventDestroy(s.done);
             if (s.st) cudaStreamDestroy(s.st);
         }
         if (rep.d_stats) cudaFree(rep.d_stats);
@@ -657,9 +661,9 @@ int sa_align_batch(sa_context* ctx, const sa_params* params, const char* bases,
                     if ((bad = ensure_scratch(&local_err, rep, sh))) break;
                 }
                 const uint64_t b0 = offsets[r0], b1 = offsets[r1];
-                Stage& stg = rep.stage[k & 1];
+                Stage& stg = rep.stage[k % kPipeStages];
                 if ((bad = ensure_stage(&local_err, stg, b1 - b0, r1 - r0))) break;
-                if (k < 2) {
+                if (k < kPipeStages) {
                     if (k == 0) {
                         if (defer && (bad = ensure_defer(&local_err, rep, n_reads))) break;
                         if (defer)
@@ -673,7 +677,7 @@ int sa_align_batch(sa_context* ctx, const sa_params* params, const char* bases,
                     }
                 }
                 // stage reuse: collect the kernel events of its previous chunk
-                if (k >= 2) CUDA_TRY(&local_err, stage_times(stg, kms[ri], kslow[ri]));
+                if (k >= kPipeStages) CUDA_TRY(&local_err, stage_times(stg, kms[ri], kslow[ri]));
                 CUDA_TRY(&local_err, cudaMemcpyAsync(stg.d_bases, bases + b0, b1 - b0, cudaMemcpyHostToDevice, stg.st));
                 CUDA_TRY(&local_err, cudaMemcpyAsync(stg.d_offsets, offsets + r0, (r1 - r0 + 1) * sizeof(uint64_t),
                                                      cudaMemcpyHostToDevice, stg.st));
@@ -686,18 +690,17 @@ int sa_align_batch(sa_context* ctx, const sa_params* params, const char* bases,
                 ++k;
             }
             if (bad || k == 0) {  // drain whatever was enqueued before returning
-                for (int j = 0; j < 2; ++j)
+                for (int j = 0; j < kPipeStages; ++j)
                     if (rep.stage[j].st) cudaStreamSynchronize(rep.stage[j].st);
                 std::memset(&part[ri], 0, sizeof(sa_stats));
                 return bad;
             }
-            if (k == 1) {  // stage[1] never joined: let the end event cover stage[0] only
-                CUDA_TRY(&local_err, cudaEventRecord(rep.e_join, rep.stage[0].st));
+            for (int j = 0; j < kPipeStages && j < k; ++j)
+                CUDA_TRY(&local_err, stage_times(rep.stage[(k - 1 - j) % kPipeStages], kms[ri], kslow[ri]));
+            for (int j = 1; j < kPipeStages && j < k; ++j) {  // join the other stages into stage[0]
+                CUDA_TRY(&local_err, cudaEventRecord(rep.stage[j].done, rep.stage[j].st));
+                CUDA_TRY(&local_err, cudaStreamWaitEvent(rep.stage[0].st, rep.stage[j].done, 0));
             }
-            for (int j = 0; j < 2 && j < k; ++j)
-                CUDA_TRY(&local_err, stage_times(rep.stage[(k - 1 - j) & 1], kms[ri], kslow[ri]));
-            if (k >= 2) CUDA_TRY(&local_err, cudaEventRecord(rep.e_join, rep.stage[1].st));
-            CUDA_TRY(&local_err, cudaStreamWaitEvent(rep.stage[0].st, rep.e_join, 0));
             if (defer) {
                 uint64_t redone = 0;
                 if (int rc = overflow_pass(&local_err, rep, rep.stage[0], sh, bases, offsets, results, launches[ri],
@@ -758,9 +761,9 @@ int sa_align_device(sa_context* ctx, const sa_params* params, const char* d_base
     LaunchShape sh;
     if (int rc = cached_shape(rep, params, max_read_length, sh, why)) return fail(ctx, rc, why);
     if (int rc = ensure_scratch(ctx, rep, sh)) return rc;
-    Stage& stg = rep.stage[2];
+    Stage& stg = rep.stage[kPipeStages];
     if (int rc = ensure_stage(ctx, stg, 0, n_reads)) return rc;
-    // the caller's stream drives; stage[2] keeps only control words
+    // the caller's stream drives; this stage keeps only control words
     Stage tmp = stg;
     tmp.st = st;
     unsigned long long* stats_dst = reinterpret_cast<unsigned long long*>(d_stats);
@@ -780,7 +783,7 @@ int sa_last_kernel_times(sa_context* ctx, float* fast_ms, float* slow_ms) {
         Replica& rep = ctx->reps[0];
         CUDA_TRY(ctx, cudaSetDevice(rep.device));
         float f = 0, s = 0;
-        CUDA_TRY(ctx, stage_times(rep.stage[2], f, s));
+        CUDA_TRY(ctx, stage_times(rep.stage[kPipeStages], f, s));
         ctx->last_kernel_ms = f;
         ctx->last_slow_ms = s;
         ctx->device_timing_pending = false;
