@@ -11,6 +11,8 @@
  *   SA_EINVAL   1  invalid argument   (reference: std::invalid_argument)
  *   SA_ERUNTIME 2  CUDA / runtime      (reference: IoError / runtime_error)
  *   SA_EFORMAT  3  format mismatch     (reference: FormatError)
+ *   SA_EPARSE   4  malformed text input (reference: ParseError, FASTA/FASTQ)
+ *   SA_EIO      5  file cannot be opened/written (reference: IoError)
  *
  * and leaves a message retrievable with sa_last_error().  The C++ adapter in
  * snap_b200.hpp rethrows these as the reference's exception types.
@@ -29,7 +31,7 @@
 extern "C" {
 #endif
 
-enum { SA_OK = 0, SA_EINVAL = 1, SA_ERUNTIME = 2, SA_EFORMAT = 3 };
+enum { SA_OK = 0, SA_EINVAL = 1, SA_ERUNTIME = 2, SA_EFORMAT = 3, SA_EPARSE = 4, SA_EIO = 5 };
 
 /* ResultKind, REF include/seedaln/aligner.hpp:32 */
 enum { SA_SINGLE_HIT = 0, SA_MULTIPLE_HITS = 1, SA_NOT_FOUND = 2 };
@@ -187,6 +189,59 @@ int sa_last_kernel_times(sa_context* ctx, float* fast_ms, float* slow_ms);
 
 /* Number of CUDA kernels launched by the last sa_align_batch call. */
 int sa_last_launches(const sa_context* ctx, uint64_t* launches);
+
+/* ------------------------------------------------------------------ genome and index files
+ * sa_genome = PackedGenome (REF include/seedaln/genome.hpp:36-100): packed
+ * words, N mask and the contig table. */
+typedef struct sa_genome sa_genome;
+
+enum { SA_INDEX_SNAPIDX1 = 0, /* the reference's file, REF include/seedaln/seed_index.hpp:74-85 */
+       SA_INDEX_SNAPGPU1 = 1  /* compact: SNAPIDX1 header + genome, no CSR tables (the GPU
+                                 rebuilds its index from the genome in seconds) */ };
+
+/* PackedGenome::from_fasta (REF src/genome.cpp:48-94): '>' headers (name =
+ * first whitespace-delimited token), IUPAC letters, case and whitespace
+ * ignored.  SA_EPARSE with the reference's messages; SA_EIO if unreadable. */
+int sa_genome_from_fasta(const char* path, sa_genome** out);
+
+/* A genome from PackedGenome words and its contig table (names[i] NUL-terminated). */
+int sa_genome_from_words(const uint64_t* packed, uint64_t n_packed, const uint64_t* nmask, uint64_t n_nmask,
+                         uint64_t length, const char* const* names, const uint64_t* starts,
+                         const uint64_t* lengths, uint64_t n_contigs, sa_genome** out);
+void sa_genome_free(sa_genome* g);
+
+/* size(), contigs().size() and checksum() (REF genome.hpp:59, 91, 95; genome.cpp:158-179). */
+int sa_genome_info(const sa_genome* g, uint64_t* length, uint64_t* n_contigs, uint64_t* checksum);
+/* packed_words() / n_mask_words() (REF genome.hpp:98-99); pointers valid while g lives. */
+int sa_genome_words(const sa_genome* g, const uint64_t** packed, uint64_t* n_packed, const uint64_t** nmask,
+                    uint64_t* n_nmask);
+/* contigs()[i] (REF genome.hpp:24-28); name valid while g lives. */
+int sa_genome_contig(const sa_genome* g, uint64_t i, const char** name, uint64_t* start, uint64_t* length);
+
+/* sa_create over a genome object. */
+int sa_create_from_genome(const sa_genome* g, int32_t seed_size, const int32_t* devices, int32_t n_devices,
+                          sa_context** out);
+
+/* run_index + save_index_file (REF src/driver.cpp:37-45, src/seed_index.cpp:145-170).
+ * SA_INDEX_SNAPIDX1: the CSR tables (REF SeedIndex::build, seed_index.cpp:80-126)
+ * are built on GPU `device`; the file is byte-identical to the reference's.
+ * SA_INDEX_SNAPGPU1: header + genome only. */
+int sa_index_write(const sa_genome* g, int32_t seed_size, int32_t format, int32_t device, const char* path);
+
+/* load_index_file (REF src/seed_index.cpp:173-228) followed by sa_create on
+ * `devices`: reads SNAPIDX1 or SNAPGPU1 with the reference's checks and
+ * messages (SA_EFORMAT).  With verify != 0 the SNAPIDX1 tables are compared
+ * with a GPU rebuild from the embedded genome (SA_EFORMAT on mismatch), since
+ * the GPU aligns with its own index of that genome.  The caller frees both. */
+int sa_index_load(const char* path, const int32_t* devices, int32_t n_devices, int32_t verify,
+                  sa_genome** genome_out, sa_context** ctx_out);
+
+/* The reference's CSR tables of g (SeedIndex keys_/offsets_/positions_, REF
+ * include/seedaln/seed_index.hpp:69-71), built on GPU `device`.  On entry
+ * *n_keys / *n_positions are the capacities of keys (offsets: n_keys + 1) and
+ * positions; on return the sizes.  NULL arrays: sizes only. */
+int sa_index_csr(const sa_genome* g, int32_t seed_size, int32_t device, uint64_t* n_keys, uint64_t* n_positions,
+                 uint64_t* keys, uint64_t* offsets, uint64_t* positions);
 
 #ifdef __cplusplus
 }

@@ -134,6 +134,13 @@ def rlib():
         lib.ref_tracker_replay.argtypes = [C.c_int, C.POINTER(C.c_int64), C.c_int, C.POINTER(C.c_int64)]
         lib.ref_align_batch.argtypes = [C.c_void_p, C.POINTER(Params), C.c_void_p, P64, C.c_uint64,
                                         C.c_void_p, C.POINTER(Stats), C.c_int]
+        lib.ref_genome_from_fasta.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
+        lib.ref_genome_free.argtypes = [C.c_void_p]
+        lib.ref_genome_info.argtypes = [C.c_void_p, P64, P64, P64]
+        lib.ref_genome_words.argtypes = [C.c_void_p, C.POINTER(P64), P64, C.POINTER(P64), P64]
+        lib.ref_genome_contig.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_char_p), P64, P64]
+        lib.ref_run_index.argtypes = [C.c_char_p, C.c_char_p, C.c_int]
+        lib.ref_load_index.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
         _r = lib
     return _r
 
@@ -293,6 +300,60 @@ class RefIndex:
         if rc:
             raise ValueError(rlib().ref_last_error().decode())
         return res, st.as_dict()
+
+
+# ----------------------------------------------------------------- reference files
+
+def ref_genome_from_fasta(path: str):
+    """PackedGenome::from_fasta of the reference -> (packed, nmask, length,
+    contigs [(name, start, length)], checksum), or (code, message) on error."""
+    lib = rlib()
+    h = C.c_void_p()
+    rc = lib.ref_genome_from_fasta(os.fsencode(path), C.byref(h))
+    if rc:
+        return rc, lib.ref_last_error().decode()
+    try:
+        n, nc, ck = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        lib.ref_genome_info(h, C.byref(n), C.byref(nc), C.byref(ck))
+        pp, pn = P64(), P64()
+        a, b = C.c_uint64(), C.c_uint64()
+        lib.ref_genome_words(h, C.byref(pp), C.byref(a), C.byref(pn), C.byref(b))
+        packed = np.ctypeslib.as_array(pp, (a.value,)).copy() if a.value else np.zeros(0, np.uint64)
+        nmask = np.ctypeslib.as_array(pn, (b.value,)).copy() if b.value else np.zeros(0, np.uint64)
+        contigs = []
+        for i in range(nc.value):
+            nm, st, ln = C.c_char_p(), C.c_uint64(), C.c_uint64()
+            lib.ref_genome_contig(h, i, C.byref(nm), C.byref(st), C.byref(ln))
+            contigs.append((nm.value.decode(), st.value, ln.value))
+        return packed, nmask, n.value, contigs, ck.value
+    finally:
+        lib.ref_genome_free(h)
+
+
+def ref_run_index(fasta: str, index_path: str, seed_size: int):
+    """run_index (REF src/driver.cpp:37-45): 0, or (code, message)."""
+    lib = rlib()
+    rc = lib.ref_run_index(os.fsencode(fasta), os.fsencode(index_path), seed_size)
+    return 0 if rc == 0 else (rc, lib.ref_last_error().decode())
+
+
+class RefLoadedIndex(RefIndex):
+    """load_index_file (REF src/seed_index.cpp:173-228) of the reference."""
+
+    def __init__(self, path: str):  # noqa: D401 -- no RefIndex.__init__ (no build)
+        lib = rlib()
+        h = C.c_void_p()
+        rc = lib.ref_load_index(os.fsencode(path), C.byref(h))
+        if rc:
+            self.h = None
+            raise RefError(rc, lib.ref_last_error().decode())
+        self.h = h.value
+
+
+class RefError(Exception):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code, self.msg = code, msg
 
 
 def ref_tracker_replay(merge_radius: int, ops: list[tuple[int, int, int]]) -> list[tuple[int, int, int, int]]:

@@ -7,6 +7,8 @@
 //   SeedIndex::build / lookup    (REF src/seed_index.cpp:80-143)
 //   bounded_distance / full_dp   (REF src/edit_distance.cpp:19-95)
 //   seed_offsets / Aligner::align(REF src/aligner.cpp:50-79,223-364)
+//   PackedGenome::from_fasta, save/load_index_file, run_index, run_align
+//                                (REF src/genome.cpp, seed_index.cpp:145-228, driver.cpp)
 // and the align_corpus threading pattern of the acceptance suite
 // (REF tests/acceptance/acceptance_main.cpp:52-67,106-124).
 // Used by tests/ as the parity pin for the C restatement, and by bench.py's
@@ -22,7 +24,10 @@
 #include <vector>
 
 #include "../include/snap_b200.h"
+#include <fstream>
+
 #include "seedaln/aligner.hpp"
+#include "seedaln/driver.hpp"
 #include "seedaln/edit_distance.hpp"
 #include "seedaln/errors.hpp"
 #include "seedaln/genome.hpp"
@@ -223,6 +228,103 @@ int ref_align_batch(void* hv, const sa_params* p, const char* bases, const uint6
     }
     if (stats) fill_stats(total, stats);
     return failed ? 1 : 0;
+}
+
+
+// ---------------------------------------------------------------- files
+
+// exception class -> sa status code (include/snap_b200.h)
+static int code_of(const std::exception_ptr& ep) {
+    try {
+        std::rethrow_exception(ep);
+    } catch (const ParseError& e) {
+        g_err = e.what();
+        return 4;
+    } catch (const FormatError& e) {
+        g_err = e.what();
+        return 3;
+    } catch (const IoError& e) {
+        g_err = e.what();
+        return 5;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 2;
+    }
+}
+
+struct RefGenome {
+    PackedGenome g;
+};
+
+int ref_genome_from_fasta(const char* path, void** out) {
+    try {
+        std::ifstream in(path, std::ios::binary);
+        if (!in) throw IoError(std::string("cannot open ") + path + " for reading");
+        auto* h = new RefGenome{PackedGenome::from_fasta(in)};
+        *out = h;
+        return 0;
+    } catch (...) {
+        return code_of(std::current_exception());
+    }
+}
+
+void ref_genome_free(void* h) { delete static_cast<RefGenome*>(h); }
+
+void ref_genome_info(void* hv, uint64_t* len, uint64_t* n_contigs, uint64_t* checksum) {
+    const PackedGenome& g = static_cast<RefGenome*>(hv)->g;
+    *len = g.size();
+    *n_contigs = g.contigs().size();
+    *checksum = g.checksum();
+}
+
+void ref_genome_words(void* hv, const uint64_t** packed, uint64_t* n_packed, const uint64_t** nmask,
+                      uint64_t* n_nmask) {
+    const PackedGenome& g = static_cast<RefGenome*>(hv)->g;
+    *packed = g.packed_words().data();
+    *n_packed = g.packed_words().size();
+    *nmask = g.n_mask_words().data();
+    *n_nmask = g.n_mask_words().size();
+}
+
+void ref_genome_contig(void* hv, uint64_t i, const char** name, uint64_t* start, uint64_t* len) {
+    const Contig& c = static_cast<RefGenome*>(hv)->g.contigs()[i];
+    *name = c.name.c_str();
+    *start = c.start;
+    *len = c.length;
+}
+
+// run_index (REF src/driver.cpp:37-45)
+int ref_run_index(const char* fasta, const char* index_path, int seed_size) {
+    try {
+        IndexOptions o;
+        o.fasta_path = fasta;
+        o.index_path = index_path;
+        o.seed_size = seed_size;
+        run_index(o);
+        return 0;
+    } catch (...) {
+        return code_of(std::current_exception());
+    }
+}
+
+// load_index_file (REF src/seed_index.cpp:173-228) -> a handle usable with
+// ref_align_batch / ref_lookup
+int ref_load_index(const char* path, void** out) {
+    try {
+        std::ifstream in(path, std::ios::binary);
+        if (!in) throw IoError(std::string("cannot open ") + path + " for reading");
+        auto [idx, g] = load_index_file(in);
+        auto* h = new RefHandle;
+        h->genome = std::move(g);
+        h->index = std::move(idx);
+        *out = h;
+        return 0;
+    } catch (...) {
+        return code_of(std::current_exception());
+    }
 }
 
 }  // extern "C"

@@ -30,7 +30,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SNAP_B200_LIB") or os.path.join(_HERE, "lib", "libsnapb200.so")
 SYNTH_PATH = os.path.join(_HERE, "lib", "libsnap_synth.so")
 
-SA_OK, SA_EINVAL, SA_ERUNTIME, SA_EFORMAT = 0, 1, 2, 3
+SA_OK, SA_EINVAL, SA_ERUNTIME, SA_EFORMAT, SA_EPARSE, SA_EIO = 0, 1, 2, 3, 4, 5
+SA_INDEX_SNAPIDX1, SA_INDEX_SNAPGPU1 = 0, 1
 
 RESULT_DTYPE = np.dtype(
     [("position", "<u8"), ("distance", "<i4"), ("gap", "<i4"), ("kind", "u1"),
@@ -51,6 +52,14 @@ REFERENCE_STAT_FIELDS = STAT_FIELDS[:16]
 
 class FormatError(RuntimeError):
     """Bad binary artifact or mismatched index (REF include/seedaln/errors.hpp:22-25)."""
+
+
+class ParseError(RuntimeError):
+    """Malformed FASTA/FASTQ text (REF include/seedaln/errors.hpp:10-19)."""
+
+
+class IoError(RuntimeError):
+    """File cannot be opened or written (REF include/seedaln/errors.hpp:27-30)."""
 
 
 class ResultKind(enum.IntEnum):  # REF aligner.hpp:32
@@ -113,6 +122,21 @@ def _load():
         "sa_last_timing": (C.c_int, [C.c_void_p, P(C.c_float), P(C.c_float)]),
         "sa_last_launches": (C.c_int, [C.c_void_p, P(C.c_uint64)]),
         "sa_last_kernel_times": (C.c_int, [C.c_void_p, P(C.c_float), P(C.c_float)]),
+        "sa_genome_from_fasta": (C.c_int, [C.c_char_p, P(C.c_void_p)]),
+        "sa_genome_from_words": (C.c_int, [P(C.c_uint64), C.c_uint64, P(C.c_uint64), C.c_uint64, C.c_uint64,
+                                           P(C.c_char_p), P(C.c_uint64), P(C.c_uint64), C.c_uint64,
+                                           P(C.c_void_p)]),
+        "sa_genome_free": (None, [C.c_void_p]),
+        "sa_genome_info": (C.c_int, [C.c_void_p, P(C.c_uint64), P(C.c_uint64), P(C.c_uint64)]),
+        "sa_genome_words": (C.c_int, [C.c_void_p, P(P(C.c_uint64)), P(C.c_uint64), P(P(C.c_uint64)),
+                                      P(C.c_uint64)]),
+        "sa_genome_contig": (C.c_int, [C.c_void_p, C.c_uint64, P(C.c_char_p), P(C.c_uint64), P(C.c_uint64)]),
+        "sa_create_from_genome": (C.c_int, [C.c_void_p, C.c_int32, P(C.c_int32), C.c_int32, P(C.c_void_p)]),
+        "sa_index_write": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_char_p]),
+        "sa_index_load": (C.c_int, [C.c_char_p, P(C.c_int32), C.c_int32, C.c_int32, P(C.c_void_p),
+                                    P(C.c_void_p)]),
+        "sa_index_csr": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, P(C.c_uint64), P(C.c_uint64),
+                                   P(C.c_uint64), P(C.c_uint64), P(C.c_uint64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -137,6 +161,10 @@ def _raise(code: int, ctx=None):
         raise ValueError(msg)
     if code == SA_EFORMAT:
         raise FormatError(msg)
+    if code == SA_EPARSE:
+        raise ParseError(msg)
+    if code == SA_EIO:
+        raise IoError(msg)
     raise RuntimeError(msg)
 
 
@@ -239,15 +267,17 @@ def pack_sequence(seq: bytes | np.ndarray) -> tuple[np.ndarray, np.ndarray]:
 
 
 class PackedGenome:
-    """2-bit packed genome + N mask (REF include/seedaln/genome.hpp:36-85).
-    One contig covering [0, size())."""
+    """2-bit packed genome + N mask + contig table (REF include/seedaln/genome.hpp:36-100).
+    Without an explicit contig table the genome is one contig "chr1"."""
 
-    def __init__(self, packed: np.ndarray, nmask: np.ndarray, length: int):
+    def __init__(self, packed: np.ndarray, nmask: np.ndarray, length: int,
+                 contigs: Sequence[tuple[str, int, int]] | None = None):
         self.packed = np.ascontiguousarray(packed, dtype=np.uint64)
         self.nmask = np.ascontiguousarray(nmask, dtype=np.uint64)
         self.length = int(length)
         if self.packed.size != (self.length + 31) // 32 or self.nmask.size != (self.length + 63) // 64:
             raise FormatError("packed/n-mask sizes do not match the genome length")
+        self._contigs = [tuple(c) for c in contigs] if contigs is not None else [("chr1", 0, self.length)]
 
     @classmethod
     def from_sequence(cls, seq: bytes | str) -> "PackedGenome":
@@ -258,9 +288,71 @@ class PackedGenome:
 
     @classmethod
     def from_contigs(cls, named_seqs: Sequence[tuple[str, str]]) -> "PackedGenome":
-        # contigs are concatenated; alignment windows ignore contig boundaries
-        # (REF src/genome.cpp:114-123)
-        return cls.from_sequence("".join(s for _, s in named_seqs))
+        # REF src/genome.cpp:96-112: contigs tile the genome in order
+        # (alignment windows ignore contig boundaries, REF genome.cpp:114-123)
+        contigs, start = [], 0
+        for name, sq in named_seqs:
+            contigs.append((name, start, len(sq)))
+            start += len(sq)
+        g = cls.from_sequence("".join(sq for _, sq in named_seqs))
+        g._contigs = contigs
+        return g
+
+    @classmethod
+    def from_fasta(cls, path: str) -> "PackedGenome":  # REF src/genome.cpp:48-94
+        lib = _load()
+        h = C.c_void_p()
+        rc = lib.sa_genome_from_fasta(os.fsencode(path), C.byref(h))
+        if rc:
+            _raise(rc)
+        try:
+            return cls._from_handle(h.value)
+        finally:
+            lib.sa_genome_free(h)
+
+    @classmethod
+    def _from_handle(cls, h) -> "PackedGenome":
+        lib = _load()
+        n, nc = C.c_uint64(), C.c_uint64()
+        lib.sa_genome_info(h, C.byref(n), C.byref(nc), None)
+        pp, pn = C.POINTER(C.c_uint64)(), C.POINTER(C.c_uint64)()
+        np_, nn = C.c_uint64(), C.c_uint64()
+        lib.sa_genome_words(h, C.byref(pp), C.byref(np_), C.byref(pn), C.byref(nn))
+        packed = np.ctypeslib.as_array(pp, (np_.value,)).copy() if np_.value else np.zeros(0, np.uint64)
+        nmask = np.ctypeslib.as_array(pn, (nn.value,)).copy() if nn.value else np.zeros(0, np.uint64)
+        contigs = []
+        for i in range(nc.value):
+            nm, st, ln = C.c_char_p(), C.c_uint64(), C.c_uint64()
+            lib.sa_genome_contig(h, i, C.byref(nm), C.byref(st), C.byref(ln))
+            contigs.append((nm.value.decode(), st.value, ln.value))
+        return cls(packed, nmask, n.value, contigs)
+
+    def _handle(self):
+        """A native sa_genome for this genome (caller frees with sa_genome_free)."""
+        lib = _load()
+        names = (C.c_char_p * max(1, len(self._contigs)))(*[c[0].encode() for c in self._contigs])
+        starts = np.array([c[1] for c in self._contigs], np.uint64)
+        lens = np.array([c[2] for c in self._contigs], np.uint64)
+        h = C.c_void_p()
+        rc = lib.sa_genome_from_words(_u64p(self.packed), self.packed.size, _u64p(self.nmask), self.nmask.size,
+                                      self.length, names, _u64p(starts), _u64p(lens), len(self._contigs),
+                                      C.byref(h))
+        if rc:
+            _raise(rc)
+        return h
+
+    def contigs(self) -> list[tuple[str, int, int]]:  # REF genome.hpp:91 (name, start, length)
+        return list(self._contigs)
+
+    def checksum(self) -> int:  # REF src/genome.cpp:158-179
+        lib = _load()
+        h = self._handle()
+        try:
+            v = C.c_uint64()
+            lib.sa_genome_info(h, None, None, C.byref(v))
+            return v.value
+        finally:
+            lib.sa_genome_free(h)
 
     def size(self) -> int:
         return self.length
@@ -275,6 +367,49 @@ class PackedGenome:
             raise IndexError(f"genome position {pos} past end {self.length}")
         n = min(length, self.length - pos)
         return "".join("ACGTN"[self.at(pos + i)] for i in range(n))
+
+    def to_contig_coordinate(self, pos: int) -> tuple[str, int]:  # REF genome.cpp:121-131
+        if pos >= self.length:
+            raise IndexError(f"genome position {pos} past end {self.length}")
+        starts = [c[1] for c in self._contigs]
+        import bisect
+        i = bisect.bisect_right(starts, pos) - 1
+        return self._contigs[i][0], pos - self._contigs[i][1]
+
+
+def save_index_file(seed_size: int, g: PackedGenome, path: str, fmt: int = SA_INDEX_SNAPIDX1,
+                    device: int = 0) -> None:
+    """run_index / save_index_file (REF src/driver.cpp:37-45, src/seed_index.cpp:145-170):
+    CSR tables built on the GPU; SNAPIDX1 byte-identical to the reference's."""
+    lib = _load()
+    h = g._handle()
+    try:
+        rc = lib.sa_index_write(h, seed_size, fmt, device, os.fsencode(path))
+        if rc:
+            _raise(rc)
+    finally:
+        lib.sa_genome_free(h)
+
+
+def index_csr(g: PackedGenome, seed_size: int, device: int = 0) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """The reference SeedIndex's keys_/offsets_/positions_ (REF seed_index.hpp:69-71), GPU-built."""
+    lib = _load()
+    h = g._handle()
+    try:
+        nk, npos = C.c_uint64(0), C.c_uint64(0)
+        rc = lib.sa_index_csr(h, seed_size, device, C.byref(nk), C.byref(npos), None, None, None)
+        if rc:
+            _raise(rc)
+        keys = np.zeros(nk.value, np.uint64)
+        offs = np.zeros(nk.value + 1, np.uint64)
+        pos = np.zeros(npos.value, np.uint64)
+        rc = lib.sa_index_csr(h, seed_size, device, C.byref(nk), C.byref(npos), _u64p(keys), _u64p(offs),
+                              _u64p(pos))
+        if rc:
+            _raise(rc)
+        return keys, offs, pos
+    finally:
+        lib.sa_genome_free(h)
 
 
 # ----------------------------------------------------------------------- index
@@ -314,6 +449,29 @@ class SeedIndex:
         if ctx and _lib is not None:
             _lib.sa_destroy(ctx)
             self._ctx = None
+
+    @classmethod
+    def load(cls, path: str, devices: Iterable[int] | None = None, verify: bool = True
+             ) -> tuple["SeedIndex", PackedGenome]:
+        """load_index_file (REF src/seed_index.cpp:173-228) -> (index, genome)."""
+        lib = _load()
+        devs = list(devices) if devices is not None else [0]
+        darr = (C.c_int32 * len(devs))(*devs)
+        gh, ctx = C.c_void_p(), C.c_void_p()
+        rc = lib.sa_index_load(os.fsencode(path), darr, len(devs), 1 if verify else 0, C.byref(gh), C.byref(ctx))
+        if rc:
+            _raise(rc)
+        try:
+            g = PackedGenome._from_handle(gh.value)
+        finally:
+            lib.sa_genome_free(gh)
+        d, t, b = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        lib.sa_index_info(ctx.value, C.byref(d), C.byref(t), C.byref(b))
+        # the seed size is the file's; read it back from the header
+        with open(path, "rb") as f:
+            f.seek(12)
+            s = int.from_bytes(f.read(4), "little")
+        return cls(ctx.value, s, g), g
 
     def seed_size(self) -> int:
         return self._seed_size

@@ -19,8 +19,8 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "lib")
 OBJ = os.path.join(HERE, "build", "obj")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-CUDA_SOURCES = ["index.cu", "align.cu", "capi.cu"]
-HEADERS = ["common.cuh", "align_kernels.cuh", "device_index.h"]
+CUDA_SOURCES = ["index.cu", "align.cu", "capi.cu", "csr.cu", "genome_io.cpp"]
+HEADERS = ["common.cuh", "align_kernels.cuh", "device_index.h", "host_common.h"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
@@ -50,7 +50,7 @@ def build(verbose: bool = False) -> dict[str, str]:
     jobs = []
     for src in CUDA_SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(OBJ, src.replace(".cu", ".o"))
+        o = os.path.join(OBJ, os.path.splitext(src)[0] + ".o")
         objs.append(o)
         if _stale(o, [s] + hdrs):
             jobs.append([NVCC, *NVCC_FLAGS, "-c", s, "-o", o])
@@ -79,7 +79,7 @@ def build_variant(name: str, defines: list[str]) -> str:
     os.makedirs(vobj, exist_ok=True)
     objs, jobs = [], []
     for src in CUDA_SOURCES:
-        o = os.path.join(vobj, src.replace(".cu", ".o"))
+        o = os.path.join(vobj, os.path.splitext(src)[0] + ".o")
         objs.append(o)
         jobs.append([NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", o])
     with ThreadPoolExecutor(max_workers=len(jobs)) as ex:

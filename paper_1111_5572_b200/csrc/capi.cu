@@ -22,12 +22,25 @@
 #include "../../include/snap_b200.h"
 #include "align_kernels.cuh"
 #include "device_index.h"
+#include "host_common.h"
 
 using namespace sab;
 
 namespace {
 
 thread_local std::string g_thread_err;
+
+}  // namespace
+
+namespace sab {
+void set_thread_error(const std::string& msg) { g_thread_err = msg; }
+int fail_thread(int code, const std::string& msg) {
+    g_thread_err = msg;
+    return code;
+}
+}  // namespace sab
+
+namespace {
 
 constexpr int kPipeStages = 3;  // chunk buffers in flight per replica (copy / kernel / copy-back)
 constexpr int kCtlWords = 4;  // cursor_fast, cursor_slow, overflow_count, error_flag

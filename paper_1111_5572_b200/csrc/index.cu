@@ -281,6 +281,34 @@ void free_device_index(DeviceIndex* ix) {
     *ix = DeviceIndex{};
 }
 
+int upload_planes(const uint64_t* h_packed, uint64_t n_packed, const uint64_t* h_nmask, uint64_t n_nmask,
+                  uint64_t glen, cudaStream_t st, uint4** d_planes, std::string& err) {
+    const uint64_t n_blocks = (glen + 31) / 32 + 2;
+    *d_planes = nullptr;
+#define UP(x)                                                              \
+    do {                                                                   \
+        cudaError_t e_ = (x);                                              \
+        if (e_ != cudaSuccess) {                                           \
+            err = std::string(#x) + ": " + cudaGetErrorString(e_);         \
+            if (*d_planes) cudaFree(*d_planes);                            \
+            *d_planes = nullptr;                                           \
+            return 2;                                                      \
+        }                                                                  \
+    } while (0)
+    UP(cudaMalloc(d_planes, n_blocks * sizeof(uint4)));
+    Scratch up;
+    uint64_t *d_packed = nullptr, *d_nmask = nullptr;
+    UP(up.alloc(&d_packed, n_packed + 1));
+    UP(up.alloc(&d_nmask, n_nmask + 1));
+    UP(cudaMemcpyAsync(d_packed, h_packed, n_packed * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+    UP(cudaMemcpyAsync(d_nmask, h_nmask, n_nmask * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+    planes_kernel<<<grid_for(n_blocks, 256), 256, 0, st>>>(d_packed, n_packed, d_nmask, glen, *d_planes, n_blocks);
+    UP(cudaGetLastError());
+    UP(cudaStreamSynchronize(st));
+#undef UP
+    return 0;
+}
+
 int build_device_index(const uint64_t* h_packed, uint64_t n_packed, const uint64_t* h_nmask,
                        uint64_t n_nmask, uint64_t glen, int s, cudaStream_t st, DeviceIndex* out,
                        std::string& err) {
@@ -292,18 +320,9 @@ int build_device_index(const uint64_t* h_packed, uint64_t n_packed, const uint64
     const int end_bit = s <= 31 ? 2 * s + 1 : 64;
 
     // ---- genome planes
-    CK(cudaMalloc(&ix.planes, ix.n_blocks * sizeof(uint4)));
-    {
-        Scratch up;
-        uint64_t *d_packed = nullptr, *d_nmask = nullptr;
-        CK(up.alloc(&d_packed, n_packed + 1));
-        CK(up.alloc(&d_nmask, n_nmask + 1));
-        CK(cudaMemcpyAsync(d_packed, h_packed, n_packed * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(d_nmask, h_nmask, n_nmask * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
-        planes_kernel<<<grid_for(ix.n_blocks, 256), 256, 0, st>>>(d_packed, n_packed, d_nmask, glen,
-                                                                   ix.planes, ix.n_blocks);
-        CK(cudaGetLastError());
-        CK(cudaStreamSynchronize(st));
+    if (upload_planes(h_packed, n_packed, h_nmask, n_nmask, glen, st, &ix.planes, err) != 0) {
+        free_device_index(&ix);
+        return 2;
     }
 
     // ---- table sized from the window count (upper bound on distinct keys):
