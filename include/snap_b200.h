@@ -159,6 +159,9 @@ int sa_lookup_batch(sa_context* ctx, const char* seeds, uint64_t n_seeds,
                     uint32_t* counts, uint64_t* fwd_out, uint32_t* n_fwd,
                     uint64_t* rc_out, uint32_t* n_rc, uint32_t cap);
 
+/* Seed size the context's index was built with (REF SeedIndex::seed_size, seed_index.hpp:60). */
+int sa_index_seed_size(const sa_context* ctx, int32_t* seed_size);
+
 /* Index shape: distinct seeds (REF SeedIndex::distinct_seeds, seed_index.hpp:62),
  * total positions (SeedIndex::total_positions, :61) and device bytes held. */
 int sa_index_info(const sa_context* ctx, uint64_t* distinct_seeds,
@@ -242,6 +245,50 @@ int sa_index_load(const char* path, const int32_t* devices, int32_t n_devices, i
  * positions; on return the sizes.  NULL arrays: sizes only. */
 int sa_index_csr(const sa_genome* g, int32_t seed_size, int32_t device, uint64_t* n_keys, uint64_t* n_positions,
                  uint64_t* keys, uint64_t* offsets, uint64_t* positions);
+
+/* ------------------------------------------------------------------ FASTQ -> SAM driver
+ * AlignOptions (REF include/seedaln/driver.hpp:20-32) plus the devices to use. */
+typedef struct sa_align_options {
+    const char* index_path;    /* SNAPIDX1 or SNAPGPU1 */
+    const char* fastq_path;
+    const char* output_path;   /* SAM */
+    sa_params params;
+    uint32_t threads;          /* host workers; 0 = hardware concurrency */
+    uint64_t chunk_min_bytes;  /* scheduler minimum chunk (REF scheduler.cpp:8-16) */
+    int32_t stable_order;      /* write records in input order */
+    uint64_t tolerance;        /* truth-scoring window, bases */
+    const char* report_path;   /* optional key=value metrics file (NULL/"" = none) */
+    const char* command_line;  /* @PG CL: */
+    const int32_t* devices;    /* GPUs (NULL = device 0) */
+    int32_t n_devices;
+    int32_t verify_index;      /* see sa_index_load */
+} sa_align_options;
+
+/* EvalReport (REF include/seedaln/eval.hpp:24-46). */
+typedef struct sa_eval_report {
+    uint64_t total, single, multiple, notfound, correct, wrong, no_truth;
+    double elapsed_seconds;
+    sa_stats stats;
+} sa_eval_report;
+
+/* AlignOptions{} defaults (REF driver.hpp:20-32). */
+void sa_default_align_options(sa_align_options* out);
+
+/* run_index (REF src/driver.cpp:37-45): FASTA -> index file (see sa_index_write). */
+int sa_run_index(const char* fasta_path, const char* index_path, int32_t seed_size, int32_t format,
+                 int32_t device);
+
+/* run_align (REF src/driver.cpp:47-156): index + FASTQ -> SAM, one record
+ * per read (REF src/sam.cpp:11-87), the reference's chunk scheduler over host
+ * workers, every chunk's reads aligned on the GPU in one batch, truth scored
+ * from read names (REF src/eval.cpp:12-33).  With stable_order the SAM is
+ * byte-identical to the reference's.  Errors carry the reference's exception
+ * class (SA_EINVAL / SA_EFORMAT / SA_EPARSE / SA_EIO) and message. */
+int sa_run_align(const sa_align_options* opt, sa_eval_report* report);
+
+/* EvalReport::to_text (REF src/eval.cpp:75-120) into out (capacity cap, NUL
+ * terminated); *len = full length. */
+int sa_report_text(const sa_eval_report* r, char* out, uint64_t cap, uint64_t* len);
 
 #ifdef __cplusplus
 }

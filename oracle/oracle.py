@@ -141,6 +141,8 @@ def rlib():
         lib.ref_genome_contig.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_char_p), P64, P64]
         lib.ref_run_index.argtypes = [C.c_char_p, C.c_char_p, C.c_int]
         lib.ref_load_index.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
+        lib.ref_run_simulate.argtypes = [C.c_char_p, C.c_char_p, C.c_uint64, C.c_uint64, C.c_double,
+                                         C.c_double, C.c_double, C.c_double, C.c_uint64]
         _r = lib
     return _r
 
@@ -335,6 +337,37 @@ def ref_run_index(fasta: str, index_path: str, seed_size: int):
     lib = rlib()
     rc = lib.ref_run_index(os.fsencode(fasta), os.fsencode(index_path), seed_size)
     return 0 if rc == 0 else (rc, lib.ref_last_error().decode())
+
+
+def ref_run_simulate(fasta: str, out: str, count: int, read_length: int = 100, snp_rate: float = 0.0009,
+                     indel_mutation_rate: float = 0.0001, seq_error_rate: float = 0.02,
+                     indel_error_fraction: float = 0.0, rng_seed: int = 1):
+    """run_simulate (REF src/driver.cpp:158-168): FASTQ with truth-encoded names."""
+    lib = rlib()
+    rc = lib.ref_run_simulate(os.fsencode(fasta), os.fsencode(out), count, read_length, snp_rate,
+                              indel_mutation_rate, seq_error_rate, indel_error_fraction, rng_seed)
+    if rc:
+        raise RefError(rc, lib.ref_last_error().decode())
+
+
+REF_CLI = os.path.join(HERE, "_ref", "seedaln_ref_cli")
+
+
+def ref_run_align(index_path: str, fastq: str, out: str, params, threads: int = 1, chunk_min: int = 4 << 20,
+                  stable: bool = True, tolerance: int = 50, report_path: str | None = None,
+                  command_line: str = "seedaln align") -> str:
+    """run_align (REF src/driver.cpp:47-156) of the reference, run out of
+    process (oracle/ref_cli.cpp explains why); returns EvalReport::to_text()."""
+    p = params
+    args = [REF_CLI, "align", index_path, fastq, out, str(p.seed_size), str(p.seeds_to_try), str(p.max_distance),
+            str(p.confidence_threshold), str(p.max_hits), str(p.bucket_size), "1" if p.force_max_dlimit else "0",
+            str(threads), str(chunk_min), "1" if stable else "0", str(tolerance), report_path or "-", command_line]
+    r = subprocess.run(args, capture_output=True, text=True)
+    if r.returncode != 0:
+        line = (r.stdout.strip().splitlines() or ["ERROR 2 " + r.stderr.strip()])[-1]
+        _, code, msg = line.split(" ", 2)
+        raise RefError(int(code), msg)
+    return r.stdout
 
 
 class RefLoadedIndex(RefIndex):

@@ -327,4 +327,28 @@ int ref_load_index(const char* path, void** out) {
     }
 }
 
+
+// run_simulate (REF src/driver.cpp:158-168) with a SimProfile
+int ref_run_simulate(const char* fasta, const char* out_path, uint64_t count, uint64_t read_length,
+                     double snp_rate, double indel_mutation_rate, double seq_error_rate,
+                     double indel_error_fraction, uint64_t rng_seed) {
+    try {
+        SimulateOptions o;
+        o.fasta_path = fasta;
+        o.output_path = out_path;
+        o.count = count;
+        o.profile.read_length = read_length;
+        o.profile.snp_rate = snp_rate;
+        o.profile.indel_mutation_rate = indel_mutation_rate;
+        o.profile.seq_error_rate = seq_error_rate;
+        o.profile.indel_error_fraction = indel_error_fraction;
+        o.profile.rng_seed = rng_seed;
+        run_simulate(o);
+        return 0;
+    } catch (...) {
+        return code_of(std::current_exception());
+    }
+}
+
+
 }  // extern "C"

@@ -84,6 +84,19 @@ class _Stats(C.Structure):
     _fields_ = [(f, C.c_uint64) for f in STAT_FIELDS]
 
 
+class _AlignOptions(C.Structure):  # sa_align_options
+    _fields_ = [("index_path", C.c_char_p), ("fastq_path", C.c_char_p), ("output_path", C.c_char_p),
+                ("params", _Params), ("threads", C.c_uint32), ("chunk_min_bytes", C.c_uint64),
+                ("stable_order", C.c_int32), ("tolerance", C.c_uint64), ("report_path", C.c_char_p),
+                ("command_line", C.c_char_p), ("devices", C.POINTER(C.c_int32)), ("n_devices", C.c_int32),
+                ("verify_index", C.c_int32)]
+
+
+class _EvalReport(C.Structure):  # sa_eval_report
+    _fields_ = [(f, C.c_uint64) for f in ("total", "single", "multiple", "notfound", "correct", "wrong",
+                                           "no_truth")] + [("elapsed_seconds", C.c_double), ("stats", _Stats)]
+
+
 _lib = None
 
 
@@ -137,6 +150,11 @@ def _load():
                                     P(C.c_void_p)]),
         "sa_index_csr": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, P(C.c_uint64), P(C.c_uint64),
                                    P(C.c_uint64), P(C.c_uint64), P(C.c_uint64)]),
+        "sa_index_seed_size": (C.c_int, [C.c_void_p, P(C.c_int32)]),
+        "sa_default_align_options": (None, [P(_AlignOptions)]),
+        "sa_run_index": (C.c_int, [C.c_char_p, C.c_char_p, C.c_int32, C.c_int32, C.c_int32]),
+        "sa_run_align": (C.c_int, [P(_AlignOptions), P(_EvalReport)]),
+        "sa_report_text": (C.c_int, [P(_EvalReport), C.c_char_p, C.c_uint64, P(C.c_uint64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -465,13 +483,9 @@ class SeedIndex:
             g = PackedGenome._from_handle(gh.value)
         finally:
             lib.sa_genome_free(gh)
-        d, t, b = C.c_uint64(), C.c_uint64(), C.c_uint64()
-        lib.sa_index_info(ctx.value, C.byref(d), C.byref(t), C.byref(b))
-        # the seed size is the file's; read it back from the header
-        with open(path, "rb") as f:
-            f.seek(12)
-            s = int.from_bytes(f.read(4), "little")
-        return cls(ctx.value, s, g), g
+        s = C.c_int32()
+        lib.sa_index_seed_size(ctx.value, C.byref(s))
+        return cls(ctx.value, s.value, g), g
 
     def seed_size(self) -> int:
         return self._seed_size
@@ -700,3 +714,65 @@ class PinnedBuffer:
         if getattr(self, "ptr", None) and _lib is not None:
             _lib.sa_host_free(self.ptr)
             self.ptr = None
+
+
+# ----------------------------------------------------------------------- driver
+
+@dataclass
+class EvalReport:  # REF include/seedaln/eval.hpp:24-46
+    total: int = 0
+    single: int = 0
+    multiple: int = 0
+    notfound: int = 0
+    correct: int = 0
+    wrong: int = 0
+    no_truth: int = 0
+    elapsed_seconds: float = 0.0
+    stats: AlignStats = field(default_factory=AlignStats)
+    _c: object = None
+
+    def to_text(self) -> str:  # REF src/eval.cpp:75-120
+        lib = _load()
+        n = C.c_uint64()
+        lib.sa_report_text(C.byref(self._c), None, 0, C.byref(n))
+        buf = C.create_string_buffer(n.value + 1)
+        lib.sa_report_text(C.byref(self._c), buf, n.value + 1, C.byref(n))
+        return buf.value.decode()
+
+
+def run_index(fasta_path: str, index_path: str, seed_size: int = 20, fmt: int = SA_INDEX_SNAPIDX1,
+              device: int = 0) -> None:
+    """run_index (REF src/driver.cpp:37-45) with the CSR built on the GPU."""
+    rc = _load().sa_run_index(os.fsencode(fasta_path), os.fsencode(index_path), seed_size, fmt, device)
+    if rc:
+        _raise(rc)
+
+
+def run_align(index_path: str, fastq_path: str, output_path: str, params: AlignerParams | None = None,
+              threads: int = 1, chunk_min_bytes: int = 4 << 20, stable_order: bool = False, tolerance: int = 50,
+              report_path: str | None = None, command_line: str = "seedaln align",
+              devices: Iterable[int] | None = None, verify_index: bool = True) -> EvalReport:
+    """run_align (REF src/driver.cpp:47-156): FASTQ -> SAM through the GPU."""
+    lib = _load()
+    o = _AlignOptions()
+    lib.sa_default_align_options(C.byref(o))
+    keep = [os.fsencode(index_path), os.fsencode(fastq_path), os.fsencode(output_path),
+            os.fsencode(report_path) if report_path else None, command_line.encode()]
+    o.index_path, o.fastq_path, o.output_path, o.report_path, o.command_line = keep
+    o.params = (params or AlignerParams())._c()
+    o.threads = threads
+    o.chunk_min_bytes = chunk_min_bytes
+    o.stable_order = 1 if stable_order else 0
+    o.tolerance = tolerance
+    devs = list(devices) if devices is not None else [0]
+    darr = (C.c_int32 * len(devs))(*devs)
+    o.devices = darr
+    o.n_devices = len(devs)
+    o.verify_index = 1 if verify_index else 0
+    rep = _EvalReport()
+    rc = lib.sa_run_align(C.byref(o), C.byref(rep))
+    del keep
+    if rc:
+        _raise(rc)
+    return EvalReport(rep.total, rep.single, rep.multiple, rep.notfound, rep.correct, rep.wrong, rep.no_truth,
+                      rep.elapsed_seconds, AlignStats._from_c(rep.stats), rep)

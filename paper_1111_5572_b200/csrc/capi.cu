@@ -603,6 +603,12 @@ int sa_index_info(const sa_context* ctx, uint64_t* distinct_seeds, uint64_t* tot
     return SA_OK;
 }
 
+int sa_index_seed_size(const sa_context* ctx, int32_t* seed_size) {
+    if (!ctx || !seed_size) return fail(nullptr, SA_EINVAL, "null argument");
+    *seed_size = ctx->seed_size;
+    return SA_OK;
+}
+
 int sa_align_batch(sa_context* ctx, const sa_params* params, const char* bases,
                    const uint64_t* offsets, uint64_t n_reads, sa_result* results, sa_stats* stats) {
     if (!ctx) return fail(nullptr, SA_EINVAL, "null context");
