@@ -428,7 +428,6 @@ int sa_run_align(const sa_align_options* opt, sa_eval_report* report) {
     if (!opt || !opt->index_path || !opt->fastq_path || !opt->output_path)
         return fail_thread(SA_EINVAL, "null argument");
     if (int rc = sa_validate_params(&opt->params)) return rc;  // REF driver.cpp:48
-    const auto t_start = std::chrono::steady_clock::now();
     sa_genome* g_raw = nullptr;
     sa_context* ctx = nullptr;
     // REF driver.cpp:50-55: load the index, then the seed-size check
@@ -560,6 +559,7 @@ int sa_run_align(const sa_align_options* opt, sa_eval_report* report) {
         total.merge(local);
         add_stats(stats_total, local_stats);
     };
+    const auto t_start = std::chrono::steady_clock::now();  // REF driver.cpp:139: workers only
     if (workers == 1) {
         worker();
     } else {
