@@ -246,6 +246,38 @@ int sa_index_load(const char* path, const int32_t* devices, int32_t n_devices, i
 int sa_index_csr(const sa_genome* g, int32_t seed_size, int32_t device, uint64_t* n_keys, uint64_t* n_positions,
                  uint64_t* keys, uint64_t* offsets, uint64_t* positions);
 
+/* ------------------------------------------------------------------ referee
+ * The exhaustive referee of the evaluation harness on the GPU: OracleContext,
+ * oracle_scan, oracle_align (REF include/seedaln/eval.hpp:49-117,
+ * src/eval.cpp:122-306).  Exact; used for accuracy evaluation at scale. */
+typedef struct sa_referee sa_referee;
+
+/* OracleHit (REF eval.hpp:93-97). */
+typedef struct sa_referee_hit {
+    uint64_t position;
+    int32_t distance;
+    uint8_t direction;
+    uint8_t reserved[3];
+} sa_referee_hit;
+
+/* OracleContext(g) (REF src/eval.cpp:155-165): genome planes and the q-gram
+ * tables (q_hi sized to the genome, then 7, 6, 5) built on `device`. */
+int sa_referee_create(const sa_genome* g, int32_t device, sa_referee** out);
+void sa_referee_destroy(sa_referee* r);
+
+/* oracle_align (REF src/eval.cpp:270-306) per read: staged limits, the
+ * aligner's BestTracker and classify_confidence.  Reads as in sa_align_batch;
+ * SA_EINVAL on a character outside {A,C,G,T,N} (REF genome.cpp:194-195). */
+int sa_referee_align(sa_referee* r, const sa_params* params, const char* bases, const uint64_t* offsets,
+                     uint64_t n_reads, sa_result* results);
+
+/* oracle_scan (REF src/eval.cpp:244-268) per read: read i's hits (best-first,
+ * ties by position, Forward first) are hits[hit_offsets[i] .. hit_offsets[i+1]).
+ * hit_offsets has n_reads + 1 entries; hits (capacity cap) may be NULL to size. */
+int sa_referee_scan(sa_referee* r, int32_t d_limit, int32_t bucket_size, const char* bases,
+                    const uint64_t* offsets, uint64_t n_reads, uint64_t* hit_offsets, sa_referee_hit* hits,
+                    uint64_t cap);
+
 /* ------------------------------------------------------------------ FASTQ -> SAM driver
  * AlignOptions (REF include/seedaln/driver.hpp:20-32) plus the devices to use. */
 typedef struct sa_align_options {

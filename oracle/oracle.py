@@ -141,6 +141,14 @@ def rlib():
         lib.ref_genome_contig.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_char_p), P64, P64]
         lib.ref_run_index.argtypes = [C.c_char_p, C.c_char_p, C.c_int]
         lib.ref_load_index.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
+        lib.ref_referee_create.argtypes = [P64, C.c_uint64, P64, C.c_uint64, C.c_uint64]
+        lib.ref_referee_create.restype = C.c_void_p
+        lib.ref_referee_destroy.argtypes = [C.c_void_p]
+        lib.ref_oracle_align.argtypes = [C.c_void_p, C.POINTER(Params), C.c_void_p, P64, C.c_uint64, C.c_void_p,
+                                         C.c_int]
+        lib.ref_oracle_scan.argtypes = [C.c_void_p, C.c_char_p, C.c_uint64, C.c_int, C.c_int, P64,
+                                        C.POINTER(C.c_int32), C.POINTER(C.c_uint8), C.c_uint64]
+        lib.ref_oracle_scan.restype = C.c_int64
         lib.ref_run_simulate.argtypes = [C.c_char_p, C.c_char_p, C.c_uint64, C.c_uint64, C.c_double,
                                          C.c_double, C.c_double, C.c_double, C.c_uint64]
         _r = lib
@@ -381,6 +389,46 @@ class RefLoadedIndex(RefIndex):
             self.h = None
             raise RefError(rc, lib.ref_last_error().decode())
         self.h = h.value
+
+
+class RefReferee:
+    """OracleContext + oracle_align / oracle_scan of the reference (REF src/eval.cpp:122-306)."""
+
+    def __init__(self, packed, nmask, length):
+        lib = rlib()
+        self.packed = np.ascontiguousarray(packed, np.uint64)
+        self.nmask = np.ascontiguousarray(nmask, np.uint64)
+        self.h = lib.ref_referee_create(_u64p(self.packed), self.packed.size, _u64p(self.nmask), self.nmask.size,
+                                        length)
+        if not self.h:
+            raise RuntimeError(lib.ref_last_error().decode())
+
+    def __del__(self):
+        if _r is not None and getattr(self, "h", None):
+            _r.ref_referee_destroy(self.h)
+            self.h = None
+
+    def align(self, params, bases, offsets, threads=8):
+        offsets = np.ascontiguousarray(offsets, np.uint64)
+        n = offsets.size - 1
+        res = np.zeros(n, RESULT_DTYPE)
+        b = np.ascontiguousarray(bases, np.uint8)
+        p = Params.of(params)
+        if rlib().ref_oracle_align(self.h, C.byref(p), b.ctypes.data, _u64p(offsets), n, res.ctypes.data, threads):
+            raise RefError(1, rlib().ref_last_error().decode())
+        return res
+
+    def scan(self, read: bytes, d_limit: int, bucket: int, cap: int = 1 << 16):
+        pos = np.zeros(cap, np.uint64)
+        dist = np.zeros(cap, np.int32)
+        dr = np.zeros(cap, np.uint8)
+        n = rlib().ref_oracle_scan(self.h, read, len(read), d_limit, bucket, _u64p(pos),
+                                   dist.ctypes.data_as(C.POINTER(C.c_int32)), dr.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                   cap)
+        if n < 0:
+            raise RefError(1, rlib().ref_last_error().decode())
+        n = min(n, cap)
+        return [(int(pos[i]), int(dist[i]), int(dr[i])) for i in range(n)]
 
 
 class RefError(Exception):

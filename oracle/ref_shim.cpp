@@ -17,6 +17,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <memory>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -30,6 +31,7 @@
 #include "seedaln/driver.hpp"
 #include "seedaln/edit_distance.hpp"
 #include "seedaln/errors.hpp"
+#include "seedaln/eval.hpp"
 #include "seedaln/genome.hpp"
 #include "seedaln/seed_index.hpp"
 
@@ -350,5 +352,87 @@ int ref_run_simulate(const char* fasta, const char* out_path, uint64_t count, ui
     }
 }
 
+
+
+// ---------------------------------------------------------------- referee
+
+struct RefReferee {
+    PackedGenome g;
+    std::unique_ptr<OracleContext> ctx;
+};
+
+// OracleContext over a one-contig genome (REF src/eval.cpp:155-165)
+void* ref_referee_create(const uint64_t* packed, uint64_t n_packed, const uint64_t* nmask, uint64_t n_nmask,
+                         uint64_t len) {
+    try {
+        auto* h = new RefReferee;
+        std::vector<Contig> contigs{{"c1", 0, len}};
+        h->g.adopt_storage(std::move(contigs), len, std::vector<uint64_t>(packed, packed + n_packed),
+                           std::vector<uint64_t>(nmask, nmask + n_nmask));
+        h->ctx = std::make_unique<OracleContext>(h->g);
+        return h;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
+void ref_referee_destroy(void* h) { delete static_cast<RefReferee*>(h); }
+
+// oracle_align (REF src/eval.cpp:270-306) over a batch, `threads` workers
+int ref_oracle_align(void* hv, const sa_params* p, const char* bases, const uint64_t* offsets, uint64_t n,
+                     sa_result* results, int threads) {
+    auto* h = static_cast<RefReferee*>(hv);
+    AlignerParams prm;
+    prm.seed_size = p->seed_size;
+    prm.seeds_to_try = p->seeds_to_try;
+    prm.max_distance = p->max_distance;
+    prm.confidence_threshold = p->confidence_threshold;
+    prm.max_hits = p->max_hits;
+    prm.bucket_size = p->bucket_size;
+    std::atomic<uint64_t> cursor{0};
+    std::atomic<bool> failed{false};
+    std::mutex mu;
+    auto body = [&]() {
+        try {
+            for (;;) {
+                uint64_t i = cursor.fetch_add(1);
+                if (i >= n || failed.load()) break;
+                Read r;
+                r.bases.assign(bases + offsets[i], offsets[i + 1] - offsets[i]);
+                to_result(oracle_align(r, *h->ctx, prm), &results[i]);
+            }
+        } catch (const std::exception& e) {
+            std::lock_guard<std::mutex> lock(mu);
+            g_err = e.what();
+            failed = true;
+        }
+    };
+    std::vector<std::thread> th;
+    for (int t = 0; t < std::max(1, threads); ++t) th.emplace_back(body);
+    for (auto& t : th) t.join();
+    return failed ? 1 : 0;
+}
+
+// oracle_scan (REF src/eval.cpp:244-268) of one read: hits into out (cap),
+// returns the hit count or -1 on error
+int64_t ref_oracle_scan(void* hv, const char* read, uint64_t len, int d_limit, int bucket, uint64_t* pos,
+                        int32_t* dist, uint8_t* dir, uint64_t cap) {
+    try {
+        auto* h = static_cast<RefReferee*>(hv);
+        Read r;
+        r.bases.assign(read, len);
+        std::vector<OracleHit> hits = oracle_scan(r, *h->ctx, d_limit, bucket);
+        for (size_t i = 0; i < hits.size() && i < cap; ++i) {
+            pos[i] = hits[i].position;
+            dist[i] = hits[i].distance;
+            dir[i] = static_cast<uint8_t>(hits[i].direction);
+        }
+        return static_cast<int64_t>(hits.size());
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
 
 }  // extern "C"

@@ -151,6 +151,11 @@ def _load():
         "sa_index_csr": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, P(C.c_uint64), P(C.c_uint64),
                                    P(C.c_uint64), P(C.c_uint64), P(C.c_uint64)]),
         "sa_index_seed_size": (C.c_int, [C.c_void_p, P(C.c_int32)]),
+        "sa_referee_create": (C.c_int, [C.c_void_p, C.c_int32, P(C.c_void_p)]),
+        "sa_referee_destroy": (None, [C.c_void_p]),
+        "sa_referee_align": (C.c_int, [C.c_void_p, P(_Params), C.c_void_p, P(C.c_uint64), C.c_uint64, C.c_void_p]),
+        "sa_referee_scan": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, P(C.c_uint64), C.c_uint64,
+                                      P(C.c_uint64), C.c_void_p, C.c_uint64]),
         "sa_default_align_options": (None, [P(_AlignOptions)]),
         "sa_run_index": (C.c_int, [C.c_char_p, C.c_char_p, C.c_int32, C.c_int32, C.c_int32]),
         "sa_run_align": (C.c_int, [P(_AlignOptions), P(_EvalReport)]),
@@ -776,3 +781,63 @@ def run_align(index_path: str, fastq_path: str, output_path: str, params: Aligne
         _raise(rc)
     return EvalReport(rep.total, rep.single, rep.multiple, rep.notfound, rep.correct, rep.wrong, rep.no_truth,
                       rep.elapsed_seconds, AlignStats._from_c(rep.stats), rep)
+
+
+# ----------------------------------------------------------------------- referee
+
+REFEREE_HIT_DTYPE = np.dtype([("position", "<u8"), ("distance", "<i4"), ("direction", "u1"), ("reserved", "u1", (3,))])
+
+
+class Referee:
+    """OracleContext / oracle_align / oracle_scan on the GPU (REF include/seedaln/eval.hpp:49-117)."""
+
+    def __init__(self, g: PackedGenome, device: int = 0):
+        lib = _load()
+        h = g._handle()
+        try:
+            out = C.c_void_p()
+            rc = lib.sa_referee_create(h, device, C.byref(out))
+            if rc:
+                _raise(rc)
+            self._r = out.value
+        finally:
+            lib.sa_genome_free(h)
+
+    def __del__(self):
+        r = getattr(self, "_r", None)
+        if r and _lib is not None:
+            _lib.sa_referee_destroy(r)
+            self._r = None
+
+    def align_arrays(self, params: AlignerParams, bases, offsets: np.ndarray) -> np.ndarray:
+        """oracle_align per read (REF src/eval.cpp:270-306)."""
+        offsets = np.ascontiguousarray(offsets, np.uint64)
+        n = offsets.size - 1
+        res = np.zeros(n, RESULT_DTYPE)
+        b = np.ascontiguousarray(np.frombuffer(bases, np.uint8) if isinstance(bases, (bytes, bytearray)) else bases,
+                                 np.uint8)
+        p = params._c()
+        rc = _load().sa_referee_align(self._r, C.byref(p), C.c_void_p(b.ctypes.data), _u64p(offsets), n,
+                                      C.c_void_p(res.ctypes.data))
+        if rc:
+            _raise(rc)
+        return res
+
+    def scan_arrays(self, d_limit: int, bucket_size: int, bases, offsets: np.ndarray):
+        """oracle_scan per read (REF src/eval.cpp:244-268): (hit_offsets, hits)."""
+        lib = _load()
+        offsets = np.ascontiguousarray(offsets, np.uint64)
+        n = offsets.size - 1
+        b = np.ascontiguousarray(np.frombuffer(bases, np.uint8) if isinstance(bases, (bytes, bytearray)) else bases,
+                                 np.uint8)
+        ho = np.zeros(n + 1, np.uint64)
+        rc = lib.sa_referee_scan(self._r, d_limit, bucket_size, C.c_void_p(b.ctypes.data), _u64p(offsets), n,
+                                 _u64p(ho), None, 0)
+        if rc:
+            _raise(rc)
+        hits = np.zeros(int(ho[-1]), REFEREE_HIT_DTYPE)
+        rc = lib.sa_referee_scan(self._r, d_limit, bucket_size, C.c_void_p(b.ctypes.data), _u64p(offsets), n,
+                                 _u64p(ho), C.c_void_p(hits.ctypes.data), hits.size)
+        if rc:
+            _raise(rc)
+        return ho, hits

@@ -32,6 +32,7 @@
 
 #include "align_kernels.cuh"
 #include "common.cuh"
+#include "lv.cuh"
 
 namespace sab {
 
@@ -54,111 +55,6 @@ SA_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "mem
 SA_DEV void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
 SA_DEV void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
-
-// ------------------------------------------------------------------ LV
-
-// Extend diagonal k from read index i while bases match (REF
-// edit_distance.cpp:35-42; N never matches, :11-13).  R/W are shared-memory
-// plane arrays; window index j lives at plane bit wofs + j.
-SA_DEV int lv_slide(const uint4* R, const uint4* W, uint32_t wofs, int i, int k, int cap,
-                    uint32_t& cells) {
-    const int start = i;
-    while (i < cap) {
-        uint32_t rl, rh, rn, wl, wh, wn;
-        extract32(R, static_cast<uint64_t>(i), rl, rh, rn);
-        extract32(W, static_cast<uint64_t>(wofs + static_cast<uint32_t>(i + k)), wl, wh, wn);
-        const uint32_t mism = (rl ^ wl) | (rh ^ wh) | rn | wn;
-        if (mism == 0) {
-            i += 32;
-        } else {
-            i += __ffs(mism) - 1;
-            break;
-        }
-    }
-    if (i > cap) i = cap;
-    cells += static_cast<uint32_t>(i - start) + 1;
-    return i;
-}
-
-// One LV iteration for diagonal k given the previous frontier values of
-// k-1, k, k+1 (REF edit_distance.cpp:46-67).
-SA_DEV int lv_step(int e, int k, int prev_km1, int prev_k, int prev_kp1, int m, int w,
-                   const uint4* R, const uint4* W, uint32_t wofs, uint32_t& cells) {
-    if (k > w) return kUnreach;  // whole diagonal outside the window (:47)
-    int cand;
-    if (e == 0) {
-        cand = 0;
-    } else {
-        cand = prev_k + 1;                // substitution
-        cand = max(cand, prev_kp1 + 1);   // extra read char
-        cand = max(cand, prev_km1);       // extra window char
-    }
-    if (cand < max(0, -k)) return kUnreach;  // (:56-59)
-    const int cap = min(m, w - k);
-    cand = min(cand, cap);  // (:60)
-    return lv_slide(R, W, wofs, cand, k, cap, cells);
-}
-
-// Register wavefront for d_limit <= 15: lane l owns diagonal k = l - d_limit.
-SA_DEV int lv_warp_reg(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, int dl,
-                       int lane, uint32_t& cells) {
-    const int k = lane - dl;
-    const bool mine = lane <= 2 * dl;
-    int fr = kUnreach;
-    for (int e = 0; e <= dl; ++e) {
-        int up = __shfl_down_sync(FULL, fr, 1);
-        int dn = __shfl_up_sync(FULL, fr, 1);
-        if (lane == 31) up = kUnreach;
-        if (lane == 0) dn = kUnreach;
-        const bool active = mine && k >= -e && k <= e;
-        if (active) fr = lv_step(e, k, dn, fr, up, m, w, R, W, wofs, cells);
-        if (__any_sync(FULL, active && fr == m)) return e;
-    }
-    return -1;
-}
-
-// Shared-memory wavefront for any d_limit: F holds 2 * (2*dl + 3) ints.
-SA_DEV int lv_warp_smem(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, int dl,
-                        int* F, int lane, uint32_t& cells) {
-    const int width = 2 * dl + 3;
-    int* cur = F;
-    int* nxt = F + width;
-    for (int t = lane; t < 2 * width; t += 32) F[t] = kUnreach;
-    __syncwarp();
-    const int off = dl + 1;
-    for (int e = 0; e <= dl; ++e) {
-        bool found = false;
-        for (int k = -e + lane; k <= e; k += 32) {
-            const int v = lv_step(e, k, cur[k - 1 + off], cur[k + off], cur[k + 1 + off], m, w, R,
-                                  W, wofs, cells);
-            nxt[k + off] = v;
-            found |= (v == m);
-        }
-        __syncwarp();
-        if (__any_sync(FULL, found)) return e;
-        int* t = cur;
-        cur = nxt;
-        nxt = t;
-    }
-    return -1;
-}
-
-// kRegLV: every d_limit of the launch is <= 15 (register wavefront only);
-// otherwise the shared-memory wavefront serves every limit.  One variant per
-// kernel keeps the inlined code small.
-template <bool kRegLV>
-SA_DEV int lv_warp(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, int dl, int* F,
-                   int lane, uint32_t& cells) {
-    if (kRegLV) return lv_warp_reg(R, m, W, wofs, w, dl, lane, cells);
-    return lv_warp_smem(R, m, W, wofs, w, dl, F, lane, cells);
-}
-
-// standalone LV (lv_batch_kernel): any limit
-SA_DEV int lv_warp_any(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, int dl, int* F,
-                       int lane, uint32_t& cells) {
-    if (dl <= 15) return lv_warp_reg(R, m, W, wofs, w, dl, lane, cells);
-    return lv_warp_smem(R, m, W, wofs, w, dl, F, lane, cells);
-}
 
 // ------------------------------------------------------------------ read staging
 
