@@ -5,8 +5,13 @@
 //   seedaln::Aligner(idx, genome, params)       -> snap_b200::Aligner(idx, params)
 //   Aligner::align(const Read&)                 -> Aligner::align(std::string_view)   (batch of 1; tests)
 //                                               -> Aligner::align_batch(...)          (production)
-//   std::invalid_argument / FormatError / IoError are rethrown from the status
-//   codes (REF include/seedaln/errors.hpp:10-30).
+//   PackedGenome::from_fasta                    -> snap_b200::Genome::from_fasta
+//   run_index / save_index_file                 -> snap_b200::run_index / save_index_file
+//   load_index_file                             -> snap_b200::load_index_file
+//   run_align (FASTQ -> SAM)                    -> snap_b200::run_align
+//   OracleContext / oracle_align / oracle_scan  -> snap_b200::Referee
+//   std::invalid_argument / FormatError / ParseError / IoError are rethrown
+//   from the status codes (REF include/seedaln/errors.hpp:10-30).
 //
 // Link with paper_1111_5572_b200/lib/libsnapb200.so.  See INTEGRATION.md.
 #pragma once
@@ -15,6 +20,7 @@
 #include <stdexcept>
 #include <string>
 #include <string_view>
+#include <utility>
 #include <vector>
 
 #include "snap_b200.h"
@@ -25,12 +31,22 @@ class FormatError : public std::runtime_error {
 public:
     using std::runtime_error::runtime_error;
 };
+class ParseError : public std::runtime_error {
+public:
+    using std::runtime_error::runtime_error;
+};
+class IoError : public std::runtime_error {
+public:
+    using std::runtime_error::runtime_error;
+};
 
 inline void check(int rc, const sa_context* ctx) {
     if (rc == SA_OK) return;
     std::string msg = sa_last_error(ctx);
     if (rc == SA_EINVAL) throw std::invalid_argument(msg);
     if (rc == SA_EFORMAT) throw FormatError(msg);
+    if (rc == SA_EPARSE) throw ParseError(msg);
+    if (rc == SA_EIO) throw IoError(msg);
     throw std::runtime_error(msg);
 }
 
@@ -52,6 +68,8 @@ public:
               nullptr);
         seed_size_ = seed_size;
     }
+    // adopt a context made elsewhere (load_index_file)
+    SeedIndex(sa_context* ctx, int seed_size) : ctx_(ctx), seed_size_(seed_size) {}
     SeedIndex(const SeedIndex&) = delete;
     SeedIndex& operator=(const SeedIndex&) = delete;
     SeedIndex(SeedIndex&& o) noexcept : ctx_(o.ctx_), seed_size_(o.seed_size_) { o.ctx_ = nullptr; }
@@ -123,6 +141,81 @@ private:
     const SeedIndex* idx_;
     sa_params params_;
     sa_stats stats_{};
+};
+
+// PackedGenome with its contig table (REF include/seedaln/genome.hpp:36-100).
+class Genome {
+public:
+    static Genome from_fasta(const std::string& path) {  // REF src/genome.cpp:48-94
+        sa_genome* g = nullptr;
+        check(sa_genome_from_fasta(path.c_str(), &g), nullptr);
+        return Genome(g);
+    }
+    explicit Genome(sa_genome* g) : g_(g) {}
+    Genome(const Genome&) = delete;
+    Genome& operator=(const Genome&) = delete;
+    Genome(Genome&& o) noexcept : g_(o.g_) { o.g_ = nullptr; }
+    ~Genome() { sa_genome_free(g_); }
+    uint64_t size() const {
+        uint64_t n = 0;
+        check(sa_genome_info(g_, &n, nullptr, nullptr), nullptr);
+        return n;
+    }
+    uint64_t checksum() const {
+        uint64_t c = 0;
+        check(sa_genome_info(g_, nullptr, nullptr, &c), nullptr);
+        return c;
+    }
+    const sa_genome* get() const { return g_; }
+
+private:
+    sa_genome* g_ = nullptr;
+};
+
+// save_index_file (REF src/seed_index.cpp:145-170), CSR built on the GPU
+inline void save_index_file(const Genome& g, int seed_size, const std::string& path,
+                            int format = SA_INDEX_SNAPIDX1, int device = 0) {
+    check(sa_index_write(g.get(), seed_size, format, device, path.c_str()), nullptr);
+}
+
+// run_index (REF src/driver.cpp:37-45)
+inline void run_index(const std::string& fasta, const std::string& index_path, int seed_size = 20,
+                      int format = SA_INDEX_SNAPIDX1, int device = 0) {
+    check(sa_run_index(fasta.c_str(), index_path.c_str(), seed_size, format, device), nullptr);
+}
+
+// load_index_file (REF src/seed_index.cpp:173-228) -> (GPU index, genome)
+inline std::pair<SeedIndex, Genome> load_index_file(const std::string& path, const std::vector<int32_t>& devices = {0},
+                                                    bool verify = true) {
+    sa_genome* g = nullptr;
+    sa_context* ctx = nullptr;
+    check(sa_index_load(path.c_str(), devices.data(), static_cast<int32_t>(devices.size()), verify ? 1 : 0, &g, &ctx),
+          nullptr);
+    int32_t s = 0;
+    sa_index_seed_size(ctx, &s);
+    return {SeedIndex(ctx, s), Genome(g)};
+}
+
+// run_align (REF src/driver.cpp:47-156): options as AlignOptions
+inline sa_eval_report run_align(const sa_align_options& opt) {
+    sa_eval_report r{};
+    check(sa_run_align(&opt, &r), nullptr);
+    return r;
+}
+
+// OracleContext + oracle_align / oracle_scan on the GPU (REF src/eval.cpp:155-306)
+class Referee {
+public:
+    explicit Referee(const Genome& g, int device = 0) { check(sa_referee_create(g.get(), device, &r_), nullptr); }
+    Referee(const Referee&) = delete;
+    Referee& operator=(const Referee&) = delete;
+    ~Referee() { sa_referee_destroy(r_); }
+    void align_batch(const sa_params& p, const char* bases, const uint64_t* offsets, uint64_t n, sa_result* out) {
+        check(sa_referee_align(r_, &p, bases, offsets, n, out), nullptr);
+    }
+
+private:
+    sa_referee* r_ = nullptr;
 };
 
 }  // namespace snap_b200

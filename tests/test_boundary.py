@@ -140,6 +140,11 @@ def test_cpp_adapter_compiles_and_links(tmp_path):
         "  if (argc > 5) { snap_b200::SeedIndex idx({0}, {0}, 20, 20);\n"
         "    snap_b200::Aligner al(idx, snap_b200::default_params());\n"
         "    auto r = al.align(\"ACGT\"); return r.kind; }\n"
+        "  if (argc > 6) { auto g = snap_b200::Genome::from_fasta(\"x.fa\");\n"
+        "    snap_b200::save_index_file(g, 20, \"x.idx\");\n"
+        "    auto [idx, g2] = snap_b200::load_index_file(\"x.idx\");\n"
+        "    sa_align_options o; sa_default_align_options(&o); snap_b200::run_align(o);\n"
+        "    snap_b200::Referee rf(g2); return static_cast<int>(idx.seed_size()); }\n"
         "  return 0; }\n")
     exe = tmp_path / "use"
     r = subprocess.run(["g++", "-std=c++17", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe),
