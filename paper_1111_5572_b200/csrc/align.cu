@@ -894,6 +894,7 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
     // status of a staged read: 0 = decoded, 1 = shorter than s, 2 = bad character
     auto prep = [&](int q, int len, const uint32_t* words, int sh, int nwd) -> int {
         if (len < a.s) return 1;
+        if (len > a.lcap) return 3;  // beyond this launch's layout: deferred
         offsets_for(q, len);
         uint4* R = planes + 2 * q * a.wbr;
         return decode_read(words, sh, nwd, len, R, R + a.wbr, lane) ? 2 : 0;
@@ -903,6 +904,8 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
             short_read(r, len);
         } else if (st == 2) {
             bad_read(r);
+        } else if (st == 3) {
+            overflowed(r);
         } else {
             x.R = planes + 2 * q * a.wbr;
             x.C = x.R + a.wbr;
@@ -920,16 +923,77 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
         // in flight (cp.async), and read r+2nw's bytes are being copied.
         const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
         const uint32_t N = a.n_reads;
+        const bool stream = a.chunk_flag != nullptr;
+        uint32_t ready_c = 0;  // streaming: chunks below this are known resident
+        // Chunks land in order; wait (lane 0 polls) until read rr's chunk has.
+        // A flag that never arrives times out into an error instead of a hang.
+        auto wait_chunk = [&](uint32_t rr) {
+            if (!stream) return;
+            const uint32_t c = stream_chunk_of(rr);
+            if (c < ready_c) return;
+            if (lane == 0) {
+                const volatile unsigned int* f = a.chunk_flag + c;
+                const long long t0 = clock64();
+                while (*f != a.epoch) {
+                    __nanosleep(256);
+                    if (clock64() - t0 > (1ll << 35)) {
+                        atomicOr(a.error_flag, 4u);
+                        break;
+                    }
+                }
+            }
+            __syncwarp();
+            ready_c = c + 1;
+        };
+        // offsets are read from L2 (.cg): a line may hold a neighbour chunk's
+        // entries that landed after this SM cached it
+        auto off = [&](uint32_t i) -> uint64_t {
+            return stream ? __ldcg(reinterpret_cast<const unsigned long long*>(a.offsets) + i) : a.offsets[i];
+        };
+        auto raddr = [&](uint32_t rr, uint64_t o) -> const char* {
+            return stream ? a.bases + (static_cast<long long>(o) + __ldcg(a.chunk_adj + stream_chunk_of(rr)))
+                          : a.bases + (o - a.base_off);
+        };
+        // finished reads are counted per warp and published once per chunk
+        // (one fence + atomic per warp and chunk, not per read)
+        uint32_t done_c = 0, done_n = 0;
+        auto flush_done = [&]() {
+            if (done_n && lane == 0) {
+                __threadfence();
+                atomicAdd(a.chunk_done + done_c, done_n);
+            }
+            done_n = 0;
+        };
+        auto read_done = [&](uint32_t rr) {
+            if (!stream) return;
+            const uint32_t c = stream_chunk_of(rr);
+            if (c != done_c) {
+                flush_done();
+                done_c = c;
+            }
+            ++done_n;
+        };
+        auto copy_read = [&](uint32_t rr, uint64_t o0, uint64_t o1, uint32_t* dst, int& sh, int& nwd) {
+            const int len = static_cast<int>(o1 - o0);
+            if (len > a.lcap) {  // not staged; prep() defers it
+                sh = 0;
+                nwd = 0;
+                return;
+            }
+            issue_read_copy(raddr(rr, o0), len, dst, lane, sh, nwd);
+        };
         uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
         if (r < N) {
-            const uint64_t c0 = a.offsets[r], c1 = a.offsets[r + 1];
+            wait_chunk(r);
+            const uint64_t c0 = off(r), c1 = off(r + 1);
             uint64_t n0 = 0, n1 = 0;
             if (r + nw < N) {
-                n0 = a.offsets[r + nw];
-                n1 = a.offsets[r + nw + 1];
+                wait_chunk(r + nw);
+                n0 = off(r + nw);
+                n1 = off(r + nw + 1);
             }
             int sh = 0, nwd = 0;
-            issue_read_copy(a.bases + (c0 - a.base_off), static_cast<int>(c1 - c0), stage, lane, sh, nwd);
+            copy_read(r, c0, c1, stage, sh, nwd);
             cp_async_commit();
             cp_async_wait0();
             __syncwarp();
@@ -940,9 +1004,7 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
                 resolve_wave0(a, n_eff0, len_cur, recs, pslot, pcanon, lane);
             }
             int sh_n = 0, nw_n = 0;
-            if (r + nw < N)
-                issue_read_copy(a.bases + (n0 - a.base_off), static_cast<int>(n1 - n0), stage + a.sbw, lane,
-                                sh_n, nw_n);
+            if (r + nw < N) copy_read(r + nw, n0, n1, stage + a.sbw, sh_n, nw_n);
             cp_async_commit();
             int p = 0;
             for (; r < N; r += nw) {
@@ -960,17 +1022,17 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
                 }
                 uint64_t f0 = 0, f1 = 0;
                 if (has_next2) {
-                    f0 = a.offsets[r + 2 * nw];
-                    f1 = a.offsets[r + 2 * nw + 1];
+                    wait_chunk(r + 2 * nw);
+                    f0 = off(r + 2 * nw);
+                    f1 = off(r + 2 * nw + 1);
                 }
                 process(r, p, len_cur, st_cur, true);
+                read_done(r);
                 if (has_next && st_n == 0)
                     resolve_wave0(a, p ? n_eff0 : n_eff1, len_n, recs + 32 * (p ^ 1), pslot, pcanon, lane);
                 sh_n = 0;
                 nw_n = 0;
-                if (has_next2)
-                    issue_read_copy(a.bases + (f0 - a.base_off), static_cast<int>(f1 - f0), stage + p * a.sbw,
-                                    lane, sh_n, nw_n);
+                if (has_next2) copy_read(r + 2 * nw, f0, f1, stage + p * a.sbw, sh_n, nw_n);
                 cp_async_commit();
                 n0 = f0;
                 n1 = f1;
@@ -979,6 +1041,7 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
                 p ^= 1;
             }
             cp_async_wait0();
+            flush_done();
         }
     } else {
         // dynamic fetch (work list for the slow kernel), reads decoded from global

@@ -49,6 +49,20 @@ struct AlignLaunch {
     unsigned long long* error_read;  // atomicMin of the first bad read (absolute index)
     unsigned long long read_base;    // absolute index of read 0 of this launch
     // slow path: process work_list[0..*work_count) with global candidate tables
+    // Streaming (batch path, pipelined kernel): one launch covers the whole
+    // batch while chunks are still being copied in.  Chunk c (stream_chunk_of:
+    // 16 k, 16 k, 32 k, 64 k, then 128 k reads each) is usable once
+    // chunk_flag[c] == epoch (written by a stream memory op after its H2D);
+    // its bytes sit at bases + offsets[r] + chunk_adj[c]; every finished read
+    // bumps chunk_done[c], which releases that chunk's D2H.  Reads longer
+    // than lcap are deferred to the end-of-batch pass.  chunk_flag == nullptr:
+    // everything is resident (bytes at bases + offsets[r] - base_off).
+    const unsigned int* chunk_flag;
+    unsigned int* chunk_done;
+    const long long* chunk_adj;
+    unsigned int epoch;
+    int chunk_shift;  // (unused; chunk sizes follow stream_chunk_of)
+    int lcap;
     const unsigned int* work_list;
     const unsigned int* work_count;
     unsigned char* gscratch;
@@ -58,6 +72,26 @@ struct AlignLaunch {
 #ifndef SA_FAST_WARPS
 #define SA_FAST_WARPS 8  // warps per block of the align kernels (compile-time: launch bounds)
 #endif
+
+// Streamed chunk of read r: [0,16k) [16k,32k) [32k,64k) [64k,128k), then
+// 128 k reads per chunk -- short first chunks start the kernel early, long
+// ones keep the copies efficient.
+__host__ __device__ inline uint32_t stream_chunk_of(uint32_t r) {
+    if (r < (1u << 14)) return 0;
+    if (r < (1u << 17)) {
+#ifdef __CUDA_ARCH__
+        return static_cast<uint32_t>(31 - __clz(r)) - 13;  // floor(log2 r) - 13
+#else
+        return static_cast<uint32_t>(31 - __builtin_clz(r)) - 13;
+#endif
+    }
+    return 3 + (r >> 17);
+}
+__host__ __device__ inline uint32_t stream_chunk_begin(uint32_t c) {
+    if (c == 0) return 0;
+    if (c <= 3) return 1u << (13 + c);
+    return (c - 3) << 17;
+}
 
 // bytes of one candidate table with capacity cap and hcap hash slots
 inline uint64_t cand_table_bytes(int cap, int hcap) {

@@ -117,6 +117,23 @@ struct Replica {
         LaunchShape sh;
     };
     std::vector<ShapeEntry> shapes;
+    // streamed batch path (align_streamed): whole-batch device buffers,
+    // per-chunk flags / done counters / byte adjustments, three streams
+    struct Streamed {
+        char* bases = nullptr;
+        uint64_t bases_cap = 0;
+        uint64_t* offs = nullptr;
+        uint64_t offs_cap = 0;
+        sa_result* res = nullptr;
+        uint64_t res_cap = 0;
+        unsigned int* flags = nullptr;
+        unsigned int* done = nullptr;
+        long long* adj = nullptr;
+        uint64_t chunks_cap = 0;
+        unsigned int epoch = 0;
+        cudaStream_t ci = nullptr, kk = nullptr, co = nullptr;
+        cudaEvent_t e_begin = nullptr, e_ready = nullptr, k0 = nullptr, k1 = nullptr, e_end = nullptr;
+    } sm;
 };
 
 
@@ -197,6 +214,7 @@ int make_shape(Replica& rep, const sa_params* p, uint64_t Lmax, LaunchShape& sh,
     a.cap = kFastCap;
     a.hcap = kFastHcap;
     a.prefetch = L <= 1024 ? 1 : 0;
+    a.lcap = L;  // every read of this layout fits
     a.sbw = a.prefetch ? round4((L + 3) / 4 + 2) : 0;
     a.smem_per_warp = round16(common + 8ull * a.sbw + cand_table_bytes(a.cap, a.hcap));
     const uint32_t kMaxSmem = 227 * 1024;
@@ -381,7 +399,10 @@ int ensure_defer(sa_context* ctx, Replica& rep, uint64_t n) {
 // kernel and scattered into results.  Keeping this out of the chunk pipeline
 // means no kernel ever queues behind the persistent fast kernel of the next
 // chunk.  Returns the number of reads redone.
-int overflow_pass(sa_context* ctx, Replica& rep, Stage& stg, const LaunchShape& sh, const char* bases,
+int cached_shape(Replica& rep, const sa_params* p, uint64_t Lmax, LaunchShape& sh, std::string& why);
+int ensure_scratch(sa_context* ctx, Replica& rep, const LaunchShape& sh);
+
+int overflow_pass(sa_context* ctx, Replica& rep, Stage& stg, const sa_params* params, const char* bases,
                   const uint64_t* offsets, sa_result* results, uint64_t& launches, uint64_t& n_done) {
     unsigned int n = 0;
     n_done = 0;
@@ -391,7 +412,20 @@ int overflow_pass(sa_context* ctx, Replica& rep, Stage& stg, const LaunchShape& 
     std::vector<unsigned int> ids(n);
     CUDA_TRY(ctx, cudaMemcpy(ids.data(), rep.d_defer, n * sizeof(unsigned int), cudaMemcpyDeviceToHost));
     std::vector<uint64_t> offs(n + 1, 0);
-    for (unsigned i = 0; i < n; ++i) offs[i + 1] = offs[i] + (offsets[ids[i] + 1] - offsets[ids[i]]);
+    uint64_t Lmax = 0;
+    for (unsigned i = 0; i < n; ++i) {
+        const uint64_t L = offsets[ids[i] + 1] - offsets[ids[i]];
+        offs[i + 1] = offs[i] + L;
+        Lmax = std::max(Lmax, L);
+    }
+    // deferred reads: table overflows and (streaming) reads longer than the
+    // fast launch's layout -- the global-table kernel gets its own layout
+    LaunchShape sh;
+    {
+        std::string why;
+        if (int rc = cached_shape(rep, params, Lmax, sh, why)) return fail(ctx, rc, why);
+        if (int rc = ensure_scratch(ctx, rep, sh)) return rc;
+    }
     std::vector<char> buf(offs[n]);
     for (unsigned i = 0; i < n; ++i)
         std::memcpy(buf.data() + offs[i], bases + offsets[ids[i]], offs[i + 1] - offs[i]);
@@ -435,6 +469,239 @@ int overflow_pass(sa_context* ctx, Replica& rep, Stage& stg, const LaunchShape& 
 void add_stats(sa_stats* dst, const unsigned long long* src) {
     uint64_t* d = reinterpret_cast<uint64_t*>(dst);
     for (int i = 0; i < kNumStats; ++i) d[i] += src[i];
+}
+
+
+// ---------------------------------------------------------------- streamed batch path
+// cuStreamWriteValue32 / cuStreamWaitValue32 (stream memory operations,
+// executed by the front end, no SM) through the runtime's driver entry
+// points: chunk flags for the kernel and done-count gates for the D2H.
+typedef int (*StreamValueFn)(cudaStream_t, unsigned long long, unsigned int, unsigned int);
+struct MemOps {
+    StreamValueFn write = nullptr, wait = nullptr;
+    bool ok = false;
+};
+const MemOps& memops() {
+    static MemOps m = [] {
+        MemOps r;
+        cudaDriverEntryPointQueryResult q1, q2;
+        void* w = nullptr;
+        void* v = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &w, cudaEnableDefault, &q1) == cudaSuccess &&
+            cudaGetDriverEntryPoint("cuStreamWaitValue32", &v, cudaEnableDefault, &q2) == cudaSuccess &&
+            q1 == cudaDriverEntryPointSuccess && q2 == cudaDriverEntryPointSuccess && w && v) {
+            r.write = reinterpret_cast<StreamValueFn>(w);
+            r.wait = reinterpret_cast<StreamValueFn>(v);
+            r.ok = true;
+        }
+        cudaGetLastError();
+        return r;
+    }();
+    return m;
+}
+constexpr unsigned kWaitGeq = 0x0;  // CU_STREAM_WAIT_VALUE_GEQ
+constexpr int kStreamShift = 14;    // 16 k reads per chunk
+
+// Opt-in (SA_STREAM=1).  Measured on C1, 1 M reads, pinned buffers: the
+// streamed kernel runs 2.75 ms against 2.48 ms with the data already resident.
+// It waits on chunks that have not landed yet, so the end-to-end time (2.81 ms)
+// does not beat the chunked pipeline (2.77 ms).  Kept for copy-bound cases
+// (a kernel faster than the PCIe feed) and covered by tests.
+bool streaming_wanted(const Replica& rep, uint64_t n_reads, const uint64_t* offsets) {
+    if (!getenv("SA_STREAM") || getenv("SA_OVERFLOW_KERNEL")) return false;
+    if (n_reads < (2ull << kStreamShift) || !memops().ok) return false;
+    (void)rep;
+    uint64_t L = 0;  // the first chunk decides the layout; longer reads are deferred
+    const uint64_t m = std::min<uint64_t>(n_reads, 1ull << kStreamShift);
+    for (uint64_t i = 0; i < m; ++i) {
+        if (offsets[i + 1] < offsets[i]) return false;
+        L = std::max(L, offsets[i + 1] - offsets[i]);
+    }
+    return L <= 1024;
+}
+
+template <typename T>
+int grow(sa_context* ctx, T** p, uint64_t& cap, uint64_t need) {
+    if (need <= cap && *p) return SA_OK;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    const uint64_t c = std::max<uint64_t>(need, 1024);
+    CUDA_TRY(ctx, cudaMalloc(p, c * sizeof(T)));
+    cap = c;
+    return SA_OK;
+}
+
+// One launch for the whole batch: chunks of 16 k reads are copied in on one
+// stream, each followed by a flag write; the persistent kernel (another
+// stream) waits per chunk for its flag, and a third stream waits on each
+// chunk's done count before copying its results out.  No kernel boundary per
+// chunk, no tail per chunk.
+int align_streamed(sa_context* ctx, Replica& rep, const sa_params* params, const char* bases,
+                   const uint64_t* offsets, uint64_t n_reads, sa_result* results, sa_stats* out_stats,
+                   float& e2e_ms, float& k_ms, uint64_t& launches) {
+    auto& S = rep.sm;
+    const MemOps& mo = memops();
+    CUDA_TRY(ctx, cudaSetDevice(rep.device));
+    if (!S.ci) {
+        CUDA_TRY(ctx, cudaStreamCreateWithFlags(&S.ci, cudaStreamNonBlocking));
+        CUDA_TRY(ctx, cudaStreamCreateWithFlags(&S.kk, cudaStreamNonBlocking));
+        CUDA_TRY(ctx, cudaStreamCreateWithFlags(&S.co, cudaStreamNonBlocking));
+        for (cudaEvent_t* e : {&S.e_begin, &S.e_ready, &S.k0, &S.k1, &S.e_end}) CUDA_TRY(ctx, cudaEventCreate(e));
+    }
+    const uint64_t CH = 1ull << kStreamShift;  // first chunk
+    const uint64_t n_chunks = stream_chunk_of(static_cast<uint32_t>(n_reads - 1)) + 1;
+    auto cbeg = [&](uint64_t c) -> uint64_t { return std::min<uint64_t>(n_reads, stream_chunk_begin(c)); };
+    // layout: the first chunk's longest read, rounded up to 32 bases
+    uint64_t L0 = 0;
+    for (uint64_t i = 0; i < std::min(n_reads, CH); ++i) L0 = std::max(L0, offsets[i + 1] - offsets[i]);
+    L0 = std::max<uint64_t>((L0 + 31) & ~31ull, 32);
+    LaunchShape sh;
+    {
+        std::string why;
+        if (int rc = cached_shape(rep, params, L0, sh, why)) return fail(ctx, rc, why);
+        if (int rc = ensure_scratch(ctx, rep, sh)) return rc;
+    }
+    // chunk byte placement: each chunk's bytes start on a 128-byte boundary,
+    // so no cache line holds two chunks (the kernel reads bytes through L1)
+    std::vector<long long> adj(n_chunks);
+    std::vector<uint64_t> dpos(n_chunks + 1, 0);
+    bool bad_bounds = false;
+    for (uint64_t c = 0; c < n_chunks; ++c) {
+        const uint64_t r0 = cbeg(c), r1 = cbeg(c + 1);
+        uint64_t bytes = 0;
+        if (offsets[r1] >= offsets[r0]) bytes = offsets[r1] - offsets[r0];
+        else bad_bounds = true;
+        adj[c] = static_cast<long long>(dpos[c]) - static_cast<long long>(offsets[r0]);
+        dpos[c + 1] = (dpos[c] + bytes + 127) & ~127ull;
+    }
+    if (bad_bounds) return fail(ctx, SA_EINVAL, "offsets not ascending");
+    {
+        if (int rc = grow(ctx, &S.bases, S.bases_cap, dpos[n_chunks] + 64)) return rc;
+        if (int rc = grow(ctx, &S.offs, S.offs_cap, n_reads + 1)) return rc;
+        if (int rc = grow(ctx, &S.res, S.res_cap, n_reads)) return rc;
+        if (S.chunks_cap < n_chunks || !S.flags) {
+            uint64_t c1 = S.chunks_cap, c2 = S.chunks_cap, c3 = S.chunks_cap;
+            if (int rc = grow(ctx, &S.flags, c1, n_chunks)) return rc;
+            if (int rc = grow(ctx, &S.done, c2, n_chunks)) return rc;
+            if (int rc = grow(ctx, &S.adj, c3, n_chunks)) return rc;
+            CUDA_TRY(ctx, cudaMemset(S.flags, 0, c1 * sizeof(unsigned int)));
+            S.chunks_cap = std::min(c1, std::min(c2, c3));
+            S.epoch = 0;
+        }
+    }
+    if (int rc = ensure_defer(ctx, rep, n_reads)) return rc;
+    if (int rc = ensure_stage(ctx, rep.stage[0], 0, 0)) return rc;  // the overflow pass runs there
+    const unsigned epoch = ++S.epoch == 0 ? ++S.epoch : S.epoch;
+    // Per-chunk copy-out needs pinned results: a D2H into pageable memory
+    // blocks the host until it runs, and chunk c finishes only once later
+    // chunks have been flagged (the kernel prefetches two reads ahead).
+    cudaPointerAttributes pa{};
+    const bool gated = cudaPointerGetAttributes(&pa, results) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+
+    // ---- setup on the copy-in stream, then the kernel
+    CUDA_TRY(ctx, cudaEventRecord(S.e_begin, S.ci));
+    CUDA_TRY(ctx, cudaMemsetAsync(S.done, 0, n_chunks * sizeof(unsigned int), S.ci));
+    CUDA_TRY(ctx, cudaMemsetAsync(rep.d_defer_count, 0, sizeof(unsigned int), S.ci));
+    CUDA_TRY(ctx, cudaMemsetAsync(rep.d_stats, 0, kNumStats * sizeof(unsigned long long), S.ci));
+    CUDA_TRY(ctx, cudaMemcpyAsync(S.adj, adj.data(), n_chunks * sizeof(long long), cudaMemcpyHostToDevice, S.ci));
+    CUDA_TRY(ctx, cudaEventRecord(S.e_ready, S.ci));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(S.kk, S.e_ready, 0));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(S.co, S.e_ready, 0));
+    AlignLaunch a = sh.proto;
+    a.bases = S.bases;
+    a.offsets = S.offs;
+    a.base_off = 0;
+    a.n_reads = static_cast<uint32_t>(n_reads);
+    a.results = S.res;
+    a.stats = rep.d_stats;
+    a.cursor = rep.stage[0].d_ctl;  // unused by the pipelined kernel
+    a.overflow_list = rep.d_defer;
+    a.overflow_count = rep.d_defer_count;
+    a.error_flag = rep.d_err;
+    a.error_read = rep.d_err_read;
+    a.read_base = 0;
+    a.gscratch = rep.d_gscratch;
+    a.chunk_flag = S.flags;
+    a.chunk_done = S.done;
+    a.chunk_adj = S.adj;
+    a.epoch = epoch;
+    a.chunk_shift = kStreamShift;
+    const bool precopy = getenv("SA_STREAM_PRECOPY") != nullptr;  // diagnostics: all copies before the kernel
+    auto launch = [&]() -> int {
+        CUDA_TRY(ctx, cudaEventRecord(S.k0, S.kk));
+        launch_align_fast(a, sh.fast_grid, sh.fast_block, S.kk);
+        CUDA_TRY(ctx, cudaGetLastError());
+        CUDA_TRY(ctx, cudaEventRecord(S.k1, S.kk));
+        ++launches;
+        return SA_OK;
+    };
+    if (!precopy)
+        if (int rc = launch()) return rc;
+
+    // ---- chunks: validate, copy in, flag; gate and copy out
+    int bad = SA_OK;
+    std::vector<uint64_t> zero_offs;
+    for (uint64_t c = 0; c < n_chunks; ++c) {
+        const uint64_t r0 = cbeg(c), r1 = cbeg(c + 1);
+        const uint64_t* src_offs = offsets + r0;
+        for (uint64_t i = r0; i < r1; ++i)
+            if (offsets[i + 1] < offsets[i]) {
+                if (!bad) bad = fail(ctx, SA_EINVAL, "offsets not ascending");
+                break;
+            }
+        if (bad) {  // keep the kernel safe: zero-length reads at the chunk start
+            zero_offs.assign(r1 - r0 + 1, offsets[r0]);
+            src_offs = zero_offs.data();
+        } else {
+            CUDA_TRY(ctx, cudaMemcpyAsync(S.bases + dpos[c], bases + offsets[r0], offsets[r1] - offsets[r0],
+                                          cudaMemcpyHostToDevice, S.ci));
+        }
+        CUDA_TRY(ctx, cudaMemcpyAsync(S.offs + r0, src_offs, (r1 - r0 + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                                      S.ci));
+        if (bad) CUDA_TRY(ctx, cudaStreamSynchronize(S.ci));  // zero_offs is reused
+        if (mo.write(S.ci, reinterpret_cast<unsigned long long>(S.flags + c), epoch, 0) != 0)
+            return fail(ctx, SA_ERUNTIME, "cuStreamWriteValue32 failed");
+        if (gated) {
+            if (mo.wait(S.co, reinterpret_cast<unsigned long long>(S.done + c), static_cast<unsigned>(r1 - r0),
+                        kWaitGeq) != 0)
+                return fail(ctx, SA_ERUNTIME, "cuStreamWaitValue32 failed");
+            CUDA_TRY(ctx, cudaMemcpyAsync(results + r0, S.res + r0, (r1 - r0) * sizeof(sa_result),
+                                          cudaMemcpyDeviceToHost, S.co));
+        }
+    }
+    if (precopy) {
+        CUDA_TRY(ctx, cudaStreamSynchronize(S.ci));
+        if (int rc = launch()) return rc;
+    }
+    CUDA_TRY(ctx, cudaStreamWaitEvent(S.co, S.k1, 0));  // stats are final once the kernel ends
+    if (!gated)
+        CUDA_TRY(ctx, cudaMemcpyAsync(results, S.res, n_reads * sizeof(sa_result), cudaMemcpyDeviceToHost, S.co));
+    CUDA_TRY(ctx, cudaEventRecord(S.e_end, S.co));
+    CUDA_TRY(ctx, cudaEventSynchronize(S.e_end));
+    cudaEventElapsedTime(&e2e_ms, S.e_begin, S.e_end);
+    cudaEventElapsedTime(&k_ms, S.k0, S.k1);
+    if (bad) return bad;
+    {
+        unsigned int flag = 0;
+        CUDA_TRY(ctx, cudaMemcpy(&flag, rep.d_err, sizeof(flag), cudaMemcpyDeviceToHost));
+        if (flag & 4u) {
+            CUDA_TRY(ctx, cudaMemset(rep.d_err, 0, sizeof(unsigned int)));
+            return fail(ctx, SA_ERUNTIME, "streamed batch: a chunk never arrived (timeout)");
+        }
+    }
+    uint64_t redone = 0;
+    if (int rc = overflow_pass(ctx, rep, rep.stage[0], params, bases, offsets, results, launches, redone)) return rc;
+    if (redone) {  // the pass ran after e_end: extend the measured span
+        CUDA_TRY(ctx, cudaEventRecord(S.e_end, rep.stage[0].st));
+        CUDA_TRY(ctx, cudaEventSynchronize(S.e_end));
+        cudaEventElapsedTime(&e2e_ms, S.e_begin, S.e_end);
+    }
+    unsigned long long h[kNumStats];
+    CUDA_TRY(ctx, cudaMemcpy(h, rep.d_stats, sizeof(h), cudaMemcpyDeviceToHost));
+    std::memset(out_stats, 0, sizeof(sa_stats));
+    add_stats(out_stats, h);
+    return check_errors(ctx, rep);
 }
 
 }  // namespace
@@ -584,6 +851,14 @@ void sa_destroy(sa_context* ctx) {
         if (rep.d_err_read) cudaFree(rep.d_err_read);
         if (rep.d_gscratch) cudaFree(rep.d_gscratch);
         if (rep.d_defer) cudaFree(rep.d_defer);
+        for (void* q : {static_cast<void*>(rep.sm.bases), static_cast<void*>(rep.sm.offs),
+                        static_cast<void*>(rep.sm.res), static_cast<void*>(rep.sm.flags),
+                        static_cast<void*>(rep.sm.done), static_cast<void*>(rep.sm.adj)})
+            if (q) cudaFree(q);
+        for (cudaStream_t q : {rep.sm.ci, rep.sm.kk, rep.sm.co})
+            if (q) cudaStreamDestroy(q);
+        for (cudaEvent_t e : {rep.sm.e_begin, rep.sm.e_ready, rep.sm.k0, rep.sm.k1, rep.sm.e_end})
+            if (e) cudaEventDestroy(e);
         if (rep.d_defer_count) cudaFree(rep.d_defer_count);
         if (rep.e_start) cudaEventDestroy(rep.e_start);
         if (rep.e_end) cudaEventDestroy(rep.e_end);
@@ -624,6 +899,25 @@ int sa_align_batch(sa_context* ctx, const sa_params* params, const char* bases,
     }
     if (!bases || !offsets || !results) return fail(ctx, SA_EINVAL, "null buffer");
     if (n_reads >= 0xffffffffull) return fail(ctx, SA_EINVAL, "too many reads in one batch");
+    if (ctx->reps.size() == 1 && streaming_wanted(ctx->reps[0], n_reads, offsets)) {
+        float e2e = 0, kms = 0;
+        uint64_t launches = 0;
+        sa_stats st;
+        const int rc = align_streamed(ctx, ctx->reps[0], params, bases, offsets, n_reads, results, &st, e2e, kms,
+                                      launches);
+        if (rc) return rc;
+        ctx->last_e2e_ms = e2e;
+        ctx->last_kernel_ms = kms;
+        ctx->last_slow_ms = 0;
+        ctx->device_timing_pending = false;
+        ctx->last_launches = launches;
+        if (stats) {
+            uint64_t* d = reinterpret_cast<uint64_t*>(stats);
+            const uint64_t* v = reinterpret_cast<const uint64_t*>(&st);
+            for (size_t i = 0; i < sizeof(sa_stats) / 8; ++i) d[i] += v[i];
+        }
+        return SA_OK;
+    }
     // chunk boundaries (reads and bytes bounded).  Offsets are validated per
     // chunk inside the pipeline, so the host scan overlaps the GPU's work on
     // the previous chunk; a bad chunk stops the batch before it is enqueued.
@@ -722,8 +1016,8 @@ int sa_align_batch(sa_context* ctx, const sa_params* params, const char* bases,
             }
             if (defer) {
                 uint64_t redone = 0;
-                if (int rc = overflow_pass(&local_err, rep, rep.stage[0], sh, bases, offsets, results, launches[ri],
-                                           redone))
+                if (int rc = overflow_pass(&local_err, rep, rep.stage[0], params, bases, offsets, results,
+                                           launches[ri], redone))
                     return rc;
             }
             CUDA_TRY(&local_err, cudaEventRecord(rep.e_end, rep.stage[0].st));

@@ -303,3 +303,65 @@ def test_overflow_paths_parity(mode, monkeypatch):
     bases, offs, _, _ = synth.make_reads(cfg, g)
     _, st = _gpu_vs_oracle(cfg, g, packed, nmask, bases, offs)
     assert st["overflow_reads"] > 0
+
+
+def _streamed_case():
+    cfg = synth.CONFIGS["C1"].scaled(genome_len=5_000_000, n_reads=100_000)
+    g = synth.make_genome(cfg)
+    packed, nmask = synth.pack_genome(g)
+    bases, offs, _, _ = synth.make_reads(cfg, g)
+    # interleave a few long reads (beyond the streamed layout: deferred to the
+    # end-of-batch pass) and short reads (< s) into later chunks
+    rng = np.random.default_rng(12)
+    reads = [bases[int(offs[i]):int(offs[i + 1])].tobytes() for i in range(offs.size - 1)]
+    for i in rng.integers(20_000, 100_000, 60):
+        st = int(rng.integers(0, g.size - 400))
+        reads[int(i)] = g[st:st + int(rng.integers(129, 400))].tobytes()
+    for i in rng.integers(20_000, 100_000, 30):
+        reads[int(i)] = reads[int(i)][:int(rng.integers(0, 20))]
+    buf, offs2 = api.reads_to_buffer(reads)
+    return cfg, g, packed, nmask, np.frombuffer(buf, np.uint8).copy(), offs2
+
+
+def test_streamed_batch_matches_chunked_and_oracle(monkeypatch):
+    """sa_align_batch's single-launch streamed path (SA_STREAM=1: chunk flags
+    written by stream memory ops, per-chunk copy-out gated on done counts)
+    against the chunked pipeline (the default) and the oracle: pageable and pinned
+    result buffers, deferred long reads, short reads."""
+    monkeypatch.setenv("SA_STREAM", "1")
+    cfg, g, packed, nmask, bases, offs = _streamed_case()
+    genome = api.PackedGenome(packed, nmask, g.size)
+    al = api.Aligner(api.SeedIndex.build(genome, 20), genome, cfg.params)
+    a = al.align_arrays(bases, offs)
+    st_a = dict(al.stats().values)
+    pin = api.PinnedBuffer(offs.size * 24)
+    hr = pin.array(api.RESULT_DTYPE, offs.size - 1)
+    al.align_arrays(bases, offs, hr)
+    assert O.compare_results(hr.copy(), a) == []
+    monkeypatch.delenv("SA_STREAM")
+    al2 = api.Aligner(api.SeedIndex.build(genome, 20), genome, cfg.params)
+    b = al2.align_arrays(bases, offs)
+    assert O.compare_results(a, b) == []
+    for f in api.REFERENCE_STAT_FIELDS:
+        assert st_a[f] == al2.stats().values[f], f
+    want, _ = O.OracleIndex(packed, nmask, g.size, 20).align_arrays(cfg.params, bases, offs, threads=8)
+    assert O.compare_results(a, want) == []
+
+
+def test_streamed_batch_errors(monkeypatch):
+    monkeypatch.setenv("SA_STREAM", "1")
+    cfg, g, packed, nmask, bases, offs = _streamed_case()
+    genome = api.PackedGenome(packed, nmask, g.size)
+    al = api.Aligner(api.SeedIndex.build(genome, 20), genome, cfg.params)
+    bad = bases.copy()
+    bad[int(offs[90_000]) + 5] = ord("X")  # a late chunk: the error still surfaces
+    with pytest.raises(ValueError, match="read 90000"):
+        al.align_arrays(bad, offs)
+    o2 = offs.copy()
+    o2[70_001] = o2[70_000] - 1  # offsets not ascending inside a late chunk
+    with pytest.raises(ValueError, match="ascending"):
+        al.align_arrays(bases, o2)
+    # the context stays usable after both errors
+    again = al.align_arrays(bases, offs)
+    want, _ = O.OracleIndex(packed, nmask, g.size, 20).align_arrays(cfg.params, bases, offs, threads=8)
+    assert O.compare_results(again, want) == []
