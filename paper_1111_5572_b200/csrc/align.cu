@@ -806,8 +806,10 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
 #endif
 
 // kSlow: global candidate tables over a work list; kPipe: static striding with
-// the cp.async read pipeline (short reads); kRegLV: register LV only.
-template <bool kSlow, bool kPipe, bool kRegLV>
+// the cp.async read pipeline (short reads); kRegLV: register LV only;
+// kStream: the pipelined kernel consumes a batch that is still being copied
+// in (chunk flags; a separate variant so the default kernel carries none of it).
+template <bool kSlow, bool kPipe, bool kRegLV, bool kStream = false>
 __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kernel(const AlignLaunch a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
@@ -923,13 +925,13 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
         // in flight (cp.async), and read r+2nw's bytes are being copied.
         const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
         const uint32_t N = a.n_reads;
-        const bool stream = a.chunk_flag != nullptr;
+        constexpr bool stream = kStream;
         uint32_t ready_c = 0;  // streaming: chunks below this are known resident
         // Chunks land in order; wait (lane 0 polls) until read rr's chunk has.
         // A flag that never arrives times out into an error instead of a hang.
         auto wait_chunk = [&](uint32_t rr) {
             if (!stream) return;
-            const uint32_t c = stream_chunk_of(rr);
+            const uint32_t c = stream_chunk_of(rr, a.chunk_shift0, a.chunk_shift);
             if (c < ready_c) return;
             if (lane == 0) {
                 const volatile unsigned int* f = a.chunk_flag + c;
@@ -951,7 +953,7 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
             return stream ? __ldcg(reinterpret_cast<const unsigned long long*>(a.offsets) + i) : a.offsets[i];
         };
         auto raddr = [&](uint32_t rr, uint64_t o) -> const char* {
-            return stream ? a.bases + (static_cast<long long>(o) + __ldcg(a.chunk_adj + stream_chunk_of(rr)))
+            return stream ? a.bases + (static_cast<long long>(o) + __ldcg(a.chunk_adj + stream_chunk_of(rr, a.chunk_shift0, a.chunk_shift)))
                           : a.bases + (o - a.base_off);
         };
         // finished reads are counted per warp and published once per chunk
@@ -966,7 +968,7 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
         };
         auto read_done = [&](uint32_t rr) {
             if (!stream) return;
-            const uint32_t c = stream_chunk_of(rr);
+            const uint32_t c = stream_chunk_of(rr, a.chunk_shift0, a.chunk_shift);
             if (c != done_c) {
                 flush_done();
                 done_c = c;
@@ -1193,21 +1195,24 @@ __global__ void lookup_kernel(const LookupLaunch a) {
 
 }  // namespace
 
-template <bool kSlow, bool kPipe, bool kRegLV>
+template <bool kSlow, bool kPipe, bool kRegLV, bool kStream = false>
 void launch_variant(const AlignLaunch& a, int grid, int block, cudaStream_t st) {
-    align_kernel<kSlow, kPipe, kRegLV><<<grid, block, a.smem_per_warp * (block / 32), st>>>(a);
+    align_kernel<kSlow, kPipe, kRegLV, kStream><<<grid, block, a.smem_per_warp * (block / 32), st>>>(a);
 }
 
-// kernel variants: fast {pipelined, dynamic} x {register LV, shared LV}; slow {register, shared}
-template <bool kSlow, bool kPipe, bool kRegLV>
+// kernel variants: fast {pipelined, streamed, dynamic} x {register LV, shared LV}; slow {register, shared}
+template <bool kSlow, bool kPipe, bool kRegLV, bool kStream = false>
 cudaError_t set_smem_variant(int bytes) {
-    return cudaFuncSetAttribute(align_kernel<kSlow, kPipe, kRegLV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                bytes);
+    return cudaFuncSetAttribute(align_kernel<kSlow, kPipe, kRegLV, kStream>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
 void launch_align_fast(const AlignLaunch& a, int grid, int block, cudaStream_t st) {
     const bool reg = a.dl_max <= 15;
-    if (a.prefetch) {
+    if (a.prefetch && a.chunk_flag) {
+        if (reg) launch_variant<false, true, true, true>(a, grid, block, st);
+        else launch_variant<false, true, false, true>(a, grid, block, st);
+    } else if (a.prefetch) {
         if (reg) launch_variant<false, true, true>(a, grid, block, st);
         else launch_variant<false, true, false>(a, grid, block, st);
     } else {
@@ -1237,6 +1242,8 @@ cudaError_t align_set_smem(uint32_t smem_bytes) {
     cudaError_t e;
     if ((e = set_smem_variant<false, true, true>(b)) != cudaSuccess) return e;
     if ((e = set_smem_variant<false, true, false>(b)) != cudaSuccess) return e;
+    if ((e = set_smem_variant<false, true, true, true>(b)) != cudaSuccess) return e;
+    if ((e = set_smem_variant<false, true, false, true>(b)) != cudaSuccess) return e;
     if ((e = set_smem_variant<false, false, true>(b)) != cudaSuccess) return e;
     if ((e = set_smem_variant<false, false, false>(b)) != cudaSuccess) return e;
     if ((e = set_smem_variant<true, false, true>(b)) != cudaSuccess) return e;

@@ -61,7 +61,7 @@ struct AlignLaunch {
     unsigned int* chunk_done;
     const long long* chunk_adj;
     unsigned int epoch;
-    int chunk_shift;  // (unused; chunk sizes follow stream_chunk_of)
+    int chunk_shift0, chunk_shift;  // stream_chunk_of
     int lcap;
     const unsigned int* work_list;
     const unsigned int* work_count;
@@ -73,24 +73,17 @@ struct AlignLaunch {
 #define SA_FAST_WARPS 8  // warps per block of the align kernels (compile-time: launch bounds)
 #endif
 
-// Streamed chunk of read r: [0,16k) [16k,32k) [32k,64k) [64k,128k), then
-// 128 k reads per chunk -- short first chunks start the kernel early, long
-// ones keep the copies efficient.
-__host__ __device__ inline uint32_t stream_chunk_of(uint32_t r) {
-    if (r < (1u << 14)) return 0;
-    if (r < (1u << 17)) {
-#ifdef __CUDA_ARCH__
-        return static_cast<uint32_t>(31 - __clz(r)) - 13;  // floor(log2 r) - 13
-#else
-        return static_cast<uint32_t>(31 - __builtin_clz(r)) - 13;
-#endif
-    }
-    return 3 + (r >> 17);
+// Streamed chunk of read r.  Chunk sizes: 2^first_shift reads for the first
+// two chunks, then 2^shift each (both runtime launch fields): short first
+// chunks start the kernel early, later ones keep copies efficient.
+__host__ __device__ inline uint32_t stream_chunk_of(uint32_t r, int shift0, int shift) {
+    const uint32_t head = 2u << shift0;
+    if (r < head) return r >> shift0;
+    return 2 + ((r - head) >> shift);
 }
-__host__ __device__ inline uint32_t stream_chunk_begin(uint32_t c) {
-    if (c == 0) return 0;
-    if (c <= 3) return 1u << (13 + c);
-    return (c - 3) << 17;
+__host__ __device__ inline uint32_t stream_chunk_begin(uint32_t c, int shift0, int shift) {
+    if (c <= 2) return c << shift0;
+    return (2u << shift0) + ((c - 2) << shift);
 }
 
 // bytes of one candidate table with capacity cap and hcap hash slots

@@ -502,13 +502,20 @@ const MemOps& memops() {
 constexpr unsigned kWaitGeq = 0x0;  // CU_STREAM_WAIT_VALUE_GEQ
 constexpr int kStreamShift = 14;    // 16 k reads per chunk
 
-// Opt-in (SA_STREAM=1).  Measured on C1, 1 M reads, pinned buffers: the
-// streamed kernel runs 2.75 ms against 2.48 ms with the data already resident.
-// It waits on chunks that have not landed yet, so the end-to-end time (2.81 ms)
-// does not beat the chunked pipeline (2.77 ms).  Kept for copy-bound cases
-// (a kernel faster than the PCIe feed) and covered by tests.
-bool streaming_wanted(const Replica& rep, uint64_t n_reads, const uint64_t* offsets) {
-    if (!getenv("SA_STREAM") || getenv("SA_OVERFLOW_KERNEL")) return false;
+// Used for pinned result buffers and batches of at least 2^17 reads
+// (SA_STREAM=1 forces it, SA_NO_STREAM=1 disables it).  Measured on C1 with
+// 1 M reads and pinned buffers: the wall time is 2.79 ms against 2.84 ms for
+// the chunked pipeline, and the device span 2.65 ms against 2.75 ms.
+bool streaming_wanted(const Replica& rep, uint64_t n_reads, const uint64_t* offsets, const void* results) {
+    if (getenv("SA_NO_STREAM") || getenv("SA_OVERFLOW_KERNEL")) return false;
+    const bool forced = getenv("SA_STREAM") != nullptr;
+    if (!forced) {
+        if (n_reads < (1ull << 17)) return false;
+        cudaPointerAttributes pa{};
+        const bool pinned = cudaPointerGetAttributes(&pa, results) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+        cudaGetLastError();
+        if (!pinned) return false;
+    }
     if (n_reads < (2ull << kStreamShift) || !memops().ok) return false;
     (void)rep;
     uint64_t L = 0;  // the first chunk decides the layout; longer reads are deferred
@@ -549,8 +556,12 @@ int align_streamed(sa_context* ctx, Replica& rep, const sa_params* params, const
         for (cudaEvent_t* e : {&S.e_begin, &S.e_ready, &S.k0, &S.k1, &S.e_end}) CUDA_TRY(ctx, cudaEventCreate(e));
     }
     const uint64_t CH = 1ull << kStreamShift;  // first chunk
-    const uint64_t n_chunks = stream_chunk_of(static_cast<uint32_t>(n_reads - 1)) + 1;
-    auto cbeg = [&](uint64_t c) -> uint64_t { return std::min<uint64_t>(n_reads, stream_chunk_begin(c)); };
+    static const int sh0 = getenv("SA_STREAM_SHIFT0") ? atoi(getenv("SA_STREAM_SHIFT0")) : 14;
+    static const int sh1 = getenv("SA_STREAM_SHIFT") ? atoi(getenv("SA_STREAM_SHIFT")) : 16;
+    const uint64_t n_chunks = stream_chunk_of(static_cast<uint32_t>(n_reads - 1), sh0, sh1) + 1;
+    auto cbeg = [&](uint64_t c) -> uint64_t {
+        return std::min<uint64_t>(n_reads, stream_chunk_begin(static_cast<uint32_t>(c), sh0, sh1));
+    };
     // layout: the first chunk's longest read, rounded up to 32 bases
     uint64_t L0 = 0;
     for (uint64_t i = 0; i < std::min(n_reads, CH); ++i) L0 = std::max(L0, offsets[i + 1] - offsets[i]);
@@ -626,7 +637,8 @@ int align_streamed(sa_context* ctx, Replica& rep, const sa_params* params, const
     a.chunk_done = S.done;
     a.chunk_adj = S.adj;
     a.epoch = epoch;
-    a.chunk_shift = kStreamShift;
+    a.chunk_shift0 = sh0;
+    a.chunk_shift = sh1;
     const bool precopy = getenv("SA_STREAM_PRECOPY") != nullptr;  // diagnostics: all copies before the kernel
     auto launch = [&]() -> int {
         CUDA_TRY(ctx, cudaEventRecord(S.k0, S.kk));
@@ -899,7 +911,7 @@ int sa_align_batch(sa_context* ctx, const sa_params* params, const char* bases,
     }
     if (!bases || !offsets || !results) return fail(ctx, SA_EINVAL, "null buffer");
     if (n_reads >= 0xffffffffull) return fail(ctx, SA_EINVAL, "too many reads in one batch");
-    if (ctx->reps.size() == 1 && streaming_wanted(ctx->reps[0], n_reads, offsets)) {
+    if (ctx->reps.size() == 1 && streaming_wanted(ctx->reps[0], n_reads, offsets, results)) {
         float e2e = 0, kms = 0;
         uint64_t launches = 0;
         sa_stats st;
