@@ -30,6 +30,8 @@
 // tables in global memory sized for the worst case n * h_max).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "align_kernels.cuh"
 #include "common.cuh"
 #include "lv.cuh"
@@ -566,7 +568,7 @@ SA_DEV void resolve_wave0(const AlignLaunch& a, int n_eff, int len, uint4* recs,
 // table overflowed (nothing committed).
 template <bool kRegLV>
 SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
-                      unsigned long long& acc, uint4* recs, bool wave0_ready) {
+                      unsigned long long& acc, uint4* recs, bool wave0_ready, const uint4* grecs = nullptr) {
     const AlignLaunch& a = *x.a;
     const int lane = x.lane;
     const int len = x.len;
@@ -595,8 +597,15 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
     for (;;) {
         if (!pruning) {
             if (i >= n_eff) break;
-            if ((i & 31) == 0 && (i > 0 || !wave0_ready))  // speculative probes, seeds i .. i+31
-                compute_wave_sync(a, x.R, offs, i, n_eff, len, recs, lane);
+            if ((i & 31) == 0 && (i > 0 || !wave0_ready)) {  // speculative probes, seeds i .. i+31
+                if (grecs) {  // resolved by the seed kernel
+                    __syncwarp();
+                    if (i + lane < n_eff) recs[lane] = grecs[i + lane];
+                    __syncwarp();
+                } else {
+                    compute_wave_sync(a, x.R, offs, i, n_eff, len, recs, lane);
+                }
+            }
             if (x.n_unscored == 0) {
                 // Fast-forward over a run of seeds that cannot change the
                 // candidate choice: N seeds, popular seeds, and lookups whose
@@ -801,6 +810,226 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
     return true;
 }
 
+// ------------------------------------------------------------------ seed kernel
+// Stage 1 of the two-kernel path: one thread per read (full lane use, and
+// the probes of a whole warp of reads in flight at once).  Decodes the read
+// into forward and reverse-complement planes (REF genome.cpp:182-200), lists
+// its seed offsets (REF aligner.cpp:50-79) and resolves every seed against
+// the index (REF seed_index.cpp:128-143) into the same records the align
+// kernel's waves use.
+// A group of G lanes (G = power of two >= the launch's blocks per read, at
+// most 32) handles one read: lane g decodes 32-base block g with coalesced
+// word loads and SWAR compares, the reverse-complement blocks and the seed
+// windows are assembled with shuffles inside the group, and the read's seeds
+// are dealt round-robin to the lanes so their index probes are in flight
+// together.
+template <int G>
+__global__ void __launch_bounds__(256) seed_kernel(const AlignLaunch a) {
+    const int lane = threadIdx.x & 31;
+    const int g = lane & (G - 1);
+    const int gbase = lane & ~(G - 1);
+    const uint32_t groups = (gridDim.x * blockDim.x) / G;
+    const int half = a.pre_pstride >> 1;
+    const uint32_t gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << gbase);
+    // all groups of a warp iterate the same number of times (shuffles)
+    const uint32_t first = (blockIdx.x * blockDim.x + threadIdx.x) / G;
+    const uint32_t n_iter = (a.n_reads + groups - 1) / groups;
+    for (uint32_t it = 0; it < n_iter; ++it) {
+        const uint32_t r = first + it * groups;
+        const bool live = r < a.n_reads;
+        int len = 0;
+        uint64_t o0 = 0;
+        if (live) {
+            o0 = a.offsets[r];
+            len = static_cast<int>(a.offsets[r + 1] - o0);
+        }
+        uint32_t status = 0;
+        if (!live) status = 4;
+        else if (len < a.s) status = 1;
+        else if (len > a.lcap) status = 3;
+        const int nb = (len + 31) >> 5;
+        // ---- decode block g (REF genome.cpp:182-200 alphabet)
+        uint32_t lo = 0, hi = 0, nn = 0xffffffffu, bad = 0;
+        if (status == 0 && g < nb) {
+            const uintptr_t addr = reinterpret_cast<uintptr_t>(a.bases + (o0 - a.base_off)) + 32u * g;
+            const uint32_t* W = reinterpret_cast<const uint32_t*>(addr & ~static_cast<uintptr_t>(3));
+            const uint32_t sh = 8u * static_cast<uint32_t>(addr & 3);
+            const int avail = len - 32 * g;  // bases of this block present
+            const uint32_t* Wend = reinterpret_cast<const uint32_t*>(
+                (reinterpret_cast<uintptr_t>(a.bases + (o0 - a.base_off)) + len + 3) & ~static_cast<uintptr_t>(3));
+            nn = 0;
+            uint32_t w0 = __ldg(W);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                uint32_t v = 0x4E4E4E4Eu;
+                if (4 * k < avail) {
+                    const uint32_t w1 = (W + k + 1 < Wend) ? __ldg(W + k + 1) : 0u;
+                    v = __funnelshift_r(w0, w1, sh);
+                    w0 = w1;
+                    const int valid = avail - 4 * k;
+                    if (valid < 4) {
+                        const uint32_t keep = (1u << (8 * valid)) - 1u;
+                        v = (v & keep) | (0x4E4E4E4Eu & ~keep);
+                    }
+                }
+                const uint32_t isC = __vcmpeq4(v, 0x43434343u), isG = __vcmpeq4(v, 0x47474747u);
+                const uint32_t isT = __vcmpeq4(v, 0x54545454u), isN = __vcmpeq4(v, 0x4E4E4E4Eu);
+                const uint32_t isA = __vcmpeq4(v, 0x41414141u);
+                bad |= ~(isA | isC | isG | isT | isN);
+                lo |= byte_bits((isC | isT) & 0x01010101u) << (4 * k);
+                hi |= byte_bits((isG | isT) & 0x01010101u) << (4 * k);
+                nn |= byte_bits(isN & 0x01010101u) << (4 * k);
+            }
+        }
+        const bool any_bad = (__ballot_sync(gmask, bad != 0) & gmask) != 0;
+        if (status == 0 && any_bad) status = 2;
+        // 32 forward bases starting at base p (< len), from the group's blocks
+        auto fwd32 = [&](int pq, uint32_t& l, uint32_t& h, uint32_t& n) {
+            const int b = pq >> 5, sft = pq & 31;
+            const int src0 = gbase + (b < G ? b : G - 1), src1 = gbase + (b + 1 < G ? b + 1 : G - 1);
+            const uint32_t l0 = __shfl_sync(gmask, lo, src0), l1 = __shfl_sync(gmask, lo, src1);
+            const uint32_t h0 = __shfl_sync(gmask, hi, src0), h1 = __shfl_sync(gmask, hi, src1);
+            const uint32_t n0 = __shfl_sync(gmask, nn, src0), n1 = __shfl_sync(gmask, nn, src1);
+            const bool in1 = b + 1 < nb;  // beyond the read: N
+            l = __funnelshift_r(l0, in1 ? l1 : 0u, sft);
+            h = __funnelshift_r(h0, in1 ? h1 : 0u, sft);
+            n = __funnelshift_r(n0, in1 ? n1 : 0xffffffffu, sft);
+        };
+        // ---- reverse complement block g: bit b = complement of base len-1-32g-b
+        uint32_t rl = 0, rh = 0, rn = 0xffffffffu;
+        {
+            const int p_lo = len - 32 * (g + 1);
+            uint32_t l, h, n;
+            fwd32(p_lo >= 0 ? p_lo : 0, l, h, n);
+            if (p_lo < 0) {
+                const int sft = -p_lo;
+                l = sft >= 32 ? 0u : l << sft;
+                h = sft >= 32 ? 0u : h << sft;
+                n = sft >= 32 ? 0xffffffffu : ((n << sft) | ((1u << sft) - 1u));
+            }
+            if (status == 0 && g < nb) {
+                rl = __brev(~l);
+                rh = __brev(~h);
+                rn = __brev(n);
+            }
+        }
+        if (status == 0) {
+            uint4* P = a.pre_planes + static_cast<uint64_t>(r) * a.pre_pstride;
+            if (g <= nb && g < half) {
+                P[g] = g < nb ? make_uint4(lo, hi, nn, 0) : make_uint4(0, 0, 0xFFFFFFFFu, 0);
+                P[half + g] = g < nb ? make_uint4(rl, rh, rn, 0) : make_uint4(0, 0, 0xFFFFFFFFu, 0);
+            }
+            if (g == 0 && nb == G && nb < half) {  // the all-N pad block has no lane of its own
+                P[nb] = make_uint4(0, 0, 0xFFFFFFFFu, 0);
+                P[half + nb] = make_uint4(0, 0, 0xFFFFFFFFu, 0);
+            }
+        }
+        // ---- seeds: offsets (REF aligner.cpp:50-79) dealt round-robin; every
+        // lane walks the same generator so the group's shuffles line up
+        uint32_t n_eff = 0;
+        {
+            const int n_cap = status == 0 ? min(a.n, a.n_off_cap) : 0;
+            const int max_off = len - a.s;
+            uint32_t used = 0;
+            int level = 0, odd = -1, o = 0;
+            bool active = false, done = n_cap == 0;
+            auto next_off = [&]() -> int {
+                for (;;) {
+                    if (active) {
+                        if (o <= max_off) {
+                            const int v = o;
+                            o += a.s;
+                            return v;
+                        }
+                        active = false;
+                    }
+                    if (done) return -1;
+                    int shift;
+                    if (odd < 0) {
+                        odd = 1;
+                        level = 1;
+                        shift = 0;
+                    } else {
+                        if ((1 << level) > 4 * a.s) {
+                            done = true;
+                            return -1;
+                        }
+                        shift = (odd * a.s) >> level;
+                        odd += 2;
+                        if (odd >= (1 << level)) {
+                            ++level;
+                            odd = 1;
+                        }
+                    }
+                    if ((used >> shift) & 1u) continue;
+                    used |= 1u << shift;
+                    o = shift;
+                    active = true;
+                }
+            };
+            uint4* rec = live ? a.pre_recs + static_cast<uint64_t>(r) * a.pre_rstride : nullptr;
+            int cnt = 0;
+            // rounds of G seeds; the group agrees on when to stop
+            for (;;) {
+                int my_off = -1;
+                int k = 0;
+                for (; k < G; ++k) {
+                    const int ov = cnt + k < n_cap ? next_off() : -1;
+                    if (ov < 0) break;
+                    if (k == g) my_off = ov;
+                }
+                const int round_n = __shfl_sync(gmask, k, gbase);  // same in every lane
+                uint32_t l, h, n;
+                fwd32(my_off >= 0 ? my_off : 0, l, h, n);
+                if (my_off >= 0) {
+                    uint4 rv;
+                    if (n & seed_mask32(a.s)) {
+                        rv = make_uint4(kSeedN, 0, 0, static_cast<uint32_t>(my_off));
+                    } else {
+                        const uint64_t key = planar_key(l, h, a.s);
+                        const uint64_t rck = planar_rc_key(l, h, a.s);
+                        const uint64_t canon = key < rck ? key : rck;
+                        uint32_t fl = 0;
+                        if (key != canon) fl |= kSeedQflip;
+                        if (key == rck) fl |= kSeedPal;
+                        unsigned pl = 0, m = 0;
+                        const bool found = probe_slot(a.table, a.n_slots, canon, pl, m);
+                        uint32_t c = 0;
+                        if (found) {
+                            const uint32_t ntot = m & 0x7fffffffu;
+                            c = (fl & kSeedPal) ? 2u * ntot : ntot;
+                            if (m & 0x80000000u) fl |= kSeedSingleRc;
+                        }
+                        rv = make_uint4(fl, c, found ? pl : 0u, static_cast<uint32_t>(my_off));
+                    }
+                    rec[cnt + g] = rv;
+                }
+                cnt += round_n;
+                // continue while any read of the warp still has seeds
+                if (__ballot_sync(0xffffffffu, round_n == G && cnt < n_cap) == 0) break;
+            }
+            n_eff = static_cast<uint32_t>(cnt);
+        }
+        if (live && g == 0) a.pre_meta[r] = make_uint2(static_cast<uint32_t>(len), (status << 16) | n_eff);
+    }
+}
+
+// L2 prefetch of the genome windows of a read's singleton seed hits (what
+// seed_record does on the in-kernel path), one read ahead of its alignment.
+SA_DEV void prefetch_windows(const AlignLaunch& a, const uint4* recs, int n, int len, int lane) {
+    if (lane < n && lane < 32) {
+        const uint4 rr = recs[lane];
+        if (!(rr.x & kSeedN) && rr.y == 1u) {
+            const uint32_t dir = ((rr.x & kSeedSingleRc) ? 1u : 0u) ^ ((rr.x & kSeedQflip) ? 1u : 0u);
+            const int o = static_cast<int>(rr.w);
+            const int64_t anc = static_cast<int64_t>(rr.z) - (dir ? (len - a.s - o) : o);
+            const uint64_t b = anc < 0 ? 0 : (static_cast<uint64_t>(anc) >> 5);
+            prefetch_l2(a.planes + b);
+            prefetch_l2(a.planes + b + ((len + a.dl_max + 32) >> 5));
+        }
+    }
+}
+
 #ifndef SA_MIN_BLOCKS
 #define SA_MIN_BLOCKS 3  // blocks of SA_FAST_WARPS warps per SM the register budget must allow
 #endif
@@ -809,7 +1038,7 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
 // the cp.async read pipeline (short reads); kRegLV: register LV only;
 // kStream: the pipelined kernel consumes a batch that is still being copied
 // in (chunk flags; a separate variant so the default kernel carries none of it).
-template <bool kSlow, bool kPipe, bool kRegLV, bool kStream = false>
+template <bool kSlow, bool kPipe, bool kRegLV, bool kStream = false, bool kPre = false>
 __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kernel(const AlignLaunch a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
@@ -901,7 +1130,8 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
         uint4* R = planes + 2 * q * a.wbr;
         return decode_read(words, sh, nwd, len, R, R + a.wbr, lane) ? 2 : 0;
     };
-    auto process = [&](uint32_t r, int q, int len, int st, bool wave0_ready) {
+    auto process = [&](uint32_t r, int q, int len, int st, bool wave0_ready, int ne_pre = -1,
+                       const uint4* grecs = nullptr) {
         if (st == 1) {
             short_read(r, len);
         } else if (st == 2) {
@@ -913,13 +1143,62 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
             x.C = x.R + a.wbr;
             x.len = len;
             x.d_max = a.dmax_param >= 0 ? a.dmax_param : (12 * len + 99) / 100;
-            const int ne = q ? n_eff1 : n_eff0;
-            if (!align_one<kRegLV>(x, r, ne, offs + q * a.n_off_cap, len / a.s, acc, recs + 32 * q, wave0_ready))
+            const int ne = ne_pre >= 0 ? ne_pre : (q ? n_eff1 : n_eff0);
+            if (!align_one<kRegLV>(x, r, ne, offs + q * a.n_off_cap, len / a.s, acc, recs + 32 * q, wave0_ready,
+                                   grecs))
                 overflowed(r);
         }
     };
 
-    if (kPipe) {
+    if (kPre) {
+        // Two-kernel path: planes and seed records come from seed_kernel.
+        // Static striding, one read ahead: while read r is aligned, the
+        // planes and wave-0 records of read r+nw are copied into the other
+        // buffer (cp.async) and its singleton windows are prefetched to L2.
+        const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+        const uint32_t N = a.n_reads;
+        const int half = a.pre_pstride >> 1;
+        const int nrec = min(32, a.pre_rstride);
+        auto issue_copy = [&](uint32_t rr, int q) {
+            const uint4* gp = a.pre_planes + static_cast<uint64_t>(rr) * a.pre_pstride;
+            uint4* R = planes + 2 * q * a.wbr;
+            for (int t = lane; t < half; t += 32) {
+                cp_async16(R + t, gp + t);
+                cp_async16(R + a.wbr + t, gp + half + t);
+            }
+            const uint4* gr = a.pre_recs + static_cast<uint64_t>(rr) * a.pre_rstride;
+            for (int t = lane; t < nrec; t += 32) cp_async16(recs + 32 * q + t, gr + t);
+        };
+        uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+        if (r < N) {
+            uint2 m_c = __ldg(a.pre_meta + r), m_n = make_uint2(0, 1u << 16);
+            issue_copy(r, 0);
+            cp_async_commit();
+            if (r + nw < N) {
+                m_n = __ldg(a.pre_meta + r + nw);
+                issue_copy(r + nw, 1);
+            }
+            cp_async_commit();
+            int p = 0;
+            for (; r < N; r += nw) {
+                cp_async_wait0();  // read r (and r+nw, issued an iteration ago) have landed
+                __syncwarp();
+                if (r + nw < N && (m_n.y >> 16) == 0)
+                    prefetch_windows(a, recs + 32 * (p ^ 1), static_cast<int>(m_n.y & 0xffffu),
+                                     static_cast<int>(m_n.x), lane);
+                uint2 m_nn = make_uint2(0, 1u << 16);
+                if (r + 2 * nw < N) m_nn = __ldg(a.pre_meta + r + 2 * nw);
+                process(r, p, static_cast<int>(m_c.x), static_cast<int>(m_c.y >> 16), true,
+                        static_cast<int>(m_c.y & 0xffffu), a.pre_recs + static_cast<uint64_t>(r) * a.pre_rstride);
+                if (r + 2 * nw < N) issue_copy(r + 2 * nw, p);
+                cp_async_commit();
+                m_c = m_n;
+                m_n = m_nn;
+                p ^= 1;
+            }
+            cp_async_wait0();
+        }
+    } else if (kPipe) {
         // Static striding, software-pipelined one read ahead: while read r is
         // aligned, read r+nw is already decoded and its wave-0 index probes are
         // in flight (cp.async), and read r+2nw's bytes are being copied.
@@ -1195,15 +1474,15 @@ __global__ void lookup_kernel(const LookupLaunch a) {
 
 }  // namespace
 
-template <bool kSlow, bool kPipe, bool kRegLV, bool kStream = false>
+template <bool kSlow, bool kPipe, bool kRegLV, bool kStream = false, bool kPre = false>
 void launch_variant(const AlignLaunch& a, int grid, int block, cudaStream_t st) {
-    align_kernel<kSlow, kPipe, kRegLV, kStream><<<grid, block, a.smem_per_warp * (block / 32), st>>>(a);
+    align_kernel<kSlow, kPipe, kRegLV, kStream, kPre><<<grid, block, a.smem_per_warp * (block / 32), st>>>(a);
 }
 
 // kernel variants: fast {pipelined, streamed, dynamic} x {register LV, shared LV}; slow {register, shared}
-template <bool kSlow, bool kPipe, bool kRegLV, bool kStream = false>
+template <bool kSlow, bool kPipe, bool kRegLV, bool kStream = false, bool kPre = false>
 cudaError_t set_smem_variant(int bytes) {
-    return cudaFuncSetAttribute(align_kernel<kSlow, kPipe, kRegLV, kStream>,
+    return cudaFuncSetAttribute(align_kernel<kSlow, kPipe, kRegLV, kStream, kPre>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
@@ -1219,6 +1498,31 @@ void launch_align_fast(const AlignLaunch& a, int grid, int block, cudaStream_t s
         if (reg) launch_variant<false, false, true>(a, grid, block, st);
         else launch_variant<false, false, false>(a, grid, block, st);
     }
+}
+
+void launch_seed(const AlignLaunch& a, cudaStream_t st) {
+    // G lanes per read: the smallest power of two covering the blocks
+    const int nbmax = (a.pre_pstride >> 1) - 1;
+    auto go = [&](auto kernel, int G) {
+        const uint64_t groups_per_block = 256 / G;
+        uint64_t g = (static_cast<uint64_t>(a.n_reads) + groups_per_block - 1) / groups_per_block;
+        g = std::max<uint64_t>(1, std::min<uint64_t>(g, 148ull * 32));
+        kernel<<<static_cast<int>(g), 256, 0, st>>>(a);
+    };
+    if (nbmax <= 4) go(seed_kernel<4>, 4);
+    else if (nbmax <= 8) go(seed_kernel<8>, 8);
+    else if (nbmax <= 16) go(seed_kernel<16>, 16);
+    else go(seed_kernel<32>, 32);
+}
+
+void launch_align_seeded(const AlignLaunch& a, int grid, int block, cudaStream_t st) {
+    if (a.dl_max <= 15) launch_variant<false, true, true, false, true>(a, grid, block, st);
+    else launch_variant<false, true, false, false, true>(a, grid, block, st);
+}
+
+void launch_align_pre(const AlignLaunch& a, int grid, int block, cudaStream_t st) {
+    launch_seed(a, st);
+    launch_align_seeded(a, grid, block, st);
 }
 
 void launch_align_slow(const AlignLaunch& a, int grid, int block, cudaStream_t st) {
@@ -1243,6 +1547,8 @@ cudaError_t align_set_smem(uint32_t smem_bytes) {
     if ((e = set_smem_variant<false, true, true>(b)) != cudaSuccess) return e;
     if ((e = set_smem_variant<false, true, false>(b)) != cudaSuccess) return e;
     if ((e = set_smem_variant<false, true, true, true>(b)) != cudaSuccess) return e;
+    if ((e = set_smem_variant<false, true, true, false, true>(b)) != cudaSuccess) return e;
+    if ((e = set_smem_variant<false, true, false, false, true>(b)) != cudaSuccess) return e;
     if ((e = set_smem_variant<false, true, false, true>(b)) != cudaSuccess) return e;
     if ((e = set_smem_variant<false, false, true>(b)) != cudaSuccess) return e;
     if ((e = set_smem_variant<false, false, false>(b)) != cudaSuccess) return e;

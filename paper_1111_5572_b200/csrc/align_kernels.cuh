@@ -63,6 +63,16 @@ struct AlignLaunch {
     unsigned int epoch;
     int chunk_shift0, chunk_shift;  // stream_chunk_of
     int lcap;
+    // Two-kernel path (seed_kernel + align_kernel<.., kPre>): per read, the
+    // seed kernel writes forward then reverse-complement planes
+    // (pre_pstride blocks: two halves), every seed record (pre_rstride
+    // entries: {flags, count, payload, offset}) and {length, status << 16 |
+    // n_eff}; status 0 ok, 1 shorter than s, 2 bad character, 3 longer than
+    // the layout (deferred).
+    uint4* pre_planes;
+    uint4* pre_recs;
+    uint2* pre_meta;
+    int pre_pstride, pre_rstride;
     const unsigned int* work_list;
     const unsigned int* work_count;
     unsigned char* gscratch;
@@ -121,6 +131,10 @@ struct LookupLaunch {
 };
 
 void launch_align_fast(const AlignLaunch& a, int grid, int block, cudaStream_t st);
+// seed_kernel then the kPre align kernel (a.pre_* set); reads <= 1 kbp
+void launch_align_pre(const AlignLaunch& a, int grid, int block, cudaStream_t st);
+void launch_seed(const AlignLaunch& a, cudaStream_t st);                                    // stage 1 only
+void launch_align_seeded(const AlignLaunch& a, int grid, int block, cudaStream_t st);      // stage 2 only
 void launch_align_slow(const AlignLaunch& a, int grid, int block, cudaStream_t st);
 void launch_lv_batch(const LvLaunch& a, int grid, int block, cudaStream_t st);
 void launch_lookup(const LookupLaunch& a, cudaStream_t st);

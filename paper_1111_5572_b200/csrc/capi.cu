@@ -42,7 +42,7 @@ int fail_thread(int code, const std::string& msg) {
 
 namespace {
 
-constexpr int kPipeStages = 3;  // chunk buffers in flight per replica (copy / kernel / copy-back)
+constexpr int kPipeStages = 6;  // chunk buffers in flight per replica (copies run ahead of compute)
 constexpr int kCtlWords = 4;  // cursor_fast, cursor_slow, overflow_count, error_flag
 constexpr uint64_t kChunkReads = 1u << 17;  // default; SA_CHUNK_READS overrides (tuning)
 
@@ -69,6 +69,14 @@ struct Stage {  // one of the two pipeline slots of a replica
     unsigned int* d_ctl = nullptr;
     cudaEvent_t k0 = nullptr, km = nullptr, k1 = nullptr;  // fast kernel [k0,km), slow [km,k1)
     cudaEvent_t done = nullptr;                             // after the stage's last D2H
+    // seed-kernel outputs of the two-kernel path (launch_align_pre)
+    uint4* pre_planes = nullptr;
+    uint4* pre_recs = nullptr;
+    uint2* pre_meta = nullptr;
+    uint64_t pre_planes_cap = 0, pre_recs_cap = 0, pre_meta_cap = 0;
+    // seeded pipeline: input landed / consumed by the seed kernel / aligned /
+    // results copied out
+    cudaEvent_t e_in = nullptr, e_seeded = nullptr, e_al = nullptr, e_out = nullptr;
 };
 
 cudaError_t stage_times(Stage& s, float& fast_ms, float& slow_ms) {
@@ -274,6 +282,8 @@ int ensure_stage(sa_context* ctx, Stage& s, uint64_t bytes, uint64_t reads) {
         CUDA_TRY(ctx, cudaEventCreate(&s.km));
         CUDA_TRY(ctx, cudaEventCreate(&s.k1));
         CUDA_TRY(ctx, cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
+        for (cudaEvent_t* e : {&s.e_in, &s.e_seeded, &s.e_al, &s.e_out})
+            CUDA_TRY(ctx, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
         CUDA_TRY(ctx, cudaMalloc(&s.d_ctl, kCtlWords * sizeof(unsigned int)));
     }
     if (bytes > s.bases_cap) {
@@ -296,6 +306,43 @@ int ensure_stage(sa_context* ctx, Stage& s, uint64_t bytes, uint64_t reads) {
         CUDA_TRY(ctx, cudaMalloc(&s.d_overflow, nr * sizeof(unsigned int)));
         s.reads_cap = nr;
     }
+    return SA_OK;
+}
+
+// the seeded pipeline serves batches whose first chunk holds only reads of
+// at most 1 kbp (longer reads later in the batch are deferred)
+bool seeded_wanted(const uint64_t* offsets, const std::vector<uint64_t>& bounds) {
+    if (bounds.size() < 2) return false;
+    for (uint64_t i = bounds[0]; i < bounds[1]; ++i)
+        if (offsets[i + 1] < offsets[i] || offsets[i + 1] - offsets[i] > 1024) return false;
+    return true;
+}
+
+bool use_pre() {
+    static const bool v = getenv("SA_NO_PRE") == nullptr;
+    return v;
+}
+
+// per-read strides of the seed kernel's outputs for a launch layout
+int pre_pstride(const AlignLaunch& a) { return 2 * (a.wbr - 1); }  // (nb + 1) blocks per orientation
+int pre_rstride(const AlignLaunch& a) { return a.n_off_cap; }
+
+int ensure_pre(sa_context* ctx, Stage& s, uint64_t n_reads, const LaunchShape& sh) {
+    if (!use_pre() || !sh.proto.prefetch) return SA_OK;
+    const uint64_t np = n_reads * static_cast<uint64_t>(pre_pstride(sh.proto));
+    const uint64_t nr = n_reads * static_cast<uint64_t>(pre_rstride(sh.proto));
+    auto grow = [&](auto** p, uint64_t& cap, uint64_t need, size_t elem) -> int {
+        if (need <= cap && *p) return SA_OK;
+        if (*p) cudaFree(*p);
+        *p = nullptr;
+        const uint64_t c = std::max<uint64_t>(need, 1024);
+        CUDA_TRY(ctx, cudaMalloc(reinterpret_cast<void**>(p), c * elem));
+        cap = c;
+        return SA_OK;
+    };
+    if (int rc = grow(&s.pre_planes, s.pre_planes_cap, np, sizeof(uint4))) return rc;
+    if (int rc = grow(&s.pre_recs, s.pre_recs_cap, nr, sizeof(uint4))) return rc;
+    if (int rc = grow(&s.pre_meta, s.pre_meta_cap, n_reads, sizeof(uint2))) return rc;
     return SA_OK;
 }
 
@@ -335,7 +382,17 @@ int enqueue_align(sa_context* ctx, Replica& rep, Stage& stg, const LaunchShape& 
     a.gscratch = rep.d_gscratch;
     CUDA_TRY(ctx, cudaMemsetAsync(stg.d_ctl, 0, kCtlWords * sizeof(unsigned int), stg.st));
     if (time_it) CUDA_TRY(ctx, cudaEventRecord(stg.k0, stg.st));
-    launch_align_fast(a, sh.fast_grid, sh.fast_block, stg.st);
+    if (use_pre() && a.prefetch && stg.pre_planes) {  // seed kernel + align kernel
+        a.pre_planes = stg.pre_planes;
+        a.pre_recs = stg.pre_recs;
+        a.pre_meta = stg.pre_meta;
+        a.pre_pstride = pre_pstride(a);
+        a.pre_rstride = pre_rstride(a);
+        launch_align_pre(a, sh.fast_grid, sh.fast_block, stg.st);
+        launches += 1;
+    } else {
+        launch_align_fast(a, sh.fast_grid, sh.fast_block, stg.st);
+    }
     CUDA_TRY(ctx, cudaGetLastError());
     if (time_it) CUDA_TRY(ctx, cudaEventRecord(stg.km, stg.st));
     launches += 1;
@@ -502,20 +559,13 @@ const MemOps& memops() {
 constexpr unsigned kWaitGeq = 0x0;  // CU_STREAM_WAIT_VALUE_GEQ
 constexpr int kStreamShift = 14;    // 16 k reads per chunk
 
-// Used for pinned result buffers and batches of at least 2^17 reads
-// (SA_STREAM=1 forces it, SA_NO_STREAM=1 disables it).  Measured on C1 with
-// 1 M reads and pinned buffers: the wall time is 2.79 ms against 2.84 ms for
-// the chunked pipeline, and the device span 2.65 ms against 2.75 ms.
+// Opt-in (SA_STREAM=1): one launch per batch with the in-kernel read
+// preparation, chunk flags via stream memory ops.  The default batch path is
+// the seeded chunk pipeline (seed kernel + align kernel per chunk), which
+// measured faster on C1 once the seed kernel existed.
 bool streaming_wanted(const Replica& rep, uint64_t n_reads, const uint64_t* offsets, const void* results) {
-    if (getenv("SA_NO_STREAM") || getenv("SA_OVERFLOW_KERNEL")) return false;
-    const bool forced = getenv("SA_STREAM") != nullptr;
-    if (!forced) {
-        if (n_reads < (1ull << 17)) return false;
-        cudaPointerAttributes pa{};
-        const bool pinned = cudaPointerGetAttributes(&pa, results) == cudaSuccess && pa.type == cudaMemoryTypeHost;
-        cudaGetLastError();
-        if (!pinned) return false;
-    }
+    if (!getenv("SA_STREAM") || getenv("SA_OVERFLOW_KERNEL")) return false;
+    (void)results;
     if (n_reads < (2ull << kStreamShift) || !memops().ok) return false;
     (void)rep;
     uint64_t L = 0;  // the first chunk decides the layout; longer reads are deferred
@@ -716,6 +766,166 @@ int align_streamed(sa_context* ctx, Replica& rep, const sa_params* params, const
     return check_errors(ctx, rep);
 }
 
+
+// ---------------------------------------------------------------- seeded chunk pipeline
+// Batch path for reads <= 1 kbp: three streams per replica.
+//   copy-in:  H2D of chunk k into stage k % S (after seed(k - S) consumed it)
+//   compute:  align(k - 1), then seed(k) -- one kernel at a time, so the seed
+//             kernel never waits for SMs held by a persistent align kernel
+//   copy-out: D2H of chunk k's results once align(k) is done
+// Reads longer than the layout are deferred (status 3) to the overflow pass.
+struct SeededChunk {
+    uint64_t r0 = 0, r1 = 0;
+    int stage = 0;
+    AlignLaunch a{};
+    int grid = 0, block = 0;
+};
+
+int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, const char* bases,
+                    const uint64_t* offsets, const std::vector<uint64_t>& bounds, std::atomic<size_t>& next,
+                    uint64_t n_reads, sa_result* results, float& e2e_ms, float& k_ms, uint64_t& launches,
+                    sa_stats* out) {
+    auto& S = rep.sm;
+    if (!S.ci) {
+        CUDA_TRY(ctx, cudaStreamCreateWithFlags(&S.ci, cudaStreamNonBlocking));
+        CUDA_TRY(ctx, cudaStreamCreateWithFlags(&S.kk, cudaStreamNonBlocking));
+        CUDA_TRY(ctx, cudaStreamCreateWithFlags(&S.co, cudaStreamNonBlocking));
+        for (cudaEvent_t* e : {&S.e_begin, &S.e_ready, &S.k0, &S.k1, &S.e_end}) CUDA_TRY(ctx, cudaEventCreate(e));
+    }
+    const size_t n_chunks = bounds.size() - 1;
+    LaunchShape sh;
+    uint64_t shape_L = 0;
+    int k = 0, bad = SA_OK;
+    SeededChunk pend;
+    bool have_pend = false;
+    auto align_pending = [&]() -> int {
+        Stage& st = rep.stage[pend.stage];
+        CUDA_TRY(ctx, cudaStreamWaitEvent(S.kk, st.e_out, 0));  // results buffer free (no-op first time)
+        launch_align_seeded(pend.a, pend.grid, pend.block, S.kk);
+        CUDA_TRY(ctx, cudaGetLastError());
+        ++launches;
+        CUDA_TRY(ctx, cudaEventRecord(st.e_al, S.kk));
+        CUDA_TRY(ctx, cudaStreamWaitEvent(S.co, st.e_al, 0));
+        CUDA_TRY(ctx, cudaMemcpyAsync(results + pend.r0, st.d_results, (pend.r1 - pend.r0) * sizeof(sa_result),
+                                      cudaMemcpyDeviceToHost, S.co));
+        CUDA_TRY(ctx, cudaEventRecord(st.e_out, S.co));
+        return SA_OK;
+    };
+    for (;;) {
+        const size_t c = next.fetch_add(1);
+        if (c >= n_chunks) break;
+        const uint64_t r0 = bounds[c], r1 = bounds[c + 1];
+        uint64_t Lc = 0;
+        for (uint64_t i = r0; i < r1; ++i) {
+            if (offsets[i + 1] < offsets[i]) {
+                bad = fail(ctx, SA_EINVAL, "offsets not ascending");
+                break;
+            }
+            Lc = std::max(Lc, offsets[i + 1] - offsets[i]);
+        }
+        if (bad) break;
+        Lc = std::min<uint64_t>(Lc, 1024);  // longer reads are deferred by the seed kernel
+        if (k == 0 || Lc > shape_L) {
+            std::string w;
+            if ((bad = cached_shape(rep, params, std::max(Lc, shape_L), sh, w))) {
+                fail(ctx, bad, w);
+                break;
+            }
+            shape_L = std::max(Lc, shape_L);
+            if ((bad = ensure_scratch(ctx, rep, sh))) break;
+        }
+        const int si = k % kPipeStages;
+        Stage& st = rep.stage[si];
+        const uint64_t b0 = offsets[r0], b1 = offsets[r1];
+        if ((bad = ensure_stage(ctx, st, b1 - b0, r1 - r0))) break;
+        if ((bad = ensure_pre(ctx, st, r1 - r0, sh))) break;
+        if (k == 0) {
+            if ((bad = ensure_defer(ctx, rep, n_reads))) break;
+            CUDA_TRY(ctx, cudaEventRecord(S.e_begin, S.ci));
+            CUDA_TRY(ctx, cudaMemsetAsync(rep.d_defer_count, 0, sizeof(unsigned int), S.ci));
+            CUDA_TRY(ctx, cudaMemsetAsync(rep.d_stats, 0, kNumStats * sizeof(unsigned long long), S.ci));
+            CUDA_TRY(ctx, cudaEventRecord(S.e_ready, S.ci));
+            CUDA_TRY(ctx, cudaStreamWaitEvent(S.kk, S.e_ready, 0));
+            CUDA_TRY(ctx, cudaStreamWaitEvent(S.co, S.e_ready, 0));
+        }
+        // copy in (the stage's bytes are free once seed(k - S) has run)
+        if (k >= kPipeStages) CUDA_TRY(ctx, cudaStreamWaitEvent(S.ci, st.e_seeded, 0));
+        CUDA_TRY(ctx, cudaMemcpyAsync(st.d_bases, bases + b0, b1 - b0, cudaMemcpyHostToDevice, S.ci));
+        CUDA_TRY(ctx, cudaMemcpyAsync(st.d_offsets, offsets + r0, (r1 - r0 + 1) * sizeof(uint64_t),
+                                      cudaMemcpyHostToDevice, S.ci));
+        CUDA_TRY(ctx, cudaEventRecord(st.e_in, S.ci));
+        // compute: seed(k), then align(k - 1)
+        AlignLaunch a = sh.proto;
+        a.bases = st.d_bases;
+        a.offsets = st.d_offsets;
+        a.base_off = b0;
+        a.n_reads = static_cast<uint32_t>(r1 - r0);
+        a.results = st.d_results;
+        a.stats = rep.d_stats;
+        a.cursor = st.d_ctl;
+        a.overflow_list = rep.d_defer;
+        a.overflow_count = rep.d_defer_count;
+        a.error_flag = rep.d_err;
+        a.error_read = rep.d_err_read;
+        a.read_base = r0;
+        a.gscratch = rep.d_gscratch;
+        a.pre_planes = st.pre_planes;
+        a.pre_recs = st.pre_recs;
+        a.pre_meta = st.pre_meta;
+        a.pre_pstride = pre_pstride(a);
+        a.pre_rstride = pre_rstride(a);
+        // align(k - 1) first: its data is ready, while seed(k) may still
+        // wait for chunk k's copy
+        if (have_pend)
+            if (int rc = align_pending()) return rc;
+        CUDA_TRY(ctx, cudaStreamWaitEvent(S.kk, st.e_in, 0));
+        if (k == 0) CUDA_TRY(ctx, cudaEventRecord(S.k0, S.kk));
+        launch_seed(a, S.kk);
+        CUDA_TRY(ctx, cudaGetLastError());
+        ++launches;
+        CUDA_TRY(ctx, cudaEventRecord(st.e_seeded, S.kk));
+        pend.r0 = r0;
+        pend.r1 = r1;
+        pend.stage = si;
+        pend.a = a;
+        pend.grid = sh.fast_grid;
+        pend.block = sh.fast_block;
+        have_pend = true;
+        ++k;
+    }
+    if (have_pend && !bad)
+        if (int rc = align_pending()) return rc;
+    if (k > 0) {
+        CUDA_TRY(ctx, cudaEventRecord(S.k1, S.kk));
+        CUDA_TRY(ctx, cudaStreamWaitEvent(S.co, S.k1, 0));
+    }
+    static const bool dbg = getenv("SA_DEBUG_PIPE") != nullptr;
+    if (dbg && k > 0) CUDA_TRY(ctx, cudaEventRecord(S.e_ready, S.ci));  // copy-in span end (diagnostics)
+    CUDA_TRY(ctx, cudaStreamSynchronize(S.co));
+    CUDA_TRY(ctx, cudaStreamSynchronize(S.ci));
+    if (dbg && k > 0) {
+        float ci = 0, kb = 0, ke = 0;
+        cudaEventElapsedTime(&ci, S.e_begin, S.e_ready);
+        cudaEventElapsedTime(&kb, S.e_begin, S.k0);
+        cudaEventElapsedTime(&ke, S.e_begin, S.k1);
+        fprintf(stderr, "[pipe] chunks=%d copy-in ends %.3f ms, compute %.3f..%.3f ms\n", k, ci, kb, ke);
+    }
+    std::memset(out, 0, sizeof(sa_stats));
+    if (bad || k == 0) return bad;
+    cudaEventElapsedTime(&k_ms, S.k0, S.k1);
+    // the overflow pass (stage 0's stream) follows everything above
+    if (int rc = ensure_stage(ctx, rep.stage[0], 0, 0)) return rc;
+    uint64_t redone = 0;
+    if (int rc = overflow_pass(ctx, rep, rep.stage[0], params, bases, offsets, results, launches, redone)) return rc;
+    CUDA_TRY(ctx, cudaEventRecord(S.e_end, rep.stage[0].st));
+    CUDA_TRY(ctx, cudaEventSynchronize(S.e_end));
+    cudaEventElapsedTime(&e2e_ms, S.e_begin, S.e_end);
+    unsigned long long h[kNumStats];
+    CUDA_TRY(ctx, cudaMemcpy(h, rep.d_stats, sizeof(h), cudaMemcpyDeviceToHost));
+    add_stats(out, h);
+    return check_errors(ctx, rep);
+}
+
 }  // namespace
 
 extern "C" {
@@ -856,6 +1066,11 @@ void sa_destroy(sa_context* ctx) {
             if (s.km) cudaEventDestroy(s.km);
             if (s.k1) cudaEventDestroy(s.k1);
             if (s.done) cudaEventDestroy(s.done);
+            for (cudaEvent_t e : {s.e_in, s.e_seeded, s.e_al, s.e_out})
+                if (e) cudaEventDestroy(e);
+            if (s.pre_planes) cudaFree(s.pre_planes);
+            if (s.pre_recs) cudaFree(s.pre_recs);
+            if (s.pre_meta) cudaFree(s.pre_meta);
             if (s.st) cudaStreamDestroy(s.st);
         }
         if (rep.d_stats) cudaFree(rep.d_stats);
@@ -963,6 +1178,13 @@ int sa_align_batch(sa_context* ctx, const sa_params* params, const char* bases,
             int k = 0, bad = SA_OK;
             // SA_OVERFLOW_KERNEL (test hook): overflow kernel after every chunk
             const bool defer = getenv("SA_OVERFLOW_KERNEL") == nullptr;
+            if (defer && use_pre() && seeded_wanted(offsets, bounds)) {
+                uint64_t lnch = 0;
+                const int rc = seeded_pipeline(&local_err, rep, params, bases, offsets, bounds, next, n_reads, results,
+                                               e2e[ri], kms[ri], lnch, &part[ri]);
+                launches[ri] += lnch;
+                return rc;
+            }
             for (;;) {
                 size_t c = next.fetch_add(1);
                 if (c >= n_chunks) break;
@@ -1006,6 +1228,7 @@ int sa_align_batch(sa_context* ctx, const sa_params* params, const char* bases,
                 CUDA_TRY(&local_err, cudaMemcpyAsync(stg.d_bases, bases + b0, b1 - b0, cudaMemcpyHostToDevice, stg.st));
                 CUDA_TRY(&local_err, cudaMemcpyAsync(stg.d_offsets, offsets + r0, (r1 - r0 + 1) * sizeof(uint64_t),
                                                      cudaMemcpyHostToDevice, stg.st));
+                if ((bad = ensure_pre(&local_err, stg, r1 - r0, sh))) break;
                 if (int rc = enqueue_align(&local_err, rep, stg, sh, stg.d_bases, stg.d_offsets, b0, r1 - r0, r0,
                                            stg.d_results, rep.d_stats, defer ? rep.d_defer : stg.d_overflow, true,
                                            launches[ri], defer ? rep.d_defer_count : nullptr))
@@ -1088,6 +1311,7 @@ int sa_align_device(sa_context* ctx, const sa_params* params, const char* d_base
     if (int rc = ensure_scratch(ctx, rep, sh)) return rc;
     Stage& stg = rep.stage[kPipeStages];
     if (int rc = ensure_stage(ctx, stg, 0, n_reads)) return rc;
+    if (int rc = ensure_pre(ctx, stg, n_reads, sh)) return rc;
     // the caller's stream drives; this stage keeps only control words
     Stage tmp = stg;
     tmp.st = st;
