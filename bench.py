@@ -279,7 +279,7 @@ def run_ours(args) -> None:
                  + st["window_bases"] / 4.0)
     fast_mean = statistics.mean(fast_ms)
     achieved = alg_bytes / (fast_mean / 1000.0) / 1e9
-    traffic = None
+    traffic = None  # DRAM bytes of both kernels per launch, from one ncu --set full capture
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
@@ -295,7 +295,8 @@ def run_ours(args) -> None:
         "config": _workload(cfg, R),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "align_kernel<false> (fused seed/probe/vote/LV/classify)",
+                     "kernel": "hot path = seed_kernel (decode, seeds, index probes) + align_kernel<kPre> "
+                               "(vote, LV, classify); timed together with CUDA events around both launches",
                      "kernel_ms": fast_mean, "overflow_kernel_ms": statistics.mean(slow_ms),
                      "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(bases.nbytes + offs.nbytes),

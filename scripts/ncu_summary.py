@@ -53,11 +53,12 @@ def launches(path: str) -> list[tuple[str, float]]:
     return [(r[ki], _num(r[vi])) for r in rows[1:] if r[h.index("Metric Name")] == "gpu__time_duration.sum"]
 
 
-def raw(report: str) -> tuple[dict, dict]:
+def raw(report: str) -> tuple[list[dict], dict]:
+    """One dict per captured kernel launch, and the units."""
     out = subprocess.run(["ncu", "-i", report, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
-    h, u, d = rows[0], rows[1], rows[2]
-    return dict(zip(h, d)), dict(zip(h, u))
+    h, u = rows[0], rows[1]
+    return [dict(zip(h, d)) for d in rows[2:]], dict(zip(h, u))
 
 
 def to_bytes(v: str, unit: str) -> float:
@@ -106,41 +107,39 @@ def main() -> None:
         a = agg.setdefault(short, [0, 0.0])
         a[0] += 1
         a[1] += ns
-    d, u = raw(args.report)
+    ds, u = raw(args.report)
     lines = [f"# ncu evidence {args.tag} ({args.config}, {args.reads} reads per launch)", "",
              "## Launch list (`--metrics gpu__time_duration.sum --clock-control none`, cold, serialised)", "",
              "| kernel | launches | total us | mean us |", "|---|---|---|---|"]
     for k, (c, t) in agg.items():
         lines.append(f"| `{k}` | {c} | {t / 1e3:.1f} | {t / 1e3 / c:.1f} |")
-    align = [t for n, t in lst if "align_kernel<0>" in n or "align_kernel<(bool)0" in n]
-    step = [t for n, t in lst if "align_kernel" in n]
-    if align:
-        big = [t for t in align if t > 0.5 * max(align)]
-        lines += ["", f"Fast align kernel on full batches: {len(big)} launches, mean "
-                      f"{sum(big) / len(big) / 1e6:.3f} ms; share of align-kernel time in the list "
-                      f"{100 * sum(align) / sum(step):.1f}%."]
-    lines += ["", f"## Full capture: `{d.get('Kernel Name', '?')[:80]}`", "", "| metric | value |", "|---|---|"]
-    for key, label in METRICS:
-        if key in d:
-            lines.append(f"| {label} (`{key}`) | {d[key]} {u.get(key, '')} |")
-    dram = None
-    if "dram__bytes_read.sum" in d:
-        dram = to_bytes(d["dram__bytes_read.sum"], u["dram__bytes_read.sum"]) + to_bytes(
-            d["dram__bytes_write.sum"], u["dram__bytes_write.sum"])
-        lines.append(f"| DRAM bytes per read | {dram / args.reads:.0f} B |")
-        if args.alg_bytes_per_read:
-            lines.append(f"| algorithmic bytes per read (DESIGN.md §5) | {args.alg_bytes_per_read:.0f} B |")
-    st = {}
-    for k, v in d.items():
-        if k.startswith("smsp__pcsamp_warps_issue_stalled_") and "not_issued" not in k:
-            try:
-                st[k.replace("smsp__pcsamp_warps_issue_stalled_", "")] = _num(v)
-            except ValueError:
-                pass
-    tot = sum(st.values()) or 1
-    lines += ["", "## Warp-state samples (all samples)", "", "| stall | share |", "|---|---|"]
-    for k, v in sorted(st.items(), key=lambda x: -x[1])[:12]:
-        lines.append(f"| {k} | {100 * v / tot:.1f}% |")
+    hot = [t for n, t in lst if "align_kernel" in n or "seed_kernel" in n]
+    if hot:
+        lines += ["", f"Hot-path kernels (seed + align, all launches in the list): {sum(hot) / 1e6:.3f} ms total."]
+    dram = 0.0
+    for d in ds:
+        lines += ["", f"## Full capture: `{d.get('Kernel Name', '?')[:80]}`", "", "| metric | value |", "|---|---|"]
+        for key, label in METRICS:
+            if key in d:
+                lines.append(f"| {label} (`{key}`) | {d[key]} {u.get(key, '')} |")
+        if "dram__bytes_read.sum" in d:
+            b = to_bytes(d["dram__bytes_read.sum"], u["dram__bytes_read.sum"]) + to_bytes(
+                d["dram__bytes_write.sum"], u["dram__bytes_write.sum"])
+            dram += b
+            lines.append(f"| DRAM bytes per read | {b / args.reads:.0f} B |")
+        st = {}
+        for k, v in d.items():
+            if k.startswith("smsp__pcsamp_warps_issue_stalled_") and "not_issued" not in k:
+                try:
+                    st[k.replace("smsp__pcsamp_warps_issue_stalled_", "")] = _num(v)
+                except ValueError:
+                    pass
+        tot = sum(st.values()) or 1
+        lines += ["", "Warp-state samples: " + ", ".join(
+            f"{k} {100 * v / tot:.1f}%" for k, v in sorted(st.items(), key=lambda x: -x[1])[:8])]
+    if args.alg_bytes_per_read:
+        lines += ["", f"Algorithmic bytes per read (DESIGN.md §5): {args.alg_bytes_per_read:.0f} B; DRAM bytes per "
+                      f"read of the captured kernels together: {dram / args.reads:.0f} B."]
     lines += ["", "## Top source lines by stall samples", "", "| file:line | samples | inst | source |",
               "|---|---|---|---|"]
     for f, ln, s, i, src in source_lines(args.report):
@@ -149,10 +148,10 @@ def main() -> None:
         fh.write("\n".join(lines) + "\n")
     tp = os.path.join(PROF, "ncu_traffic.json")
     tj = json.load(open(tp)) if os.path.exists(tp) else {}
-    if dram is not None:
+    if dram:
         tj[args.config] = {"dram_bytes_per_launch": dram, "reads_per_launch": args.reads, "tag": args.tag,
-                           "kernel": d.get("Kernel Name", "")[:80],
-                           "source": "ncu --set full --clock-control none, one launch"}
+                           "kernels": [d.get("Kernel Name", "")[:80] for d in ds],
+                           "source": "ncu --set full --clock-control none, one launch of each kernel, summed"}
         json.dump(tj, open(tp, "w"), indent=1)
     print("\n".join(lines[:40]))
 
