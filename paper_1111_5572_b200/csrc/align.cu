@@ -606,7 +606,12 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
                     compute_wave_sync(a, x.R, offs, i, n_eff, len, recs, lane);
                 }
             }
-            if (x.n_unscored == 0) {
+            bool try_ff = x.n_unscored == 0;
+            if (try_ff && x.n_cands == 0) {  // with no candidate yet, a seed with usable hits stops the run at once
+                const uint4 r0 = recs[i & 31];
+                try_ff = (r0.x & kSeedN) || r0.y == 0u || r0.y > static_cast<uint32_t>(a.hmax);
+            }
+            if (try_ff) {
                 // Fast-forward over a run of seeds that cannot change the
                 // candidate choice: N seeds, popular seeds, and lookups whose
                 // hits (none, or one) land in existing candidates -- all
@@ -800,7 +805,15 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
                                                            : x.tr.best_pos - x.first_pos;
         first_best = delta <= static_cast<uint64_t>(a.bs);
     }
-    if (lane == 0) a.results[r] = res;
+    {  // sa_result as three 8-byte words, one lane each
+        uint64_t w = 0;
+        if (lane == 0) w = res.position;
+        else if (lane == 1)
+            w = static_cast<uint32_t>(res.distance) | (static_cast<uint64_t>(static_cast<uint32_t>(res.gap)) << 32);
+        else if (lane == 2)
+            w = res.kind | (static_cast<uint64_t>(res.has_position) << 8) | (static_cast<uint64_t>(res.direction) << 16);
+        if (lane < 3) reinterpret_cast<uint64_t*>(a.results + r)[lane] = w;
+    }
     stat_add(x, S_READS, 1u);
     stat_add(x, S_ALL_POP, all_pop ? 1u : 0u);
     stat_add(x, S_FIRST_BEST, first_best ? 1u : 0u);
