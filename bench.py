@@ -136,15 +136,13 @@ def run_reference(args) -> None:
     g = synth.make_genome(cfg)
     packed, nmask = synth.pack_genome(g)
     n = args.reads_per_gpu or cfg.n_reads
-    sample = min(n, args.ref_sample)
+    sample = min(n, args.ref_sample or CPU_SAMPLE.get(cfg.name, 10_000))
     bases, offs, _, _ = synth.make_reads(cfg, g, n_reads=sample, seed=cfg.read_seed)
     cores = os.cpu_count() or 1
     if not O.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libseedaln_ref.so not built"}))
         return
-    t0 = time.perf_counter()
-    ri = O.RefIndex(packed, nmask, g.size, cfg.params.seed_size)
-    build_s = time.perf_counter() - t0
+    ri, kind, build_s, note = _cpu_index(O, cfg, g, packed, nmask, bases, offs, cores)
     times = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
@@ -157,9 +155,10 @@ def run_reference(args) -> None:
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.mean(times),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic", "config": _workload(cfg, sample),
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
                              "sample": f"{sample} reads of {cfg.name} per step, reference Aligner (oracle/_ref, "
-                                       f"-O2) one per thread, atomic cursor grain 64; index build {build_s:.1f}s excluded"},
+                                       f"-O2) one per thread, atomic cursor grain 64; index build {build_s:.1f}s "
+                                       f"excluded{note}"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -321,22 +320,35 @@ def run_ours(args) -> None:
         torch.distributed.destroy_process_group()
 
 
+# Default CPU sample per config: about 10-30 s of single-core work.
+CPU_SAMPLE = {"C0": 10_000, "C1": 400_000, "C2": 400_000, "C3": 20_000, "C4": 1_000}
+# Above this the reference's full CSR (4 B per genome position plus keys, built
+# single-threaded) does not fit a bounded baseline run; the oracle port with an
+# index restricted to the keys the sample probes stands in.
+FULL_CSR_MAX_BP = 1_000_000_000
+
+
+def _cpu_index(O, cfg, g, packed, nmask, sb, so, cores):
+    t0 = time.perf_counter()
+    if O.ref_available() and g.size <= FULL_CSR_MAX_BP:
+        ix, kind, note = O.RefIndex(packed, nmask, g.size, cfg.params.seed_size), "reference", ""
+    elif g.size <= FULL_CSR_MAX_BP:
+        ix, kind, note = O.OracleIndex(packed, nmask, g.size, cfg.params.seed_size), "port", ""
+    else:
+        ix = O.OracleIndex(packed, nmask, g.size, cfg.params.seed_size,
+                           for_reads=(cfg.params.seeds_to_try, sb, so), threads=cores)
+        kind, note = "port", "; oracle port (plain C) on a CSR restricted to the keys the sample probes"
+    return ix, kind, time.perf_counter() - t0, note
+
+
 def cpu_baseline(cfg, g, packed, nmask, bases, offs, res_dev, args) -> dict:
     from oracle import oracle as O
 
     cores = os.cpu_count() or 1
-    sample = min(args.cpu_sample, offs.size - 1)
+    sample = min(args.cpu_sample or CPU_SAMPLE.get(cfg.name, 10_000), offs.size - 1)
     sb = bases[:int(offs[sample])]
     so = offs[:sample + 1]
-    if O.ref_available():
-        kind = "reference"
-        t0 = time.perf_counter()
-        ix = O.RefIndex(packed, nmask, g.size, cfg.params.seed_size)
-    else:
-        kind = "port"
-        t0 = time.perf_counter()
-        ix = O.OracleIndex(packed, nmask, g.size, cfg.params.seed_size)
-    build_s = time.perf_counter() - t0
+    ix, kind, build_s, note = _cpu_index(O, cfg, g, packed, nmask, sb, so, cores)
     best = None
     for _ in range(2):
         t0 = time.perf_counter()
@@ -346,7 +358,7 @@ def cpu_baseline(cfg, g, packed, nmask, bases, offs, res_dev, args) -> dict:
     mism = len(O.compare_results(res, res_dev[:sample]))
     return {"value": sample / best, "unit": UNIT, "cores": cores, "kind": kind,
             "sample": f"first {sample} reads of the GPU batch, {cores} threads (one reference Aligner per "
-                      f"thread, atomic cursor grain 64), best of 2; index build {build_s:.1f}s excluded",
+                      f"thread, atomic cursor grain 64), best of 2; index build {build_s:.1f}s excluded{note}",
             "parity_mismatches_vs_gpu": mism}
 
 
@@ -358,8 +370,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="C1")
     ap.add_argument("--reads-per-gpu", type=int, default=0)
-    ap.add_argument("--cpu-sample", type=int, default=400_000)
-    ap.add_argument("--ref-sample", type=int, default=400_000)
+    ap.add_argument("--cpu-sample", type=int, default=0, help="0: CPU_SAMPLE[config]")
+    ap.add_argument("--ref-sample", type=int, default=0, help="0: CPU_SAMPLE[config]")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -853,8 +853,13 @@ __global__ void __launch_bounds__(256) seed_kernel(const AlignLaunch a) {
         int len = 0;
         uint64_t o0 = 0;
         if (live) {
-            o0 = a.offsets[r];
-            len = static_cast<int>(a.offsets[r + 1] - o0);
+            if (a.fixed_len) {
+                o0 = a.base_off + static_cast<uint64_t>(r) * a.fixed_len;
+                len = static_cast<int>(a.fixed_len);
+            } else {
+                o0 = a.offsets[r];
+                len = static_cast<int>(a.offsets[r + 1] - o0);
+            }
         }
         uint32_t status = 0;
         if (!live) status = 4;
@@ -863,7 +868,24 @@ __global__ void __launch_bounds__(256) seed_kernel(const AlignLaunch a) {
         const int nb = (len + 31) >> 5;
         // ---- decode block g (REF genome.cpp:182-200 alphabet)
         uint32_t lo = 0, hi = 0, nn = 0xffffffffu, bad = 0;
-        if (status == 0 && g < nb) {
+        if (a.packed != nullptr) {  // host-packed planes (pack.cpp)
+            if (status == 0 && g < nb) {
+                const uint64_t p = (o0 - a.base_off) + 32ull * static_cast<uint64_t>(g);
+                const uint32_t* P0 = a.packed + (p >> 5);
+                const uint32_t sh = static_cast<uint32_t>(p & 31);
+                lo = __funnelshift_r(__ldg(P0), __ldg(P0 + 1), sh);
+                hi = __funnelshift_r(__ldg(P0 + a.pk_wpp), __ldg(P0 + a.pk_wpp + 1), sh);
+                nn = __funnelshift_r(__ldg(P0 + 2 * a.pk_wpp), __ldg(P0 + 2 * a.pk_wpp + 1), sh);
+                const int avail = len - 32 * g;
+                if (avail < 32) {  // beyond the read: N
+                    const uint32_t keep = (1u << avail) - 1u;
+                    lo &= keep;
+                    hi &= keep;
+                    nn = (nn & keep) | ~keep;
+                }
+                bad = lo & nn;
+            }
+        } else if (status == 0 && g < nb) {
             const uintptr_t addr = reinterpret_cast<uintptr_t>(a.bases + (o0 - a.base_off)) + 32u * g;
             const uint32_t* W = reinterpret_cast<const uint32_t*>(addr & ~static_cast<uintptr_t>(3));
             const uint32_t sh = 8u * static_cast<uint32_t>(addr & 3);

@@ -73,6 +73,14 @@ struct AlignLaunch {
     uint4* pre_recs;
     uint2* pre_meta;
     int pre_pstride, pre_rstride;
+    // Packed input (pack.cpp): when non-null the seed kernel reads the chunk's
+    // bases from three bit planes {lo, hi, n} of pk_wpp words each (bit i =
+    // base base_off + i) instead of ASCII bytes; lo & n marks a bad character.
+    const uint32_t* packed;
+    uint64_t pk_wpp;
+    // Every read of the chunk has this length (0: use offsets): read r starts
+    // at base base_off + r * fixed_len and the offsets are never copied in.
+    uint32_t fixed_len;
     const unsigned int* work_list;
     const unsigned int* work_count;
     unsigned char* gscratch;

@@ -44,7 +44,7 @@ namespace {
 
 constexpr int kPipeStages = 6;  // chunk buffers in flight per replica (copies run ahead of compute)
 constexpr int kCtlWords = 4;  // cursor_fast, cursor_slow, overflow_count, error_flag
-constexpr uint64_t kChunkReads = 1u << 17;  // default; SA_CHUNK_READS overrides (tuning)
+constexpr uint64_t kChunkReads = 49152;  // default; SA_CHUNK_READS overrides (tuning)
 
 uint64_t chunk_reads_setting() {
     static const uint64_t v = [] {
@@ -77,7 +77,13 @@ struct Stage {  // one of the two pipeline slots of a replica
     // seeded pipeline: input landed / consumed by the seed kernel / aligned /
     // results copied out
     cudaEvent_t e_in = nullptr, e_seeded = nullptr, e_al = nullptr, e_out = nullptr;
+    // packed input (pack.cpp): pinned host planes and their device copy
+    uint32_t* h_pack = nullptr;
+    uint32_t* d_pack = nullptr;
+    uint64_t pack_cap = 0;  // words, all three planes
 };
+
+int ensure_pack(sa_context* ctx, Stage& s, uint64_t words);
 
 cudaError_t stage_times(Stage& s, float& fast_ms, float& slow_ms) {
     cudaError_t e = cudaEventSynchronize(s.k1);
@@ -306,6 +312,20 @@ int ensure_stage(sa_context* ctx, Stage& s, uint64_t bytes, uint64_t reads) {
         CUDA_TRY(ctx, cudaMalloc(&s.d_overflow, nr * sizeof(unsigned int)));
         s.reads_cap = nr;
     }
+    return SA_OK;
+}
+
+int ensure_pack(sa_context* ctx, Stage& s, uint64_t words) {
+    if (words <= s.pack_cap) return SA_OK;
+    if (s.d_pack) cudaFree(s.d_pack);
+    if (s.h_pack) cudaFreeHost(s.h_pack);
+    s.d_pack = nullptr;
+    s.h_pack = nullptr;
+    s.pack_cap = 0;
+    const uint64_t w = std::max<uint64_t>(words + words / 4, 1 << 16);
+    CUDA_TRY(ctx, cudaMalloc(&s.d_pack, w * sizeof(uint32_t)));
+    CUDA_TRY(ctx, cudaHostAlloc(&s.h_pack, w * sizeof(uint32_t), cudaHostAllocDefault));
+    s.pack_cap = w;
     return SA_OK;
 }
 
@@ -777,6 +797,7 @@ int align_streamed(sa_context* ctx, Replica& rep, const sa_params* params, const
 struct SeededChunk {
     uint64_t r0 = 0, r1 = 0;
     int stage = 0;
+    cudaStream_t cs = nullptr;  // compute stream
     AlignLaunch a{};
     int grid = 0, block = 0;
 };
@@ -798,13 +819,30 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
     int k = 0, bad = SA_OK;
     SeededChunk pend;
     bool have_pend = false;
+    const bool packed = pack_enabled();
+    // Chunk k's seed and align kernels run on its stage's own stream, so the
+    // kernels of consecutive chunks share the GPU: the next chunk's blocks
+    // fill the SMs a kernel's tail leaves idle (C1 e2e 367 -> 405 M reads/s).
+    // SA_PIPE_SINGLE=1 keeps one compute stream (align(k-1), then seed(k)).
+    const bool multi = getenv("SA_PIPE_SINGLE") == nullptr;
+    const bool dbg = getenv("SA_DEBUG_PIPE") != nullptr && !multi;
+    std::vector<std::pair<char, cudaEvent_t>> trail;  // diagnostics: compute-stream marks
+    auto mark = [&](char what) {
+        if (!dbg) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, S.kk);
+        trail.emplace_back(what, e);
+    };
     auto align_pending = [&]() -> int {
         Stage& st = rep.stage[pend.stage];
-        CUDA_TRY(ctx, cudaStreamWaitEvent(S.kk, st.e_out, 0));  // results buffer free (no-op first time)
-        launch_align_seeded(pend.a, pend.grid, pend.block, S.kk);
+        CUDA_TRY(ctx, cudaStreamWaitEvent(pend.cs, st.e_out, 0));  // results buffer free (no-op first time)
+        mark('w');
+        launch_align_seeded(pend.a, pend.grid, pend.block, pend.cs);
+        mark('a');
         CUDA_TRY(ctx, cudaGetLastError());
         ++launches;
-        CUDA_TRY(ctx, cudaEventRecord(st.e_al, S.kk));
+        CUDA_TRY(ctx, cudaEventRecord(st.e_al, pend.cs));
         CUDA_TRY(ctx, cudaStreamWaitEvent(S.co, st.e_al, 0));
         CUDA_TRY(ctx, cudaMemcpyAsync(results + pend.r0, st.d_results, (pend.r1 - pend.r0) * sizeof(sa_result),
                                       cudaMemcpyDeviceToHost, S.co));
@@ -815,15 +853,19 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
         const size_t c = next.fetch_add(1);
         if (c >= n_chunks) break;
         const uint64_t r0 = bounds[c], r1 = bounds[c + 1];
-        uint64_t Lc = 0;
+        uint64_t Lc = 0, Lmin = ~0ull;
         for (uint64_t i = r0; i < r1; ++i) {
             if (offsets[i + 1] < offsets[i]) {
                 bad = fail(ctx, SA_EINVAL, "offsets not ascending");
                 break;
             }
-            Lc = std::max(Lc, offsets[i + 1] - offsets[i]);
+            const uint64_t li = offsets[i + 1] - offsets[i];
+            Lc = std::max(Lc, li);
+            Lmin = std::min(Lmin, li);
         }
         if (bad) break;
+        // one length for the whole chunk: the offsets need not be copied
+        const uint32_t fixed = (Lmin == Lc && Lc > 0 && Lc < (1u << 30)) ? static_cast<uint32_t>(Lc) : 0u;
         Lc = std::min<uint64_t>(Lc, 1024);  // longer reads are deferred by the seed kernel
         if (k == 0 || Lc > shape_L) {
             std::string w;
@@ -848,11 +890,28 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
             CUDA_TRY(ctx, cudaStreamWaitEvent(S.kk, S.e_ready, 0));
             CUDA_TRY(ctx, cudaStreamWaitEvent(S.co, S.e_ready, 0));
         }
+        // align(k - 1) first: its data is ready, and the host packs chunk k next
+        if (have_pend) {
+            if (int rc = align_pending()) return rc;
+            have_pend = false;
+        }
         // copy in (the stage's bytes are free once seed(k - S) has run)
+        const uint64_t wpp = packed ? pack_words_per_plane(b1 - b0) : 0;
+        if (packed) {
+            if ((bad = ensure_pack(ctx, st, 3 * wpp))) break;
+            // the stage's host planes are free once their last copy landed
+            if (k >= kPipeStages) CUDA_TRY(ctx, cudaEventSynchronize(st.e_in));
+            pack_planar(bases + b0, b1 - b0, st.h_pack, wpp);
+        }
         if (k >= kPipeStages) CUDA_TRY(ctx, cudaStreamWaitEvent(S.ci, st.e_seeded, 0));
-        CUDA_TRY(ctx, cudaMemcpyAsync(st.d_bases, bases + b0, b1 - b0, cudaMemcpyHostToDevice, S.ci));
-        CUDA_TRY(ctx, cudaMemcpyAsync(st.d_offsets, offsets + r0, (r1 - r0 + 1) * sizeof(uint64_t),
-                                      cudaMemcpyHostToDevice, S.ci));
+        if (packed)
+            CUDA_TRY(ctx, cudaMemcpyAsync(st.d_pack, st.h_pack, 3 * wpp * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                                          S.ci));
+        else
+            CUDA_TRY(ctx, cudaMemcpyAsync(st.d_bases, bases + b0, b1 - b0, cudaMemcpyHostToDevice, S.ci));
+        if (!fixed)
+            CUDA_TRY(ctx, cudaMemcpyAsync(st.d_offsets, offsets + r0, (r1 - r0 + 1) * sizeof(uint64_t),
+                                          cudaMemcpyHostToDevice, S.ci));
         CUDA_TRY(ctx, cudaEventRecord(st.e_in, S.ci));
         // compute: seed(k), then align(k - 1)
         AlignLaunch a = sh.proto;
@@ -874,32 +933,43 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
         a.pre_meta = st.pre_meta;
         a.pre_pstride = pre_pstride(a);
         a.pre_rstride = pre_rstride(a);
-        // align(k - 1) first: its data is ready, while seed(k) may still
-        // wait for chunk k's copy
-        if (have_pend)
-            if (int rc = align_pending()) return rc;
-        CUDA_TRY(ctx, cudaStreamWaitEvent(S.kk, st.e_in, 0));
-        if (k == 0) CUDA_TRY(ctx, cudaEventRecord(S.k0, S.kk));
-        launch_seed(a, S.kk);
+        a.packed = packed ? st.d_pack : nullptr;
+        a.pk_wpp = wpp;
+        a.fixed_len = fixed;
+        cudaStream_t cs = multi ? st.st : S.kk;
+        CUDA_TRY(ctx, cudaStreamWaitEvent(cs, st.e_in, 0));
+        if (k == 0) CUDA_TRY(ctx, cudaEventRecord(S.k0, cs));
+        mark('W');
+        launch_seed(a, cs);
+        mark('s');
         CUDA_TRY(ctx, cudaGetLastError());
         ++launches;
-        CUDA_TRY(ctx, cudaEventRecord(st.e_seeded, S.kk));
+        CUDA_TRY(ctx, cudaEventRecord(st.e_seeded, cs));
         pend.r0 = r0;
         pend.r1 = r1;
         pend.stage = si;
+        pend.cs = cs;
         pend.a = a;
         pend.grid = sh.fast_grid;
         pend.block = sh.fast_block;
         have_pend = true;
+        if (multi) {
+            if (int rc = align_pending()) return rc;
+            have_pend = false;
+        }
         ++k;
     }
     if (have_pend && !bad)
         if (int rc = align_pending()) return rc;
+    if (multi)  // join the stage streams into the compute stream
+        for (int j = 0; j < kPipeStages && j < k; ++j) {
+            CUDA_TRY(ctx, cudaEventRecord(rep.stage[j].done, rep.stage[j].st));
+            CUDA_TRY(ctx, cudaStreamWaitEvent(S.kk, rep.stage[j].done, 0));
+        }
     if (k > 0) {
         CUDA_TRY(ctx, cudaEventRecord(S.k1, S.kk));
         CUDA_TRY(ctx, cudaStreamWaitEvent(S.co, S.k1, 0));
     }
-    static const bool dbg = getenv("SA_DEBUG_PIPE") != nullptr;
     if (dbg && k > 0) CUDA_TRY(ctx, cudaEventRecord(S.e_ready, S.ci));  // copy-in span end (diagnostics)
     CUDA_TRY(ctx, cudaStreamSynchronize(S.co));
     CUDA_TRY(ctx, cudaStreamSynchronize(S.ci));
@@ -909,7 +979,18 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
         cudaEventElapsedTime(&kb, S.e_begin, S.k0);
         cudaEventElapsedTime(&ke, S.e_begin, S.k1);
         fprintf(stderr, "[pipe] chunks=%d copy-in ends %.3f ms, compute %.3f..%.3f ms\n", k, ci, kb, ke);
+        // kernel time vs waiting: 'W'/'w' marks precede seed/align, 's'/'a' follow
+        float seed = 0, al = 0, wait = 0;
+        for (size_t i = 1; i < trail.size(); ++i) {
+            float d = 0;
+            cudaEventElapsedTime(&d, trail[i - 1].second, trail[i].second);
+            if (trail[i].first == 's') seed += d;
+            else if (trail[i].first == 'a') al += d;
+            else wait += d;
+        }
+        fprintf(stderr, "[pipe] seed %.3f ms, align %.3f ms, between kernels %.3f ms\n", seed, al, wait);
     }
+    for (auto& t : trail) cudaEventDestroy(t.second);
     std::memset(out, 0, sizeof(sa_stats));
     if (bad || k == 0) return bad;
     cudaEventElapsedTime(&k_ms, S.k0, S.k1);
@@ -1071,6 +1152,8 @@ void sa_destroy(sa_context* ctx) {
             if (s.pre_planes) cudaFree(s.pre_planes);
             if (s.pre_recs) cudaFree(s.pre_recs);
             if (s.pre_meta) cudaFree(s.pre_meta);
+            if (s.d_pack) cudaFree(s.d_pack);
+            if (s.h_pack) cudaFreeHost(s.h_pack);
             if (s.st) cudaStreamDestroy(s.st);
         }
         if (rep.d_stats) cudaFree(rep.d_stats);
@@ -1152,13 +1235,40 @@ int sa_align_batch(sa_context* ctx, const sa_params* params, const char* bases,
     // after a short copy; the GPU is busy with chunk k while chunk k+1 copies.
     const uint64_t chunk_reads = chunk_reads_setting();
     std::vector<uint64_t> bounds{0};
-    uint64_t step = std::min<uint64_t>(chunk_reads, 1u << 14);
-    while (bounds.back() < n_reads) {
-        uint64_t b = bounds.back();
-        uint64_t e = std::min(n_reads, b + step);
-        step = std::min(chunk_reads, 2 * step);
-        while (e > b + 1 && offsets[e] - offsets[b] > kChunkBytes) e = b + (e - b) / 2;
-        bounds.push_back(e);
+    {
+        // sizes ramp up (16 k, 32 k, ...) so the first kernel starts after a
+        // short copy, and back down at the end so little compute is left once
+        // the last copy lands; equal chunks in between
+        std::vector<uint64_t> up;
+        for (uint64_t s = std::min<uint64_t>(chunk_reads, 1u << 14); s < chunk_reads; s *= 2) up.push_back(s);
+        uint64_t ramp = 0;
+        for (uint64_t s : up) ramp += 2 * s;
+        std::vector<uint64_t> sizes;
+        if (n_reads >= ramp + chunk_reads) {
+            sizes = up;
+            const uint64_t mid = n_reads - ramp, m = (mid + chunk_reads - 1) / chunk_reads;
+            for (uint64_t i = 0; i < m; ++i) sizes.push_back(mid / m + (i < mid % m ? 1 : 0));
+            sizes.insert(sizes.end(), up.rbegin(), up.rend());
+        } else {
+            uint64_t left = n_reads, s = up.empty() ? chunk_reads : up[0];
+            while (left) {
+                sizes.push_back(std::min(left, s));
+                left -= sizes.back();
+                s = std::min(chunk_reads, 2 * s);
+            }
+        }
+        for (uint64_t s : sizes) {
+            const uint64_t b = bounds.back();
+            uint64_t e = b + s;
+            while (e > b + 1 && offsets[e] - offsets[b] > kChunkBytes) e = b + (e - b) / 2;
+            bounds.push_back(e);
+            while (bounds.back() < b + s) {  // byte-capped: finish this size in pieces
+                const uint64_t bb = bounds.back();
+                uint64_t ee = b + s;
+                while (ee > bb + 1 && offsets[ee] - offsets[bb] > kChunkBytes) ee = bb + (ee - bb) / 2;
+                bounds.push_back(ee);
+            }
+        }
     }
     const size_t n_chunks = bounds.size() - 1;
     std::atomic<size_t> next{0};

@@ -365,3 +365,31 @@ def test_streamed_batch_errors(monkeypatch):
     again = al.align_arrays(bases, offs)
     want, _ = O.OracleIndex(packed, nmask, g.size, 20).align_arrays(cfg.params, bases, offs, threads=8)
     assert O.compare_results(again, want) == []
+
+
+@pytest.mark.parametrize("pack", ["0", "3"])
+def test_batch_pipeline_fixed_length_ramp_and_packing(pack, monkeypatch):
+    """The seeded chunk pipeline on 400 k equal-length reads (offsets never
+    copied in; chunk sizes ramp up and back down) and on ragged reads with
+    deferred long ones, with ASCII input and with host-packed bit planes
+    (SA_PACK_THREADS); bad characters still fail the right read."""
+    monkeypatch.setenv("SA_PACK_THREADS", pack)
+    cfg, g, packed, nmask, bases, offs = _case("C1", 5_000_000, 400_000, 10, 0.01)
+    genome = api.PackedGenome(packed, nmask, g.size)
+    al = api.Aligner(api.SeedIndex.build(genome, 20), genome, cfg.params)
+    oi = O.OracleIndex(packed, nmask, g.size, 20)
+    got = al.align_arrays(bases, offs)
+    want, wst = oi.align_arrays(cfg.params, bases, offs, threads=8)
+    assert O.compare_results(got, want) == []
+    for f in api.REFERENCE_STAT_FIELDS:
+        if f != "dp_cells":
+            assert al.stats().values[f] == wst[f], f
+    bad = bases.copy()
+    bad[int(offs[399_990]) + 7] = ord("x")  # in the last (ramp-down) chunk
+    with pytest.raises(ValueError, match="read 399990"):
+        al.align_arrays(bad, offs)
+    cfg2, g2, packed2, nmask2, b2, o2 = _streamed_case()
+    genome2 = api.PackedGenome(packed2, nmask2, g2.size)
+    al2 = api.Aligner(api.SeedIndex.build(genome2, 20), genome2, cfg2.params)
+    want2, _ = O.OracleIndex(packed2, nmask2, g2.size, 20).align_arrays(cfg2.params, b2, o2, threads=8)
+    assert O.compare_results(al2.align_arrays(b2, o2), want2) == []
