@@ -825,7 +825,8 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
     // fill the SMs a kernel's tail leaves idle (C1 e2e 367 -> 405 M reads/s).
     // SA_PIPE_SINGLE=1 keeps one compute stream (align(k-1), then seed(k)).
     const bool multi = getenv("SA_PIPE_SINGLE") == nullptr;
-    const bool dbg = getenv("SA_DEBUG_PIPE") != nullptr && !multi;
+    const bool dbg_span = getenv("SA_DEBUG_PIPE") != nullptr;
+    const bool dbg = dbg_span && !multi;  // per-kernel trail: single compute stream only
     std::vector<std::pair<char, cudaEvent_t>> trail;  // diagnostics: compute-stream marks
     auto mark = [&](char what) {
         if (!dbg) return;
@@ -970,10 +971,10 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
         CUDA_TRY(ctx, cudaEventRecord(S.k1, S.kk));
         CUDA_TRY(ctx, cudaStreamWaitEvent(S.co, S.k1, 0));
     }
-    if (dbg && k > 0) CUDA_TRY(ctx, cudaEventRecord(S.e_ready, S.ci));  // copy-in span end (diagnostics)
+    if (dbg_span && k > 0) CUDA_TRY(ctx, cudaEventRecord(S.e_ready, S.ci));  // copy-in span end (diagnostics)
     CUDA_TRY(ctx, cudaStreamSynchronize(S.co));
     CUDA_TRY(ctx, cudaStreamSynchronize(S.ci));
-    if (dbg && k > 0) {
+    if (dbg_span && k > 0) {
         float ci = 0, kb = 0, ke = 0;
         cudaEventElapsedTime(&ci, S.e_begin, S.e_ready);
         cudaEventElapsedTime(&kb, S.e_begin, S.k0);
