@@ -380,7 +380,7 @@ SA_DEV void score_candidate(Ctx& x, uint32_t idx) {
         const uint64_t want = static_cast<uint64_t>(x.len) + static_cast<uint64_t>(d_limit);
         const int w = static_cast<int>(want < rem ? want : rem);
         const uint32_t wofs = static_cast<uint32_t>(anchor - gb0 * 32);
-        const int d = lv_warp<kRegLV>(orient, x.len, x.W, wofs, w, d_limit, x.F, lane, x.cells);
+        const int d = lv_warp<kRegLV>(orient, x.len, x.W, wofs, w, d_limit, x.F, lane, x.cells, a.f16 != 0);
         stat_add(x, S_DIST, 1u);
         x.calls++;
         stat_add(x, S_WINDOW, static_cast<uint32_t>(w));
@@ -1090,7 +1090,7 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
     x.a = &a;
     x.lane = lane;
     uint4* planes = reinterpret_cast<uint4*>(ws);  // buffer q: R = planes + 2q*wbr, C = R + wbr
-    x.W = planes + 4 * a.wbr;
+    x.W = planes + (a.prefetch ? 4 : 2) * a.wbr;  // one {R, C} buffer without the read pipeline
     uint4* recs = x.W + a.wbw;                      // 2 x 32
     uint4* pslot = recs + 64;                       // 32
     unsigned long long* pcanon = reinterpret_cast<unsigned long long*>(pslot + 32);  // 32

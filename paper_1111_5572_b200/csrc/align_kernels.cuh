@@ -63,6 +63,7 @@ struct AlignLaunch {
     unsigned int epoch;
     int chunk_shift0, chunk_shift;  // stream_chunk_of
     int lcap;
+    int f16;  // LV frontier as 16-bit entries (reads < 32 k bases)
     // Two-kernel path (seed_kernel + align_kernel<.., kPre>): per read, the
     // seed kernel writes forward then reverse-complement planes
     // (pre_pstride blocks: two halves), every seed record (pre_rstride

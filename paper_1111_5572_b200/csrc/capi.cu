@@ -56,7 +56,7 @@ uint64_t chunk_reads_setting() {
 }
 constexpr uint64_t kChunkBytes = 256ull << 20;
 constexpr int kFastCap = 64, kFastHcap = 128;
-constexpr uint64_t kSlowScratchBudget = 2ull << 30;
+constexpr uint64_t kSlowScratchBudget = 6ull << 30;  // global candidate tables of the overflow kernel
 
 struct Stage {  // one of the two pipeline slots of a replica
     cudaStream_t st = nullptr;
@@ -220,17 +220,39 @@ int make_shape(Replica& rep, const sa_params* p, uint64_t Lmax, LaunchShape& sh,
     a.wbr = (L + 31) / 32 + 2;
     a.wbw = (64 + L + a.dl_max + 31) / 32 + 4;
     a.n_off_cap = round4(std::max(1, std::min(p->seeds_to_try, L - p->seed_size + 1)));
-    a.f_ints = a.dl_max > 15 ? round4(2 * (2 * a.dl_max + 3)) : 0;
-    // per warp: planes[2]{R,C}, window, seed records[2][32], probe landing
-    // zone[32] + keys[32], offsets[2], LV frontier, stats (align.cu kernel)
-    const uint64_t common = 16ull * (4 * a.wbr + a.wbw + 64 + 32) + 8ull * 32 +
-                            4ull * (2 * a.n_off_cap + a.f_ints) + 8ull * kNumStats;
+    // per warp: planes {R,C} (two buffers for the read pipeline of reads
+    // <= 1 kbp, one otherwise), window, seed records[2][32], probe landing
+    // zone[32] + keys[32], offsets[2], LV frontier, read staging, candidate
+    // table, stats (align.cu kernel)
+    a.prefetch = L <= 1024 ? 1 : 0;
     a.cap = kFastCap;
     a.hcap = kFastHcap;
-    a.prefetch = L <= 1024 ? 1 : 0;
     a.lcap = L;  // every read of this layout fits
     a.sbw = a.prefetch ? round4((L + 3) / 4 + 2) : 0;
-    a.smem_per_warp = round16(common + 8ull * a.sbw + cand_table_bytes(a.cap, a.hcap));
+    auto f_ints_for = [&](int f16) {
+        return a.dl_max > 15 ? round4(f16 ? (2 * a.dl_max + 3) : 2 * (2 * a.dl_max + 3)) : 0;
+    };
+    auto common_for = [&](int f16) {
+        return 16ull * ((a.prefetch ? 4 : 2) * a.wbr + a.wbw + 64 + 32) + 8ull * 32 +
+               4ull * (2 * a.n_off_cap + f_ints_for(f16)) + 8ull * kNumStats;
+    };
+    auto spw_for = [&](int f16) {
+        return round16(common_for(f16) + 8ull * a.sbw + cand_table_bytes(a.cap, a.hcap));
+    };
+    // A 16-bit LV frontier (lv.cuh) is slower per step (C3: 224 vs 162 ms), so
+    // it is used only where the smaller layout fits more warps per SM (C4:
+    // 8 instead of 7 warps, 364 -> 324 ms).
+    auto warps_per_sm = [&](uint32_t spw) {  // shared memory and 80 registers (24 warps)
+        const int w = std::min<int>(8, (227 * 1024) / spw);
+        return w < 1 ? 0 : std::min<int>(24 / w, (227 * 1024) / (w * spw)) * w;
+    };
+    a.f16 = (L < 32000 && a.dl_max > 15 && getenv("SA_LV_F16_OFF") == nullptr &&
+             warps_per_sm(spw_for(1)) > warps_per_sm(spw_for(0)))
+                ? 1
+                : 0;
+    a.f_ints = f_ints_for(a.f16);
+    const uint64_t common = common_for(a.f16);
+    a.smem_per_warp = spw_for(a.f16);
     const uint32_t kMaxSmem = 227 * 1024;
     if (a.smem_per_warp > kMaxSmem) {
         why = "read too long for the shared-memory layout (limit ~60 kbp)";
@@ -259,7 +281,7 @@ int make_shape(Replica& rep, const sa_params* p, uint64_t Lmax, LaunchShape& sh,
     sh.slow_hcap = static_cast<int>(hcap_slow);
     sh.slow_table_bytes = (cand_table_bytes(sh.slow_cap, sh.slow_hcap) + 255) & ~255ull;
     sh.slow_smem_per_warp = round16(common);
-    uint64_t slow_warps = std::min<uint64_t>(static_cast<uint64_t>(rep.sm_count) * 8,
+    uint64_t slow_warps = std::min<uint64_t>(static_cast<uint64_t>(rep.sm_count) * 24,
                                              std::max<uint64_t>(32, kSlowScratchBudget / sh.slow_table_bytes));
     sh.slow_block = 32;
     sh.slow_grid = static_cast<int>(slow_warps);

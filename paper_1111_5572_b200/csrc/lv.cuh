@@ -77,13 +77,18 @@ SA_DEV int lv_warp_reg(const uint4* R, int m, const uint4* W, uint32_t wofs, int
     return -1;
 }
 
-// Shared-memory wavefront for any d_limit: F holds 2 * (2*dl + 3) ints.
+// Shared-memory wavefront for any d_limit: F holds 2 * (2*dl + 3) entries of
+// T.  T = short halves the frontier for reads < 32 k bases (every stored value
+// is a read index <= m or "unreachable", kept as -32768: any negative value
+// stays unreachable after +1, REF edit_distance.cpp:56-59).
+template <typename T = int>
 SA_DEV int lv_warp_smem(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, int dl,
-                        int* F, int lane, uint32_t& cells) {
+                        T* F, int lane, uint32_t& cells) {
+    constexpr int kStoreUnreach = sizeof(T) == 2 ? -32768 : kUnreach;
     const int width = 2 * dl + 3;
-    int* cur = F;
-    int* nxt = F + width;
-    for (int t = lane; t < 2 * width; t += 32) F[t] = kUnreach;
+    T* cur = F;
+    T* nxt = F + width;
+    for (int t = lane; t < 2 * width; t += 32) F[t] = static_cast<T>(kStoreUnreach);
     __syncwarp();
     const int off = dl + 1;
     for (int e = 0; e <= dl; ++e) {
@@ -91,12 +96,12 @@ SA_DEV int lv_warp_smem(const uint4* R, int m, const uint4* W, uint32_t wofs, in
         for (int k = -e + lane; k <= e; k += 32) {
             const int v = lv_step(e, k, cur[k - 1 + off], cur[k + off], cur[k + 1 + off], m, w, R,
                                   W, wofs, cells);
-            nxt[k + off] = v;
+            nxt[k + off] = static_cast<T>(v < 0 ? kStoreUnreach : v);
             found |= (v == m);
         }
         __syncwarp();
         if (__any_sync(kLvFull, found)) return e;
-        int* t = cur;
+        T* t = cur;
         cur = nxt;
         nxt = t;
     }
@@ -108,8 +113,9 @@ SA_DEV int lv_warp_smem(const uint4* R, int m, const uint4* W, uint32_t wofs, in
 // kernel keeps the inlined code small.
 template <bool kRegLV>
 SA_DEV int lv_warp(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, int dl, int* F,
-                   int lane, uint32_t& cells) {
+                   int lane, uint32_t& cells, bool f16 = false) {
     if (kRegLV) return lv_warp_reg(R, m, W, wofs, w, dl, lane, cells);
+    if (f16) return lv_warp_smem(R, m, W, wofs, w, dl, reinterpret_cast<short*>(F), lane, cells);
     return lv_warp_smem(R, m, W, wofs, w, dl, F, lane, cells);
 }
 
