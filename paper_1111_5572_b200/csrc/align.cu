@@ -236,8 +236,12 @@ struct Ctx {
 
 SA_DEV void stat_add(Ctx& x, int slot, uint32_t v) { x.rs += x.lane == slot ? v : 0u; }
 
+// Slot of a candidate key (bucket << 1 | dir, < 2^33) in the candidate hash
+// index: 32-bit multiplicative hash, high half rotated down.  Only placement
+// depends on it; candidate order is the insertion order (REF aligner.cpp:124-134).
 SA_DEV uint32_t cand_hash(unsigned long long key, int hcap) {
-    return static_cast<uint32_t>((key * 0x9E3779B97F4A7C15ull) >> 40) & static_cast<uint32_t>(hcap - 1);
+    const uint32_t h = static_cast<uint32_t>(key) * 0x9E3779B1u + static_cast<uint32_t>(key >> 32) * 0x85EBCA77u;
+    return __funnelshift_l(h, h, 16) & static_cast<uint32_t>(hcap - 1);
 }
 
 // Warp-cooperative add_hit for up to 32 hits (REF aligner.cpp:124-134).
@@ -581,8 +585,8 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
     const AlignLaunch& a = *x.a;
     const int lane = x.lane;
     const int len = x.len;
-    const bool bs_pow2 = (a.bs & (a.bs - 1)) == 0;
-    const int bs_shift = __ffs(a.bs) - 1;
+    const bool bs_pow2 = a.bs_shift >= 0;
+    const int bs_shift = a.bs_shift;
 
     x.n_cands = 0;
     x.n_unscored = 0;

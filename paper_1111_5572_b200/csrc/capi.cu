@@ -208,6 +208,7 @@ int make_shape(Replica& rep, const sa_params* p, uint64_t Lmax, LaunchShape& sh,
     a.c = p->confidence_threshold;
     a.hmax = p->max_hits;
     a.bs = p->bucket_size;
+    a.bs_shift = (a.bs & (a.bs - 1)) == 0 ? __builtin_ctz(static_cast<unsigned>(a.bs)) : -1;
     a.force = p->force_max_dlimit ? 1 : 0;
     if (Lmax < static_cast<uint64_t>(p->seed_size)) Lmax = p->seed_size;
     if (Lmax > (1u << 20)) {
