@@ -42,7 +42,10 @@ int fail_thread(int code, const std::string& msg) {
 
 namespace {
 
-constexpr int kPipeStages = 6;  // chunk buffers in flight per replica (copies run ahead of compute)
+#ifndef SA_PIPE_STAGES
+#define SA_PIPE_STAGES 6
+#endif
+constexpr int kPipeStages = SA_PIPE_STAGES;  // chunk buffers in flight per replica (copies run ahead of compute)
 constexpr int kCtlWords = 4;  // cursor_fast, cursor_slow, overflow_count, error_flag
 constexpr uint64_t kChunkReads = 49152;  // default; SA_CHUNK_READS overrides (tuning)
 
@@ -114,6 +117,13 @@ struct Replica {
     unsigned long long* d_stats = nullptr;
     unsigned int* d_err = nullptr;         // error flag
     unsigned long long* d_err_read = nullptr;
+    // pinned landing zone for the end-of-batch control words: the stats, the
+    // error flag and the deferred-read count come back in one synchronisation
+    struct HostCtl {
+        unsigned long long stats[kNumStats];
+        unsigned int err, defer;
+    };
+    HostCtl* h_ctl = nullptr;
     unsigned char* d_gscratch = nullptr;
     uint64_t gscratch_bytes = 0;
     uint32_t smem_attr = 0;
@@ -993,6 +1003,13 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
     if (k > 0) {
         CUDA_TRY(ctx, cudaEventRecord(S.k1, S.kk));
         CUDA_TRY(ctx, cudaStreamWaitEvent(S.co, S.k1, 0));
+        if (!rep.h_ctl) CUDA_TRY(ctx, cudaHostAlloc(&rep.h_ctl, sizeof(Replica::HostCtl), cudaHostAllocDefault));
+        CUDA_TRY(ctx, cudaMemcpyAsync(rep.h_ctl->stats, rep.d_stats, sizeof(rep.h_ctl->stats), cudaMemcpyDeviceToHost,
+                                      S.co));
+        CUDA_TRY(ctx, cudaMemcpyAsync(&rep.h_ctl->err, rep.d_err, sizeof(unsigned int), cudaMemcpyDeviceToHost, S.co));
+        CUDA_TRY(ctx, cudaMemcpyAsync(&rep.h_ctl->defer, rep.d_defer_count, sizeof(unsigned int),
+                                      cudaMemcpyDeviceToHost, S.co));
+        CUDA_TRY(ctx, cudaEventRecord(S.e_end, S.co));
     }
     if (dbg_span && k > 0) CUDA_TRY(ctx, cudaEventRecord(S.e_ready, S.ci));  // copy-in span end (diagnostics)
     CUDA_TRY(ctx, cudaStreamSynchronize(S.co));
@@ -1018,6 +1035,11 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
     std::memset(out, 0, sizeof(sa_stats));
     if (bad || k == 0) return bad;
     cudaEventElapsedTime(&k_ms, S.k0, S.k1);
+    if (rep.h_ctl->defer == 0 && rep.h_ctl->err == 0) {  // the common case: one synchronisation in all
+        cudaEventElapsedTime(&e2e_ms, S.e_begin, S.e_end);
+        add_stats(out, rep.h_ctl->stats);
+        return SA_OK;
+    }
     // the overflow pass (stage 0's stream) follows everything above
     if (int rc = ensure_stage(ctx, rep.stage[0], 0, 0)) return rc;
     uint64_t redone = 0;
@@ -1183,6 +1205,7 @@ void sa_destroy(sa_context* ctx) {
         if (rep.d_stats) cudaFree(rep.d_stats);
         if (rep.d_err) cudaFree(rep.d_err);
         if (rep.d_err_read) cudaFree(rep.d_err_read);
+        if (rep.h_ctl) cudaFreeHost(rep.h_ctl);
         if (rep.d_gscratch) cudaFree(rep.d_gscratch);
         if (rep.d_defer) cudaFree(rep.d_defer);
         for (void* q : {static_cast<void*>(rep.sm.bases), static_cast<void*>(rep.sm.offs),
