@@ -47,15 +47,19 @@ namespace {
 #endif
 constexpr int kPipeStages = SA_PIPE_STAGES;  // chunk buffers in flight per replica (copies run ahead of compute)
 constexpr int kCtlWords = 4;  // cursor_fast, cursor_slow, overflow_count, error_flag
-constexpr uint64_t kChunkReads = 49152;  // default; SA_CHUNK_READS overrides (tuning)
-
-uint64_t chunk_reads_setting() {
-    static const uint64_t v = [] {
+// Chunk size of the batch pipeline: about 1/24 of the batch, between
+// 48 k and 512 k reads.  Each chunk costs a kernel ramp and tail (~15 us), so
+// big batches want big chunks (C2, 10 M reads: e2e 152 M reads/s at 48 k,
+// 196 M at 512 k), while a 1 M batch wants enough chunks to overlap copy and
+// compute (C1: 48 k best).  SA_CHUNK_READS overrides (tuning).
+uint64_t chunk_reads_setting(uint64_t n_reads) {
+    static const long long forced = [] {
         const char* e = getenv("SA_CHUNK_READS");
-        const long long x = e ? atoll(e) : 0;
-        return x >= 1024 ? static_cast<uint64_t>(x) : kChunkReads;
+        return e ? atoll(e) : 0ll;
     }();
-    return v;
+    if (forced >= 1024) return static_cast<uint64_t>(forced);
+    const uint64_t want = ((n_reads / 24 + 16383) / 16384) * 16384;
+    return std::min<uint64_t>(512u << 10, std::max<uint64_t>(49152, want));
 }
 constexpr uint64_t kChunkBytes = 256ull << 20;
 constexpr int kFastCap = 64, kFastHcap = 128;
@@ -1280,7 +1284,7 @@ int sa_align_batch(sa_context* ctx, const sa_params* params, const char* bases,
     // the previous chunk; a bad chunk stops the batch before it is enqueued.
     // Chunk sizes ramp up (16 k, 32 k, ... reads) so the first kernel starts
     // after a short copy; the GPU is busy with chunk k while chunk k+1 copies.
-    const uint64_t chunk_reads = chunk_reads_setting();
+    const uint64_t chunk_reads = chunk_reads_setting(n_reads);
     std::vector<uint64_t> bounds{0};
     {
         // sizes ramp up (16 k, 32 k, ...) so the first kernel starts after a
