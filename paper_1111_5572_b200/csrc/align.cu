@@ -372,7 +372,7 @@ SA_DEV void score_candidate(Ctx& x, uint32_t idx) {
     // genome end only): global reads measured 6-8% slower there.
     uint64_t gb0 = 0;
     const uint4* Wsrc = a.planes;
-    if (!kRegLV) {
+    if (!kRegLV && !a.gw) {
         gb0 = amin >> 5;
         uint64_t end = amax + static_cast<uint64_t>(x.len) + static_cast<uint64_t>(d_limit);
         if (end > a.glen) end = a.glen;
@@ -1104,7 +1104,7 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
     x.lane = lane;
     uint4* planes = reinterpret_cast<uint4*>(ws);  // buffer q: R = planes + 2q*wbr, C = R + wbr
     x.W = planes + (a.prefetch ? 4 : 2) * a.wbr;  // one {R, C} buffer without the read pipeline
-    uint4* recs = x.W + a.wbw;                      // 2 x 32
+    uint4* recs = x.W + (a.gw ? 0 : a.wbw);  // 2 x 32; no window area when the LV reads the genome in place
     uint4* pslot = recs + 64;                       // 32
     unsigned long long* pcanon = reinterpret_cast<unsigned long long*>(pslot + 32);  // 32
     int* offs = reinterpret_cast<int*>(pcanon + 32);  // 2 x n_off_cap

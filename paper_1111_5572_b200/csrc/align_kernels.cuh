@@ -64,6 +64,7 @@ struct AlignLaunch {
     int chunk_shift0, chunk_shift;  // stream_chunk_of
     int lcap;
     int f16;  // LV frontier as 16-bit entries (reads < 32 k bases)
+    int gw;   // shared-memory LV reads the genome window from global memory (no staging area)
     int bs_shift;  // log2(bucket_size) when it is a power of two, else -1
     // Two-kernel path (seed_kernel + align_kernel<.., kPre>): per read, the
     // seed kernel writes forward then reverse-complement planes

@@ -106,6 +106,7 @@ cudaError_t stage_times(Stage& s, float& fast_ms, float& slow_ms) {
 struct LaunchShape {
     AlignLaunch proto;  // layout + params fields filled
     int fast_block, fast_grid;
+    int pipe_block, pipe_grid;  // the same kernel in the chunked batch pipeline
     int slow_block, slow_grid;
     uint32_t slow_smem_per_warp;
     uint64_t slow_table_bytes;
@@ -247,34 +248,86 @@ int make_shape(Replica& rep, const sa_params* p, uint64_t Lmax, LaunchShape& sh,
     auto f_ints_for = [&](int f16) {
         return a.dl_max > 15 ? round4(f16 ? (2 * a.dl_max + 3) : 2 * (2 * a.dl_max + 3)) : 0;
     };
-    auto common_for = [&](int f16) {
-        return 16ull * ((a.prefetch ? 4 : 2) * a.wbr + a.wbw + 64 + 32) + 8ull * 32 +
+    // gw: the LV reads the genome window from global memory (always for the
+    // register LV; for the shared-memory LV only when dropping the staged
+    // window fits more warps)
+    auto common_for = [&](int f16, int gw) {
+        return 16ull * ((a.prefetch ? 4 : 2) * a.wbr + (gw ? 0 : a.wbw) + 64 + 32) + 8ull * 32 +
                4ull * (2 * a.n_off_cap + f_ints_for(f16)) + 8ull * kNumStats;
     };
-    auto spw_for = [&](int f16) {
-        return round16(common_for(f16) + 8ull * a.sbw + cand_table_bytes(a.cap, a.hcap));
+    auto spw_for = [&](int f16, int gw) {
+        return round16(common_for(f16, gw) + 8ull * a.sbw + cand_table_bytes(a.cap, a.hcap));
     };
-    // A 16-bit LV frontier (lv.cuh) is slower per step (C3: 224 vs 162 ms), so
-    // it is used only where the smaller layout fits more warps per SM (C4:
-    // 8 instead of 7 warps, 364 -> 324 ms).
-    auto warps_per_sm = [&](uint32_t spw) {  // shared memory and 80 registers (24 warps)
-        const int w = std::min<int>(8, (227 * 1024) / spw);
-        return w < 1 ? 0 : std::min<int>(24 / w, (227 * 1024) / (w * spw)) * w;
-    };
-    a.f16 = (L < 32000 && a.dl_max > 15 && getenv("SA_LV_F16_OFF") == nullptr &&
-             warps_per_sm(spw_for(1)) > warps_per_sm(spw_for(0)))
-                ? 1
-                : 0;
-    a.f_ints = f_ints_for(a.f16);
-    const uint64_t common = common_for(a.f16);
-    a.smem_per_warp = spw_for(a.f16);
     const uint32_t kMaxSmem = 227 * 1024;
+    // warps per block (<= SA_FAST_WARPS) that fit the most warps per SM under
+    // shared memory and the 80-register budget (24 warps)
+    auto best_block = [&](uint32_t spw, int& warps_sm) {
+        int best_w = 0;
+        warps_sm = 0;
+        for (int w = 1; w <= SA_FAST_WARPS; ++w) {
+            if (static_cast<uint64_t>(w) * spw > kMaxSmem) break;
+            const int tot = std::min<int>(24 / w, static_cast<int>(kMaxSmem / (w * spw))) * w;
+            if (tot >= warps_sm) {
+                warps_sm = tot;
+                best_w = w;
+            }
+        }
+        return best_w;
+    };
+    // Layout choice (measured, SA_FORCE_LAYOUT / SA_FORCE_WARPS sweeps):
+    // - reads <= 1 kbp (the seeded kernel): the LV reads the genome in place
+    //   (C3: 158 -> 149 ms at equal occupancy, 139 ms with the 22 warps/SM the
+    //   smaller layout allows) and keeps a 32-bit frontier (16-bit: 219 ms);
+    // - longer reads: the 16-bit frontier and the in-place window cost little
+    //   per step, so whichever of them fits the most warps per SM wins (C4:
+    //   7 warps 372 ms, 8 warps 332-341 ms, both 10 warps 287 ms).
+    a.f16 = 0;
+    a.gw = 1;
+    if (a.dl_max > 15 && !a.prefetch) {
+        const bool can16 = L < 32000 && getenv("SA_LV_F16_OFF") == nullptr;
+        const int opts[4][2] = {{0, 0}, {1, 0}, {0, 1}, {1, 1}};
+        int best = -1;
+        for (int o = 0; o < 4; ++o) {
+            if (opts[o][0] && !can16) continue;
+            int wsm = 0;
+            best_block(spw_for(opts[o][0], opts[o][1]), wsm);
+            if (wsm > best) {
+                best = wsm;
+                a.f16 = opts[o][0];
+                a.gw = opts[o][1];
+            }
+        }
+    }
+    if (const char* fl = getenv("SA_FORCE_LAYOUT")) {  // tuning: "f16,gw"
+        int f = 0, g = 0;
+        if (sscanf(fl, "%d,%d", &f, &g) == 2) {
+            a.f16 = f && L < 32000 && a.dl_max > 15;
+            a.gw = g || a.dl_max <= 15;
+        }
+    }
+    a.f_ints = f_ints_for(a.f16);
+    const uint64_t common = common_for(a.f16, a.gw);
+    a.smem_per_warp = spw_for(a.f16, a.gw);
     if (a.smem_per_warp > kMaxSmem) {
         why = "read too long for the shared-memory layout (limit ~60 kbp)";
         return SA_EINVAL;
     }
-    int warps = std::min<int>(SA_FAST_WARPS, kMaxSmem / a.smem_per_warp);
+    int warps_sm = 0;
+    int warps = best_block(a.smem_per_warp, warps_sm);
+    // shared-memory-limited layouts run best in small blocks (C3: 2-warp
+    // blocks 139 ms, 7-warp 149 ms per 500 k reads)
+    if (warps_sm < 24 && warps > 2 && 2 * a.smem_per_warp <= kMaxSmem) {
+        const int tot2 = std::min<int>(12, static_cast<int>(kMaxSmem / (2 * a.smem_per_warp))) * 2;
+        if (tot2 >= warps_sm - 1) warps = 2;
+    }
+    if (const char* fw = getenv("SA_FORCE_WARPS")) {  // tuning: warps per block
+        const int w = atoi(fw);
+        if (w >= 1 && w <= SA_FAST_WARPS && static_cast<uint64_t>(w) * a.smem_per_warp <= kMaxSmem) warps = w;
+    }
     sh.fast_block = 32 * warps;
+    if (getenv("SA_DEBUG_SHAPE"))
+        fprintf(stderr, "[shape] L=%d dl_max=%d f16=%d gw=%d smem/warp=%u block=%d warps/SM=%d\n", L, a.dl_max, a.f16,
+                a.gw, a.smem_per_warp, warps, warps_sm);
     int bps = 0;
     if (rep.smem_attr < kMaxSmem) {
         if (align_set_smem(kMaxSmem) != cudaSuccess) {
@@ -285,6 +338,26 @@ int make_shape(Replica& rep, const sa_params* p, uint64_t Lmax, LaunchShape& sh,
     }
     if (align_fast_occupancy(a, sh.fast_block, a.smem_per_warp * warps, &bps) != cudaSuccess || bps < 1) bps = 1;
     sh.fast_grid = bps * rep.sm_count;
+    // In the chunked pipeline the kernels of consecutive chunks overlap, and
+    // small blocks let the next chunk's blocks take SMs as this one's drain:
+    // 2-warp blocks there (C1 e2e 414 -> 419 M reads/s, C2 195 -> 205 M,
+    // C3 2.57 -> 2.99 M), the largest block for one big launch (C1 device
+    // 506 vs 499 M).  Kept only when 2-warp blocks fit as many warps per SM.
+    sh.pipe_block = sh.fast_block;
+    sh.pipe_grid = sh.fast_grid;
+    {
+        int w2 = 0;
+        const int pw = getenv("SA_FORCE_WARPS") ? warps : 2;
+        if (pw <= warps && static_cast<uint64_t>(pw) * a.smem_per_warp <= kMaxSmem) {
+            const int tot = std::min<int>(24 / pw, static_cast<int>(kMaxSmem / (pw * a.smem_per_warp))) * pw;
+            best_block(a.smem_per_warp, w2);
+            if (tot >= w2 - 1 &&
+                align_fast_occupancy(a, 32 * pw, a.smem_per_warp * pw, &bps) == cudaSuccess && bps >= 1) {
+                sh.pipe_block = 32 * pw;
+                sh.pipe_grid = bps * rep.sm_count;
+            }
+        }
+    }
 
     // slow path: candidate tables in global memory, worst case n_eff * h_max
     const uint64_t n_eff = static_cast<uint64_t>(std::min(p->seeds_to_try, L - p->seed_size + 1));
@@ -988,8 +1061,8 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
         pend.stage = si;
         pend.cs = cs;
         pend.a = a;
-        pend.grid = sh.fast_grid;
-        pend.block = sh.fast_block;
+        pend.grid = sh.pipe_grid;
+        pend.block = sh.pipe_block;
         have_pend = true;
         if (multi) {
             if (int rc = align_pending()) return rc;
