@@ -1128,8 +1128,13 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
     x.t.ccnt = reinterpret_cast<uint32_t*>(x.t.hkey + a.hcap);
     x.t.chslot = x.t.ccnt + a.cap;
     x.t.hval = x.t.chslot + a.cap;
-    for (int j = lane; j < a.hcap; j += 32) x.t.hkey[j] = kEmptyKey;
-    __syncwarp();
+    // the global tables of the overflow kernel are cleared by a warp only when
+    // it gets work (usually none: the launch follows every device batch)
+    bool table_ready = !kSlow;
+    if (!kSlow) {
+        for (int j = lane; j < a.hcap; j += 32) x.t.hkey[j] = kEmptyKey;
+        __syncwarp();
+    }
 
     int cached_len0 = -1, cached_len1 = -1, n_eff0 = 0, n_eff1 = 0;
     // offsets for read length len into buffer q (cached per buffer)
@@ -1383,6 +1388,11 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
             if (lane == 0) r = atomicAdd(a.cursor, 1u);
             r = __shfl_sync(FULL, r, 0);
             if (r >= n_work) break;
+            if (!table_ready) {
+                for (int j = lane; j < a.hcap; j += 32) x.t.hkey[j] = kEmptyKey;
+                __syncwarp();
+                table_ready = true;
+            }
             if (kSlow && a.work_list) r = a.work_list[r];  // no list: every read of the launch
             const uint64_t o0 = a.offsets[r], o1 = a.offsets[r + 1];
             const int len = static_cast<int>(o1 - o0);
