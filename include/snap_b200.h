@@ -322,6 +322,52 @@ int sa_run_align(const sa_align_options* opt, sa_eval_report* report);
  * terminated); *len = full length. */
 int sa_report_text(const sa_eval_report* r, char* out, uint64_t cap, uint64_t* len);
 
+/* ------------------------------------------------------------------ read simulator
+ * SimProfile (REF include/seedaln/simulator.hpp:17-26). */
+typedef struct sa_sim_profile {
+    uint64_t read_length;
+    double snp_rate;
+    double indel_mutation_rate;
+    double seq_error_rate;
+    double indel_error_fraction;
+    uint64_t rng_seed;
+} sa_sim_profile;
+
+/* Truth (REF simulator.hpp:30-36); contig = index into the genome's contig
+ * table; the read name is encode_truth (REF src/simulator.cpp:43-48):
+ * "<contig name>_<position+1>_<F|R>_<serial>". */
+typedef struct sa_sim_truth {
+    uint64_t contig;
+    uint64_t position;  /* 0-based offset within the contig */
+    uint64_t serial;
+    uint8_t direction;  /* SA_FORWARD / SA_REVERSE_COMPLEMENT */
+} sa_sim_truth;
+
+typedef struct sa_simulator sa_simulator;
+
+/* SimProfile{} defaults (REF simulator.hpp:17-24). */
+void sa_default_sim_profile(sa_sim_profile* out);
+
+/* ReadSimulator(genome, profile) (REF src/simulator.cpp:90-99): validates the
+ * profile (SA_EINVAL, SimProfile::validate messages) and that some contig
+ * fits a read.  g must outlive the simulator. */
+int sa_simulator_create(const sa_genome* g, const sa_sim_profile* p, sa_simulator** out);
+void sa_simulator_destroy(sa_simulator* s);
+
+/* `count` calls of ReadSimulator::next (REF src/simulator.cpp:117-192): the
+ * same mt19937_64 draw stream, so the reads are the reference's.  bases gets
+ * count * read_length chars (the read as Read::bases, reverse-complemented
+ * for R reads), truth gets count entries.  SA_ERUNTIME "failed to place a
+ * read; genome may be mostly N" after 10,000 redraws (reads before it stay). */
+int sa_simulator_next(sa_simulator* s, uint64_t count, char* bases, sa_sim_truth* truth);
+
+/* run_simulate (REF src/driver.cpp:158-168): FASTA -> `count` FASTQ records
+ * (to_fastq, REF simulator.cpp:194-206), byte-identical to the reference's
+ * file.  Generation is one sequential stream; `threads` host threads (0 =
+ * hardware concurrency) format the records while the next batch is drawn. */
+int sa_run_simulate(const char* fasta_path, const char* output_path, uint64_t count, const sa_sim_profile* p,
+                    uint32_t threads);
+
 #ifdef __cplusplus
 }
 #endif

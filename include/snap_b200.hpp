@@ -9,6 +9,7 @@
 //   run_index / save_index_file                 -> snap_b200::run_index / save_index_file
 //   load_index_file                             -> snap_b200::load_index_file
 //   run_align (FASTQ -> SAM)                    -> snap_b200::run_align
+//   ReadSimulator / run_simulate               -> snap_b200::ReadSimulator / run_simulate
 //   OracleContext / oracle_align / oracle_scan  -> snap_b200::Referee
 //   std::invalid_argument / FormatError / ParseError / IoError are rethrown
 //   from the status codes (REF include/seedaln/errors.hpp:10-30).
@@ -217,5 +218,32 @@ public:
 private:
     sa_referee* r_ = nullptr;
 };
+
+// ReadSimulator (REF include/seedaln/simulator.hpp:48-66): the reference's reads, in order.
+class ReadSimulator {
+public:
+    ReadSimulator(const Genome& g, const sa_sim_profile& p) : len_(p.read_length) {
+        check(sa_simulator_create(g.get(), &p, &s_), nullptr);
+    }
+    ReadSimulator(const ReadSimulator&) = delete;
+    ReadSimulator& operator=(const ReadSimulator&) = delete;
+    ~ReadSimulator() { sa_simulator_destroy(s_); }
+    // n reads: bases (n * read_length chars) and truths
+    void next(uint64_t n, std::string& bases, std::vector<sa_sim_truth>& truth) {
+        bases.resize(n * len_);
+        truth.resize(n);
+        check(sa_simulator_next(s_, n, bases.data(), truth.data()), nullptr);
+    }
+
+private:
+    sa_simulator* s_ = nullptr;
+    uint64_t len_;
+};
+
+// run_simulate (REF src/driver.cpp:158-168)
+inline void run_simulate(const std::string& fasta, const std::string& out, uint64_t count, const sa_sim_profile& p,
+                         uint32_t threads = 0) {
+    check(sa_run_simulate(fasta.c_str(), out.c_str(), count, &p, threads), nullptr);
+}
 
 }  // namespace snap_b200

@@ -92,6 +92,16 @@ class _AlignOptions(C.Structure):  # sa_align_options
                 ("verify_index", C.c_int32)]
 
 
+class _SimProfile(C.Structure):  # sa_sim_profile = SimProfile (REF simulator.hpp:17-26)
+    _fields_ = [("read_length", C.c_uint64), ("snp_rate", C.c_double), ("indel_mutation_rate", C.c_double),
+                ("seq_error_rate", C.c_double), ("indel_error_fraction", C.c_double), ("rng_seed", C.c_uint64)]
+
+
+TRUTH_DTYPE = np.dtype([("contig", "<u8"), ("position", "<u8"), ("serial", "<u8"), ("direction", "u1"),
+                        ("pad", "u1", (7,))])
+assert TRUTH_DTYPE.itemsize == 32
+
+
 class _EvalReport(C.Structure):  # sa_eval_report
     _fields_ = [(f, C.c_uint64) for f in ("total", "single", "multiple", "notfound", "correct", "wrong",
                                            "no_truth")] + [("elapsed_seconds", C.c_double), ("stats", _Stats)]
@@ -160,6 +170,11 @@ def _load():
         "sa_run_index": (C.c_int, [C.c_char_p, C.c_char_p, C.c_int32, C.c_int32, C.c_int32]),
         "sa_run_align": (C.c_int, [P(_AlignOptions), P(_EvalReport)]),
         "sa_report_text": (C.c_int, [P(_EvalReport), C.c_char_p, C.c_uint64, P(C.c_uint64)]),
+        "sa_default_sim_profile": (None, [P(_SimProfile)]),
+        "sa_simulator_create": (C.c_int, [C.c_void_p, P(_SimProfile), P(C.c_void_p)]),
+        "sa_simulator_destroy": (None, [C.c_void_p]),
+        "sa_simulator_next": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]),
+        "sa_run_simulate": (C.c_int, [C.c_char_p, C.c_char_p, C.c_uint64, P(_SimProfile), C.c_uint32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -841,3 +856,89 @@ class Referee:
         if rc:
             _raise(rc)
         return ho, hits
+
+
+# ----------------------------------------------------------------------- simulator
+
+@dataclass
+class SimProfile:  # REF include/seedaln/simulator.hpp:17-26 (same defaults)
+    read_length: int = 100
+    snp_rate: float = 0.0009
+    indel_mutation_rate: float = 0.0001
+    seq_error_rate: float = 0.02
+    indel_error_fraction: float = 0.0
+    rng_seed: int = 1
+
+    def _c(self) -> _SimProfile:
+        return _SimProfile(self.read_length, self.snp_rate, self.indel_mutation_rate, self.seq_error_rate,
+                           self.indel_error_fraction, self.rng_seed)
+
+
+@dataclass
+class Truth:  # REF simulator.hpp:30-36
+    contig: str
+    position: int
+    direction: Direction
+    serial: int
+
+
+def encode_truth(t: Truth) -> str:  # REF src/simulator.cpp:43-48
+    return f"{t.contig}_{t.position + 1}_{'F' if t.direction == Direction.Forward else 'R'}_{t.serial}"
+
+
+class ReadSimulator:
+    """ReadSimulator(genome, profile) (REF src/simulator.cpp:90-192) in
+    libsnapb200.so: the reference's mt19937_64 draw stream, so next() yields
+    the reference's reads in the same order."""
+
+    def __init__(self, g: PackedGenome, profile: SimProfile | None = None):
+        lib = _load()
+        self._g = g
+        self.profile = profile or SimProfile()
+        self._gh = g._handle()
+        h = C.c_void_p()
+        rc = lib.sa_simulator_create(self._gh, C.byref(self.profile._c()), C.byref(h))
+        if rc:
+            lib.sa_genome_free(self._gh)
+            self._gh = None
+            _raise(rc)
+        self._h = h
+        self._names = [c[0] for c in g.contigs()]
+
+    def __del__(self):
+        lib = _lib
+        if lib is not None:
+            if getattr(self, "_h", None):
+                lib.sa_simulator_destroy(self._h)
+                self._h = None
+            if getattr(self, "_gh", None):
+                lib.sa_genome_free(self._gh)
+                self._gh = None
+
+    def next_batch(self, count: int) -> tuple[np.ndarray, np.ndarray]:
+        """`count` reads: (bases uint8[count, read_length], truth TRUTH_DTYPE[count])."""
+        L = self.profile.read_length
+        bases = np.empty((count, L), dtype=np.uint8)
+        truth = np.zeros(count, dtype=TRUTH_DTYPE)
+        rc = _load().sa_simulator_next(self._h, count, bases.ctypes.data, truth.ctypes.data)
+        if rc:
+            _raise(rc)
+        return bases, truth
+
+    def truth_of(self, t) -> Truth:
+        return Truth(self._names[int(t["contig"])], int(t["position"]), Direction(int(t["direction"])),
+                     int(t["serial"]))
+
+    def next(self) -> tuple[str, str, Truth]:  # REF simulator.cpp:117: (name, bases, truth)
+        b, t = self.next_batch(1)
+        tr = self.truth_of(t[0])
+        return encode_truth(tr), b[0].tobytes().decode(), tr
+
+
+def run_simulate(fasta_path: str, output_path: str, count: int, profile: SimProfile | None = None,
+                 threads: int = 0) -> None:
+    """run_simulate (REF src/driver.cpp:158-168): FASTA -> FASTQ, the reference's bytes."""
+    p = (profile or SimProfile())._c()
+    rc = _load().sa_run_simulate(os.fsencode(fasta_path), os.fsencode(output_path), count, C.byref(p), threads)
+    if rc:
+        _raise(rc)

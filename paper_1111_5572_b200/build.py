@@ -19,7 +19,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "lib")
 OBJ = os.path.join(HERE, "build", "obj")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-CUDA_SOURCES = ["index.cu", "align.cu", "capi.cu", "csr.cu", "genome_io.cpp", "run_align.cpp", "referee.cu", "pack.cpp"]
+CUDA_SOURCES = ["index.cu", "align.cu", "capi.cu", "csr.cu", "genome_io.cpp", "run_align.cpp", "referee.cu", "pack.cpp", "simulate.cpp"]
 HEADERS = ["common.cuh", "align_kernels.cuh", "device_index.h", "host_common.h", "lv.cuh"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

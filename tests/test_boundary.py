@@ -145,6 +145,10 @@ def test_cpp_adapter_compiles_and_links(tmp_path):
         "    auto [idx, g2] = snap_b200::load_index_file(\"x.idx\");\n"
         "    sa_align_options o; sa_default_align_options(&o); snap_b200::run_align(o);\n"
         "    snap_b200::Referee rf(g2); return static_cast<int>(idx.seed_size()); }\n"
+        "  if (argc > 7) { auto g = snap_b200::Genome::from_fasta(\"x.fa\"); sa_sim_profile sp;\n"
+        "    sa_default_sim_profile(&sp); snap_b200::ReadSimulator sim(g, sp); std::string b;\n"
+        "    std::vector<sa_sim_truth> t; sim.next(10, b, t); snap_b200::run_simulate(\"x.fa\", \"x.fq\", 10, sp);\n"
+        "    return static_cast<int>(t[0].serial); }\n"
         "  return 0; }\n")
     exe = tmp_path / "use"
     r = subprocess.run(["g++", "-std=c++17", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe),
