@@ -31,6 +31,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "align_kernels.cuh"
 #include "common.cuh"
@@ -836,6 +837,283 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
     return true;
 }
 
+// ------------------------------------------------------------------ solo kernel
+// Thread-per-read aligner for the common read (two-kernel path, register-LV
+// launches, power-of-two bucket <= 32).  The warp-per-read kernel spends most
+// of its ~1,300 warp-instructions per read on control flow that is the same
+// for all 32 lanes; here one thread replays Aligner::align (REF
+// src/aligner.cpp:223-364) for its own read from the seed kernel's records,
+// with the candidate table and the LV frontier in its own shared-memory
+// column, so all 32 lanes do useful work.  A read it cannot finish within its
+// limits -- a seed with several hits (palindromes included), more than
+// kSoloCands candidates, a bad character or a deferred length -- is appended
+// to pre_list untouched and the warp kernel redoes it from scratch, so the
+// result is the same whichever kernel finishes a read.  The steps below are
+// align_one's (same d_limit rule, candidate order, LV steps, tracker, exits,
+// classification and counters), written sequentially.
+constexpr int kSoloCands = 8;
+constexpr int kSoloThreads = 128;
+constexpr int kSoloF = 2 * 15 + 3;  // frontier entries at d_limit <= 15
+
+struct SoloRead {
+    uint32_t lookups = 0, skip_n = 0, skip_pop = 0, hits = 0, dist = 0, dist_after = 0, early_out = 0;
+    uint32_t window = 0, cells = 0, multi = 0, prune = 0;
+};
+
+__global__ void __launch_bounds__(kSoloThreads) solo_kernel(const AlignLaunch a) {
+    __shared__ uint32_t s_key[kSoloCands][kSoloThreads];   // bucket << 1 | dir
+    __shared__ uint32_t s_mask[kSoloCands][kSoloThreads];  // anchor bits (bucket <= 32)
+    __shared__ uint32_t s_cnt[kSoloCands][kSoloThreads];   // seeds_hitting | kScored
+    __shared__ short s_F[kSoloF][kSoloThreads];
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    uint32_t* ckey = &s_key[0][tid];
+    uint32_t* cmask = &s_mask[0][tid];
+    uint32_t* ccnt = &s_cnt[0][tid];
+    constexpr int cs = kSoloThreads;  // column stride
+    const int half = a.pre_pstride >> 1;
+    const int bsh = a.bs_shift;
+    unsigned long long acc = 0;  // lane k: stats slot k of the warp
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t base = blockIdx.x * blockDim.x; base < a.n_reads; base += stride) {
+        const uint32_t r = base + tid;
+        // per-read outcome: 0 none, 1 committed, 2 complex (warp kernel)
+        int outcome = 0;
+        SoloRead c;
+        int kind = SA_NOT_FOUND, len = 0;
+        bool all_pop = false, first_best = false, too_short = false;
+        if (r < a.n_reads) {
+            const uint2 meta = __ldg(a.pre_meta + r);
+            len = static_cast<int>(meta.x);
+            const uint32_t st = meta.y >> 16;
+            const int n_eff = static_cast<int>(meta.y & 0xffffu);
+            outcome = 2;
+            if (st == 1) {  // REF aligner.cpp:231-235
+                sa_result res;
+                res.position = 0;
+                res.distance = -1;
+                res.gap = 0;
+                res.kind = SA_NOT_FOUND;
+                res.has_position = 0;
+                res.direction = 0;
+#pragma unroll
+                for (int i = 0; i < 5; ++i) res.reserved[i] = 0;
+                a.results[r] = res;
+                too_short = true;
+                outcome = 1;
+            } else if (st == 0) {
+                const uint4* recs = a.pre_recs + static_cast<uint64_t>(r) * a.pre_rstride;
+                const uint4* Rp = a.pre_planes + static_cast<uint64_t>(r) * a.pre_pstride;
+                const int d_max = a.dmax_param >= 0 ? a.dmax_param : (12 * len + 99) / 100;
+                const int tier0 = len / a.s;
+                Tracker tr;
+                tr.d_best = kInfDistance;
+                tr.d_second = kInfDistance;
+                tr.best_pos = 0;
+                tr.best_dir = 0;
+                uint32_t n_cands = 0, n_unscored = 0, calls = 0;
+                bool first_done = false, first_valid = false;
+                int first_dir = 0;
+                uint64_t first_pos = 0;
+                int tested = 0;
+                bool any_lookup = false, any_popular = false, early_multi = false, bail = false, pruning = false;
+                int i = 0;
+                for (;;) {
+                    if (!pruning) {
+                        if (i >= n_eff) break;
+                        const uint4 rec = __ldg(recs + i);
+                        if (rec.x & kSeedN) {  // REF :259-262
+                            c.skip_n++;
+                            ++i;
+                            continue;
+                        }
+                        c.lookups++;
+                        if (rec.y > static_cast<uint32_t>(a.hmax)) {  // REF :265-269
+                            any_popular = true;
+                            c.skip_pop++;
+                            ++i;
+                            continue;
+                        }
+                        any_lookup = true;
+                        c.hits += rec.y;
+                        if (i < tier0) ++tested;
+                        if (rec.y > 1u) {  // several hits (or a palindrome): the warp kernel votes them
+                            bail = true;
+                            break;
+                        }
+                        if (rec.y == 1u) {  // REF :273-286, one hit
+                            const uint32_t dir = ((rec.x & kSeedSingleRc) ? 1u : 0u) ^ ((rec.x & kSeedQflip) ? 1u : 0u);
+                            const int o = static_cast<int>(rec.w);
+                            const int64_t anchor = static_cast<int64_t>(rec.z) - (dir ? (len - a.s - o) : o);
+                            const uint32_t aa = anchor < 0 ? 0u : static_cast<uint32_t>(anchor);
+                            const uint32_t key = ((aa >> bsh) << 1) | dir;
+                            const uint32_t bit = 1u << (aa & ((1u << bsh) - 1u));
+                            uint32_t j = 0;
+                            while (j < n_cands && ckey[j * cs] != key) ++j;
+                            if (j < n_cands) {
+                                ccnt[j * cs] += 1u;
+                                cmask[j * cs] |= bit;
+                            } else if (n_cands == kSoloCands) {
+                                bail = true;
+                                break;
+                            } else {
+                                ckey[j * cs] = key;
+                                cmask[j * cs] = bit;
+                                ccnt[j * cs] = 1u;
+                                ++n_cands;
+                                ++n_unscored;
+                            }
+                        }
+                    } else if (n_unscored == 0) {
+                        break;
+                    }
+                    // score_best_candidate (REF :141-167)
+                    if (n_unscored > 0) {
+                        uint32_t bi = 0, bc = 0;
+                        uint64_t bord = ~0ull;
+                        for (uint32_t j = 0; j < n_cands; ++j) {
+                            const uint32_t cc = ccnt[j * cs];
+                            if (cc & kScored) continue;
+                            const uint32_t kk = ckey[j * cs];
+                            // amin = bucket * bs + lowest bit; order (amin, dir) as (amin << 1 | dir)
+                            const uint64_t amin = (static_cast<uint64_t>(kk >> 1) << bsh) + (__ffs(cmask[j * cs]) - 1);
+                            const uint64_t ord = (amin << 1) | (kk & 1u);
+                            if (cc > bc || (cc == bc && ord < bord)) {
+                                bc = cc;
+                                bord = ord;
+                                bi = j;
+                            }
+                        }
+                        // score_candidate (REF :169-221)
+                        const uint32_t kk = ckey[bi * cs];
+                        const uint32_t mm = cmask[bi * cs];
+                        ccnt[bi * cs] |= kScored;
+                        --n_unscored;
+                        int d_limit;
+                        if (tr.d_best > d_max) d_limit = d_max + a.c - 1;
+                        else if (tr.d_second >= tr.d_best + a.c) d_limit = tr.d_best + a.c - 1;
+                        else d_limit = tr.d_best - 1;
+                        if (a.force) d_limit = d_max + a.c - 1;
+                        if (d_limit >= 0) {  // (:184)
+                            const int dir = static_cast<int>(kk & 1u);
+                            const uint64_t base_pos = static_cast<uint64_t>(kk >> 1) << bsh;
+                            const uint4* orient = Rp + (dir ? half : 0);
+                            int best_d = kInfDistance;
+                            uint64_t best_anchor = 0;
+                            for (uint32_t m = mm; m != 0u; m &= m - 1u) {
+                                const uint64_t anchor = base_pos + static_cast<uint64_t>(__ffs(m) - 1);
+                                if (anchor >= a.glen) continue;
+                                const uint64_t rem = a.glen - anchor;
+                                const uint64_t want = static_cast<uint64_t>(len) + static_cast<uint64_t>(d_limit);
+                                const int w = static_cast<int>(want < rem ? want : rem);
+                                const int d = lv_thread(orient, len, a.planes, static_cast<uint32_t>(anchor), w, d_limit,
+                                                        &s_F[0][tid], cs, c.cells);
+                                c.dist++;
+                                calls++;
+                                c.window += static_cast<uint32_t>(w);
+                                if (calls > 1) {
+                                    c.dist_after++;
+                                    if (d < 0) c.early_out++;
+                                }
+                                if (d >= 0 && d < best_d) {
+                                    best_d = d;
+                                    best_anchor = anchor;
+                                }
+                            }
+                            if (!first_done) {
+                                first_done = true;
+                                if (best_d < kInfDistance) {
+                                    first_valid = true;
+                                    first_pos = best_anchor;
+                                    first_dir = dir;
+                                }
+                            }
+                            if (best_d < kInfDistance) tracker_observe(tr, a.bs, best_d, best_anchor, dir);
+                        }
+                    }
+                    if (tr.d_best < a.c && tr.d_second < tr.d_best + a.c) {  // REF :290-295 / :307-312
+                        c.multi++;
+                        early_multi = true;
+                        break;
+                    }
+                    if (!pruning) {
+                        if (tested >= tr.d_best + a.c) {  // REF :296-315
+                            c.prune++;
+                            pruning = true;
+                        }
+                        ++i;
+                    }
+                }
+                if (!bail) {  // classification, REF :318-363
+                    if (early_multi) {
+                        kind = SA_MULTIPLE_HITS;
+                    } else {
+                        if (tr.d_best <= d_max && tr.d_second >= tr.d_best + a.c) kind = SA_SINGLE_HIT;
+                        else if (tr.d_best <= d_max) kind = SA_MULTIPLE_HITS;
+                        else kind = SA_NOT_FOUND;
+                        if (kind == SA_NOT_FOUND && any_popular && !any_lookup) {
+                            all_pop = true;
+                            kind = SA_MULTIPLE_HITS;
+                        }
+                    }
+                    uint64_t w0 = 0, w1 = static_cast<uint32_t>(-1), w2 = static_cast<uint64_t>(kind);
+                    if (kind == SA_SINGLE_HIT || (kind == SA_MULTIPLE_HITS && tr.d_best <= d_max)) {
+                        w0 = tr.best_pos;
+                        w1 = static_cast<uint32_t>(tr.d_best) |
+                             (static_cast<uint64_t>(static_cast<uint32_t>(tracker_gap(tr))) << 32);
+                        w2 |= (1ull << 8) | (static_cast<uint64_t>(tr.best_dir) << 16);
+                    }
+                    if (kind == SA_SINGLE_HIT && first_valid && first_dir == tr.best_dir) {
+                        const uint64_t delta = first_pos > tr.best_pos ? first_pos - tr.best_pos : tr.best_pos - first_pos;
+                        first_best = delta <= static_cast<uint64_t>(a.bs);
+                    }
+                    uint64_t* out = reinterpret_cast<uint64_t*>(a.results + r);
+                    out[0] = w0;
+                    out[1] = w1;
+                    out[2] = w2;
+                    outcome = 1;
+                }
+            }
+        }
+        // reads for the warp kernel, warp-aggregated
+        const uint32_t cm = __ballot_sync(FULL, outcome == 2);
+        if (cm) {
+            unsigned int slot0 = 0;
+            if (lane == __ffs(cm) - 1) slot0 = atomicAdd(a.pre_list_count, static_cast<unsigned>(__popc(cm)));
+            slot0 = __shfl_sync(FULL, slot0, __ffs(cm) - 1);
+            if (outcome == 2) a.pre_list[slot0 + __popc(cm & lanemask_lt())] = r;
+        }
+        if (__any_sync(FULL, outcome == 1)) {  // counters of the committed reads, one slot per lane
+            const bool ok = outcome == 1;
+            const bool full = ok && !too_short;
+            auto put = [&](int slot, uint32_t v) {
+                const uint32_t t = __reduce_add_sync(FULL, v);
+                if (lane == slot) acc += t;
+            };
+            put(S_READS, ok ? 1u : 0u);
+            put(S_TOO_SHORT, too_short ? 1u : 0u);
+            put(S_READ_BASES, ok ? static_cast<uint32_t>(len) : 0u);
+            put(S_SINGLE, full && kind == SA_SINGLE_HIT ? 1u : 0u);
+            put(S_MULTIPLE, full && kind == SA_MULTIPLE_HITS ? 1u : 0u);
+            put(S_NOT_FOUND, ok && kind == SA_NOT_FOUND ? 1u : 0u);
+            put(S_ALL_POP, full && all_pop ? 1u : 0u);
+            put(S_FIRST_BEST, full && first_best ? 1u : 0u);
+            put(S_LOOKUPS, full ? c.lookups : 0u);
+            put(S_SKIP_N, full ? c.skip_n : 0u);
+            put(S_SKIP_POP, full ? c.skip_pop : 0u);
+            put(S_HITS, full ? c.hits : 0u);
+            put(S_DIST, full ? c.dist : 0u);
+            put(S_DIST_AFTER, full ? c.dist_after : 0u);
+            put(S_EARLY_OUT, full ? c.early_out : 0u);
+            put(S_WINDOW, full ? c.window : 0u);
+            put(S_CELLS, full ? c.cells : 0u);
+            put(S_MULTI, full ? c.multi : 0u);
+            put(S_PRUNE, full ? c.prune : 0u);
+        }
+    }
+    if (lane < kNumStats && acc) atomicAdd(a.stats + lane, acc);
+}
+
 // ------------------------------------------------------------------ seed kernel
 // Stage 1 of the two-kernel path: one thread per read (full lane use, and
 // the probes of a whole warp of reads in flight at once).  Decodes the read
@@ -855,6 +1133,7 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
 template <int G>
 __global__ void __launch_bounds__(256, SA_SEED_MIN_BLOCKS) seed_kernel(const AlignLaunch a) {
     const int lane = threadIdx.x & 31;
+    if (a.pre_list_count && blockIdx.x == 0 && threadIdx.x == 0) *a.pre_list_count = 0;  // solo_kernel appends next
     const int g = lane & (G - 1);
     const int gbase = lane & ~(G - 1);
     const uint32_t groups = (gridDim.x * blockDim.x) / G;
@@ -1212,10 +1491,14 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
         // planes and wave-0 records of read r+nw are copied into the other
         // buffer (cp.async) and its singleton windows are prefetched to L2.
         const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-        const uint32_t N = a.n_reads;
+        // after solo_kernel: only the reads it left in pre_list
+        const bool listed = a.pre_list != nullptr;
+        const uint32_t N = listed ? *a.pre_list_count : a.n_reads;
         const int half = a.pre_pstride >> 1;
         const int nrec = min(32, a.pre_rstride);
+        auto rid = [&](uint32_t k) -> uint32_t { return listed ? __ldg(a.pre_list + k) : k; };
         auto issue_copy = [&](uint32_t rr, int q) {
+            rr = rid(rr);
             const uint4* gp = a.pre_planes + static_cast<uint64_t>(rr) * a.pre_pstride;
             uint4* R = planes + 2 * q * a.wbr;
             for (int t = lane; t < half; t += 32) {
@@ -1227,11 +1510,11 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
         };
         uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
         if (r < N) {
-            uint2 m_c = __ldg(a.pre_meta + r), m_n = make_uint2(0, 1u << 16);
+            uint2 m_c = __ldg(a.pre_meta + rid(r)), m_n = make_uint2(0, 1u << 16);
             issue_copy(r, 0);
             cp_async_commit();
             if (r + nw < N) {
-                m_n = __ldg(a.pre_meta + r + nw);
+                m_n = __ldg(a.pre_meta + rid(r + nw));
                 issue_copy(r + nw, 1);
             }
             cp_async_commit();
@@ -1243,9 +1526,10 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
                     prefetch_windows(a, recs + 32 * (p ^ 1), static_cast<int>(m_n.y & 0xffffu),
                                      static_cast<int>(m_n.x), lane);
                 uint2 m_nn = make_uint2(0, 1u << 16);
-                if (r + 2 * nw < N) m_nn = __ldg(a.pre_meta + r + 2 * nw);
-                process(r, p, static_cast<int>(m_c.x), static_cast<int>(m_c.y >> 16), true,
-                        static_cast<int>(m_c.y & 0xffffu), a.pre_recs + static_cast<uint64_t>(r) * a.pre_rstride);
+                if (r + 2 * nw < N) m_nn = __ldg(a.pre_meta + rid(r + 2 * nw));
+                const uint32_t rr = rid(r);
+                process(rr, p, static_cast<int>(m_c.x), static_cast<int>(m_c.y >> 16), true,
+                        static_cast<int>(m_c.y & 0xffffu), a.pre_recs + static_cast<uint64_t>(rr) * a.pre_rstride);
                 if (r + 2 * nw < N) issue_copy(r + 2 * nw, p);
                 cp_async_commit();
                 m_c = m_n;
@@ -1576,9 +1860,23 @@ void launch_seed(const AlignLaunch& a, cudaStream_t st) {
     else go(seed_kernel<32>, 32);
 }
 
+bool solo_eligible(const AlignLaunch& a) {
+    static const bool off = getenv("SA_NO_SOLO") != nullptr;  // A/B switch: warp kernel for every read
+    return !off && a.pre_list != nullptr && a.dl_max <= 15 && a.bs_shift >= 0 && a.bs_shift <= 5;
+}
+
 void launch_align_seeded(const AlignLaunch& a, int grid, int block, cudaStream_t st) {
-    if (a.dl_max <= 15) launch_variant<false, true, true, false, true>(a, grid, block, st);
-    else launch_variant<false, true, false, false, true>(a, grid, block, st);
+    AlignLaunch b = a;
+    if (solo_eligible(a)) {
+        const uint64_t g = std::min<uint64_t>((static_cast<uint64_t>(a.n_reads) + kSoloThreads - 1) / kSoloThreads,
+                                              148ull * 16);
+        solo_kernel<<<static_cast<int>(std::max<uint64_t>(g, 1)), kSoloThreads, 0, st>>>(a);
+    } else {
+        b.pre_list = nullptr;
+        b.pre_list_count = nullptr;
+    }
+    if (b.dl_max <= 15) launch_variant<false, true, true, false, true>(b, grid, block, st);
+    else launch_variant<false, true, false, false, true>(b, grid, block, st);
 }
 
 void launch_align_pre(const AlignLaunch& a, int grid, int block, cudaStream_t st) {

@@ -76,6 +76,11 @@ struct AlignLaunch {
     uint4* pre_recs;
     uint2* pre_meta;
     int pre_pstride, pre_rstride;
+    // solo_kernel (thread per read) runs between the two when pre_list is set:
+    // it finishes the reads it can and lists the others (pre_list[0 ..
+    // *pre_list_count), zeroed by the seed kernel) for the align kernel.
+    unsigned int* pre_list;
+    unsigned int* pre_list_count;
     // Packed input (pack.cpp): when non-null the seed kernel reads the chunk's
     // bases from three bit planes {lo, hi, n} of pk_wpp words each (bit i =
     // base base_off + i) instead of ASCII bytes; lo & n marks a bad character.

@@ -80,7 +80,8 @@ struct Stage {  // one of the two pipeline slots of a replica
     uint4* pre_planes = nullptr;
     uint4* pre_recs = nullptr;
     uint2* pre_meta = nullptr;
-    uint64_t pre_planes_cap = 0, pre_recs_cap = 0, pre_meta_cap = 0;
+    unsigned int* pre_list = nullptr;  // solo_kernel's list for the warp kernel; count in the last entry
+    uint64_t pre_planes_cap = 0, pre_recs_cap = 0, pre_meta_cap = 0, pre_list_cap = 0;
     // seeded pipeline: input landed / consumed by the seed kernel / aligned /
     // results copied out
     cudaEvent_t e_in = nullptr, e_seeded = nullptr, e_al = nullptr, e_out = nullptr;
@@ -478,6 +479,7 @@ int ensure_pre(sa_context* ctx, Stage& s, uint64_t n_reads, const LaunchShape& s
     if (int rc = grow(&s.pre_planes, s.pre_planes_cap, np, sizeof(uint4))) return rc;
     if (int rc = grow(&s.pre_recs, s.pre_recs_cap, nr, sizeof(uint4))) return rc;
     if (int rc = grow(&s.pre_meta, s.pre_meta_cap, n_reads, sizeof(uint2))) return rc;
+    if (int rc = grow(&s.pre_list, s.pre_list_cap, n_reads + 1, sizeof(unsigned int))) return rc;
     return SA_OK;
 }
 
@@ -521,6 +523,8 @@ int enqueue_align(sa_context* ctx, Replica& rep, Stage& stg, const LaunchShape& 
         a.pre_planes = stg.pre_planes;
         a.pre_recs = stg.pre_recs;
         a.pre_meta = stg.pre_meta;
+        a.pre_list = stg.pre_list;
+        a.pre_list_count = stg.pre_list + (stg.pre_list_cap - 1);
         a.pre_pstride = pre_pstride(a);
         a.pre_rstride = pre_rstride(a);
         launch_align_pre(a, sh.fast_grid, sh.fast_block, stg.st);
@@ -1047,6 +1051,8 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
         a.pre_planes = st.pre_planes;
         a.pre_recs = st.pre_recs;
         a.pre_meta = st.pre_meta;
+        a.pre_list = st.pre_list;
+        a.pre_list_count = st.pre_list + (st.pre_list_cap - 1);
         a.pre_pstride = pre_pstride(a);
         a.pre_rstride = pre_rstride(a);
         a.packed = packed ? st.d_pack : nullptr;
@@ -1280,6 +1286,7 @@ void sa_destroy(sa_context* ctx) {
             if (s.pre_planes) cudaFree(s.pre_planes);
             if (s.pre_recs) cudaFree(s.pre_recs);
             if (s.pre_meta) cudaFree(s.pre_meta);
+            if (s.pre_list) cudaFree(s.pre_list);
             if (s.d_pack) cudaFree(s.d_pack);
             if (s.h_pack) cudaFreeHost(s.h_pack);
             if (s.st) cudaStreamDestroy(s.st);

@@ -119,6 +119,34 @@ SA_DEV int lv_warp(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, 
     return lv_warp_smem(R, m, W, wofs, w, dl, F, lane, cells);
 }
 
+// Serial LV for one thread (d_limit <= 15): the frontier is 2*dl+3 16-bit
+// entries at F[0], F[fs], F[2*fs], ... (shared memory, one column per thread)
+// and is updated in place, diagonal by diagonal, carrying the old value of
+// k-1 in a register.  Every diagonal of iteration e is stepped before the
+// result is taken -- the steps, and so the dp_cells count, are exactly those
+// of lv_warp_reg.  R and W are global plane arrays (read-only in this kernel).
+SA_DEV int lv_thread(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, int dl, short* F, int fs,
+                     uint32_t& cells) {
+    constexpr short kU = -32768;  // unreachable: stays negative after +1 (REF edit_distance.cpp:56-59)
+    for (int t = 0; t < 2 * dl + 3; ++t) F[t * fs] = kU;
+    const int off = dl + 1;
+    for (int e = 0; e <= dl; ++e) {
+        bool found = false;
+        int left = kU;  // old value of diagonal k-1
+        int cur = F[(off - e) * fs];
+        for (int k = -e; k <= e; ++k) {
+            const int right = F[(k + 1 + off) * fs];
+            const int v = lv_step(e, k, left, cur, right, m, w, R, W, wofs, cells);
+            left = cur;
+            cur = right;
+            F[(k + off) * fs] = static_cast<short>(v < 0 ? kU : v);
+            found |= v == m;
+        }
+        if (found) return e;
+    }
+    return -1;
+}
+
 // standalone LV (lv_batch_kernel): any limit
 SA_DEV int lv_warp_any(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, int dl, int* F,
                        int lane, uint32_t& cells) {
