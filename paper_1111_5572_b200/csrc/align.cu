@@ -860,7 +860,13 @@ struct SoloRead {
     uint32_t window = 0, cells = 0, multi = 0, prune = 0;
 };
 
-__global__ void __launch_bounds__(kSoloThreads) solo_kernel(const AlignLaunch a) {
+#ifndef SA_SOLO_MIN_BLOCKS
+#define SA_SOLO_MIN_BLOCKS 1
+#endif
+#ifndef SA_SOLO_MAX_E
+#define SA_SOLO_MAX_E 4  // LV iterations a thread runs before handing its read to the warp kernel
+#endif
+__global__ void __launch_bounds__(kSoloThreads, SA_SOLO_MIN_BLOCKS) solo_kernel(const AlignLaunch a) {
     __shared__ uint32_t s_key[kSoloCands][kSoloThreads];   // bucket << 1 | dir
     __shared__ uint32_t s_mask[kSoloCands][kSoloThreads];  // anchor bits (bucket <= 32)
     __shared__ uint32_t s_cnt[kSoloCands][kSoloThreads];   // seeds_hitting | kScored
@@ -1007,7 +1013,11 @@ __global__ void __launch_bounds__(kSoloThreads) solo_kernel(const AlignLaunch a)
                                 const uint64_t want = static_cast<uint64_t>(len) + static_cast<uint64_t>(d_limit);
                                 const int w = static_cast<int>(want < rem ? want : rem);
                                 const int d = lv_thread(orient, len, a.planes, static_cast<uint32_t>(anchor), w, d_limit,
-                                                        &s_F[0][tid], cs, c.cells);
+                                                        &s_F[0][tid], cs, c.cells, SA_SOLO_MAX_E);
+                                if (d == -2) {
+                                    bail = true;
+                                    break;
+                                }
                                 c.dist++;
                                 calls++;
                                 c.window += static_cast<uint32_t>(w);
@@ -1020,6 +1030,7 @@ __global__ void __launch_bounds__(kSoloThreads) solo_kernel(const AlignLaunch a)
                                     best_anchor = anchor;
                                 }
                             }
+                            if (bail) break;
                             if (!first_done) {
                                 first_done = true;
                                 if (best_d < kInfDistance) {
@@ -1860,9 +1871,18 @@ void launch_seed(const AlignLaunch& a, cudaStream_t st) {
     else go(seed_kernel<32>, 32);
 }
 
+// Small launches stay on the warp kernel: with one read per thread a launch
+// of a few thousand reads is as long as its slowest read (C0, 10 k reads:
+// 135 M reads/s with the solo kernel, 171 M without).  SA_SOLO_MIN_READS
+// overrides the threshold; SA_NO_SOLO switches the solo kernel off.
 bool solo_eligible(const AlignLaunch& a) {
-    static const bool off = getenv("SA_NO_SOLO") != nullptr;  // A/B switch: warp kernel for every read
-    return !off && a.pre_list != nullptr && a.dl_max <= 15 && a.bs_shift >= 0 && a.bs_shift <= 5;
+    static const bool off = getenv("SA_NO_SOLO") != nullptr;
+    static const uint32_t min_reads = [] {
+        const char* e = getenv("SA_SOLO_MIN_READS");
+        return e ? static_cast<uint32_t>(atoll(e)) : 12288u;
+    }();
+    return !off && a.pre_list != nullptr && a.n_reads >= min_reads && a.dl_max <= 15 && a.bs_shift >= 0 &&
+           a.bs_shift <= 5;
 }
 
 void launch_align_seeded(const AlignLaunch& a, int grid, int block, cudaStream_t st) {

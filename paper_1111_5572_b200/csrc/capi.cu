@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <cstdio>
 #include <cstring>
@@ -925,6 +926,7 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
                     const uint64_t* offsets, const std::vector<uint64_t>& bounds, std::atomic<size_t>& next,
                     uint64_t n_reads, sa_result* results, float& e2e_ms, float& k_ms, uint64_t& launches,
                     sa_stats* out) {
+    const auto t_host0 = std::chrono::steady_clock::now();  // diagnostics (SA_DEBUG_PIPE)
     auto& S = rep.sm;
     if (!S.ci) {
         CUDA_TRY(ctx, cudaStreamCreateWithFlags(&S.ci, cudaStreamNonBlocking));
@@ -974,16 +976,18 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
         if (c >= n_chunks) break;
         const uint64_t r0 = bounds[c], r1 = bounds[c + 1];
         uint64_t Lc = 0, Lmin = ~0ull;
-        for (uint64_t i = r0; i < r1; ++i) {
-            if (offsets[i + 1] < offsets[i]) {
-                bad = fail(ctx, SA_EINVAL, "offsets not ascending");
-                break;
-            }
-            const uint64_t li = offsets[i + 1] - offsets[i];
-            Lc = std::max(Lc, li);
-            Lmin = std::min(Lmin, li);
+        bool desc = false;
+        for (uint64_t i = r0; i < r1; ++i) {  // branch-free scan
+            const uint64_t o0 = offsets[i], o1 = offsets[i + 1];
+            desc |= o1 < o0;
+            const uint64_t li = o1 - o0;
+            Lc = li > Lc ? li : Lc;
+            Lmin = li < Lmin ? li : Lmin;
         }
-        if (bad) break;
+        if (desc) {
+            bad = fail(ctx, SA_EINVAL, "offsets not ascending");
+            break;
+        }
         // one length for the whole chunk: the offsets need not be copied
         const uint32_t fixed = (Lmin == Lc && Lc > 0 && Lc < (1u << 30)) ? static_cast<uint32_t>(Lc) : 0u;
         Lc = std::min<uint64_t>(Lc, 1024);  // longer reads are deferred by the seed kernel
@@ -1100,6 +1104,7 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
         CUDA_TRY(ctx, cudaEventRecord(S.e_end, S.co));
     }
     if (dbg_span && k > 0) CUDA_TRY(ctx, cudaEventRecord(S.e_ready, S.ci));  // copy-in span end (diagnostics)
+    const auto t_enq = std::chrono::steady_clock::now();
     CUDA_TRY(ctx, cudaStreamSynchronize(S.co));
     CUDA_TRY(ctx, cudaStreamSynchronize(S.ci));
     if (dbg_span && k > 0) {
@@ -1107,7 +1112,10 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
         cudaEventElapsedTime(&ci, S.e_begin, S.e_ready);
         cudaEventElapsedTime(&kb, S.e_begin, S.k0);
         cudaEventElapsedTime(&ke, S.e_begin, S.k1);
-        fprintf(stderr, "[pipe] chunks=%d copy-in ends %.3f ms, compute %.3f..%.3f ms\n", k, ci, kb, ke);
+        const double host_ms = std::chrono::duration<double, std::milli>(t_enq - t_host0).count();
+        const double all_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_host0).count();
+        fprintf(stderr, "[pipe] chunks=%d copy-in ends %.3f ms, compute %.3f..%.3f ms; host enqueue %.3f ms, host total %.3f ms\n",
+                k, ci, kb, ke, host_ms, all_ms);
         // kernel time vs waiting: 'W'/'w' marks precede seed/align, 's'/'a' follow
         float seed = 0, al = 0, wait = 0;
         for (size_t i = 1; i < trail.size(); ++i) {
@@ -1376,7 +1384,12 @@ int sa_align_batch(sa_context* ctx, const sa_params* params, const char* bases,
         // short copy, and back down at the end so little compute is left once
         // the last copy lands; equal chunks in between
         std::vector<uint64_t> up;
-        for (uint64_t s = std::min<uint64_t>(chunk_reads, 1u << 14); s < chunk_reads; s *= 2) up.push_back(s);
+        static const uint64_t ramp0 = [] {  // SA_RAMP0: first ramp size (tuning; >= chunk size: no ramp)
+            const char* e = getenv("SA_RAMP0");
+            return e ? static_cast<uint64_t>(atoll(e)) : uint64_t{1} << 14;
+        }();
+        for (uint64_t s = std::min<uint64_t>(chunk_reads, std::max<uint64_t>(ramp0, 1024)); s < chunk_reads; s *= 2)
+            up.push_back(s);
         uint64_t ramp = 0;
         for (uint64_t s : up) ramp += 2 * s;
         std::vector<uint64_t> sizes;

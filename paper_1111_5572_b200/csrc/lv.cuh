@@ -125,12 +125,15 @@ SA_DEV int lv_warp(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, 
 // k-1 in a register.  Every diagonal of iteration e is stepped before the
 // result is taken -- the steps, and so the dp_cells count, are exactly those
 // of lv_warp_reg.  R and W are global plane arrays (read-only in this kernel).
+// Returns -2 once e would exceed e_cap (< dl): the caller hands the read to
+// the warp kernel, so one thread's long wavefront does not hold up its warp.
 SA_DEV int lv_thread(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, int dl, short* F, int fs,
-                     uint32_t& cells) {
+                     uint32_t& cells, int e_cap) {
     constexpr short kU = -32768;  // unreachable: stays negative after +1 (REF edit_distance.cpp:56-59)
     for (int t = 0; t < 2 * dl + 3; ++t) F[t * fs] = kU;
     const int off = dl + 1;
     for (int e = 0; e <= dl; ++e) {
+        if (e > e_cap) return -2;
         bool found = false;
         int left = kU;  // old value of diagonal k-1
         int cur = F[(off - e) * fs];

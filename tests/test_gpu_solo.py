@@ -1,0 +1,29 @@
+"""The thread-per-read solo kernel (align.cu solo_kernel) against the oracle.
+
+The solo kernel finishes the reads whose seeds have at most one hit and
+hands every other read to the warp kernel, so by default each batch is split
+between the two kernels.  These runs force each side: SA_SOLO_MIN_READS=1
+puts every launch (small batches, ragged and short reads, N seeds, the
+repeat corpora whose reads bail part-way, force_max_dlimit, the golden
+corpora) through the solo kernel first; SA_NO_SOLO=1 runs the warp kernel
+alone.  Both must match the oracle read for read and counter for counter.
+The switches are read once per process, so each run is a subprocess.
+"""
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SELECT = "align_parity or ragged or force_max or align_golden or overflow_paths or fixed_length"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("env", [{"SA_SOLO_MIN_READS": "1"}, {"SA_NO_SOLO": "1"}], ids=["solo-everywhere", "warp-only"])
+def test_parity_with_solo_forced(env):
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-x", "-q",
+                        "-m", "gpu", "-k", SELECT, "-p", "no:cacheprovider"],
+                       cwd=ROOT, env={**os.environ, **env}, capture_output=True, text=True, timeout=1500)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
