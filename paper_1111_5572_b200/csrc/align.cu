@@ -861,7 +861,14 @@ struct SoloRead {
 };
 
 #ifndef SA_SOLO_MIN_BLOCKS
-#define SA_SOLO_MIN_BLOCKS 1
+#define SA_SOLO_MIN_BLOCKS 6  // 80 registers, 24 warps per SM (C1 934 -> 971 M reads/s over the unbounded 109)
+#endif
+#ifndef SA_SOLO_LV
+// solo LV: 0 serial wavefront (lv_thread); 1 banded bit-parallel (lv_bitpar).
+// Measured at C1: 0 -> 934 M reads/s, 1 -> 591 M (a fixed m + d_limit column
+// steps per call against the wavefront's few steps for a close read), and a
+// single-loop (flattened) wavefront 737 M.
+#define SA_SOLO_LV 0
 #endif
 #ifndef SA_SOLO_MAX_E
 #define SA_SOLO_MAX_E 4  // LV iterations a thread runs before handing its read to the warp kernel
@@ -870,7 +877,9 @@ __global__ void __launch_bounds__(kSoloThreads, SA_SOLO_MIN_BLOCKS) solo_kernel(
     __shared__ uint32_t s_key[kSoloCands][kSoloThreads];   // bucket << 1 | dir
     __shared__ uint32_t s_mask[kSoloCands][kSoloThreads];  // anchor bits (bucket <= 32)
     __shared__ uint32_t s_cnt[kSoloCands][kSoloThreads];   // seeds_hitting | kScored
+#if SA_SOLO_LV != 1
     __shared__ short s_F[kSoloF][kSoloThreads];
+#endif
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     uint32_t* ckey = &s_key[0][tid];
@@ -1012,8 +1021,13 @@ __global__ void __launch_bounds__(kSoloThreads, SA_SOLO_MIN_BLOCKS) solo_kernel(
                                 const uint64_t rem = a.glen - anchor;
                                 const uint64_t want = static_cast<uint64_t>(len) + static_cast<uint64_t>(d_limit);
                                 const int w = static_cast<int>(want < rem ? want : rem);
+#if SA_SOLO_LV == 1
+                                const int d = lv_bitpar(orient, half, len, a.planes, static_cast<uint32_t>(anchor), w,
+                                                        d_limit, c.cells);
+#else
                                 const int d = lv_thread(orient, len, a.planes, static_cast<uint32_t>(anchor), w, d_limit,
                                                         &s_F[0][tid], cs, c.cells, SA_SOLO_MAX_E);
+#endif
                                 if (d == -2) {
                                     bail = true;
                                     break;
@@ -1755,6 +1769,11 @@ __global__ void __launch_bounds__(256) lv_batch_kernel(const LvLaunch a) {
             continue;
         }
         uint32_t cells = 0;
+        if (a.bitpar && dl <= 15) {  // test hook: the solo kernel's bit-parallel LV, lane 0 alone
+            if (lane == 0) a.out[p] = lv_bitpar(R, rb, m, W, 0u, w, dl, cells);
+            __syncwarp();
+            continue;
+        }
         const int d = lv_warp_any(R, m, W, 0u, w, dl, F, lane, cells);
         if (lane == 0) a.out[p] = d;
         __syncwarp();
@@ -1910,7 +1929,10 @@ void launch_align_slow(const AlignLaunch& a, int grid, int block, cudaStream_t s
 }
 
 void launch_lv_batch(const LvLaunch& a, int grid, int block, cudaStream_t st) {
-    lv_batch_kernel<<<grid, block, a.smem_per_warp * (block / 32), st>>>(a);
+    static const int bitpar = getenv("SA_LV_BITPAR") != nullptr;  // test hook (lv_bitpar for d_limit <= 15)
+    LvLaunch b = a;
+    b.bitpar = bitpar;
+    lv_batch_kernel<<<grid, block, b.smem_per_warp * (block / 32), st>>>(b);
 }
 
 void launch_lookup(const LookupLaunch& a, cudaStream_t st) {

@@ -128,6 +128,7 @@ struct LvLaunch {
     uint32_t smem_per_warp;
     int32_t* out;
     unsigned int* error_flag;
+    int bitpar;  // test hook: lv_bitpar for limits <= 15 (set by launch_lv_batch from SA_LV_BITPAR)
 };
 
 struct LookupLaunch {

@@ -150,6 +150,81 @@ SA_DEV int lv_thread(const uint4* R, int m, const uint4* W, uint32_t wofs, int w
     return -1;
 }
 
+
+// Banded bit-parallel bounded edit distance for one thread (d_limit <= 15),
+// same value as bounded_distance (REF src/edit_distance.cpp:19-75), computed
+// with Myers' bit-vector column steps (Hyyrö's formulation, global variant)
+// restricted to the diagonal band |j - i| <= dl, one 32-bit word per column:
+// bit b of the column-j word is row i = j - dl + b.
+//  * Cells outside the band are replaced by boundary values >= dl + 1 chosen
+//    so every delta stays in {-1, 0, +1}: the row above the band's top enters
+//    with horizontal delta +1 (the "| 1" shift-in), and the row that enters
+//    at the bottom with vertical delta +1.  A path through a boundary cell
+//    costs more than dl, so every value <= dl is exact, and every value > dl
+//    stays > dl.
+//  * Rows <= 0 are virtual never-matching rows with H[-r][j] = j + r (row 0 is
+//    the anchored window start, D[0][j] = j); they satisfy the recurrence and
+//    feed row 1 exactly as row 0 does.
+//  * `top` tracks H at the band's top row along its diagonal (+1 unless the
+//    top bit of D0 says the diagonal step is free); H[m][j] = top + the
+//    vertical deltas from the top bit down to row m.
+// Every thread with the same limit runs the same number of column steps, so
+// a warp of reads stays converged (the serial wavefront diverged to ~3 active
+// lanes per instruction).  dp_cells counts band cells (implementation-specific).
+// R: read planes (nblk blocks; positions past the read carry N bits), W:
+// genome planes with the window starting at base wofs, w bases long.
+SA_DEV int lv_bitpar(const uint4* R, int nblk, int m, const uint4* W, uint32_t wofs, int w, int dl,
+                     uint32_t& cells) {
+    const int width = 2 * dl + 1;
+    const uint32_t wmask = width >= 32 ? 0xffffffffu : ((1u << width) - 1u);
+    uint32_t VP = wmask & ~((2u << dl) - 1u);  // column 0: rows 1..dl rise by 1
+    uint32_t VN = (2u << dl) - 1u;             // rows -dl..0 fall by 1 (H[-r][0] = r)
+    int top = dl;                              // H[-dl][0]
+    int best = m <= dl ? m : 0x7fffffff;       // H[m][0] = m
+    const int jend = min(w, m + dl);
+    // read planes for positions q .. q+31, q = j - 1 - dl (blocks qb, qb + 1)
+    auto blk = [&](int b) -> uint4 {
+        return (b < 0 || b >= nblk) ? make_uint4(0u, 0u, 0xffffffffu, 0u) : R[b];
+    };
+    int q = -dl;  // j = 1
+    int qb = q >> 5;
+    uint4 A = blk(qb), B = blk(qb + 1);
+    uint32_t gp = wofs;  // window base j - 1
+    uint4 G = W[gp >> 5];
+    for (int j = 1; j <= jend; ++j) {
+        if ((q >> 5) != qb) {
+            ++qb;
+            A = B;
+            B = blk(qb + 1);
+        }
+        if ((gp & 31u) == 0u && j > 1) G = W[gp >> 5];
+        const uint32_t sh = static_cast<uint32_t>(q & 31);
+        const uint32_t rl = __funnelshift_r(A.x, B.x, sh), rh = __funnelshift_r(A.y, B.y, sh);
+        const uint32_t rn = __funnelshift_r(A.z, B.z, sh);
+        const uint32_t gb = gp & 31u;
+        const uint32_t tl = 0u - ((G.x >> gb) & 1u), th = 0u - ((G.y >> gb) & 1u), tn = 0u - ((G.z >> gb) & 1u);
+        const uint32_t eq = ~((rl ^ tl) | (rh ^ th) | rn | tn);  // N never matches (REF edit_distance.cpp:11-13)
+        VP = (VP >> 1) | (1u << (width - 1));
+        VN >>= 1;
+        const uint32_t D0 = ((((eq & VP) + VP) ^ VP) | eq | VN);
+        const uint32_t HP = VN | ~(D0 | VP);
+        const uint32_t HN = VP & D0;
+        top += (D0 & 1u) ^ 1u;
+        const uint32_t X = (HP << 1) | 1u;
+        VN = X & D0 & wmask;
+        VP = ((HN << 1) | ~(X | D0)) & wmask;
+        const int bm = m - j + dl;  // bit of row m (>= 0 since j <= m + dl)
+        if (bm < width) {
+            const uint32_t mk = (bm >= 31 ? 0xffffffffu : ((2u << bm) - 1u)) & ~1u;
+            best = min(best, top + __popc(VP & mk) - __popc(VN & mk));
+        }
+        ++q;
+        ++gp;
+    }
+    cells += static_cast<uint32_t>(jend > 0 ? jend : 0) * static_cast<uint32_t>(width);
+    return best <= dl ? best : -1;
+}
+
 // standalone LV (lv_batch_kernel): any limit
 SA_DEV int lv_warp_any(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, int dl, int* F,
                        int lane, uint32_t& cells) {

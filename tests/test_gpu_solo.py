@@ -27,3 +27,16 @@ def test_parity_with_solo_forced(env):
                        cwd=ROOT, env={**os.environ, **env}, capture_output=True, text=True, timeout=1500)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
+
+
+@pytest.mark.gpu
+def test_bitparallel_lv_vs_oracle():
+    """lv_bitpar (the solo kernel's banded bit-parallel LV) through the
+    standalone LV entry point (SA_LV_BITPAR=1: lane 0 of each warp runs it for
+    limits <= 15): the reference's known answers, the golden LV triples and
+    random pairs with edits and N against the oracle."""
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-x", "-q",
+                        "-m", "gpu", "-k", "lv_known or lv_random or lv_wide or lv_golden", "-p", "no:cacheprovider"],
+                       cwd=ROOT, env={**os.environ, "SA_LV_BITPAR": "1"}, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
