@@ -31,6 +31,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "align_kernels.cuh"
@@ -870,6 +871,9 @@ struct SoloRead {
 // single-loop (flattened) wavefront 737 M.
 #define SA_SOLO_LV 0
 #endif
+#ifndef SA_SOLO_MAX_HITS
+#define SA_SOLO_MAX_HITS 4  // hits of one seed the thread votes itself (more: the warp kernel; C2 1/4/8/32: 245/244/238/236 M reads/s)
+#endif
 #ifndef SA_SOLO_MAX_E
 #define SA_SOLO_MAX_E 4  // LV iterations a thread runs before handing its read to the warp kernel
 #endif
@@ -952,14 +956,30 @@ __global__ void __launch_bounds__(kSoloThreads, SA_SOLO_MIN_BLOCKS) solo_kernel(
                         any_lookup = true;
                         c.hits += rec.y;
                         if (i < tier0) ++tested;
-                        if (rec.y > 1u) {  // several hits (or a palindrome): the warp kernel votes them
+                        // REF :273-286: every hit of the seed votes for (anchor / bucket, dir)
+                        const uint32_t cnt = rec.y;
+                        if (cnt > static_cast<uint32_t>(SA_SOLO_MAX_HITS)) {  // long vote lists: the warp kernel
                             bail = true;
                             break;
                         }
-                        if (rec.y == 1u) {  // REF :273-286, one hit
-                            const uint32_t dir = ((rec.x & kSeedSingleRc) ? 1u : 0u) ^ ((rec.x & kSeedQflip) ? 1u : 0u);
-                            const int o = static_cast<int>(rec.w);
-                            const int64_t anchor = static_cast<int64_t>(rec.z) - (dir ? (len - a.s - o) : o);
+                        const bool pal = (rec.x & kSeedPal) != 0;
+                        const uint32_t ntot = pal ? cnt / 2 : cnt;
+                        const bool inl = ntot == 1;
+                        const uint32_t n_fwd = inl ? 0u : __ldg(a.pool + rec.z);
+                        const uint32_t qflip = (rec.x & kSeedQflip) ? 1u : 0u;
+                        const int o = static_cast<int>(rec.w);
+                        for (uint32_t t = 0; t < cnt; ++t) {
+                            const uint32_t jj = pal ? (t < ntot ? t : t - ntot) : t;
+                            uint32_t pos, eflag;
+                            if (inl) {
+                                pos = rec.z;
+                                eflag = (rec.x & kSeedSingleRc) ? 1u : 0u;
+                            } else {
+                                pos = __ldg(a.pool + rec.z + 1 + jj);
+                                eflag = jj >= n_fwd ? 1u : 0u;
+                            }
+                            const uint32_t dir = pal ? (t >= ntot ? 1u : 0u) : (eflag ^ qflip);
+                            const int64_t anchor = static_cast<int64_t>(pos) - (dir ? (len - a.s - o) : o);
                             const uint32_t aa = anchor < 0 ? 0u : static_cast<uint32_t>(anchor);
                             const uint32_t key = ((aa >> bsh) << 1) | dir;
                             const uint32_t bit = 1u << (aa & ((1u << bsh) - 1u));
@@ -979,6 +999,7 @@ __global__ void __launch_bounds__(kSoloThreads, SA_SOLO_MIN_BLOCKS) solo_kernel(
                                 ++n_unscored;
                             }
                         }
+                        if (bail) break;
                     } else if (n_unscored == 0) {
                         break;
                     }
@@ -1910,6 +1931,13 @@ void launch_align_seeded(const AlignLaunch& a, int grid, int block, cudaStream_t
         const uint64_t g = std::min<uint64_t>((static_cast<uint64_t>(a.n_reads) + kSoloThreads - 1) / kSoloThreads,
                                               148ull * 16);
         solo_kernel<<<static_cast<int>(std::max<uint64_t>(g, 1)), kSoloThreads, 0, st>>>(a);
+        static const bool dbg = getenv("SA_DEBUG_SOLO") != nullptr;  // diagnostics: reads left to the warp kernel
+        if (dbg) {
+            unsigned int n = 0;
+            cudaStreamSynchronize(st);
+            cudaMemcpy(&n, a.pre_list_count, sizeof(n), cudaMemcpyDeviceToHost);
+            fprintf(stderr, "[solo] %u of %u reads to the warp kernel\n", n, a.n_reads);
+        }
     } else {
         b.pre_list = nullptr;
         b.pre_list_count = nullptr;
