@@ -294,8 +294,8 @@ def run_ours(args) -> None:
         "config": _workload(cfg, R),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "hot path = seed_kernel (decode, seeds, index probes) + align_kernel<kPre> "
-                               "(vote, LV, classify); timed together with CUDA events around both launches",
+                     "kernel": "hot path = seed_kernel (decode, seeds, index probes) + solo_kernel (thread per read) + align_kernel<kPre> (the reads solo lists) "
+                               "(vote, LV, classify); timed together with CUDA events around all three launches",
                      "kernel_ms": fast_mean, "overflow_kernel_ms": statistics.mean(slow_ms),
                      "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src},
         # the library copies no offsets for a chunk whose reads share one length

@@ -1925,12 +1925,14 @@ bool solo_eligible(const AlignLaunch& a) {
            a.bs_shift <= 5;
 }
 
-void launch_align_seeded(const AlignLaunch& a, int grid, int block, cudaStream_t st) {
+int launch_align_seeded(const AlignLaunch& a, int grid, int block, cudaStream_t st) {
     AlignLaunch b = a;
+    int n = 1;
     if (solo_eligible(a)) {
         const uint64_t g = std::min<uint64_t>((static_cast<uint64_t>(a.n_reads) + kSoloThreads - 1) / kSoloThreads,
                                               148ull * 16);
         solo_kernel<<<static_cast<int>(std::max<uint64_t>(g, 1)), kSoloThreads, 0, st>>>(a);
+        ++n;
         static const bool dbg = getenv("SA_DEBUG_SOLO") != nullptr;  // diagnostics: reads left to the warp kernel
         if (dbg) {
             unsigned int n = 0;
@@ -1944,11 +1946,12 @@ void launch_align_seeded(const AlignLaunch& a, int grid, int block, cudaStream_t
     }
     if (b.dl_max <= 15) launch_variant<false, true, true, false, true>(b, grid, block, st);
     else launch_variant<false, true, false, false, true>(b, grid, block, st);
+    return n;
 }
 
-void launch_align_pre(const AlignLaunch& a, int grid, int block, cudaStream_t st) {
+int launch_align_pre(const AlignLaunch& a, int grid, int block, cudaStream_t st) {
     launch_seed(a, st);
-    launch_align_seeded(a, grid, block, st);
+    return 1 + launch_align_seeded(a, grid, block, st);
 }
 
 void launch_align_slow(const AlignLaunch& a, int grid, int block, cudaStream_t st) {

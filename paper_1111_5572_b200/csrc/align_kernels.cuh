@@ -149,9 +149,9 @@ struct LookupLaunch {
 
 void launch_align_fast(const AlignLaunch& a, int grid, int block, cudaStream_t st);
 // seed_kernel then the kPre align kernel (a.pre_* set); reads <= 1 kbp
-void launch_align_pre(const AlignLaunch& a, int grid, int block, cudaStream_t st);
+int launch_align_pre(const AlignLaunch& a, int grid, int block, cudaStream_t st);  // kernels launched
 void launch_seed(const AlignLaunch& a, cudaStream_t st);                                    // stage 1 only
-void launch_align_seeded(const AlignLaunch& a, int grid, int block, cudaStream_t st);      // stage 2 only
+int launch_align_seeded(const AlignLaunch& a, int grid, int block, cudaStream_t st);      // stage 2 only
 void launch_align_slow(const AlignLaunch& a, int grid, int block, cudaStream_t st);
 void launch_lv_batch(const LvLaunch& a, int grid, int block, cudaStream_t st);
 void launch_lookup(const LookupLaunch& a, cudaStream_t st);

@@ -528,8 +528,7 @@ int enqueue_align(sa_context* ctx, Replica& rep, Stage& stg, const LaunchShape& 
         a.pre_list_count = stg.pre_list + (stg.pre_list_cap - 1);
         a.pre_pstride = pre_pstride(a);
         a.pre_rstride = pre_rstride(a);
-        launch_align_pre(a, sh.fast_grid, sh.fast_block, stg.st);
-        launches += 1;
+        launches += launch_align_pre(a, sh.fast_grid, sh.fast_block, stg.st) - 1;
     } else {
         launch_align_fast(a, sh.fast_grid, sh.fast_block, stg.st);
     }
@@ -960,7 +959,7 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
         Stage& st = rep.stage[pend.stage];
         CUDA_TRY(ctx, cudaStreamWaitEvent(pend.cs, st.e_out, 0));  // results buffer free (no-op first time)
         mark('w');
-        launch_align_seeded(pend.a, pend.grid, pend.block, pend.cs);
+        launches += launch_align_seeded(pend.a, pend.grid, pend.block, pend.cs) - 1;
         mark('a');
         CUDA_TRY(ctx, cudaGetLastError());
         ++launches;
