@@ -393,3 +393,26 @@ def test_batch_pipeline_fixed_length_ramp_and_packing(pack, monkeypatch):
     al2 = api.Aligner(api.SeedIndex.build(genome2, 20), genome2, cfg2.params)
     want2, _ = O.OracleIndex(packed2, nmask2, g2.size, 20).align_arrays(cfg2.params, b2, o2, threads=8)
     assert O.compare_results(al2.align_arrays(b2, o2), want2) == []
+
+
+@pytest.mark.parametrize("bs,c,dmax,n,hmax", [
+    (32, 2, -1, 10, 300),   # automatic d_max (ceil(12 L / 100))
+    (16, 1, 6, 25, 300),
+    (8, 3, 8, 3, 50),
+    (4, 2, 10, 10, 2),      # tiny h_max: most repeat seeds are popular
+    (1, 2, 5, 10, 300),
+    (7, 2, 8, 10, 300),     # not a power of two: the warp kernel only
+    (64, 2, 10, 10, 300),   # wider than the solo kernel's 32-bit anchor mask
+])
+def test_align_param_sweep(bs, c, dmax, n, hmax):
+    """AlignerParams away from the configs' values (bucket size, confidence,
+    d_max, seeds, h_max) on a repeat-rich genome, in a batch large enough for
+    the solo kernel: bit-exact with the oracle, counters included."""
+    g = synth.make_repeat_genome(9, 3_000_000, 40, min_len=150, max_len=800, min_copies=2, max_copies=12,
+                                 min_div=0.0, max_div=0.06)
+    packed, nmask = synth.pack_genome(g)
+    cfg = synth.CONFIGS["C1"].scaled(genome_len=g.size, n_reads=14_000)
+    bases, offs, _, _ = synth.make_reads(cfg, g)
+    p = api.AlignerParams(seed_size=20, seeds_to_try=n, max_distance=dmax, confidence_threshold=c, max_hits=hmax,
+                          bucket_size=bs)
+    _gpu_vs_oracle(cfg, g, packed, nmask, bases, offs, params=p)

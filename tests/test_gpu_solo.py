@@ -16,7 +16,7 @@ import sys
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SELECT = "align_parity or ragged or force_max or align_golden or overflow_paths or fixed_length"
+SELECT = "align_parity or ragged or force_max or align_golden or overflow_paths or fixed_length or param_sweep"
 
 
 @pytest.mark.gpu
