@@ -856,6 +856,17 @@ constexpr int kSoloCands = 8;
 constexpr int kSoloThreads = 128;
 constexpr int kSoloF = 2 * 15 + 3;  // frontier entries at d_limit <= 15
 
+#ifndef SA_SOLO_PF
+#define SA_SOLO_PF 2  // prefetch a read's records and planes at its start: 1 into L2, 2 into L1 (C1 969 -> 991 M reads/s)
+#endif
+SA_DEV void solo_prefetch(const void* p) {
+#if SA_SOLO_PF == 2
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+#else
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+#endif
+}
+
 struct SoloRead {
     uint32_t lookups = 0, skip_n = 0, skip_pop = 0, hits = 0, dist = 0, dist_after = 0, early_out = 0;
     uint32_t window = 0, cells = 0, multi = 0, prune = 0;
@@ -923,6 +934,13 @@ __global__ void __launch_bounds__(kSoloThreads, SA_SOLO_MIN_BLOCKS) solo_kernel(
             } else if (st == 0) {
                 const uint4* recs = a.pre_recs + static_cast<uint64_t>(r) * a.pre_rstride;
                 const uint4* Rp = a.pre_planes + static_cast<uint64_t>(r) * a.pre_pstride;
+#if SA_SOLO_PF
+                // the seed loop reads the records one by one behind data-dependent
+                // branches, and the LV walks the planes as the wavefront advances:
+                // touch their lines up front so those loads find them close
+                for (int t = 0; t < n_eff && t < 16; t += 2) solo_prefetch(recs + t);  // 2 records per 32 B sector
+                for (int t = 0; t < a.pre_pstride && t < 16; t += 2) solo_prefetch(Rp + t);
+#endif
                 const int d_max = a.dmax_param >= 0 ? a.dmax_param : (12 * len + 99) / 100;
                 const int tier0 = len / a.s;
                 Tracker tr;

@@ -497,6 +497,19 @@ int ensure_scratch(sa_context* ctx, Replica& rep, const LaunchShape& sh) {
     return SA_OK;
 }
 
+// Device-resident batches are run as slices of this many reads (0: one
+// launch sequence for the whole batch).  A slice's seed records and planes
+// (288 B per 100 bp read) then stay in L2 between the seed kernel that writes
+// them and the kernels that read them, and the next slice overwrites the same
+// lines instead of leaving them to be written back.  SA_DEV_CHUNK overrides.
+uint64_t dev_chunk_reads() {
+    static const uint64_t v = [] {
+        const char* e = getenv("SA_DEV_CHUNK");
+        return e ? static_cast<uint64_t>(atoll(e)) : uint64_t{0};
+    }();
+    return v;
+}
+
 // Enqueue fast + slow kernels for reads already on the device.
 int enqueue_align(sa_context* ctx, Replica& rep, Stage& stg, const LaunchShape& sh,
                   const char* d_bases, const uint64_t* d_offsets, uint64_t base_off,
@@ -528,7 +541,20 @@ int enqueue_align(sa_context* ctx, Replica& rep, Stage& stg, const LaunchShape& 
         a.pre_list_count = stg.pre_list + (stg.pre_list_cap - 1);
         a.pre_pstride = pre_pstride(a);
         a.pre_rstride = pre_rstride(a);
-        launches += launch_align_pre(a, sh.fast_grid, sh.fast_block, stg.st) - 1;
+        const uint64_t ch = dev_chunk_reads();
+        if (ch == 0 || n_reads <= ch) {
+            launches += launch_align_pre(a, sh.fast_grid, sh.fast_block, stg.st) - 1;
+        } else {  // L2-sized slices reusing one set of seed records (see dev_chunk_reads)
+            for (uint64_t r0 = 0; r0 < n_reads; r0 += ch) {
+                AlignLaunch c = a;
+                c.n_reads = static_cast<uint32_t>(std::min(ch, n_reads - r0));
+                c.offsets = d_offsets + r0;
+                c.results = d_results + r0;
+                c.read_base = read_base + r0;
+                launches += launch_align_pre(c, sh.fast_grid, sh.fast_block, stg.st);
+            }
+            launches -= 1;
+        }
     } else {
         launch_align_fast(a, sh.fast_grid, sh.fast_block, stg.st);
     }
@@ -1569,7 +1595,8 @@ int sa_align_device(sa_context* ctx, const sa_params* params, const char* d_base
     if (int rc = ensure_scratch(ctx, rep, sh)) return rc;
     Stage& stg = rep.stage[kPipeStages];
     if (int rc = ensure_stage(ctx, stg, 0, n_reads)) return rc;
-    if (int rc = ensure_pre(ctx, stg, n_reads, sh)) return rc;
+    const uint64_t pre_n = dev_chunk_reads() ? std::min(n_reads, dev_chunk_reads()) : n_reads;
+    if (int rc = ensure_pre(ctx, stg, pre_n, sh)) return rc;
     // the caller's stream drives; this stage keeps only control words
     Stage tmp = stg;
     tmp.st = st;
