@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
@@ -315,8 +316,14 @@ __global__ void items_kernel(JobView j, MergeView m, const unsigned long long* _
     }
 }
 
-// R4: warp per work item: bounded_distance at every position of the item
-template <bool kReg>
+// R4: warp per work item: bounded_distance at every position of the item.
+// kBit (every d_limit <= 15): lane l verifies positions lo + l, lo + l + 32,
+// ... with the banded bit-parallel LV (lv.cuh lv_bitpar) -- the same read and
+// limit for the whole item, so the warp runs in lock step, and a position far
+// from the read costs m + d_limit column steps instead of d_limit + 1 full
+// wavefront iterations.  Otherwise the warp runs the wavefront LV position by
+// position (lanes = diagonals).
+template <bool kReg, bool kBit = false>
 __global__ void verify_kernel(BatchView b, RefView rv, const Item* __restrict__ items, unsigned long long n_items,
                               uint16_t* __restrict__ dist, int f_ints) {
     extern __shared__ int smem_f[];
@@ -331,6 +338,20 @@ __global__ void verify_kernel(BatchView b, RefView rv, const Item* __restrict__ 
         const int dl = b.dl[r];
         const uint4* R = job_planes(b, it.job);
         uint32_t cells = 0;
+        if (kBit) {
+            for (uint32_t p0 = it.lo; p0 <= it.hi; p0 += 32) {
+                const uint32_t p = p0 + lane;
+                if (p <= it.hi) {
+                    const uint64_t rem = rv.glen - p;  // REF eval.cpp:223-225
+                    const uint64_t want = static_cast<uint64_t>(L) + static_cast<uint64_t>(dl);
+                    const int wlen = static_cast<int>(want < rem ? want : rem);
+                    const int d = lv_bitpar(R, static_cast<int>(b.blocks_per_read), L, rv.planes, p, wlen, dl, cells);
+                    dist[it.cand + (p - it.lo)] = d < 0 ? kNoDist : static_cast<uint16_t>(d);
+                }
+                if (p0 + 32 < p0) break;  // 32-bit wrap guard
+            }
+            continue;
+        }
         for (uint32_t p = it.lo;; ++p) {
             // REF eval.cpp:223-225: window = substring(p, L + d_limit)
             const uint64_t rem = rv.glen - p;
@@ -689,6 +710,8 @@ int run_batch(sa_referee& rf, const char* bases, const uint64_t* offs, uint32_t 
             RF_TRY(cudaFuncSetAttribute(verify_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
             verify_kernel<false><<<g, 32 * warps, smem, st>>>(bv, rv, items, tot[1], dist, f_ints);
+        } else if (getenv("SA_REF_WAVEFRONT") == nullptr) {  // A/B switch: the wavefront LV
+            verify_kernel<true, true><<<g, 32 * warps, 0, st>>>(bv, rv, items, tot[1], dist, 0);
         } else {
             verify_kernel<true><<<g, 32 * warps, 0, st>>>(bv, rv, items, tot[1], dist, 0);
         }

@@ -40,3 +40,16 @@ def test_bitparallel_lv_vs_oracle():
                        cwd=ROOT, env={**os.environ, "SA_LV_BITPAR": "1"}, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
+
+
+@pytest.mark.gpu
+def test_referee_wavefront_verify_still_matches():
+    """The referee's verify stage uses lv_bitpar for limits <= 15; the
+    wavefront LV it replaced (SA_REF_WAVEFRONT=1) must still give the
+    reference's hit lists and results."""
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_referee.py"), "-x", "-q",
+                        "-m", "gpu", "-p", "no:cacheprovider"],
+                       cwd=ROOT, env={**os.environ, "SA_REF_WAVEFRONT": "1"}, capture_output=True, text=True,
+                       timeout=1500)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
