@@ -366,6 +366,76 @@ __global__ void verify_kernel(BatchView b, RefView rv, const Item* __restrict__ 
     }
 }
 
+// R5 (warp per job): the same per-bucket minima, 32 candidate positions at a
+// time.  Positions ascend within a job, so a bucket is a contiguous segment;
+// each chunk takes a segmented min-scan of (distance << 32 | position) -- the
+// minimum is the smallest distance, earliest position on ties, as the
+// sequential `d < best` keeps -- merged with the bucket still open from the
+// previous chunk.  Closed buckets with a hit are written in order (ballot
+// prefix); the last segment of a chunk stays open.  Same output as
+// bucket_kernel; the serial pass was 76% of the referee's GPU time.
+__global__ void bucket_warp_kernel(JobView j, MergeView m, const unsigned long long* __restrict__ ikey,
+                                   const uint32_t* __restrict__ ihi, const uint16_t* __restrict__ dist, int bucket,
+                                   unsigned long long* __restrict__ hits, uint32_t* __restrict__ n_hits) {
+    constexpr unsigned kFull = 0xffffffffu;
+    constexpr unsigned long long kNone = ~0ull;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u, le = lt | (1u << lane);
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t job = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; job < j.n_jobs; job += nw) {
+        const unsigned long long b0 = j.int_off[job];
+        unsigned long long c = m.cand_off[job], o = m.hit_off[job];
+        const unsigned long long dir = job & 1;
+        long long open_b = -1;               // bucket of the open segment
+        unsigned long long open_best = kNone;  // its minimum so far
+        uint32_t cnt = 0;
+        auto emit = [&](unsigned long long key, bool mine, unsigned mask) {
+            // key = d << 32 | p  ->  hit = d << 33 | p << 1 | dir
+            const unsigned before = __popc(mask & lt);
+            if (mine) hits[o + before] = ((key >> 32) << 33) | ((key & 0xffffffffull) << 1) | dir;
+            o += __popc(mask);
+            cnt += __popc(mask);
+        };
+        for (uint32_t k = 0; k < m.n_runs[job]; ++k) {
+            const uint32_t lo = static_cast<uint32_t>(ikey[b0 + k]), hi = ihi[b0 + k];
+            for (unsigned long long base = lo; base <= hi; base += 32) {
+                const unsigned long long p = base + lane;
+                const bool valid = p <= hi;
+                const long long bk = valid ? static_cast<long long>(p / static_cast<unsigned long long>(bucket)) : -2;
+                unsigned long long key = kNone;
+                if (valid) {
+                    const uint32_t d = dist[c + (p - base)];
+                    if (d != kNoDist) key = (static_cast<unsigned long long>(d) << 32) | p;
+                }
+                const long long bk_prev = __shfl_up_sync(kFull, bk, 1);
+                const bool head = valid && (lane == 0 ? bk != open_b : bk != bk_prev);
+                const unsigned heads = __ballot_sync(kFull, head);
+                const unsigned vmask = __ballot_sync(kFull, valid);
+                // a chunk that starts a new bucket closes the open one first
+                if ((heads & 1u) && open_b >= 0) emit(open_best, lane == 0 && open_best != kNone,
+                                                       __ballot_sync(kFull, lane == 0 && open_best != kNone));
+                const unsigned hl = heads & le;
+                const int seg = hl ? 31 - __clz(hl) : -1;  // -1: continues the open bucket
+                for (int dd = 1; dd < 32; dd <<= 1) {
+                    const unsigned long long up = __shfl_up_sync(kFull, key, dd);
+                    if (lane - dd >= seg && lane >= dd && up < key) key = up;
+                }
+                if (valid && seg < 0 && open_best < key) key = open_best;
+                // tails: last lane of each segment; the chunk's final segment stays open
+                const int last = 31 - __clz(vmask);
+                const bool tail = valid && lane != last && ((heads >> (lane + 1)) & 1u);
+                const bool out = tail && key != kNone;
+                emit(key, out, __ballot_sync(kFull, out));
+                open_best = __shfl_sync(kFull, key, last);
+                open_b = __shfl_sync(kFull, bk, last);
+                c += static_cast<unsigned long long>(__popc(vmask));
+            }
+        }
+        if (open_b >= 0 && open_best != kNone) emit(open_best, lane == 0, 1u);
+        if (lane == 0) n_hits[job] = cnt;
+    }
+}
+
 // R5: thread per job: per-bucket minima (REF eval.cpp:207-232) -> hit keys
 // (distance << 33 | position << 1 | direction), sorted later per read
 __global__ void bucket_kernel(JobView j, MergeView m, const unsigned long long* __restrict__ ikey,
@@ -723,7 +793,13 @@ int run_batch(sa_referee& rf, const char* bases, const uint64_t* offs, uint32_t 
     RF_TRY(B.alloc(&hits, tot[2]));
     RF_TRY(B.alloc(&n_hits, jv.n_jobs));
     RF_TRY(cudaMemsetAsync(hits, 0xff, std::max<unsigned long long>(tot[2], 1) * 8, st));
-    bucket_kernel<<<grid(jv.n_jobs, 128), 128, 0, st>>>(jv, mv, ikey, ihi, dist, bucket, hits, n_hits);
+    if (getenv("SA_REF_BUCKET_SERIAL") == nullptr) {  // A/B switch: the thread-per-job pass
+        const uint64_t wg = std::min<uint64_t>((jv.n_jobs + 7) / 8, 148ull * 64);
+        bucket_warp_kernel<<<static_cast<int>(std::max<uint64_t>(wg, 1)), 256, 0, st>>>(jv, mv, ikey, ihi, dist, bucket,
+                                                                                       hits, n_hits);
+    } else {
+        bucket_kernel<<<grid(jv.n_jobs, 128), 128, 0, st>>>(jv, mv, ikey, ihi, dist, bucket, hits, n_hits);
+    }
     RF_TRY(cudaGetLastError());
     // read segment offsets = job hit offsets of even jobs (+ the total)
     std::vector<unsigned long long> job_off(jv.n_jobs + 1);
