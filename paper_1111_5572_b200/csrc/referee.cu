@@ -299,6 +299,126 @@ struct Item {
     unsigned long long cand;  // output index of position lo
 };
 
+// R3 (warp per job): the same merge, 32 intervals at a time.  Interval i
+// opens a run iff its lo is past every earlier hi + 1 (a prefix max carried
+// across chunks); a run's hi is the max over its intervals (segmented max).
+// Closed runs are written in place at indices no later than the intervals
+// they came from, all of which the warp has already loaded.
+__global__ void merge_warp_kernel(JobView j, MergeView m, unsigned long long* __restrict__ ikey,
+                                  uint32_t* __restrict__ ihi, int bucket) {
+    constexpr unsigned kFull = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u, le = lt | (1u << lane);
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t job = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; job < j.n_jobs; job += nw) {
+        const unsigned long long b0 = j.int_off[job], n = j.n_int[job];
+        const unsigned long long jkey = n ? (ikey[b0] & 0xffffffff00000000ull) : 0;
+        uint32_t runs = 0;
+        unsigned long long cand = 0, items = 0, hitcap = 0;
+        bool open = false;                 // a run is open (carried)
+        long long cmax = -2;               // max hi of every interval so far
+        uint32_t clo = 0, chi = 0;         // the open run
+        auto close_run = [&](uint32_t lo, uint32_t hi, bool mine, unsigned mask) {
+            const unsigned before = __popc(mask & lt);
+            if (mine) {
+                ikey[b0 + runs + before] = jkey | lo;
+                ihi[b0 + runs + before] = hi;
+            }
+            runs += __popc(mask);
+            unsigned long long cl = 0, it = 0, hc = 0;
+            if (mine) {
+                cl = static_cast<unsigned long long>(hi) - lo + 1;
+                it = (cl + kSpan - 1) / kSpan;
+                hc = hi / static_cast<uint32_t>(bucket) - lo / static_cast<uint32_t>(bucket) + 1;
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                cl += __shfl_xor_sync(kFull, cl, o);
+                it += __shfl_xor_sync(kFull, it, o);
+                hc += __shfl_xor_sync(kFull, hc, o);
+            }
+            cand += cl;
+            items += it;
+            hitcap += hc;
+        };
+        for (unsigned long long base = 0; base < n; base += 32) {
+            const unsigned long long i = base + lane;
+            uint32_t lo = 0, hi = 0;
+            bool valid = false;
+            if (i < n) {
+                lo = static_cast<uint32_t>(ikey[b0 + i]);
+                hi = ihi[b0 + i];
+                valid = hi >= lo;  // empty ranges are skipped
+            }
+            __syncwarp();  // every lane has read its interval before any run is written back
+            // exclusive prefix max of hi over earlier valid lanes, with the carry
+            long long pm = valid ? static_cast<long long>(hi) : -2;
+            for (int dd = 1; dd < 32; dd <<= 1) {
+                const long long up = __shfl_up_sync(kFull, pm, dd);
+                if (lane >= dd && up > pm) pm = up;
+            }
+            long long excl = __shfl_up_sync(kFull, pm, 1);
+            if (lane == 0) excl = -2;
+            if (cmax > excl) excl = cmax;
+            const unsigned vmask = __ballot_sync(kFull, valid);
+            const bool any_before = open || (vmask & lt) != 0u;
+            const bool start = valid && (!any_before || static_cast<long long>(lo) > excl + 1);
+            const unsigned starts = __ballot_sync(kFull, start);
+            // the open run closes where this chunk starts a new one
+            if (open && starts != 0u) {
+                // its hi grows with the valid intervals before the first start
+                const unsigned pre = vmask & ((starts & (0u - starts)) - 1u);
+                long long h = (pre >> lane) & 1u ? static_cast<long long>(hi) : -1;
+                for (int o = 16; o > 0; o >>= 1) {
+                    const long long x = __shfl_xor_sync(kFull, h, o);
+                    if (x > h) h = x;
+                }
+                if (h > static_cast<long long>(chi)) chi = static_cast<uint32_t>(h);
+                close_run(clo, chi, lane == 0, 1u);
+                open = false;
+            }
+            // runs started in this chunk: segmented max of hi from each start
+            const unsigned sl = starts & le;
+            const int seg = sl ? 31 - __clz(sl) : -1;
+            long long rh = (valid && seg >= 0) ? static_cast<long long>(hi) : -1;
+            for (int dd = 1; dd < 32; dd <<= 1) {
+                const long long up = __shfl_up_sync(kFull, rh, dd);
+                if (lane >= dd && lane - dd >= seg && seg >= 0 && up > rh) rh = up;
+            }
+            // a run ends at the last valid lane before the next start; the chunk's last run stays open
+            const int last_start = starts ? 31 - __clz(starts) : -1;
+            const unsigned after = (lane < 31) ? (starts >> (lane + 1)) : 0u;
+            const unsigned next_start_rel = after & (0u - after);  // lowest later start (relative)
+            const int nxt = next_start_rel ? lane + 1 + __ffs(next_start_rel) - 1 : 32;
+            // the lane just before the next start closes its run (valid lanes only carry hi)
+            const bool closes = seg >= 0 && seg != last_start && nxt < 32 && lane == nxt - 1;
+            const uint32_t run_lo = __shfl_sync(kFull, lo, seg < 0 ? 0 : seg);
+            close_run(run_lo, static_cast<uint32_t>(rh), closes, __ballot_sync(kFull, closes));
+            if (last_start >= 0) {  // the last run of the chunk stays open
+                const long long h_last = __shfl_sync(kFull, rh, 31);
+                clo = __shfl_sync(kFull, lo, last_start);
+                chi = static_cast<uint32_t>(h_last);
+                open = true;
+            } else if (open) {  // no start: every valid interval extends the open run
+                long long h = valid ? static_cast<long long>(hi) : -1;
+                for (int o = 16; o > 0; o >>= 1) {
+                    const long long x = __shfl_xor_sync(kFull, h, o);
+                    if (x > h) h = x;
+                }
+                if (h > static_cast<long long>(chi)) chi = static_cast<uint32_t>(h);
+            }
+            const long long cm = __shfl_sync(kFull, pm, 31);
+            if (cm > cmax) cmax = cm;
+        }
+        if (open) close_run(clo, chi, lane == 0, 1u);
+        if (lane == 0) {
+            m.n_runs[job] = runs;
+            m.n_cand[job] = cand;
+            m.n_items[job] = items;
+            m.n_hitcap[job] = hitcap;
+        }
+    }
+}
+
 // R3b: thread per job: verify work items of <= kSpan positions
 __global__ void items_kernel(JobView j, MergeView m, const unsigned long long* __restrict__ ikey,
                              const uint32_t* __restrict__ ihi, Item* __restrict__ items) {
@@ -312,6 +432,47 @@ __global__ void items_kernel(JobView j, MergeView m, const unsigned long long* _
                 items[it++] = Item{job, static_cast<uint32_t>(p), static_cast<uint32_t>(e), 0, c};
                 c += e - p + 1;
             }
+        }
+    }
+}
+
+// R3b (warp per job): the same work items, a lane per run: item and
+// candidate offsets by warp prefix sums over 32 runs at a time.
+__global__ void items_warp_kernel(JobView j, MergeView m, const unsigned long long* __restrict__ ikey,
+                                  const uint32_t* __restrict__ ihi, Item* __restrict__ items) {
+    constexpr unsigned kFull = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t job = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; job < j.n_jobs; job += nw) {
+        unsigned long long it = m.item_off[job], c = m.cand_off[job];
+        const unsigned long long b0 = j.int_off[job];
+        const uint32_t nr = m.n_runs[job];
+        for (uint32_t k0 = 0; k0 < nr; k0 += 32) {
+            const uint32_t k = k0 + lane;
+            uint32_t lo = 0, hi = 0;
+            unsigned long long len = 0, nit = 0;
+            if (k < nr) {
+                lo = static_cast<uint32_t>(ikey[b0 + k]);
+                hi = ihi[b0 + k];
+                len = static_cast<unsigned long long>(hi) - lo + 1;
+                nit = (len + kSpan - 1) / kSpan;
+            }
+            unsigned long long si = nit, sc = len;  // inclusive prefix sums
+            for (int dd = 1; dd < 32; dd <<= 1) {
+                const unsigned long long ui = __shfl_up_sync(kFull, si, dd), uc = __shfl_up_sync(kFull, sc, dd);
+                if (lane >= dd) {
+                    si += ui;
+                    sc += uc;
+                }
+            }
+            unsigned long long my_it = it + si - nit, my_c = c + sc - len;
+            for (unsigned long long p = lo; k < nr && p <= hi; p += kSpan) {
+                const unsigned long long e = p + kSpan - 1 < hi ? p + kSpan - 1 : hi;
+                items[my_it++] = Item{job, static_cast<uint32_t>(p), static_cast<uint32_t>(e), 0, my_c};
+                my_c += e - p + 1;
+            }
+            it += __shfl_sync(kFull, si, 31);
+            c += __shfl_sync(kFull, sc, 31);
         }
     }
 }
@@ -750,7 +911,12 @@ int run_batch(sa_referee& rf, const char* bases, const uint64_t* offs, uint32_t 
     RF_TRY(B.alloc(&mv.item_off, jv.n_jobs + 1));
     RF_TRY(B.alloc(&mv.hit_off, jv.n_jobs + 1));
     RF_TRY(B.alloc(&mv.n_runs, jv.n_jobs));
-    merge_kernel<<<grid(jv.n_jobs, 128), 128, 0, st>>>(jv, mv, ikey, ihi, bucket);
+    if (getenv("SA_REF_MERGE_SERIAL") == nullptr) {  // A/B switch: the thread-per-job pass
+        const uint64_t wg = std::min<uint64_t>((jv.n_jobs + 7) / 8, 148ull * 64);
+        merge_warp_kernel<<<static_cast<int>(std::max<uint64_t>(wg, 1)), 256, 0, st>>>(jv, mv, ikey, ihi, bucket);
+    } else {
+        merge_kernel<<<grid(jv.n_jobs, 128), 128, 0, st>>>(jv, mv, ikey, ihi, bucket);
+    }
     RF_TRY(cudaGetLastError());
     RF_TRY(cudaMemsetAsync(mv.n_cand + jv.n_jobs, 0, sizeof(unsigned long long), st));
     RF_TRY(cudaMemsetAsync(mv.n_items + jv.n_jobs, 0, sizeof(unsigned long long), st));
@@ -767,7 +933,12 @@ int run_batch(sa_referee& rf, const char* bases, const uint64_t* offs, uint32_t 
     uint16_t* dist = nullptr;
     RF_TRY(B.alloc(&items, tot[1]));
     RF_TRY(B.alloc(&dist, tot[0]));
-    items_kernel<<<grid(jv.n_jobs, 128), 128, 0, st>>>(jv, mv, ikey, ihi, items);
+    if (getenv("SA_REF_MERGE_SERIAL") == nullptr) {  // (same A/B switch as the merge)
+        const uint64_t wg = std::min<uint64_t>((jv.n_jobs + 7) / 8, 148ull * 64);
+        items_warp_kernel<<<static_cast<int>(std::max<uint64_t>(wg, 1)), 256, 0, st>>>(jv, mv, ikey, ihi, items);
+    } else {
+        items_kernel<<<grid(jv.n_jobs, 128), 128, 0, st>>>(jv, mv, ikey, ihi, items);
+    }
     RF_TRY(cudaGetLastError());
     if (tot[1]) {
         const int f_ints = dlmax > 15 ? 2 * (2 * dlmax + 3) : 0;

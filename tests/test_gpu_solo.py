@@ -49,7 +49,7 @@ def test_referee_wavefront_verify_still_matches():
     reference's hit lists and results."""
     r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_referee.py"), "-x", "-q",
                         "-m", "gpu", "-p", "no:cacheprovider"],
-                       cwd=ROOT, env={**os.environ, "SA_REF_WAVEFRONT": "1", "SA_REF_BUCKET_SERIAL": "1"}, capture_output=True, text=True,
+                       cwd=ROOT, env={**os.environ, "SA_REF_WAVEFRONT": "1", "SA_REF_BUCKET_SERIAL": "1", "SA_REF_MERGE_SERIAL": "1"}, capture_output=True, text=True,
                        timeout=1500)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
