@@ -18,9 +18,10 @@
 //   R0 decode      warp/read: forward + reverse-complement read planes
 //   R1 count       thread/job: pieces, table, number of candidate intervals
 //   R2 intervals   warp/job: (job, lo) keys + hi, CUB radix sort
-//   R3 merge       thread/job: disjoint candidate runs, work items of <= 256
-//   R4 verify      warp/work item: LV of the read at every position (lv.cuh)
-//   R5 buckets     thread/job: per-bucket minima -> hit keys (dist, pos, dir)
+//   R3 merge       warp/job: disjoint candidate runs, work items of <= 256
+//   R4 verify      warp/work item: LV of the read at every position (lv.cuh),
+//                  a lane per position (bit-parallel LV) when d_limit <= 15
+//   R5 buckets     warp/job: per-bucket minima -> hit keys (dist, pos, dir)
 //   R6 sort        CUB segmented sort of each read's hits
 //   R7 classify    thread/read: stage decision, BestTracker, classification
 #include <cuda_runtime.h>
