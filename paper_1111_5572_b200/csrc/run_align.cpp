@@ -161,22 +161,31 @@ void parse_chunk(int fd, uint64_t start, uint64_t end, Reads& out) {
         const uint64_t record_start = offset;
         if (!get_line(name_line)) return;
         if (name_line.empty() && r.at_eof()) return;
-        const std::string at = std::to_string(record_start);
+        auto at = [&] { return std::to_string(record_start); };  // error messages only
         if (name_line.empty() || name_line[0] != '@')
-            throw Error{SA_EPARSE, "FASTQ record at byte " + at + " does not start with '@'"};
+            throw Error{SA_EPARSE, "FASTQ record at byte " + at() + " does not start with '@'"};
         size_t nend = name_line.find_first_of(" \t");
         if (nend == std::string::npos) nend = name_line.size();
-        if (nend <= 1) throw Error{SA_EPARSE, "FASTQ record at byte " + at + " has an empty name"};
+        if (nend <= 1) throw Error{SA_EPARSE, "FASTQ record at byte " + at() + " has an empty name"};
         if (!get_line(bases) || !get_line(plus) || !get_line(quals))
-            throw Error{SA_EPARSE, "truncated FASTQ record at byte " + at};
+            throw Error{SA_EPARSE, "truncated FASTQ record at byte " + at()};
         if (plus.empty() || plus[0] != '+')
-            throw Error{SA_EPARSE, "FASTQ record at byte " + at + " lacks its '+' separator"};
+            throw Error{SA_EPARSE, "FASTQ record at byte " + at() + " lacks its '+' separator"};
         if (bases.size() != quals.size())
-            throw Error{SA_EPARSE, "FASTQ record at byte " + at + ": base and quality lengths differ"};
+            throw Error{SA_EPARSE, "FASTQ record at byte " + at() + ": base and quality lengths differ"};
+        static const struct Norm {  // char_to_code as a table: 'A'..'N' or 0 (illegal)
+            char v[256];
+            Norm() {
+                for (int c = 0; c < 256; ++c) {
+                    const int code = sab::char_to_code(static_cast<char>(c));
+                    v[c] = code < 0 ? 0 : "ACGTN"[code];
+                }
+            }
+        } norm;
         for (char& ch : bases) {  // uppercase, IUPAC -> N (REF fastq.cpp:52-60)
-            const int code = sab::char_to_code(ch);
-            if (code < 0) throw Error{SA_EPARSE, "FASTQ record at byte " + at + ": illegal base character"};
-            ch = "ACGTN"[code];
+            const char n = norm.v[static_cast<unsigned char>(ch)];
+            if (n == 0) throw Error{SA_EPARSE, "FASTQ record at byte " + at() + ": illegal base character"};
+            ch = n;
         }
         out.names.insert(out.names.end(), name_line.begin() + 1, name_line.begin() + static_cast<long>(nend));
         out.name_off.push_back(out.names.size());
@@ -291,7 +300,10 @@ void format_record(std::string& line, const sa_genome& g, const sa_result& res, 
     if (bases.empty()) {
         line += '*';
     } else if (rc) {
-        for (size_t i = bases.size(); i-- > 0;) line += complement(bases[i]);
+        const size_t o = line.size(), n = bases.size();
+        line.resize(o + n);
+        char* d = &line[o];
+        for (size_t i = 0; i < n; ++i) d[i] = complement(bases[n - 1 - i]);
     } else {
         line.append(bases);
     }
@@ -299,7 +311,10 @@ void format_record(std::string& line, const sa_genome& g, const sa_result& res, 
     if (quals.empty()) {
         line += '*';
     } else if (rc) {
-        for (size_t i = quals.size(); i-- > 0;) line += quals[i];
+        const size_t o = line.size(), n = quals.size();
+        line.resize(o + n);
+        char* d = &line[o];
+        for (size_t i = 0; i < n; ++i) d[i] = quals[n - 1 - i];
     } else {
         line.append(quals);
     }
