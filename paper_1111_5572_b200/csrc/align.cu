@@ -852,7 +852,10 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
 // result is the same whichever kernel finishes a read.  The steps below are
 // align_one's (same d_limit rule, candidate order, LV steps, tracker, exits,
 // classification and counters), written sequentially.
-constexpr int kSoloCands = 8;
+#ifndef SA_SOLO_CANDS
+#define SA_SOLO_CANDS 8
+#endif
+constexpr int kSoloCands = SA_SOLO_CANDS;
 constexpr int kSoloThreads = 128;
 constexpr int kSoloF = 2 * 15 + 3;  // frontier entries at d_limit <= 15
 
