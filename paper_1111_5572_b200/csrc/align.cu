@@ -1950,8 +1950,12 @@ int launch_align_seeded(const AlignLaunch& a, int grid, int block, cudaStream_t 
     AlignLaunch b = a;
     int n = 1;
     if (solo_eligible(a)) {
+        static const uint64_t cap = [] {  // blocks (grid-stride beyond); SA_SOLO_GRID overrides
+            const char* e = getenv("SA_SOLO_GRID");
+            return e ? static_cast<uint64_t>(atoll(e)) : 148ull * SA_SOLO_MIN_BLOCKS;  // one resident wave (C1 992 -> 1018 M)
+        }();
         const uint64_t g = std::min<uint64_t>((static_cast<uint64_t>(a.n_reads) + kSoloThreads - 1) / kSoloThreads,
-                                              148ull * 16);
+                                              std::max<uint64_t>(cap, 1));
         solo_kernel<<<static_cast<int>(std::max<uint64_t>(g, 1)), kSoloThreads, 0, st>>>(a);
         ++n;
         static const bool dbg = getenv("SA_DEBUG_SOLO") != nullptr;  // diagnostics: reads left to the warp kernel
