@@ -1923,7 +1923,11 @@ void launch_seed(const AlignLaunch& a, cudaStream_t st) {
     auto go = [&](auto kernel, int G) {
         const uint64_t groups_per_block = 256 / G;
         uint64_t g = (static_cast<uint64_t>(a.n_reads) + groups_per_block - 1) / groups_per_block;
-        g = std::max<uint64_t>(1, std::min<uint64_t>(g, 148ull * 32));
+        static const uint64_t cap = [] {  // SA_SEED_GRID overrides (tuning)
+            const char* e = getenv("SA_SEED_GRID");
+            return e ? static_cast<uint64_t>(atoll(e)) : uint64_t{1} << 24;  // a group per read (C1 1018 -> 1025 M over 148 x 32)
+        }();
+        g = std::max<uint64_t>(1, std::min<uint64_t>(g, std::max<uint64_t>(cap, 1)));
         kernel<<<static_cast<int>(g), 256, 0, st>>>(a);
     };
     if (nbmax <= 4) go(seed_kernel<4>, 4);
