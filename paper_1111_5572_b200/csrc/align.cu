@@ -856,7 +856,10 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
 #define SA_SOLO_CANDS 8
 #endif
 constexpr int kSoloCands = SA_SOLO_CANDS;
-constexpr int kSoloThreads = 128;
+#ifndef SA_SOLO_THREADS
+#define SA_SOLO_THREADS 128
+#endif
+constexpr int kSoloThreads = SA_SOLO_THREADS;
 constexpr int kSoloF = 2 * 15 + 3;  // frontier entries at d_limit <= 15
 
 #ifndef SA_SOLO_PF
