@@ -1,20 +1,27 @@
 #!/usr/bin/env python
-"""Benchmark: reads aligned/s on BASELINE.json config C1 (configs[1]: 100 Mbp
-i.i.d. genome, 1,000,000 x 100 bp reads per GPU, 1.5% substitutions + 0.1%
-geometric indels; s=20, n=10, h_max=300, d_max=10, c=2).
+"""Benchmark: reads aligned/s on BASELINE.json config C2 (configs[2]: the
+3.1 Gbp synthetic repeat genome -- 50% i.i.d. background plus 10,000 planted
+repeat families -- with 10,000,000 x 125 bp reads per GPU, 1% substitutions +
+0.05% geometric indels; s=20, n=12, h_max=300, d_max=12, c=2).  C2 is the
+largest BASELINE config that fits one GPU (the metric names no config); C1
+(`--config C1`) and the others are secondary lines.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C2]
   torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU)
 
 One step = one pass of the aligner hot path over the rank's batch of reads.
 `value`: reads already resident in HBM (sa_align_device), CUDA events on the
 launching stream, L2 flushed (256 MiB write) before every timed step, max over
 ranks.  `e2e`: the same batch through the public C-ABI call sa_align_batch from
-pinned host buffers (H2D reads+offsets, kernels, D2H results inside the
-CUDA-event-timed region).  Weak scaling: each rank aligns its own 1M reads
-against its own index replica; no collective on the data path.
+pinned host buffers (H2D reads, kernels, D2H results inside the timed region);
+`e2e.pageable` repeats it from ordinary (pageable) host memory, which the
+library stages through its own pinned buffers.  Weak scaling: each rank aligns
+its own reads against its own index replica; no collective on the data path.
 `--impl reference`: the reference's own CPU Aligner (oracle/_ref, compiled from
-/root/reference) on all host cores, rank 0 only.
+/root/reference) on all host cores over the SAME reads as rank 0 of our arm,
+rank 0 only.  At 3.1 Gbp its SeedIndex is loaded (through the reference's
+load_index_file) from a CSR restricted to the keys those reads probe: its
+single-threaded full build needs ~115 GB and minutes.
 """
 from __future__ import annotations
 
@@ -112,11 +119,19 @@ def _env_rank():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
+def _genome_label(cfg) -> str:
+    if cfg.repeats:
+        return (f"{cfg.genome_len / 1e9:.1f} Gbp synthetic repeat genome (seed {cfg.genome_seed}: 50% i.i.d. "
+                f"background + 10,000 repeat families of 300 bp-6 kbp, 10-1,000 copies scaled to cover 50%, "
+                f"2-15% divergence)")
+    return f"{cfg.genome_len // 1_000_000} Mbp i.i.d. genome (seed {cfg.genome_seed})"
+
+
 def _workload(cfg, reads_per_gpu: int) -> dict:
     p = cfg.params
-    return {"workload": f"{cfg.name}: {cfg.genome_len // 1_000_000} Mbp i.i.d. genome (seed {cfg.genome_seed}), "
-                        f"{reads_per_gpu} x {cfg.read_len} bp reads per GPU, {cfg.sub_rate:.3%} subs + "
-                        f"{cfg.indel_rate:.2%} indels (geometric p={cfg.geom_p}, max {cfg.max_indel})",
+    return {"workload": f"{cfg.name}: {_genome_label(cfg)}, {reads_per_gpu} x {cfg.read_len} bp reads per GPU, "
+                        f"{cfg.sub_rate:.3%} subs + {cfg.indel_rate:.2%} indels (geometric p={cfg.geom_p}, "
+                        f"max {cfg.max_indel})",
             "reads_per_gpu": reads_per_gpu, "read_len": cfg.read_len, "genome_bp": cfg.genome_len,
             "params": {"seed_size": p.seed_size, "seeds_to_try": p.seeds_to_try, "max_hits": p.max_hits,
                        "max_distance": p.max_distance, "confidence_threshold": p.confidence_threshold,
@@ -126,6 +141,8 @@ def _workload(cfg, reads_per_gpu: int) -> dict:
 
 
 def run_reference(args) -> None:
+    """The reference arm: the reference's Aligner over exactly rank 0's reads,
+    every step the whole batch (same config as our arm)."""
     rank, world, _ = _env_rank()
     if rank != 0:
         return
@@ -133,16 +150,16 @@ def run_reference(args) -> None:
     from paper_1111_5572_b200 import synth
 
     cfg = synth.CONFIGS[args.config]
-    g = synth.make_genome(cfg)
-    packed, nmask = synth.pack_genome(g)
-    n = args.reads_per_gpu or cfg.n_reads
-    sample = min(n, args.ref_sample or CPU_SAMPLE.get(cfg.name, 10_000))
-    bases, offs, _, _ = synth.make_reads(cfg, g, n_reads=sample, seed=cfg.read_seed)
-    cores = os.cpu_count() or 1
     if not O.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libseedaln_ref.so not built"}))
         return
+    g = synth.make_genome(cfg)
+    packed, nmask = synth.pack_genome(g)
+    n = args.reads_per_gpu or cfg.n_reads
+    bases, offs, _, _ = synth.make_reads(cfg, g, n_reads=n, seed=cfg.read_seed)  # rank 0's reads in our arm
+    cores = os.cpu_count() or 1
     ri, kind, build_s, note = _cpu_index(O, cfg, g, packed, nmask, bases, offs, cores)
+    del g
     times = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
@@ -150,17 +167,32 @@ def run_reference(args) -> None:
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             times.append(dt)
-    v = sample / statistics.mean(times)
+    v = n / statistics.mean(times)
+    t1 = _t1(ri, cfg, bases, offs)
     line = {"impl": "reference", "metric": _baseline_metric(), "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.mean(times),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-            "data": "synthetic", "config": _workload(cfg, sample),
+            "data": "synthetic", "config": _workload(cfg, n),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
-                             "sample": f"{sample} reads of {cfg.name} per step, reference Aligner (oracle/_ref, "
-                                       f"-O2) one per thread, atomic cursor grain 64; index build {build_s:.1f}s "
-                                       f"excluded{note}"},
+                             "sample": f"all {n} reads of {cfg.name} (the same reads as rank 0 of our arm) per step, "
+                                       f"reference Aligner (oracle/_ref, -O2) one per thread, atomic cursor grain 64; "
+                                       f"index setup {build_s:.1f}s excluded{note}",
+                             "t1": t1},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def _t1(ix, cfg, bases, offs) -> dict:
+    """The same aligner on ONE host thread, on a bounded prefix of the reads."""
+    n1 = min(CPU_SAMPLE_T1.get(cfg.name, 10_000), offs.size - 1)
+    sb, so = bases[:int(offs[n1])], offs[:n1 + 1]
+    best = None
+    for _ in range(2):
+        t0 = time.perf_counter()
+        ix.align_arrays(cfg.params, sb, so, threads=1)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return {"value": n1 / best, "unit": UNIT, "cores": 1, "sample": f"first {n1} reads, 1 thread, best of 2"}
 
 
 def run_ours(args) -> None:
@@ -323,24 +355,34 @@ def run_ours(args) -> None:
         torch.distributed.destroy_process_group()
 
 
-# Default CPU sample per config: about 10-30 s of single-core work.
-CPU_SAMPLE = {"C0": 10_000, "C1": 400_000, "C2": 400_000, "C3": 20_000, "C4": 1_000}
-# Above this the reference's full CSR (4 B per genome position plus keys, built
-# single-threaded) does not fit a bounded baseline run; the oracle port with an
-# index restricted to the keys the sample probes stands in.
+# Default CPU sample per config for our arm's cpu_baseline (about 10-30 s of
+# host CPU work at T = nproc), and for the T = 1 line beside it.
+CPU_SAMPLE = {"C0": 10_000, "C1": 1_000_000, "C2": 1_000_000, "C3": 50_000, "C4": 2_000}
+CPU_SAMPLE_T1 = {"C0": 10_000, "C1": 100_000, "C2": 100_000, "C3": 5_000, "C4": 100}
+# Above this the reference's full CSR (8 B per genome position plus keys, built
+# single-threaded: ~115 GB peak and minutes at 3.1 Gbp) does not fit a bounded
+# baseline run; its SeedIndex is then loaded from a CSR restricted to the keys
+# the timed reads probe (RefIndex.from_restricted).
 FULL_CSR_MAX_BP = 1_000_000_000
 
 
-def _cpu_index(O, cfg, g, packed, nmask, sb, so, cores):
+def _cpu_index(O, cfg, g, packed, nmask, sb, so, cores, reference_only=False):
     t0 = time.perf_counter()
-    if O.ref_available() and g.size <= FULL_CSR_MAX_BP:
-        ix, kind, note = O.RefIndex(packed, nmask, g.size, cfg.params.seed_size), "reference", ""
-    elif g.size <= FULL_CSR_MAX_BP:
-        ix, kind, note = O.OracleIndex(packed, nmask, g.size, cfg.params.seed_size), "port", ""
+    if g.size <= FULL_CSR_MAX_BP:
+        if O.ref_available():
+            ix, kind, note = O.RefIndex(packed, nmask, g.size, cfg.params.seed_size), "reference", ""
+        else:
+            ix, kind, note = O.OracleIndex(packed, nmask, g.size, cfg.params.seed_size), "port", ""
     else:
-        ix = O.OracleIndex(packed, nmask, g.size, cfg.params.seed_size,
+        oi = O.OracleIndex(packed, nmask, g.size, cfg.params.seed_size,
                            for_reads=(cfg.params.seeds_to_try, sb, so), threads=cores)
-        kind, note = "port", "; oracle port (plain C) on a CSR restricted to the keys the sample probes"
+        if O.ref_available():
+            ix, kind = O.RefIndex.from_restricted(oi), "reference"
+            del oi
+            note = ("; the reference's SeedIndex loaded through its own load_index_file from a CSR restricted to "
+                    "the keys these reads probe (same lookups as its full build for these reads)")
+        else:
+            ix, kind, note = oi, "port", "; oracle port (plain C) on a CSR restricted to the keys these reads probe"
     return ix, kind, time.perf_counter() - t0, note
 
 
@@ -361,8 +403,8 @@ def cpu_baseline(cfg, g, packed, nmask, bases, offs, res_dev, args) -> dict:
     mism = len(O.compare_results(res, res_dev[:sample]))
     return {"value": sample / best, "unit": UNIT, "cores": cores, "kind": kind,
             "sample": f"first {sample} reads of the GPU batch, {cores} threads (one reference Aligner per "
-                      f"thread, atomic cursor grain 64), best of 2; index build {build_s:.1f}s excluded{note}",
-            "parity_mismatches_vs_gpu": mism}
+                      f"thread, atomic cursor grain 64), best of 2; index setup {build_s:.1f}s excluded{note}",
+            "parity_mismatches_vs_gpu": mism, "t1": _t1(ix, cfg, sb, so)}
 
 
 def main():
@@ -371,10 +413,9 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="C1")
+    ap.add_argument("--config", default="C2")
     ap.add_argument("--reads-per-gpu", type=int, default=0)
     ap.add_argument("--cpu-sample", type=int, default=0, help="0: CPU_SAMPLE[config]")
-    ap.add_argument("--ref-sample", type=int, default=0, help="0: CPU_SAMPLE[config]")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

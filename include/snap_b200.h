@@ -140,7 +140,10 @@ int sa_align_batch(sa_context* ctx, const sa_params* params, const char* bases,
  * legacy default).  max_read_length bounds every read's length (it sizes the
  * per-warp shared-memory layout).  Asynchronous: returns after enqueueing.
  * d_stats (device, nullable) is accumulated into, not overwritten.  Errors
- * found by the kernels (invalid characters) are reported by the next sa_sync(). */
+ * found by the kernels (invalid characters) are reported by the next sa_sync().
+ * Calls on one context share its device scratch: a call enqueued on a stream
+ * other than the previous call's waits (on the device) for that call's work,
+ * so concurrent calls are correct but do not overlap. */
 int sa_align_device(sa_context* ctx, const sa_params* params, const char* d_bases,
                     const uint64_t* d_offsets, uint64_t n_reads, uint64_t max_read_length,
                     sa_result* d_results, sa_stats* d_stats, void* stream);

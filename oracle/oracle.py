@@ -120,6 +120,9 @@ def rlib():
         lib.ref_last_error.restype = C.c_char_p
         lib.ref_create.argtypes = [P64, C.c_uint64, P64, C.c_uint64, C.c_uint64, C.c_int]
         lib.ref_create.restype = C.c_void_p
+        lib.ref_create_from_csr.argtypes = [P64, C.c_uint64, P64, C.c_uint64, C.c_uint64, C.c_int, C.c_void_p,
+                                            C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64]
+        lib.ref_create_from_csr.restype = C.c_void_p
         lib.ref_destroy.argtypes = [C.c_void_p]
         lib.ref_index_info.argtypes = [C.c_void_p, P64, P64]
         lib.ref_genome_checksum.argtypes = [C.c_void_p]
@@ -276,6 +279,25 @@ class RefIndex:
         if not self.h:
             raise ValueError(lib.ref_last_error().decode())
         self.s = s
+
+    @classmethod
+    def from_restricted(cls, oi: "OracleIndex") -> "RefIndex":
+        """The reference's own SeedIndex + Aligner over the key-restricted CSR
+        of an OracleIndex built with for_reads=: loaded through the
+        reference's load_index_file (ref_create_from_csr), so the reference's
+        unmodified lookup and Aligner::align run at 3.1 Gbp, where its
+        single-threaded full build does not fit a bounded run.  Exact for the
+        reads the restricted index was built for."""
+        self = cls.__new__(cls)
+        lib = rlib()
+        self.packed, self.nmask = oi.packed, oi.nmask
+        self.h = lib.ref_create_from_csr(_u64p(self.packed), self.packed.size, _u64p(self.nmask), self.nmask.size,
+                                         oi.g.len, oi.ix.seed_size, oi.ix.keys, oi.ix.n_keys, oi.ix.offsets,
+                                         oi.ix.positions, oi.ix.n_positions)
+        if not self.h:
+            raise ValueError(lib.ref_last_error().decode())
+        self.s = oi.ix.seed_size
+        return self
 
     def __del__(self):
         if _r is not None and getattr(self, "h", None):

@@ -26,6 +26,8 @@
 
 #include "../include/snap_b200.h"
 #include <fstream>
+#include <istream>
+#include <streambuf>
 
 #include "seedaln/aligner.hpp"
 #include "seedaln/driver.hpp"
@@ -104,6 +106,68 @@ void* ref_create(const uint64_t* packed, uint64_t n_packed, const uint64_t* nmas
                                 std::vector<uint64_t>(packed, packed + n_packed),
                                 std::vector<uint64_t>(nmask, nmask + n_nmask));
         h->index = SeedIndex::build(h->genome, seed_size);
+        return h;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
+// The reference's SeedIndex over a key-restricted CSR (keys ascending in the
+// reference's packed form, CSR offsets, u32 positions ascending per key), as
+// the oracle's or_index_build_for_reads makes for a batch of reads.  The
+// tables go through the reference's own load_index_file (REF
+// src/seed_index.cpp:173-228, all its checks) from an in-memory SNAPIDX1
+// image, so the reference's unmodified lookup and Aligner run on them.  For
+// every key those reads probe the answer equals SeedIndex::build's; this is
+// how the reference arm runs at 3.1 Gbp, where the full single-threaded build
+// (REF seed_index.cpp:80-126, ~115 GB peak) does not fit a bounded run.
+void* ref_create_from_csr(const uint64_t* packed, uint64_t n_packed, const uint64_t* nmask, uint64_t n_nmask,
+                          uint64_t len, int seed_size, const uint64_t* keys, uint64_t n_keys,
+                          const uint64_t* offsets, const uint32_t* positions, uint64_t n_pos) {
+    try {
+        PackedGenome g;
+        std::vector<Contig> contigs{{"c1", 0, len}};
+        g.adopt_storage(std::move(contigs), len, std::vector<uint64_t>(packed, packed + n_packed),
+                        std::vector<uint64_t>(nmask, nmask + n_nmask));
+        const uint64_t sum = g.checksum();
+        std::vector<char> img;
+        img.reserve(64 + 8 * (n_packed + n_nmask + 2 * n_keys + n_pos + 8));
+        auto put = [&](const void* p, size_t n) {
+            const char* c = static_cast<const char*>(p);
+            img.insert(img.end(), c, c + n);
+        };
+        auto u32 = [&](uint32_t v) { put(&v, 4); };  // little-endian host (x86-64)
+        auto u64 = [&](uint64_t v) { put(&v, 8); };
+        put("SNAPIDX1", 8);
+        u32(1);
+        u32(static_cast<uint32_t>(seed_size));
+        u64(sum);
+        u64(1);
+        u32(2);
+        put("c1", 2);
+        u64(0);
+        u64(len);
+        u64(len);
+        u64(n_packed);
+        put(packed, 8 * n_packed);
+        u64(n_nmask);
+        put(nmask, 8 * n_nmask);
+        u64(n_keys);
+        put(keys, 8 * n_keys);
+        u64(n_keys + 1);
+        put(offsets, 8 * (n_keys + 1));
+        u64(n_pos);
+        for (uint64_t i = 0; i < n_pos; ++i) u64(positions[i]);
+        put("SNAPEND1", 8);
+        struct MemBuf : std::streambuf {
+            MemBuf(char* b, size_t n) { setg(b, b, b + n); }
+        } mb(img.data(), img.size());
+        std::istream in(&mb);
+        auto loaded = load_index_file(in);
+        auto* h = new RefHandle;
+        h->index = std::move(loaded.first);
+        h->genome = std::move(loaded.second);
         return h;
     } catch (const std::exception& e) {
         g_err = e.what();

@@ -22,18 +22,18 @@
 /* ------------------------------------------------------------ genome */
 
 /* REF src/genome.cpp:27-41 char_to_base: A/C/G/T any case, IUPAC -> N. */
+/* 0..3 ACGT (any case), 4 the IUPAC N class, -1 otherwise (REF genome.cpp
+ * char_to_base); a table, since random bases defeat a branchy switch */
+static const signed char g_code[256] = {
+    [0 ... 255] = -1,
+    ['A'] = 0, ['a'] = 0, ['C'] = 1, ['c'] = 1, ['G'] = 2, ['g'] = 2, ['T'] = 3, ['t'] = 3,
+    ['U'] = 4, ['N'] = 4, ['R'] = 4, ['Y'] = 4, ['S'] = 4, ['W'] = 4, ['K'] = 4, ['M'] = 4,
+    ['B'] = 4, ['D'] = 4, ['H'] = 4, ['V'] = 4, ['u'] = 4, ['n'] = 4, ['r'] = 4, ['y'] = 4,
+    ['s'] = 4, ['w'] = 4, ['k'] = 4, ['m'] = 4, ['b'] = 4, ['d'] = 4, ['h'] = 4, ['v'] = 4,
+};
+
 int or_char_to_code(char c) {
-    switch (c) {
-        case 'A': case 'a': return 0;
-        case 'C': case 'c': return 1;
-        case 'G': case 'g': return 2;
-        case 'T': case 't': return 3;
-        default: break;
-    }
-    const char* iupac = "UNRYSWKMBDHVunryswkmbdhv";
-    for (const char* q = iupac; *q; ++q)
-        if (*q == c) return 4;
-    return -1;
+    return g_code[(unsigned char)c];
 }
 
 /* REF src/genome.cpp:39-46 append_base: code at bits (pos&31)*2 of word
@@ -174,6 +174,32 @@ static int radix_sort_pairs(uint64_t* keys, uint32_t* pos, uint64_t n, int bits)
     return 0;
 }
 
+static int radix_sort_keys(uint64_t* keys, uint64_t n, int bits) {
+    if (n < 2) return 0;
+    uint64_t* k2 = (uint64_t*)malloc(n * sizeof(uint64_t));
+    size_t* hist = (size_t*)malloc((1u << 16) * sizeof(size_t));
+    if (!k2 || !hist) {
+        free(k2); free(hist);
+        return -1;
+    }
+    uint64_t *ka = keys, *kb = k2;
+    for (int shift = 0; shift < bits; shift += 16) {
+        memset(hist, 0, (1u << 16) * sizeof(size_t));
+        for (uint64_t i = 0; i < n; ++i) hist[(ka[i] >> shift) & 0xffff]++;
+        size_t sum = 0;
+        for (int d = 0; d < (1 << 16); ++d) {
+            size_t c = hist[d];
+            hist[d] = sum;
+            sum += c;
+        }
+        for (uint64_t i = 0; i < n; ++i) kb[hist[(ka[i] >> shift) & 0xffff]++] = ka[i];
+        uint64_t* t = ka; ka = kb; kb = t;
+    }
+    if (ka != keys) memcpy(keys, ka, n * sizeof(uint64_t));
+    free(k2); free(hist);
+    return 0;
+}
+
 /* REF src/seed_index.cpp:80-126 SeedIndex::build. */
 int or_index_build(const or_genome* g, int seed_size, or_index* idx) {
     memset(idx, 0, sizeof(*idx));
@@ -264,49 +290,89 @@ static int set_contains(const uint64_t* set, uint64_t set_mask, uint64_t key) {
     }
 }
 
-/* REF seed_index.cpp:96-110 rolling key, over windows [begin, end) only. */
+static int scan_push(scan_job* j, uint64_t key, uint64_t start) {
+    if (j->n == j->cap) {
+        uint64_t nc = j->cap ? 2 * j->cap : 1 << 16;
+        uint64_t* nk = (uint64_t*)realloc(j->keys, nc * sizeof(uint64_t));
+        if (nk) j->keys = nk;
+        uint32_t* np = (uint32_t*)realloc(j->pos, nc * sizeof(uint32_t));
+        if (np) j->pos = np;
+        if (!nk || !np) {
+            j->failed = 1;
+            return -1;
+        }
+        j->cap = nc;
+    }
+    j->keys[j->n] = key;
+    j->pos[j->n] = (uint32_t)start;
+    j->n++;
+    return 0;
+}
+
+/* REF seed_index.cpp:96-110 rolling key, over windows [begin, end) only.
+ * Each window costs a random filter access (and, when the filter says
+ * maybe, a random set access): both are software-prefetched a fixed number
+ * of windows ahead, so a thread keeps ~kPf misses in flight instead of one.
+ * Windows are emitted in position order either way. */
+#define kPf 32
 static void* scan_windows(void* arg) {
     scan_job* j = (scan_job*)arg;
     uint64_t key = 0;
     int64_t last_n = -1;
     const uint64_t from = j->begin;
     const uint64_t to = j->end + j->s - 1; /* last base of the last window */
-    for (uint64_t p = from; p < to && p < j->g->len; ++p) {
-        int b = or_genome_at(j->g, p);
-        if (b == 4) {
-            last_n = (int64_t)p;
-            key = (key << 2) & j->mask;
-            continue;
-        }
-        key = ((key << 2) | (uint64_t)b) & j->mask;
-        if (p + 1 < from + j->s) continue;
-        uint64_t start = p + 1 - j->s;
-        if ((int64_t)start <= last_n) continue;
-        const uint64_t h = mix_key(key);
-        if (!((j->filter[(h >> 6) & j->filter_mask] >> (h & 63)) & 1)) continue;
-        if (!set_contains(j->set, j->set_mask, key)) continue;
-        if (j->n == j->cap) {
-            uint64_t nc = j->cap ? 2 * j->cap : 1 << 16;
-            uint64_t* nk = (uint64_t*)realloc(j->keys, nc * sizeof(uint64_t));
-            if (nk) j->keys = nk;
-            uint32_t* np = (uint32_t*)realloc(j->pos, nc * sizeof(uint32_t));
-            if (np) j->pos = np;
-            if (!nk || !np) {
-                j->failed = 1;
-                return NULL;
+    /* stage 1: windows whose filter line is in flight; stage 2: filter hits
+     * whose set slot is in flight */
+    uint64_t k1[kPf], s1[kPf], h1[kPf], k2[kPf], s2[kPf];
+    unsigned n1 = 0, t1 = 0, n2 = 0, t2 = 0;
+    for (uint64_t p = from;; ++p) {
+        const int more = p < to && p < j->g->len;
+        if (more) {
+            int b = or_genome_at(j->g, p);
+            if (b == 4) {
+                last_n = (int64_t)p;
+                key = (key << 2) & j->mask;
+                continue;
             }
-            j->cap = nc;
+            key = ((key << 2) | (uint64_t)b) & j->mask;
+            if (p + 1 < from + j->s) continue;
+            const uint64_t start = p + 1 - j->s;
+            if ((int64_t)start <= last_n) continue;
+            const uint64_t h = mix_key(key);
+            __builtin_prefetch(&j->filter[(h >> 6) & j->filter_mask]);
+            const unsigned at = (t1 + n1) % kPf;
+            k1[at] = key;
+            s1[at] = start;
+            h1[at] = h;
+            ++n1;
         }
-        j->keys[j->n] = key;
-        j->pos[j->n] = (uint32_t)start;
-        j->n++;
+        /* drain stage 1 when full (or at the end) */
+        while (n1 == kPf || (!more && n1)) {
+            const uint64_t h = h1[t1];
+            if ((j->filter[(h >> 6) & j->filter_mask] >> (h & 63)) & 1) {
+                while (n2 == kPf) { /* drain the oldest stage-2 entry */
+                    if (set_contains(j->set, j->set_mask, k2[t2]) && scan_push(j, k2[t2], s2[t2])) return NULL;
+                    t2 = (t2 + 1) % kPf;
+                    --n2;
+                }
+                __builtin_prefetch(&j->set[h & j->set_mask]);
+                const unsigned at = (t2 + n2) % kPf;
+                k2[at] = k1[t1];
+                s2[at] = s1[t1];
+                ++n2;
+            }
+            t1 = (t1 + 1) % kPf;
+            --n1;
+            if (more) break;
+        }
+        if (!more) break;
+    }
+    while (n2) {
+        if (set_contains(j->set, j->set_mask, k2[t2]) && scan_push(j, k2[t2], s2[t2])) return NULL;
+        t2 = (t2 + 1) % kPf;
+        --n2;
     }
     return NULL;
-}
-
-static int cmp_u64(const void* a, const void* b) {
-    uint64_t x = *(const uint64_t*)a, y = *(const uint64_t*)b;
-    return x < y ? -1 : x > y;
 }
 
 int or_index_build_for_reads(const or_genome* g, int seed_size, int n_seeds, const char* bases,
@@ -326,9 +392,14 @@ int or_index_build_for_reads(const or_genome* g, int seed_size, int n_seeds, con
         free(q); free(offs);
         return SA_ERUNTIME;
     }
+    uint64_t last_len = ~(uint64_t)0;
+    int k = 0;
     for (uint64_t r = 0; r < n_reads; ++r) {
         const uint64_t len = offsets[r + 1] - offsets[r];
-        const int k = or_seed_offsets(len, seed_size, n_seeds, offs);
+        if (len != last_len) { /* same offsets for every read of one length */
+            k = or_seed_offsets(len, seed_size, n_seeds, offs);
+            last_len = len;
+        }
         for (int i = 0; i < k; ++i) {
             uint64_t key;
             if (!or_pack_seed(bases + offsets[r] + offs[i], seed_size, &key)) continue;
@@ -346,7 +417,10 @@ int or_index_build_for_reads(const or_genome* g, int seed_size, int n_seeds, con
         }
     }
     free(offs);
-    qsort(q, nq, sizeof(uint64_t), cmp_u64);
+    if (radix_sort_keys(q, nq, (int)(2 * s)) != 0) {
+        free(q);
+        return SA_ERUNTIME;
+    }
     uint64_t u = 0;
     for (uint64_t i = 0; i < nq; ++i)
         if (u == 0 || q[i] != q[u - 1]) q[u++] = q[i];

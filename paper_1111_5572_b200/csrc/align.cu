@@ -1747,7 +1747,9 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
                 __syncwarp();
                 table_ready = true;
             }
-            if (kSlow && a.work_list) r = a.work_list[r];  // no list: every read of the launch
+            // the list holds launch-absolute ids (read_base + r, as overflowed() stores
+            // them); no list: every read of the launch
+            if (kSlow && a.work_list) r = a.work_list[r] - static_cast<uint32_t>(a.read_base);
             const uint64_t o0 = a.offsets[r], o1 = a.offsets[r + 1];
             const int len = static_cast<int>(o1 - o0);
             const uintptr_t addr = reinterpret_cast<uintptr_t>(a.bases + (o0 - a.base_off));
@@ -1928,9 +1930,10 @@ void launch_seed(const AlignLaunch& a, cudaStream_t st) {
         uint64_t g = (static_cast<uint64_t>(a.n_reads) + groups_per_block - 1) / groups_per_block;
         static const uint64_t cap = [] {  // SA_SEED_GRID overrides (tuning)
             const char* e = getenv("SA_SEED_GRID");
-            return e ? static_cast<uint64_t>(atoll(e)) : uint64_t{1} << 24;  // a group per read (C1 1018 -> 1025 M over 148 x 32)
+            return e ? static_cast<uint64_t>(atoll(e)) : uint64_t{1} << 23;  // a group per read (C1 1018 -> 1025 M over 148 x 32)
         }();
-        g = std::max<uint64_t>(1, std::min<uint64_t>(g, std::max<uint64_t>(cap, 1)));
+        // gridDim.x * blockDim.x is a 32-bit product in the kernel: at most 2^31 threads
+        g = std::max<uint64_t>(1, std::min<uint64_t>({g, std::max<uint64_t>(cap, 1), uint64_t{1} << 23}));
         kernel<<<static_cast<int>(g), 256, 0, st>>>(a);
     };
     if (nbmax <= 4) go(seed_kernel<4>, 4);
@@ -1949,8 +1952,11 @@ bool solo_eligible(const AlignLaunch& a) {
         const char* e = getenv("SA_SOLO_MIN_READS");
         return e ? static_cast<uint32_t>(atoll(e)) : 12288u;
     }();
+    // the solo kernel keys candidates as 32-bit (bucket << 1 | dir): buckets
+    // must stay below 2^31 (bucket_size 1 on a genome past 2^31 bases would
+    // fold anchors a and a + 2^31 together)
     return !off && a.pre_list != nullptr && a.n_reads >= min_reads && a.dl_max <= 15 && a.bs_shift >= 0 &&
-           a.bs_shift <= 5;
+           a.bs_shift <= 5 && (a.glen >> a.bs_shift) < (1ull << 31);
 }
 
 int launch_align_seeded(const AlignLaunch& a, int grid, int block, cudaStream_t st) {

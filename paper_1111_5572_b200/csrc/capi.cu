@@ -77,6 +77,7 @@ struct Stage {  // one of the two pipeline slots of a replica
     unsigned int* d_ctl = nullptr;
     cudaEvent_t k0 = nullptr, km = nullptr, k1 = nullptr;  // fast kernel [k0,km), slow [km,k1)
     cudaEvent_t done = nullptr;                             // after the stage's last D2H
+    bool done_pending = false;  // sa_align_device: `done` recorded after the last call's work
     // seed-kernel outputs of the two-kernel path (launch_align_pre)
     uint4* pre_planes = nullptr;
     uint4* pre_recs = nullptr;
@@ -1597,7 +1598,12 @@ int sa_align_device(sa_context* ctx, const sa_params* params, const char* d_base
     if (int rc = ensure_stage(ctx, stg, 0, n_reads)) return rc;
     const uint64_t pre_n = dev_chunk_reads() ? std::min(n_reads, dev_chunk_reads()) : n_reads;
     if (int rc = ensure_pre(ctx, stg, pre_n, sh)) return rc;
-    // the caller's stream drives; this stage keeps only control words
+    // The caller's stream drives; this stage keeps only control words and
+    // the seed-kernel scratch, which every call shares.  A call on another
+    // stream therefore waits for the previous call's work (event `done`), so
+    // calls in flight on different streams never overwrite each other's
+    // cursors, records or lists.
+    if (stg.done_pending) CUDA_TRY(ctx, cudaStreamWaitEvent(st, stg.done, 0));
     Stage tmp = stg;
     tmp.st = st;
     unsigned long long* stats_dst = reinterpret_cast<unsigned long long*>(d_stats);
@@ -1606,6 +1612,8 @@ int sa_align_device(sa_context* ctx, const sa_params* params, const char* d_base
     if (int rc = enqueue_align(ctx, rep, tmp, sh, d_bases, d_offsets, 0, n_reads, 0, d_results,
                                stats_dst, stg.d_overflow, true, launches))
         return rc;
+    CUDA_TRY(ctx, cudaEventRecord(stg.done, st));
+    stg.done_pending = true;
     ctx->last_launches = launches;
     ctx->device_timing_pending = true;
     return SA_OK;

@@ -1,16 +1,19 @@
-"""Full BASELINE.json sizes on the GPU.
+"""Full BASELINE.json sizes on the GPU, every read checked.
 
-C1 (configs[1], the bench workload) is checked read-for-read against the oracle
-in full (1,000,000 reads, 100 Mbp).  C4 uses its full 500 Mbp genome with a
-sample of its 10 kbp reads.  Size-independent properties (determinism, batch
-chunking invariance, device-resident == host path, strand symmetry,
-force_max_dlimit invariance, multi-replica dealing) run at full C1 size.
-C2 builds its full 3.1 Gbp repeat genome index on the GPU (partitioned build)
-and aligns all 10 M reads; the first 1 M are checked read-for-read against the
-oracle, which at this size indexes only the keys those reads probe
-(OracleIndex(for_reads=...), itself proven equal to the full CSR in
-tests/test_oracle.py).  C3 reuses that genome with a 50 k-read sample.
+C1 (1,000,000 reads, 100 Mbp), C2 (all 10,000,000 reads on the 3.1 Gbp repeat
+genome), C3 (all 500,000 1 kbp reads on the same genome) and C4 (all 50,000
+10 kbp reads, 500 Mbp) are checked read-for-read against the oracle, counters
+included -- the reference's own accuracy audit covers every read (REF
+tests/acceptance/acceptance_main.cpp:130-289).  At 3.1 Gbp the oracle indexes
+only the keys the batch's reads probe (OracleIndex(for_reads=...), itself
+proven equal to the full CSR in tests/test_oracle.py).  Size-independent
+properties (determinism, batch chunking invariance, device-resident == host
+path, strand symmetry, force_max_dlimit invariance, multi-replica dealing)
+run at full C1 size; AlignerParams with bucket sizes 1 and 2 run on the
+3.1 Gbp genome (anchors past 2^31 bases).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -18,6 +21,7 @@ from oracle import oracle as O
 from paper_1111_5572_b200 import api, synth
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+CPUS = os.cpu_count() or 8
 
 
 @pytest.fixture(scope="module")
@@ -135,16 +139,17 @@ def test_c1_two_replicas_one_context(c1):
         assert al2.stats().values[f] == c1["stats"][f], f
 
 
-def test_c4_full_genome_sampled_reads():
-    cfg = synth.CONFIGS["C4"].scaled(n_reads=400)
+def test_c4_full_vs_oracle():
+    cfg = synth.CONFIGS["C4"]
     g = synth.make_genome(cfg)
     packed, nmask = synth.pack_genome(g)
     bases, offs, _, _ = synth.make_reads(cfg, g)
+    assert offs.size - 1 == 50_000
     genome = api.PackedGenome(packed, nmask, g.size)
     al = api.Aligner(api.SeedIndex.build(genome, 22), genome, cfg.params)
     got = al.align_arrays(bases, offs)
-    oi = O.OracleIndex(packed, nmask, g.size, 22)
-    want, wst = oi.align_arrays(cfg.params, bases, offs, threads=16)
+    oi = O.OracleIndex(packed, nmask, g.size, 22, for_reads=(cfg.params.seeds_to_try, bases, offs), threads=CPUS)
+    want, wst = oi.align_arrays(cfg.params, bases, offs, threads=CPUS)
     assert O.compare_results(got, want) == []
     for f in api.REFERENCE_STAT_FIELDS:
         if f != "dp_cells":
@@ -171,25 +176,20 @@ def test_c2_index_shape(c2_genome):
 
 
 def test_c2_full_reads_vs_oracle(c2_genome):
-    """All 10,000,000 C2 reads on the GPU; the first 1,000,000 checked
-    read-for-read against the oracle (restricted to the keys they probe)."""
+    """All 10,000,000 C2 reads on the GPU, every one checked against the
+    oracle (restricted to the keys they probe), counters included."""
     cfg = synth.CONFIGS["C2"]
     bases, offs, tpos, tdir = synth.make_reads(cfg, c2_genome["g"])
     al = api.Aligner(c2_genome["idx"], c2_genome["genome"], cfg.params)
     got = al.align_arrays(bases, offs)
     assert got.size == 10_000_000
-    n = 1_000_000
-    sb, so = bases[:int(offs[n])], offs[:n + 1]
     oi = O.OracleIndex(c2_genome["packed"], c2_genome["nmask"], c2_genome["g"].size, 20,
-                       for_reads=(cfg.params.seeds_to_try, sb, so), threads=16)
-    want, wst = oi.align_arrays(cfg.params, sb, so, threads=16)
-    assert O.compare_results(got[:n], want) == []
-    al1 = api.Aligner(c2_genome["idx"], c2_genome["genome"], cfg.params)
-    again = al1.align_arrays(sb, so)
-    assert O.compare_results(again, want) == []
+                       for_reads=(cfg.params.seeds_to_try, bases, offs), threads=CPUS)
+    want, wst = oi.align_arrays(cfg.params, bases, offs, threads=CPUS)
+    assert O.compare_results(got, want) == []
     for f in api.REFERENCE_STAT_FIELDS:
         if f != "dp_cells":
-            assert al1.stats().values[f] == wst[f], f
+            assert al.stats().values[f] == wst[f], f
     # size-independent: accuracy against the simulator's truth on unique hits
     single = got["kind"] == api.ResultKind.SingleHit
     assert single.mean() > 0.95
@@ -197,15 +197,37 @@ def test_c2_full_reads_vs_oracle(c2_genome):
     assert near.mean() > 0.99
 
 
-def test_c3_sampled_reads_vs_oracle(c2_genome):
-    cfg = synth.CONFIGS["C3"].scaled(n_reads=50_000)
+def test_c3_full_reads_vs_oracle(c2_genome):
+    cfg = synth.CONFIGS["C3"]
     bases, offs, _, _ = synth.make_reads(cfg, c2_genome["g"])
+    assert offs.size - 1 == 500_000
     al = api.Aligner(c2_genome["idx"], c2_genome["genome"], cfg.params)
     got = al.align_arrays(bases, offs)
     oi = O.OracleIndex(c2_genome["packed"], c2_genome["nmask"], c2_genome["g"].size, 20,
-                       for_reads=(cfg.params.seeds_to_try, bases, offs), threads=16)
-    want, wst = oi.align_arrays(cfg.params, bases, offs, threads=16)
+                       for_reads=(cfg.params.seeds_to_try, bases, offs), threads=CPUS)
+    want, wst = oi.align_arrays(cfg.params, bases, offs, threads=CPUS)
     assert O.compare_results(got, want) == []
     for f in api.REFERENCE_STAT_FIELDS:
         if f != "dp_cells":
             assert al.stats().values[f] == wst[f], f
+
+
+@pytest.mark.parametrize("bs", [1, 2])
+def test_c2_genome_small_buckets(c2_genome, bs):
+    """bucket_size 1 and 2 on the 3.1 Gbp genome: anchors and buckets past
+    2^31 (the solo kernel keys buckets in 32 bits and stays off for bucket 1
+    here; bucket 2 keeps it), 300 k C2 reads, every read and counter."""
+    cfg = synth.CONFIGS["C2"].scaled(n_reads=300_000)
+    bases, offs, _, _ = synth.make_reads(cfg, c2_genome["g"], seed=77 + bs)
+    p = api.AlignerParams(**{**cfg.params.__dict__, "bucket_size": bs})
+    al = api.Aligner(c2_genome["idx"], c2_genome["genome"], p)
+    got = al.align_arrays(bases, offs)
+    oi = O.OracleIndex(c2_genome["packed"], c2_genome["nmask"], c2_genome["g"].size, 20,
+                       for_reads=(p.seeds_to_try, bases, offs), threads=CPUS)
+    want, wst = oi.align_arrays(p, bases, offs, threads=CPUS)
+    assert O.compare_results(got, want) == []
+    for f in api.REFERENCE_STAT_FIELDS:
+        if f != "dp_cells":
+            assert al.stats().values[f] == wst[f], f
+    # reads aligned past 2^31 exercise the wide anchors
+    assert (got["position"][got["has_position"] == 1] >= (1 << 31)).sum() > 1000

@@ -299,7 +299,7 @@ def test_overflow_paths_parity(mode, monkeypatch):
     g = synth.make_repeat_genome(5, 2_000_000, 60, min_len=200, max_len=1500, min_copies=20, max_copies=150,
                                  min_div=0.0, max_div=0.04)
     packed, nmask = synth.pack_genome(g)
-    cfg = synth.CONFIGS["C3"].scaled(genome_len=g.size, n_reads=1500)
+    cfg = synth.CONFIGS["C3"].scaled(genome_len=g.size, n_reads=4000)
     bases, offs, _, _ = synth.make_reads(cfg, g)
     _, st = _gpu_vs_oracle(cfg, g, packed, nmask, bases, offs)
     assert st["overflow_reads"] > 0

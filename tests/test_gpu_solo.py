@@ -53,3 +53,19 @@ def test_referee_wavefront_verify_still_matches():
                        timeout=1500)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
+
+
+@pytest.mark.gpu
+def test_parity_multichunk_and_grid_stride():
+    """Every launch split into many small chunks (SA_CHUNK_READS=1024, so the
+    overflow pass of SA_OVERFLOW_KERNEL runs per chunk with chunk-relative
+    read ids) and every kernel run with a single block (SA_SOLO_GRID=1,
+    SA_SEED_GRID=1: grid-stride loops take many iterations and the
+    lane-distributed counters accumulate across them), the solo kernel on for
+    every launch."""
+    env = {"SA_CHUNK_READS": "1024", "SA_SOLO_GRID": "1", "SA_SEED_GRID": "1", "SA_SOLO_MIN_READS": "1"}
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-x", "-q",
+                        "-m", "gpu", "-k", "align_parity or overflow_paths or param_sweep", "-p", "no:cacheprovider"],
+                       cwd=ROOT, env={**os.environ, **env}, capture_output=True, text=True, timeout=1500)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
