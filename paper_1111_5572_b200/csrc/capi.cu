@@ -91,6 +91,14 @@ struct Stage {  // one of the two pipeline slots of a replica
     uint32_t* h_pack = nullptr;
     uint32_t* d_pack = nullptr;
     uint64_t pack_cap = 0;  // words, all three planes
+    // pinned staging for pageable callers: the chunk's bases (+ offsets) in,
+    // its results out (copied to the caller once their D2H has landed)
+    char* h_in = nullptr;
+    uint64_t h_in_cap = 0;
+    sa_result* h_res = nullptr;
+    uint64_t h_res_cap = 0;
+    bool res_pending = false;
+    uint64_t res_r0 = 0, res_r1 = 0;
 };
 
 int ensure_pack(sa_context* ctx, Stage& s, uint64_t words);
@@ -445,6 +453,38 @@ int ensure_pack(sa_context* ctx, Stage& s, uint64_t words) {
     CUDA_TRY(ctx, cudaHostAlloc(&s.h_pack, w * sizeof(uint32_t), cudaHostAllocDefault));
     s.pack_cap = w;
     return SA_OK;
+}
+
+int ensure_host_staging(sa_context* ctx, Stage& s, uint64_t in_bytes, uint64_t reads) {
+    if (in_bytes > s.h_in_cap) {
+        if (s.h_in) cudaFreeHost(s.h_in);
+        s.h_in = nullptr;
+        s.h_in_cap = 0;
+        const uint64_t b = std::max<uint64_t>(in_bytes + in_bytes / 4, 1 << 20);
+        CUDA_TRY(ctx, cudaHostAlloc(&s.h_in, b, cudaHostAllocDefault));
+        s.h_in_cap = b;
+    }
+    if (reads > s.h_res_cap) {
+        if (s.h_res) cudaFreeHost(s.h_res);
+        s.h_res = nullptr;
+        s.h_res_cap = 0;
+        const uint64_t r = std::max<uint64_t>(reads + reads / 4, 1 << 12);
+        CUDA_TRY(ctx, cudaHostAlloc(&s.h_res, r * sizeof(sa_result), cudaHostAllocDefault));
+        s.h_res_cap = r;
+    }
+    return SA_OK;
+}
+
+// True when p is ordinary (pageable) host memory: cudaMemcpyAsync from it
+// would be staged synchronously by the driver, so the batcher stages it
+// through its own pinned buffers instead.
+bool is_pageable(const void* p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return at.type == cudaMemoryTypeUnregistered;
 }
 
 // the seeded pipeline serves batches whose first chunk holds only reads of
@@ -967,6 +1007,20 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
     SeededChunk pend;
     bool have_pend = false;
     const bool packed = pack_enabled();
+    // pageable caller buffers go through pinned staging (SA_NO_STAGING: hand
+    // them to cudaMemcpyAsync as they are, which the driver stages synchronously)
+    static const bool no_staging = getenv("SA_NO_STAGING") != nullptr;
+    const bool stage_in = !packed && !no_staging && is_pageable(bases);
+    const bool stage_out = !no_staging && is_pageable(results);
+    // a stage's pinned results, once their D2H has landed, go to the caller
+    for (int j = 0; j < kPipeStages; ++j) rep.stage[j].res_pending = false;  // nothing owed from a failed call
+    auto drain_results = [&](Stage& st) -> int {
+        if (!st.res_pending) return SA_OK;
+        CUDA_TRY(ctx, cudaEventSynchronize(st.e_out));
+        parallel_copy(results + st.res_r0, st.h_res, (st.res_r1 - st.res_r0) * sizeof(sa_result));
+        st.res_pending = false;
+        return SA_OK;
+    };
     // Chunk k's seed and align kernels run on its stage's own stream, so the
     // kernels of consecutive chunks share the GPU: the next chunk's blocks
     // fill the SMs a kernel's tail leaves idle (C1 e2e 367 -> 405 M reads/s).
@@ -992,8 +1046,17 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
         ++launches;
         CUDA_TRY(ctx, cudaEventRecord(st.e_al, pend.cs));
         CUDA_TRY(ctx, cudaStreamWaitEvent(S.co, st.e_al, 0));
-        CUDA_TRY(ctx, cudaMemcpyAsync(results + pend.r0, st.d_results, (pend.r1 - pend.r0) * sizeof(sa_result),
-                                      cudaMemcpyDeviceToHost, S.co));
+        if (stage_out) {
+            if (int rc = drain_results(st)) return rc;  // this stage's previous chunk
+            CUDA_TRY(ctx, cudaMemcpyAsync(st.h_res, st.d_results, (pend.r1 - pend.r0) * sizeof(sa_result),
+                                          cudaMemcpyDeviceToHost, S.co));
+            st.res_pending = true;
+            st.res_r0 = pend.r0;
+            st.res_r1 = pend.r1;
+        } else {
+            CUDA_TRY(ctx, cudaMemcpyAsync(results + pend.r0, st.d_results, (pend.r1 - pend.r0) * sizeof(sa_result),
+                                          cudaMemcpyDeviceToHost, S.co));
+        }
         CUDA_TRY(ctx, cudaEventRecord(st.e_out, S.co));
         return SA_OK;
     };
@@ -1031,6 +1094,10 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
         const uint64_t b0 = offsets[r0], b1 = offsets[r1];
         if ((bad = ensure_stage(ctx, st, b1 - b0, r1 - r0))) break;
         if ((bad = ensure_pre(ctx, st, r1 - r0, sh))) break;
+        if ((stage_in || stage_out) &&
+            (bad = ensure_host_staging(ctx, st, stage_in ? (b1 - b0) + (r1 - r0 + 1) * sizeof(uint64_t) + 8 : 0,
+                                       stage_out ? r1 - r0 : 0)))
+            break;
         if (k == 0) {
             if ((bad = ensure_defer(ctx, rep, n_reads))) break;
             CUDA_TRY(ctx, cudaEventRecord(S.e_begin, S.ci));
@@ -1053,14 +1120,28 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
             if (k >= kPipeStages) CUDA_TRY(ctx, cudaEventSynchronize(st.e_in));
             pack_planar(bases + b0, b1 - b0, st.h_pack, wpp);
         }
+        const char* src_b = bases + b0;
+        const uint64_t* src_o = offsets + r0;
+        if (stage_in) {
+            // the host copies chunk k into the stage's pinned buffer (free once
+            // its previous H2D landed) while the GPU runs the earlier chunks
+            if (k >= kPipeStages) CUDA_TRY(ctx, cudaEventSynchronize(st.e_in));
+            const uint64_t ob = ((b1 - b0) + 7) & ~7ull;
+            parallel_copy(st.h_in, bases + b0, b1 - b0);
+            src_b = st.h_in;
+            if (!fixed) {
+                std::memcpy(st.h_in + ob, offsets + r0, (r1 - r0 + 1) * sizeof(uint64_t));
+                src_o = reinterpret_cast<const uint64_t*>(st.h_in + ob);
+            }
+        }
         if (k >= kPipeStages) CUDA_TRY(ctx, cudaStreamWaitEvent(S.ci, st.e_seeded, 0));
         if (packed)
             CUDA_TRY(ctx, cudaMemcpyAsync(st.d_pack, st.h_pack, 3 * wpp * sizeof(uint32_t), cudaMemcpyHostToDevice,
                                           S.ci));
         else
-            CUDA_TRY(ctx, cudaMemcpyAsync(st.d_bases, bases + b0, b1 - b0, cudaMemcpyHostToDevice, S.ci));
+            CUDA_TRY(ctx, cudaMemcpyAsync(st.d_bases, src_b, b1 - b0, cudaMemcpyHostToDevice, S.ci));
         if (!fixed)
-            CUDA_TRY(ctx, cudaMemcpyAsync(st.d_offsets, offsets + r0, (r1 - r0 + 1) * sizeof(uint64_t),
+            CUDA_TRY(ctx, cudaMemcpyAsync(st.d_offsets, src_o, (r1 - r0 + 1) * sizeof(uint64_t),
                                           cudaMemcpyHostToDevice, S.ci));
         CUDA_TRY(ctx, cudaEventRecord(st.e_in, S.ci));
         // compute: seed(k), then align(k - 1)
@@ -1133,6 +1214,8 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
     const auto t_enq = std::chrono::steady_clock::now();
     CUDA_TRY(ctx, cudaStreamSynchronize(S.co));
     CUDA_TRY(ctx, cudaStreamSynchronize(S.ci));
+    for (int j = 0; j < kPipeStages; ++j)
+        if (int rc = drain_results(rep.stage[j])) return rc;
     if (dbg_span && k > 0) {
         float ci = 0, kb = 0, ke = 0;
         cudaEventElapsedTime(&ci, S.e_begin, S.e_ready);
@@ -1323,6 +1406,8 @@ void sa_destroy(sa_context* ctx) {
             if (s.pre_list) cudaFree(s.pre_list);
             if (s.d_pack) cudaFree(s.d_pack);
             if (s.h_pack) cudaFreeHost(s.h_pack);
+            if (s.h_in) cudaFreeHost(s.h_in);
+            if (s.h_res) cudaFreeHost(s.h_res);
             if (s.st) cudaStreamDestroy(s.st);
         }
         if (rep.d_stats) cudaFree(rep.d_stats);

@@ -44,5 +44,7 @@ int char_to_code(char c);
 bool pack_enabled();
 uint64_t pack_words_per_plane(uint64_t n_bases);
 void pack_planar(const char* src, uint64_t n, uint32_t* planes, uint64_t wpp);
+// multi-threaded memcpy (host thread pool), for staging pageable input
+void parallel_copy(void* dst, const void* src, uint64_t n);
 
 }  // namespace sab

@@ -210,7 +210,101 @@ int pack_threads_setting() {
     return e ? std::max(0, std::min(64, atoi(e))) : 0;
 }
 
+// Generic persistent worker pool for host copies into pinned staging
+// buffers (the batcher's pageable-input path): tasks of one job are claimed
+// from a generation-tagged cursor exactly like PackPool's.
+class CopyPool {
+  public:
+    explicit CopyPool(int n_threads) {
+        for (int i = 0; i < n_threads; ++i) th_.emplace_back([this] { loop(); });
+    }
+    ~CopyPool() {
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    void run(char* dst, const char* src, uint64_t n) {
+        std::lock_guard<std::mutex> one(job_mu_);
+        Job j;
+        j.dst = dst;
+        j.src = src;
+        j.n = n;
+        j.n_tasks = (n + kTaskBytes - 1) / kTaskBytes;
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            j.gen = ++gen_;
+            job_ = j;
+            done_.store(0);
+            cursor_.store(j.gen << 32);
+        }
+        if (j.n_tasks > 1 && !th_.empty()) cv_.notify_all();
+        work(j);
+        while (done_.load(std::memory_order_acquire) < j.n_tasks) std::this_thread::yield();
+    }
+
+  private:
+    static constexpr uint64_t kTaskBytes = 1ull << 20;
+    struct Job {
+        char* dst = nullptr;
+        const char* src = nullptr;
+        uint64_t n = 0, n_tasks = 0, gen = 0;
+    };
+    void work(const Job& j) {
+        uint64_t c = cursor_.load();
+        for (;;) {
+            if ((c >> 32) != j.gen || (c & 0xffffffffu) >= j.n_tasks) return;
+            if (!cursor_.compare_exchange_weak(c, c + 1)) continue;
+            const uint64_t b0 = (c & 0xffffffffu) * kTaskBytes, b1 = std::min(j.n, b0 + kTaskBytes);
+            std::memcpy(j.dst + b0, j.src + b0, b1 - b0);
+            done_.fetch_add(1, std::memory_order_release);
+            c = cursor_.load();
+        }
+    }
+    void loop() {
+        uint64_t seen = 0;
+        for (;;) {
+            Job j;
+            {
+                std::unique_lock<std::mutex> g(mu_);
+                cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_;
+                j = job_;
+            }
+            work(j);
+        }
+    }
+    std::vector<std::thread> th_;
+    std::mutex mu_, job_mu_;
+    std::condition_variable cv_;
+    bool stop_ = false;
+    uint64_t gen_ = 0;
+    Job job_;
+    std::atomic<uint64_t> cursor_{0}, done_{0};
+};
+
+// SA_STAGE_THREADS=n: host threads copying pageable input into the pinned
+// staging buffers (default: half the host's threads, 4..16).
+int stage_threads_setting() {
+    const char* e = getenv("SA_STAGE_THREADS");
+    if (e) return std::max(1, std::min(64, atoi(e)));
+    const int hw = static_cast<int>(std::thread::hardware_concurrency());
+    return std::max(4, std::min(16, hw / 2));
+}
+
 }  // namespace
+
+void parallel_copy(void* dst, const void* src, uint64_t n) {
+    if (n < (4ull << 20)) {
+        std::memcpy(dst, src, n);
+        return;
+    }
+    static CopyPool pool(stage_threads_setting() - 1);  // the caller is one of the copiers
+    pool.run(static_cast<char*>(dst), static_cast<const char*>(src), n);
+}
 
 bool pack_enabled() { return pack_threads_setting() > 0; }
 

@@ -416,3 +416,26 @@ def test_align_param_sweep(bs, c, dmax, n, hmax):
     p = api.AlignerParams(seed_size=20, seeds_to_try=n, max_distance=dmax, confidence_threshold=c, max_hits=hmax,
                           bucket_size=bs)
     _gpu_vs_oracle(cfg, g, packed, nmask, bases, offs, params=p)
+
+
+def test_pageable_and_pinned_buffers_agree():
+    """sa_align_batch with the caller's buffers pageable (the library stages
+    them through its own pinned buffers, input and results), pinned, or
+    mixed: identical results, equal to the oracle, over many chunks."""
+    cfg, g, packed, nmask, bases, offs = _case("C1", 3_000_000, 300_000, 5, 0.005)
+    genome = api.PackedGenome(packed, nmask, g.size)
+    al = api.Aligner(api.SeedIndex.build(genome, 20), genome, cfg.params)
+    pageable = al.align_arrays(bases, offs)
+    pin_b, pin_r = api.PinnedBuffer(bases.nbytes), api.PinnedBuffer(pageable.nbytes)
+    hb = pin_b.array(np.uint8, bases.size)
+    hb[:] = bases
+    hr = pin_r.array(api.RESULT_DTYPE, pageable.size)
+    al.align_arrays(hb, offs, hr)
+    assert O.compare_results(hr.copy(), pageable) == []
+    mixed = al.align_arrays(hb, offs)                 # pinned in, pageable out
+    assert O.compare_results(mixed, pageable) == []
+    hr[:] = np.zeros(1, api.RESULT_DTYPE)
+    al.align_arrays(bases, offs, hr)                  # pageable in, pinned out
+    assert O.compare_results(hr.copy(), pageable) == []
+    want, _ = O.OracleIndex(packed, nmask, g.size, 20).align_arrays(cfg.params, bases, offs, threads=8)
+    assert O.compare_results(pageable, want) == []
