@@ -123,6 +123,23 @@ public:
         return out;
     }
 
+    // The run_align worker's batch (REF src/driver.cpp:104-124): any
+    // container of Read-like records with a `bases` string (seedaln::Read,
+    // REF include/seedaln/read.hpp:9-14).  The bases are gathered into one
+    // host buffer; the library stages it through its own pinned buffers.
+    template <class Reads, class = decltype(std::declval<const Reads&>().begin()->bases)>
+    std::vector<sa_result> align_reads(const Reads& reads) {
+        std::string buf;
+        std::vector<uint64_t> offs{0};
+        for (const auto& r : reads) {
+            buf.append(r.bases);
+            offs.push_back(buf.size());
+        }
+        std::vector<sa_result> out(offs.size() - 1);
+        if (!out.empty()) align_batch(buf.data(), offs.data(), out.size(), out.data());
+        return out;
+    }
+
     sa_result align(std::string_view bases) {  // REF aligner.cpp:223 (batch of one)
         uint64_t offs[2] = {0, bases.size()};
         sa_result r{};

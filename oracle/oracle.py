@@ -61,6 +61,9 @@ def build(with_ref: bool | None = None) -> None:
         with_ref = os.path.isdir(REF_DIR)
     if with_ref:
         subprocess.run(["make", "-s", "-C", HERE, "ref", f"REF={REF_DIR}"], check=True)
+        # the C++ drop-in test program (needs the product library built first)
+        if os.path.exists(os.path.join(os.path.dirname(HERE), "paper_1111_5572_b200", "lib", "libsnapb200.so")):
+            subprocess.run(["make", "-s", "-C", HERE, "dropin", f"REF={REF_DIR}"], check=True)
 
 
 def ref_available() -> bool:

@@ -419,44 +419,200 @@ SA_DEV void score_candidate(Ctx& x, uint32_t idx) {
     if (best_d < kInfDistance) tracker_observe(x.tr, a.bs, best_d, best_anchor, dir);
 }
 
-// REF aligner.cpp:141-167 score_best_candidate: unscored candidate with most
-// seeds hitting, then smallest anchor, then Forward.
+// REF aligner.cpp:141-167 score_best_candidate's choice: the unscored
+// candidate with most seeds hitting, then smallest anchor, then Forward.
+// Returns its index, -1 when nothing is unscored.
+SA_DEV int pick_best(Ctx& x) {
+    if (x.n_unscored == 0) return -1;
+    if (x.n_cands == 1) return 0;  // the only candidate is the unscored one
+    const AlignLaunch& a = *x.a;
+    uint32_t bc = 0;
+    unsigned long long bk = ~0ull;
+    int bi = -1;
+    for (uint32_t j = x.lane; j < x.n_cands; j += 32) {
+        const uint32_t cc = x.t.ccnt[j];
+        if (cc & kScored) continue;
+        const unsigned long long kk = x.t.ckey[j];
+        const unsigned long long mm = x.t.cmask[j];
+        const unsigned long long amin = (kk >> 1) * static_cast<unsigned long long>(a.bs) +
+                                        static_cast<unsigned long long>(__ffsll(static_cast<long long>(mm)) - 1);
+        const unsigned long long ord = (amin << 1) | (kk & 1ull);
+        if (cc > bc || (cc == bc && ord < bk)) {
+            bc = cc;
+            bk = ord;
+            bi = static_cast<int>(j);
+        }
+    }
+    // warp argmax of (seeds_hitting, then smallest (amin, dir)) with three
+    // single-instruction reductions instead of a 5-step shuffle tree of
+    // three values (score_best was 18% of the warp kernel at C2)
+    const uint32_t mc = __reduce_max_sync(FULL, bc);
+    const bool in = bi >= 0 && bc == mc;
+    const uint32_t khi = static_cast<uint32_t>(bk >> 32), klo = static_cast<uint32_t>(bk);
+    const uint32_t mhi = __reduce_min_sync(FULL, in ? khi : 0xffffffffu);
+    const uint32_t mlo = __reduce_min_sync(FULL, in && khi == mhi ? klo : 0xffffffffu);
+    const uint32_t win = __ballot_sync(FULL, in && khi == mhi && klo == mlo);
+    if (win == 0u) return -1;  // nothing unscored
+    return __shfl_sync(FULL, bi, __ffs(win) - 1);
+}
+
 template <bool kRegLV>
 SA_DEV void score_best(Ctx& x) {
-    if (x.n_unscored == 0) return;
-    int bi = 0;
-    if (x.n_cands > 1) {  // otherwise the only candidate is the unscored one
-        const AlignLaunch& a = *x.a;
-        uint32_t bc = 0;
-        unsigned long long bk = ~0ull;
-        bi = -1;
-        for (uint32_t j = x.lane; j < x.n_cands; j += 32) {
-            const uint32_t cc = x.t.ccnt[j];
-            if (cc & kScored) continue;
-            const unsigned long long kk = x.t.ckey[j];
-            const unsigned long long mm = x.t.cmask[j];
-            const unsigned long long amin = (kk >> 1) * static_cast<unsigned long long>(a.bs) +
-                                            static_cast<unsigned long long>(__ffsll(static_cast<long long>(mm)) - 1);
-            const unsigned long long ord = (amin << 1) | (kk & 1ull);
-            if (cc > bc || (cc == bc && ord < bk)) {
-                bc = cc;
-                bk = ord;
-                bi = static_cast<int>(j);
+    const int bi = pick_best(x);
+    if (bi >= 0) score_candidate<kRegLV>(x, static_cast<uint32_t>(bi));
+}
+
+// ------------------------------------------------------------------ pruning batch
+// The pruning loop (REF aligner.cpp:296-315) scores every remaining unscored
+// candidate, best first, each under a d_limit re-derived from the tracker.
+// No hit is added in that loop, so the order is fixed; and every d_limit it
+// can derive is at most B = d_best + c - 1 (d_best <= d_max: d_best only
+// falls, and a refined best keeps d_limit below the old d_best + c - 1; with
+// d_best > d_max or force_max_dlimit, B = d_max + c - 1).  A bounded distance
+// is exact when it is <= the bound (REF edit_distance.cpp:19-75; a longer
+// window never changes a value <= d_limit), so the
+// batch runs the LVs of up to 64 anchors of the next candidates (in selection
+// order) at once -- one anchor per lane, the thread-serial wavefront at bound
+// B -- and then replays the loop candidate by candidate: d_limit from the
+// tracker, each anchor's value cut at d_limit, calls / early-out / window
+// counters per anchor in order, min with the earliest anchor on ties, one
+// observe, the multi exit.  Same results and counters as scoring them one by
+// one (dp_cells aside, which is implementation-specific).
+// Shared memory per warp: the lanes' frontiers [kPbF][32] shorts, then 64
+// slot entries (candidate of the batch, anchor bit).
+#ifndef SA_PRUNE_BATCH
+#define SA_PRUNE_BATCH 1
+#endif
+constexpr int kPbMax = 5;                // largest bound B the batch takes
+constexpr int kPbF = 2 * kPbMax + 3;     // frontier entries per lane
+constexpr uint32_t kPbBytes = kPbF * 32 * 2 + 64 * 2;  // 960, a multiple of 16
+
+// Returns true when the multi exit fired.
+SA_DEV bool prune_batch(Ctx& x, unsigned char* pb, int B) {
+    const AlignLaunch& a = *x.a;
+    const int lane = x.lane;
+    short* PF = reinterpret_cast<short*>(pb);
+    uint8_t* slot_c = pb + kPbF * 32 * 2;  // slot -> candidate of the batch
+    uint8_t* slot_b = slot_c + 64;          // slot -> anchor bit
+    // 1. the next candidates in selection order (argmax order; nothing changes
+    //    counts in this loop), up to 32 candidates and 64 anchors
+    int my_idx = 0, nc = 0, ns = 0;
+    uint32_t my_cnt = 0;
+    while (nc < 32 && x.n_unscored > 0) {
+        const int bi = pick_best(x);
+        const int na = __popcll(static_cast<long long>(x.t.cmask[bi]));
+        if (ns + na > 64) break;
+        if (lane == nc) {
+            my_idx = bi;
+            my_cnt = static_cast<uint32_t>(na);
+        }
+        __syncwarp();
+        if (lane == 0) x.t.ccnt[bi] |= kScored;
+        __syncwarp();
+        x.n_unscored--;
+        ++nc;
+        ns += na;
+    }
+    uint32_t my_start = my_cnt;  // exclusive scan of anchor counts
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(FULL, my_start, o);
+        if (lane >= o) my_start += v;
+    }
+    my_start -= my_cnt;
+    const unsigned long long my_key = x.t.ckey[my_idx];
+    if (lane < nc) {
+        uint32_t s = my_start;
+        for (unsigned long long m = x.t.cmask[my_idx]; m != 0ull; m &= m - 1ull, ++s) {
+            slot_c[s] = static_cast<uint8_t>(lane);
+            slot_b[s] = static_cast<uint8_t>(__ffsll(static_cast<long long>(m)) - 1);
+        }
+    }
+    __syncwarp();
+    // 2. one anchor per lane (two passes when the batch holds more than 32)
+    int dist[2] = {-1, -1};
+    uint64_t anc[2] = {0, 0};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int sl = lane + 32 * h;
+        const int j = sl < ns ? slot_c[sl] : 0;
+        const unsigned long long kk = __shfl_sync(FULL, my_key, j);
+        if (sl < ns) {
+            const uint64_t anchor = (kk >> 1) * static_cast<uint64_t>(a.bs) + slot_b[sl];
+            anc[h] = anchor;
+            if (anchor < a.glen) {
+                const uint64_t rem = a.glen - anchor;
+                const uint64_t want = static_cast<uint64_t>(x.len) + static_cast<uint64_t>(B);
+                const int w = static_cast<int>(want < rem ? want : rem);
+                dist[h] = lv_thread((kk & 1ull) ? x.C : x.R, x.len, a.planes, static_cast<uint32_t>(anchor), w, B,
+                                    PF + lane, 32, x.cells, B);
             }
         }
-        // warp argmax of (seeds_hitting, then smallest (amin, dir)) with three
-        // single-instruction reductions instead of a 5-step shuffle tree of
-        // three values (score_best was 18% of the warp kernel at C2)
-        const uint32_t mc = __reduce_max_sync(FULL, bc);
-        const bool in = bi >= 0 && bc == mc;
-        const uint32_t khi = static_cast<uint32_t>(bk >> 32), klo = static_cast<uint32_t>(bk);
-        const uint32_t mhi = __reduce_min_sync(FULL, in ? khi : 0xffffffffu);
-        const uint32_t mlo = __reduce_min_sync(FULL, in && khi == mhi ? klo : 0xffffffffu);
-        const uint32_t win = __ballot_sync(FULL, in && khi == mhi && klo == mlo);
-        if (win == 0u) return;  // nothing unscored
-        bi = __shfl_sync(FULL, bi, __ffs(win) - 1);
     }
-    score_candidate<kRegLV>(x, static_cast<uint32_t>(bi));
+    // 3. replay the loop candidate by candidate (uniform control)
+    const int c = a.c, d_max = x.d_max;
+    for (int j = 0; j < nc; ++j) {
+        const uint32_t st = __shfl_sync(FULL, my_start, j), cnt = __shfl_sync(FULL, my_cnt, j);
+        const unsigned long long kk = __shfl_sync(FULL, my_key, j);
+        int d_limit;  // REF aligner.cpp:176-183
+        if (x.tr.d_best > d_max) d_limit = d_max + c - 1;
+        else if (x.tr.d_second >= x.tr.d_best + c) d_limit = x.tr.d_best + c - 1;
+        else d_limit = x.tr.d_best - 1;
+        if (a.force) d_limit = d_max + c - 1;
+        if (d_limit >= 0) {  // (:184)
+            // this candidate's anchors, ascending: slots st .. st+cnt-1
+            uint32_t valid[2], early[2], keyv = 0xffffffffu, wsum = 0;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t sl = static_cast<uint32_t>(lane + 32 * h);
+                const bool mine = sl >= st && sl < st + cnt && anc[h] < a.glen;
+                const int dd = (mine && dist[h] >= 0 && dist[h] <= d_limit) ? dist[h] : -1;
+                valid[h] = __ballot_sync(FULL, mine);
+                early[h] = __ballot_sync(FULL, mine && dd < 0);
+                if (mine) {
+                    const uint64_t rem = a.glen - anc[h];
+                    const uint64_t want = static_cast<uint64_t>(x.len) + static_cast<uint64_t>(d_limit);
+                    wsum += static_cast<uint32_t>(want < rem ? want : rem);
+                    if (dd >= 0) keyv = min(keyv, (static_cast<uint32_t>(dd) << 8) | sl);
+                }
+            }
+            const uint32_t nv = __popc(valid[0]) + __popc(valid[1]);
+            if (nv > 0) {
+                // calls, counted in anchor order: only the read's very first
+                // call is not "after first" (REF aligner.cpp:200-205)
+                const uint32_t first_lane = valid[0] ? (__ffs(valid[0]) - 1) : 32 + (__ffs(valid[1]) - 1);
+                uint32_t ne = __popc(early[0]) + __popc(early[1]);
+                uint32_t na = nv;
+                if (x.calls == 0) {
+                    --na;
+                    const uint32_t fm = first_lane < 32 ? early[0] : early[1];
+                    if ((fm >> (first_lane & 31)) & 1u) --ne;
+                }
+                stat_add(x, S_DIST, nv);
+                stat_add(x, S_DIST_AFTER, na);
+                stat_add(x, S_EARLY_OUT, ne);
+                stat_add(x, S_WINDOW, __reduce_add_sync(FULL, wsum));
+                x.calls += nv;
+            }
+            const uint32_t best = __reduce_min_sync(FULL, keyv);
+            const int dir = static_cast<int>(kk & 1ull);
+            if (!x.first_done) {
+                x.first_done = true;
+                if (best != 0xffffffffu) {
+                    x.first_valid = true;
+                    x.first_pos = (kk >> 1) * static_cast<uint64_t>(a.bs) + slot_b[best & 0xffu];
+                    x.first_dir = dir;
+                }
+            }
+            if (best != 0xffffffffu) {
+                const uint64_t anchor = (kk >> 1) * static_cast<uint64_t>(a.bs) + slot_b[best & 0xffu];
+                tracker_observe(x.tr, a.bs, static_cast<int>(best >> 8), anchor, dir);
+            }
+        }
+        if (x.tr.d_best < c && x.tr.d_second < x.tr.d_best + c) return true;  // REF :307-312
+    }
+    __syncwarp();
+    return false;
 }
 
 SA_DEV void clear_table(CandTable& t, uint32_t n_cands, bool full, int lane) {
@@ -583,7 +739,8 @@ SA_DEV void resolve_wave0(const AlignLaunch& a, int n_eff, int len, uint4* recs,
 // table overflowed (nothing committed).
 template <bool kRegLV>
 SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
-                      unsigned long long& acc, uint4* recs, bool wave0_ready, const uint4* grecs = nullptr) {
+                      unsigned long long& acc, uint4* recs, bool wave0_ready, const uint4* grecs = nullptr,
+                      unsigned char* pb = nullptr) {
     const AlignLaunch& a = *x.a;
     const int lane = x.lane;
     const int len = x.len;
@@ -761,6 +918,20 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
         } else if (x.n_unscored == 0) {
             break;
         }
+#if SA_PRUNE_BATCH
+        if (pruning && pb != nullptr) {  // the rest of the pruning loop, a batch at a time
+            const int cmax = x.d_max + a.c - 1;
+            const int B = (a.force || x.tr.d_best > x.d_max) ? cmax : x.tr.d_best + a.c - 1;
+            if (B >= 0 && B <= kPbMax) {
+                if (prune_batch(x, pb, B)) {
+                    stat_add(x, S_MULTI, 1u);
+                    early_multi = true;
+                    break;
+                }
+                continue;
+            }
+        }
+#endif
         score_best<kRegLV>(x);  // REF :288 (and :306 inside the pruning loop)
         if (x.tr.d_best < a.c && x.tr.d_second < x.tr.d_best + a.c) {  // REF :290-295 / :307-312
             stat_add(x, S_MULTI, 1u);
@@ -1451,6 +1622,8 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
     Ctx x;
     x.a = &a;
     x.lane = lane;
+    // pruning-batch area at the end of the warp's share (capi.cu make_shape)
+    unsigned char* pb = a.pb_on ? ws + a.smem_per_warp - kPbBytes : nullptr;
     uint4* planes = reinterpret_cast<uint4*>(ws);  // buffer q: R = planes + 2q*wbr, C = R + wbr
     x.W = planes + (a.prefetch ? 4 : 2) * a.wbr;  // one {R, C} buffer without the read pipeline
     uint4* recs = x.W + (a.gw ? 0 : a.wbw);  // 2 x 32; no window area when the LV reads the genome in place
@@ -1550,7 +1723,7 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
             x.d_max = a.dmax_param >= 0 ? a.dmax_param : (12 * len + 99) / 100;
             const int ne = ne_pre >= 0 ? ne_pre : (q ? n_eff1 : n_eff0);
             if (!align_one<kRegLV>(x, r, ne, offs + q * a.n_off_cap, len / a.s, acc, recs + 32 * q, wave0_ready,
-                                   grecs))
+                                   grecs, pb))
                 overflowed(r);
         }
     };
@@ -2010,6 +2183,8 @@ void launch_lookup(const LookupLaunch& a, cudaStream_t st) {
     if (g < 1) g = 1;
     lookup_kernel<<<static_cast<int>(g), 128, 0, st>>>(a);
 }
+
+uint32_t prune_batch_bytes() { return kPbBytes; }
 
 cudaError_t align_set_smem(uint32_t smem_bytes) {
     const int b = static_cast<int>(smem_bytes);

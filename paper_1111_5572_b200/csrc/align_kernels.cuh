@@ -93,6 +93,9 @@ struct AlignLaunch {
     const unsigned int* work_count;
     unsigned char* gscratch;
     uint64_t gscratch_per_warp;
+    // pruning batch (align.cu prune_batch): its shared-memory area, the last
+    // prune_batch_bytes() of each warp's share, exists
+    int pb_on;
 };
 
 #ifndef SA_FAST_WARPS
@@ -157,5 +160,6 @@ void launch_lv_batch(const LvLaunch& a, int grid, int block, cudaStream_t st);
 void launch_lookup(const LookupLaunch& a, cudaStream_t st);
 cudaError_t align_fast_occupancy(const AlignLaunch& a, int block, uint32_t smem_bytes, int* blocks_per_sm);
 cudaError_t align_set_smem(uint32_t smem_bytes);
+uint32_t prune_batch_bytes();  // per warp, appended to the align kernels' shared-memory layout
 
 }  // namespace sab

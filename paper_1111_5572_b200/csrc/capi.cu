@@ -266,8 +266,12 @@ int make_shape(Replica& rep, const sa_params* p, uint64_t Lmax, LaunchShape& sh,
         return 16ull * ((a.prefetch ? 4 : 2) * a.wbr + (gw ? 0 : a.wbw) + 64 + 32) + 8ull * 32 +
                4ull * (2 * a.n_off_cap + f_ints_for(f16)) + 8ull * kNumStats;
     };
+    // the pruning batch's area (align.cu prune_batch) closes each warp's share
+    static const bool no_pb = getenv("SA_NO_PRUNE_BATCH") != nullptr;
+    a.pb_on = no_pb ? 0 : 1;
+    const uint64_t pb_bytes = a.pb_on ? prune_batch_bytes() : 0;
     auto spw_for = [&](int f16, int gw) {
-        return round16(common_for(f16, gw) + 8ull * a.sbw + cand_table_bytes(a.cap, a.hcap));
+        return round16(common_for(f16, gw) + 8ull * a.sbw + cand_table_bytes(a.cap, a.hcap)) + pb_bytes;
     };
     const uint32_t kMaxSmem = 227 * 1024;
     // warps per block (<= SA_FAST_WARPS) that fit the most warps per SM under
@@ -379,7 +383,7 @@ int make_shape(Replica& rep, const sa_params* p, uint64_t Lmax, LaunchShape& sh,
     sh.slow_cap = static_cast<int>(cap_slow);
     sh.slow_hcap = static_cast<int>(hcap_slow);
     sh.slow_table_bytes = (cand_table_bytes(sh.slow_cap, sh.slow_hcap) + 255) & ~255ull;
-    sh.slow_smem_per_warp = round16(common);
+    sh.slow_smem_per_warp = round16(common) + pb_bytes;
     uint64_t slow_warps = std::min<uint64_t>(static_cast<uint64_t>(rep.sm_count) * 24,
                                              std::max<uint64_t>(32, kSlowScratchBudget / sh.slow_table_bytes));
     // 8-warp blocks where shared memory allows: the device path launches this

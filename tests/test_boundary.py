@@ -156,3 +156,20 @@ def test_cpp_adapter_compiles_and_links(tmp_path):
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
     assert subprocess.run([str(exe)]).returncode == 0
+
+
+@pytest.mark.gpu
+def test_cpp_dropin_runs_against_the_reference():
+    """The C++ drop-in executed (tests/cpp/dropin_main.cpp, built by
+    oracle.build() where the reference headers are): the reference's
+    Aligner and snap_b200::Aligner in one process over the same
+    run_align-style pageable reads (REF src/driver.cpp:99-132), every
+    AlignmentResult field and counter equal over three parameter sets, and
+    the same exception types for bad params, a seed-size mismatch and a bad
+    character."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "dropin_test")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/dropin_test not built (needs /root/reference at build time)")
+    r = subprocess.run([exe, "200000"], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    assert "DROPIN OK 600000 0" in r.stdout
