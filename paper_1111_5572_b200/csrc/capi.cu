@@ -1098,10 +1098,18 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
         const uint64_t b0 = offsets[r0], b1 = offsets[r1];
         if ((bad = ensure_stage(ctx, st, b1 - b0, r1 - r0))) break;
         if ((bad = ensure_pre(ctx, st, r1 - r0, sh))) break;
-        if ((stage_in || stage_out) &&
-            (bad = ensure_host_staging(ctx, st, stage_in ? (b1 - b0) + (r1 - r0 + 1) * sizeof(uint64_t) + 8 : 0,
-                                       stage_out ? r1 - r0 : 0)))
-            break;
+        if (stage_in || stage_out) {
+            // the stage's pinned buffers may grow (the chunk ramp): first
+            // finish with their previous chunk (its H2D landed, its results
+            // handed to the caller)
+            if (k >= kPipeStages) {
+                if ((bad = drain_results(st))) break;
+                CUDA_TRY(ctx, cudaEventSynchronize(st.e_in));
+            }
+            if ((bad = ensure_host_staging(ctx, st, stage_in ? (b1 - b0) + (r1 - r0 + 1) * sizeof(uint64_t) + 8 : 0,
+                                           stage_out ? r1 - r0 : 0)))
+                break;
+        }
         if (k == 0) {
             if ((bad = ensure_defer(ctx, rep, n_reads))) break;
             CUDA_TRY(ctx, cudaEventRecord(S.e_begin, S.ci));
