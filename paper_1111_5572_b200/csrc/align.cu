@@ -478,115 +478,212 @@ SA_DEV void score_best(Ctx& x) {
 // counters per anchor in order, min with the earliest anchor on ties, one
 // observe, the multi exit.  Same results and counters as scoring them one by
 // one (dp_cells aside, which is implementation-specific).
-// Shared memory per warp: the lanes' frontiers [kPbF][32] shorts, then 64
-// slot entries (candidate of the batch, anchor bit).
+// Shared memory per warp: the lanes' frontiers [kPbF][32] shorts, 64 slot
+// entries (candidate of the batch, anchor bit), and the selection order.
 #ifndef SA_PRUNE_BATCH
 #define SA_PRUNE_BATCH 1
 #endif
 constexpr int kPbMax = 5;                // largest bound B the batch takes
 constexpr int kPbF = 2 * kPbMax + 3;     // frontier entries per lane
-constexpr uint32_t kPbBytes = kPbF * 32 * 2 + 64 * 2;  // 960, a multiple of 16
+constexpr uint32_t kPbBytes = kPbF * 32 * 2 + 64 * 2 + 64;  // 1024, a multiple of 16
 
-// Returns true when the multi exit fired.
-SA_DEV bool prune_batch(Ctx& x, unsigned char* pb, int B) {
+SA_DEV unsigned long long shfl64(unsigned long long v, int src) {
+    const uint32_t lo = __shfl_sync(FULL, static_cast<uint32_t>(v), src);
+    const uint32_t hi = __shfl_sync(FULL, static_cast<uint32_t>(v >> 32), src);
+    return (static_cast<unsigned long long>(hi) << 32) | lo;
+}
+
+// Selection order of the unscored candidates (the table holds <= 64):
+// bitonic sort of 64 keys, two per lane, on (seeds_hitting desc, amin asc,
+// Forward first) -- the order score_best_candidate's repeated argmax takes
+// (REF aligner.cpp:141-167) when nothing changes the counts.  order[p] =
+// candidate index at position p.  Returns false (nothing written) when a
+// count does not fit the key.
+SA_DEV bool select_order(Ctx& x, uint8_t* order) {
+    const AlignLaunch& a = *x.a;
+    const int lane = x.lane;
+    unsigned long long v[2];
+    bool ok = true;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const uint32_t j = 2 * lane + h;
+        v[h] = ~0ull;
+        if (j < x.n_cands) {
+            const uint32_t cc = x.t.ccnt[j];
+            if (!(cc & kScored)) {
+                ok &= cc < 0xffffu;
+                const unsigned long long kk = x.t.ckey[j];
+                const unsigned long long amin =
+                    (kk >> 1) * static_cast<unsigned long long>(a.bs) +
+                    static_cast<unsigned long long>(__ffsll(static_cast<long long>(x.t.cmask[j])) - 1);
+                v[h] = (static_cast<unsigned long long>(0xffffu - cc) << 48) | (amin << 7) | ((kk & 1ull) << 6) | j;
+            }
+        }
+    }
+    if (!__all_sync(FULL, ok)) return false;
+#pragma unroll
+    for (int k = 2; k <= 64; k <<= 1) {
+        const bool up = ((2 * lane) & k) == 0;
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j == 1) {
+                const unsigned long long lo = min(v[0], v[1]), hi = max(v[0], v[1]);
+                v[0] = up ? lo : hi;
+                v[1] = up ? hi : lo;
+            } else {
+                const int pl = lane ^ (j >> 1);
+                const bool keep_min = ((lane & (j >> 1)) == 0) == up;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const unsigned long long o = shfl64(v[h], pl);
+                    v[h] = keep_min ? min(v[h], o) : max(v[h], o);
+                }
+            }
+        }
+    }
+    order[2 * lane] = static_cast<uint8_t>(v[0] & 63u);
+    order[2 * lane + 1] = static_cast<uint8_t>(v[1] & 63u);
+    __syncwarp();
+    return true;
+}
+
+// The whole rest of the pruning loop.  Returns true when the multi exit fired.
+SA_DEV bool prune_all(Ctx& x, unsigned char* pb, int B) {
     const AlignLaunch& a = *x.a;
     const int lane = x.lane;
     short* PF = reinterpret_cast<short*>(pb);
     uint8_t* slot_c = pb + kPbF * 32 * 2;  // slot -> candidate of the batch
     uint8_t* slot_b = slot_c + 64;          // slot -> anchor bit
-    // 1. the next candidates in selection order (argmax order; nothing changes
-    //    counts in this loop), up to 32 candidates and 64 anchors
-    int my_idx = 0, nc = 0, ns = 0;
-    uint32_t my_cnt = 0;
-    while (nc < 32 && x.n_unscored > 0) {
-        const int bi = pick_best(x);
-        const int na = __popcll(static_cast<long long>(x.t.cmask[bi]));
-        if (ns + na > 64) break;
-        if (lane == nc) {
-            my_idx = bi;
-            my_cnt = static_cast<uint32_t>(na);
-        }
-        __syncwarp();
-        if (lane == 0) x.t.ccnt[bi] |= kScored;
-        __syncwarp();
-        x.n_unscored--;
-        ++nc;
-        ns += na;
-    }
-    uint32_t my_start = my_cnt;  // exclusive scan of anchor counts
+    uint8_t* order = slot_b + 64;           // selection order (tables of <= 64)
+    const bool sorted = x.n_cands <= 64 && select_order(x, order);
+    const int c = a.c, d_max = x.d_max;
+    uint32_t pos = 0;  // next position in the selection order
+    while (x.n_unscored > 0) {
+        // 1. the next candidates in selection order, up to 32 candidates and
+        //    64 anchors; lane j holds the j-th
+        int my_idx = 0, nc = 0;
+        uint32_t my_cnt = 0, my_start = 0;
+        if (sorted) {
+            const uint32_t p = pos + lane;
+            const bool have = p < pos + x.n_unscored;
+            if (have) {
+                my_idx = order[p];
+                my_cnt = __popcll(static_cast<long long>(x.t.cmask[my_idx]));
+            }
+            my_start = my_cnt;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t v = __shfl_up_sync(FULL, my_start, o);
-        if (lane >= o) my_start += v;
-    }
-    my_start -= my_cnt;
-    const unsigned long long my_key = x.t.ckey[my_idx];
-    if (lane < nc) {
-        uint32_t s = my_start;
-        for (unsigned long long m = x.t.cmask[my_idx]; m != 0ull; m &= m - 1ull, ++s) {
-            slot_c[s] = static_cast<uint8_t>(lane);
-            slot_b[s] = static_cast<uint8_t>(__ffsll(static_cast<long long>(m)) - 1);
-        }
-    }
-    __syncwarp();
-    // 2. one anchor per lane (two passes when the batch holds more than 32)
-    int dist[2] = {-1, -1};
-    uint64_t anc[2] = {0, 0};
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const int sl = lane + 32 * h;
-        const int j = sl < ns ? slot_c[sl] : 0;
-        const unsigned long long kk = __shfl_sync(FULL, my_key, j);
-        if (sl < ns) {
-            const uint64_t anchor = (kk >> 1) * static_cast<uint64_t>(a.bs) + slot_b[sl];
-            anc[h] = anchor;
-            if (anchor < a.glen) {
-                const uint64_t rem = a.glen - anchor;
-                const uint64_t want = static_cast<uint64_t>(x.len) + static_cast<uint64_t>(B);
-                const int w = static_cast<int>(want < rem ? want : rem);
-                dist[h] = lv_thread((kk & 1ull) ? x.C : x.R, x.len, a.planes, static_cast<uint32_t>(anchor), w, B,
-                                    PF + lane, 32, x.cells, B);
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(FULL, my_start, o);
+                if (lane >= o) my_start += t;
+            }
+            nc = __popc(__ballot_sync(FULL, have && my_start <= 64));  // my_start is the inclusive end here
+            my_start -= my_cnt;
+            if (lane < nc) x.t.ccnt[my_idx] |= kScored;
+            __syncwarp();
+            pos += nc;
+        } else {  // repeated argmax (larger tables: the global-table kernel)
+            int ns = 0;
+            while (nc < 32 && x.n_unscored > static_cast<uint32_t>(nc)) {
+                const int bi = pick_best(x);
+                const int na = __popcll(static_cast<long long>(x.t.cmask[bi]));
+                if (ns + na > 64) break;
+                if (lane == nc) {
+                    my_idx = bi;
+                    my_cnt = static_cast<uint32_t>(na);
+                    my_start = static_cast<uint32_t>(ns);
+                }
+                __syncwarp();
+                if (lane == 0) x.t.ccnt[bi] |= kScored;
+                __syncwarp();
+                ++nc;
+                ns += na;
             }
         }
-    }
-    // 3. replay the loop candidate by candidate (uniform control)
-    const int c = a.c, d_max = x.d_max;
-    for (int j = 0; j < nc; ++j) {
-        const uint32_t st = __shfl_sync(FULL, my_start, j), cnt = __shfl_sync(FULL, my_cnt, j);
-        const unsigned long long kk = __shfl_sync(FULL, my_key, j);
-        int d_limit;  // REF aligner.cpp:176-183
-        if (x.tr.d_best > d_max) d_limit = d_max + c - 1;
-        else if (x.tr.d_second >= x.tr.d_best + c) d_limit = x.tr.d_best + c - 1;
-        else d_limit = x.tr.d_best - 1;
-        if (a.force) d_limit = d_max + c - 1;
-        if (d_limit >= 0) {  // (:184)
-            // this candidate's anchors, ascending: slots st .. st+cnt-1
-            uint32_t valid[2], early[2], keyv = 0xffffffffu, wsum = 0;
+        x.n_unscored -= nc;
+        const unsigned long long my_key = x.t.ckey[my_idx];
+        const uint32_t ns = __shfl_sync(FULL, my_start + my_cnt, nc - 1);
+        if (lane < nc) {
+            uint32_t sl = my_start;
+            for (unsigned long long m = x.t.cmask[my_idx]; m != 0ull; m &= m - 1ull, ++sl) {
+                slot_c[sl] = static_cast<uint8_t>(lane);
+                slot_b[sl] = static_cast<uint8_t>(__ffsll(static_cast<long long>(m)) - 1);
+            }
+        }
+        __syncwarp();
+        // 2. one anchor per lane (two passes when the batch holds more than 32)
+        int dist[2] = {-1, -1};
+        uint32_t cand[2] = {0xffu, 0xffu}, rem[2] = {0, 0};
+        bool valid[2] = {false, false};
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const uint32_t sl = static_cast<uint32_t>(lane + 32 * h);
-                const bool mine = sl >= st && sl < st + cnt && anc[h] < a.glen;
-                const int dd = (mine && dist[h] >= 0 && dist[h] <= d_limit) ? dist[h] : -1;
-                valid[h] = __ballot_sync(FULL, mine);
-                early[h] = __ballot_sync(FULL, mine && dd < 0);
-                if (mine) {
-                    const uint64_t rem = a.glen - anc[h];
-                    const uint64_t want = static_cast<uint64_t>(x.len) + static_cast<uint64_t>(d_limit);
-                    wsum += static_cast<uint32_t>(want < rem ? want : rem);
-                    if (dd >= 0) keyv = min(keyv, (static_cast<uint32_t>(dd) << 8) | sl);
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t sl = lane + 32 * h;
+            const int j = sl < ns ? slot_c[sl] : 0;
+            const unsigned long long kk = __shfl_sync(FULL, my_key, j);
+            if (sl < ns) {
+                cand[h] = static_cast<uint32_t>(j);
+                const uint64_t anchor = (kk >> 1) * static_cast<uint64_t>(a.bs) + slot_b[sl];
+                if (anchor < a.glen) {
+                    valid[h] = true;
+                    const uint64_t rm = a.glen - anchor;
+                    rem[h] = rm < 0xffffffffull ? static_cast<uint32_t>(rm) : 0xffffffffu;
+                    const uint64_t want = static_cast<uint64_t>(x.len) + static_cast<uint64_t>(B);
+                    const int w = static_cast<int>(want < rm ? want : rm);
+                    dist[h] = lv_thread((kk & 1ull) ? x.C : x.R, x.len, a.planes, static_cast<uint32_t>(anchor), w, B,
+                                        PF + lane, 32, x.cells, B);
                 }
             }
-            const uint32_t nv = __popc(valid[0]) + __popc(valid[1]);
+        }
+        // 3. replay (uniform control).  Between two candidates that observe
+        // something the tracker -- and so d_limit -- is constant, and a
+        // candidate none of whose anchors is within d_limit only moves
+        // counters: such runs are applied in bulk.
+        int j0 = 0;
+        while (j0 < nc) {
+            int d_limit;  // REF aligner.cpp:176-183
+            if (x.tr.d_best > d_max) d_limit = d_max + c - 1;
+            else if (x.tr.d_second >= x.tr.d_best + c) d_limit = x.tr.d_best + c - 1;
+            else d_limit = x.tr.d_best - 1;
+            if (a.force) d_limit = d_max + c - 1;
+            if (d_limit < 0) {  // (:184) scored, nothing else (not even first_scored_done_); then the multi check
+                ++j0;
+                if (x.tr.d_best < c && x.tr.d_second < x.tr.d_best + c) return true;
+                continue;
+            }
+            // first candidate (from j0) with an anchor within d_limit
+            uint32_t jh = static_cast<uint32_t>(nc);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const bool hit = valid[h] && cand[h] >= static_cast<uint32_t>(j0) && dist[h] >= 0 && dist[h] <= d_limit;
+                jh = min(jh, __reduce_min_sync(FULL, hit ? cand[h] : 0xffu));
+            }
+            // candidates j0 .. jh (jh included when < nc): their anchors' calls
+            // in order; only the read's very first call is not "after first"
+            // (REF aligner.cpp:196-205)
+            uint32_t nv = 0, ne = 0, wsum = 0, keyv = 0xffffffffu, firstv = 0xffffffffu;
+            bool mine[2], early[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t sl = lane + 32 * h;
+                mine[h] = valid[h] && cand[h] >= static_cast<uint32_t>(j0) && cand[h] <= jh;
+                const bool in_lim = mine[h] && dist[h] >= 0 && dist[h] <= d_limit;
+                early[h] = mine[h] && !in_lim;
+                nv += __popc(__ballot_sync(FULL, mine[h]));
+                ne += __popc(__ballot_sync(FULL, early[h]));
+                if (mine[h]) {
+                    const uint32_t want = static_cast<uint32_t>(x.len + d_limit);
+                    wsum += want < rem[h] ? want : rem[h];
+                    firstv = min(firstv, sl);
+                    if (in_lim) keyv = min(keyv, (static_cast<uint32_t>(dist[h]) << 8) | sl);
+                }
+            }
             if (nv > 0) {
-                // calls, counted in anchor order: only the read's very first
-                // call is not "after first" (REF aligner.cpp:200-205)
-                const uint32_t first_lane = valid[0] ? (__ffs(valid[0]) - 1) : 32 + (__ffs(valid[1]) - 1);
-                uint32_t ne = __popc(early[0]) + __popc(early[1]);
                 uint32_t na = nv;
-                if (x.calls == 0) {
+                if (x.calls == 0) {  // the first of these calls is the read's first
+                    const uint32_t fs = __reduce_min_sync(FULL, firstv);
                     --na;
-                    const uint32_t fm = first_lane < 32 ? early[0] : early[1];
-                    if ((fm >> (first_lane & 31)) & 1u) --ne;
+                    if (__any_sync(FULL, (early[0] && static_cast<uint32_t>(lane) == fs) ||
+                                             (early[1] && static_cast<uint32_t>(lane + 32) == fs)))
+                        --ne;
                 }
                 stat_add(x, S_DIST, nv);
                 stat_add(x, S_DIST_AFTER, na);
@@ -594,24 +691,25 @@ SA_DEV bool prune_batch(Ctx& x, unsigned char* pb, int B) {
                 stat_add(x, S_WINDOW, __reduce_add_sync(FULL, wsum));
                 x.calls += nv;
             }
+            if (!x.first_done && jh > static_cast<uint32_t>(j0)) x.first_done = true;  // first scored: nothing within
+            if (jh >= static_cast<uint32_t>(nc)) break;
+            // candidate jh: min distance, earliest anchor on ties, one observe
             const uint32_t best = __reduce_min_sync(FULL, keyv);
+            const unsigned long long kk = __shfl_sync(FULL, my_key, static_cast<int>(jh));
             const int dir = static_cast<int>(kk & 1ull);
+            const uint64_t anchor = (kk >> 1) * static_cast<uint64_t>(a.bs) + slot_b[best & 0xffu];
             if (!x.first_done) {
                 x.first_done = true;
-                if (best != 0xffffffffu) {
-                    x.first_valid = true;
-                    x.first_pos = (kk >> 1) * static_cast<uint64_t>(a.bs) + slot_b[best & 0xffu];
-                    x.first_dir = dir;
-                }
+                x.first_valid = true;
+                x.first_pos = anchor;
+                x.first_dir = dir;
             }
-            if (best != 0xffffffffu) {
-                const uint64_t anchor = (kk >> 1) * static_cast<uint64_t>(a.bs) + slot_b[best & 0xffu];
-                tracker_observe(x.tr, a.bs, static_cast<int>(best >> 8), anchor, dir);
-            }
+            tracker_observe(x.tr, a.bs, static_cast<int>(best >> 8), anchor, dir);
+            if (x.tr.d_best < c && x.tr.d_second < x.tr.d_best + c) return true;  // REF :307-312
+            j0 = static_cast<int>(jh) + 1;
         }
-        if (x.tr.d_best < c && x.tr.d_second < x.tr.d_best + c) return true;  // REF :307-312
+        __syncwarp();
     }
-    __syncwarp();
     return false;
 }
 
@@ -923,12 +1021,11 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
             const int cmax = x.d_max + a.c - 1;
             const int B = (a.force || x.tr.d_best > x.d_max) ? cmax : x.tr.d_best + a.c - 1;
             if (B >= 0 && B <= kPbMax) {
-                if (prune_batch(x, pb, B)) {
+                if (prune_all(x, pb, B)) {
                     stat_add(x, S_MULTI, 1u);
                     early_multi = true;
-                    break;
                 }
-                continue;
+                break;
             }
         }
 #endif
