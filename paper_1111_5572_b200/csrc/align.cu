@@ -1251,6 +1251,7 @@ __global__ void __launch_bounds__(kSoloThreads, SA_SOLO_MIN_BLOCKS) solo_kernel(
                         // REF :273-286: every hit of the seed votes for (anchor / bucket, dir)
                         const uint32_t cnt = rec.y;
                         if (cnt > static_cast<uint32_t>(SA_SOLO_MAX_HITS)) {  // long vote lists: the warp kernel
+                            if (a.dbg) atomicAdd(a.dbg + 0, 1u);
                             bail = true;
                             break;
                         }
@@ -1281,6 +1282,7 @@ __global__ void __launch_bounds__(kSoloThreads, SA_SOLO_MIN_BLOCKS) solo_kernel(
                                 ccnt[j * cs] += 1u;
                                 cmask[j * cs] |= bit;
                             } else if (n_cands == kSoloCands) {
+                                if (a.dbg) atomicAdd(a.dbg + 1, 1u);
                                 bail = true;
                                 break;
                             } else {
@@ -1342,6 +1344,7 @@ __global__ void __launch_bounds__(kSoloThreads, SA_SOLO_MIN_BLOCKS) solo_kernel(
                                                         &s_F[0][tid], cs, c.cells, SA_SOLO_MAX_E);
 #endif
                                 if (d == -2) {
+                                    if (a.dbg) atomicAdd(a.dbg + 2, 1u);
                                     bail = true;
                                     break;
                                 }
@@ -2239,14 +2242,23 @@ int launch_align_seeded(const AlignLaunch& a, int grid, int block, cudaStream_t 
         }();
         const uint64_t g = std::min<uint64_t>((static_cast<uint64_t>(a.n_reads) + kSoloThreads - 1) / kSoloThreads,
                                               std::max<uint64_t>(cap, 1));
-        solo_kernel<<<static_cast<int>(std::max<uint64_t>(g, 1)), kSoloThreads, 0, st>>>(a);
-        ++n;
         static const bool dbg = getenv("SA_DEBUG_SOLO") != nullptr;  // diagnostics: reads left to the warp kernel
+        static unsigned int* d_dbg = nullptr;
+        AlignLaunch sa = a;
         if (dbg) {
-            unsigned int n = 0;
+            if (!d_dbg) cudaMalloc(&d_dbg, 4 * sizeof(unsigned int));
+            cudaMemsetAsync(d_dbg, 0, 4 * sizeof(unsigned int), st);
+            sa.dbg = d_dbg;
+        }
+        solo_kernel<<<static_cast<int>(std::max<uint64_t>(g, 1)), kSoloThreads, 0, st>>>(sa);
+        ++n;
+        if (dbg) {
+            unsigned int n = 0, why[4] = {0, 0, 0, 0};
             cudaStreamSynchronize(st);
             cudaMemcpy(&n, a.pre_list_count, sizeof(n), cudaMemcpyDeviceToHost);
-            fprintf(stderr, "[solo] %u of %u reads to the warp kernel\n", n, a.n_reads);
+            cudaMemcpy(why, d_dbg, sizeof(why), cudaMemcpyDeviceToHost);
+            fprintf(stderr, "[solo] %u of %u reads to the warp kernel (hits %u, candidates %u, long LV %u)\n", n,
+                    a.n_reads, why[0], why[1], why[2]);
         }
     } else {
         b.pre_list = nullptr;

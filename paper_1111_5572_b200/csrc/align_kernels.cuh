@@ -96,6 +96,9 @@ struct AlignLaunch {
     // pruning batch (align.cu prune_batch): its shared-memory area, the last
     // prune_batch_bytes() of each warp's share, exists
     int pb_on;
+    // diagnostics (SA_DEBUG_SOLO): solo-kernel hand-over reasons
+    // [0] a seed with too many hits, [1] too many candidates, [2] a long LV
+    unsigned int* dbg;
 };
 
 #ifndef SA_FAST_WARPS
