@@ -341,6 +341,16 @@ SA_DEV bool insert_wave(Ctx& x, bool valid, unsigned long long key, int bit) {
     return true;
 }
 
+#ifndef SA_MASK_LV
+#define SA_MASK_LV 1  // reads <= 128 bases: the mask LV (lv.cuh lv_seg) for the warp kernel's scoring
+#endif
+
+SA_DEV unsigned long long shfl64(unsigned long long v, int src) {
+    const uint32_t lo = __shfl_sync(FULL, static_cast<uint32_t>(v), src);
+    const uint32_t hi = __shfl_sync(FULL, static_cast<uint32_t>(v >> 32), src);
+    return (static_cast<unsigned long long>(hi) << 32) | lo;
+}
+
 // REF aligner.cpp:169-221 score_candidate
 template <bool kRegLV>
 SA_DEV void score_candidate(Ctx& x, uint32_t idx) {
@@ -388,6 +398,52 @@ SA_DEV void score_candidate(Ctx& x, uint32_t idx) {
 
     int best_d = kInfDistance;
     uint64_t best_anchor = 0;
+#if SA_MASK_LV
+    if (kRegLV && x.len <= kMaskMaxLen) {
+        // mask LV (lv_seg): the bucket's anchors in segments of 2 d_limit + 1
+        // lanes, as many per pass as fit, in ascending order
+        const int wd = 2 * d_limit + 1, per = 32 / wd, seg = lane / wd;
+        const uint64_t nbg = (a.glen + 31) >> 5;
+        for (unsigned long long m = mm; m != 0ull;) {
+            unsigned long long mi = m;
+            for (int t = 0; t < seg && mi != 0ull; ++t) mi &= mi - 1ull;
+            const bool live = seg < per && mi != 0ull;
+            const uint64_t anchor = base_pos + static_cast<uint64_t>(__ffsll(static_cast<long long>(mi)) - 1);
+            const bool valid = live && anchor < a.glen;
+            int w = 0;
+            if (valid) {
+                const uint64_t rem = a.glen - anchor;
+                const uint64_t want = static_cast<uint64_t>(x.len) + static_cast<uint64_t>(d_limit);
+                w = static_cast<int>(want < rem ? want : rem);
+            }
+            const int d = lv_seg(orient, x.len, a.planes, nbg, anchor, w, valid, d_limit, lane, x.cells);
+            // per anchor, in order: one call each (REF aligner.cpp:193-210)
+            const bool leader = valid && lane == seg * wd;
+            const uint32_t vm = __ballot_sync(FULL, leader);
+            if (vm) {
+                const uint32_t em = __ballot_sync(FULL, leader && d < 0);
+                const uint32_t nv = __popc(vm);
+                uint32_t na = nv, ne = __popc(em);
+                if (x.calls == 0) {  // the read's first call is not "after first"
+                    --na;
+                    if (em & (vm & (0u - vm))) --ne;
+                }
+                stat_add(x, S_DIST, nv);
+                stat_add(x, S_DIST_AFTER, na);
+                stat_add(x, S_EARLY_OUT, ne);
+                stat_add(x, S_WINDOW, __reduce_add_sync(FULL, leader ? static_cast<uint32_t>(w) : 0u));
+                x.calls += nv;
+                const uint32_t kb = __reduce_min_sync(FULL, leader && d >= 0 ? (static_cast<uint32_t>(d) << 8) | lane
+                                                                            : 0xffffffffu);
+                if (kb != 0xffffffffu && static_cast<int>(kb >> 8) < best_d) {  // earlier passes win ties
+                    best_d = static_cast<int>(kb >> 8);
+                    best_anchor = shfl64(anchor, static_cast<int>(kb & 0xffu));
+                }
+            }
+            for (int t = 0; t < per && m != 0ull; ++t) m &= m - 1ull;
+        }
+    } else
+#endif
     for (unsigned long long m = mm; m != 0ull; m &= m - 1ull) {
         const uint64_t anchor = base_pos + static_cast<uint64_t>(__ffsll(static_cast<long long>(m)) - 1);
         if (anchor >= a.glen) continue;
@@ -485,13 +541,7 @@ SA_DEV void score_best(Ctx& x) {
 #endif
 constexpr int kPbMax = 5;                // largest bound B the batch takes
 constexpr int kPbF = 2 * kPbMax + 3;     // frontier entries per lane
-constexpr uint32_t kPbBytes = kPbF * 32 * 2 + 64 * 2 + 64;  // 1024, a multiple of 16
-
-SA_DEV unsigned long long shfl64(unsigned long long v, int src) {
-    const uint32_t lo = __shfl_sync(FULL, static_cast<uint32_t>(v), src);
-    const uint32_t hi = __shfl_sync(FULL, static_cast<uint32_t>(v >> 32), src);
-    return (static_cast<unsigned long long>(hi) << 32) | lo;
-}
+constexpr uint32_t kPbBytes = kPbF * 32 * 2 + 64 * 4;  // 1088, a multiple of 16
 
 // Selection order of the unscored candidates (the table holds <= 64):
 // bitonic sort of 64 keys, two per lane, on (seeds_hitting desc, amin asc,
@@ -555,6 +605,8 @@ SA_DEV bool prune_all(Ctx& x, unsigned char* pb, int B) {
     uint8_t* slot_c = pb + kPbF * 32 * 2;  // slot -> candidate of the batch
     uint8_t* slot_b = slot_c + 64;          // slot -> anchor bit
     uint8_t* order = slot_b + 64;           // selection order (tables of <= 64)
+    int8_t* slot_d = reinterpret_cast<int8_t*>(order + 64);  // slot -> distance (mask LV passes)
+    const bool seg_lv = a.pb_on == 2 && x.len <= kMaskMaxLen;
     const bool sorted = x.n_cands <= 64 && select_order(x, order);
     const int c = a.c, d_max = x.d_max;
     uint32_t pos = 0;  // next position in the selection order
@@ -610,10 +662,32 @@ SA_DEV bool prune_all(Ctx& x, unsigned char* pb, int B) {
             }
         }
         __syncwarp();
-        // 2. one anchor per lane (two passes when the batch holds more than 32)
+        // 2. one anchor per lane (two passes when the batch holds more than 32),
+        //    or (pb_on == 2) mask-LV passes of 2B + 1 lanes per anchor
         int dist[2] = {-1, -1};
         uint32_t cand[2] = {0xffu, 0xffu}, rem[2] = {0, 0};
         bool valid[2] = {false, false};
+        if (seg_lv) {
+            const int wd = 2 * B + 1, per = 32 / wd, seg = lane / wd;
+            const uint64_t nbg = (a.glen + 31) >> 5;
+            for (uint32_t s0 = 0; s0 < ns; s0 += per) {
+                const uint32_t sl = s0 + seg;
+                const bool live = seg < per && sl < ns;
+                const int j = live ? slot_c[sl] : 0;
+                const unsigned long long kk = __shfl_sync(FULL, my_key, j);
+                const uint64_t anchor = (kk >> 1) * static_cast<uint64_t>(a.bs) + (live ? slot_b[sl] : 0);
+                const bool ok = live && anchor < a.glen;
+                int w = 0;
+                if (ok) {
+                    const uint64_t rm = a.glen - anchor;
+                    const uint64_t want = static_cast<uint64_t>(x.len) + static_cast<uint64_t>(B);
+                    w = static_cast<int>(want < rm ? want : rm);
+                }
+                const int d = lv_seg((kk & 1ull) ? x.C : x.R, x.len, a.planes, nbg, anchor, w, ok, B, lane, x.cells);
+                if (ok && lane == seg * wd) slot_d[sl] = static_cast<int8_t>(d);
+            }
+            __syncwarp();
+        }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const uint32_t sl = lane + 32 * h;
@@ -626,10 +700,14 @@ SA_DEV bool prune_all(Ctx& x, unsigned char* pb, int B) {
                     valid[h] = true;
                     const uint64_t rm = a.glen - anchor;
                     rem[h] = rm < 0xffffffffull ? static_cast<uint32_t>(rm) : 0xffffffffu;
-                    const uint64_t want = static_cast<uint64_t>(x.len) + static_cast<uint64_t>(B);
-                    const int w = static_cast<int>(want < rm ? want : rm);
-                    dist[h] = lv_thread((kk & 1ull) ? x.C : x.R, x.len, a.planes, static_cast<uint32_t>(anchor), w, B,
-                                        PF + lane, 32, x.cells, B);
+                    if (seg_lv) {
+                        dist[h] = slot_d[sl];
+                    } else {
+                        const uint64_t want = static_cast<uint64_t>(x.len) + static_cast<uint64_t>(B);
+                        const int w = static_cast<int>(want < rm ? want : rm);
+                        dist[h] = lv_thread((kk & 1ull) ? x.C : x.R, x.len, a.planes, static_cast<uint32_t>(anchor), w,
+                                            B, PF + lane, 32, x.cells, B);
+                    }
                 }
             }
         }

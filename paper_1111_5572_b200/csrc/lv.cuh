@@ -225,6 +225,110 @@ SA_DEV int lv_bitpar(const uint4* R, int nblk, int m, const uint4* W, uint32_t w
     return best <= dl ? best : -1;
 }
 
+// ---------------------------------------------------------------- mask LV
+// Segmented register wavefront with precomputed mismatch masks, for reads of
+// at most 128 bases and d_limit <= 15 (same values as bounded_distance, REF
+// src/edit_distance.cpp:19-75).  The warp is cut into segments of
+// 2*dl + 1 lanes, one (read orientation, window) job per segment, lane
+// k + dl of a segment owning diagonal k.  Before the wavefront each lane
+// builds the 128-bit mismatch mask of its diagonal -- bit i set when read
+// base i differs from window base i + k or either is N (REF :11-13), and
+// every bit at or past cap = min(m, w - k) set -- from a handful of
+// independent loads issued together, so the slides are bit scans in
+// registers instead of a chain of dependent memory reads.  The recurrence,
+// guards and clamps are lv_step's exactly.
+constexpr int kMaskMaxLen = 128;
+
+// First set bit at or after i (0 <= i <= 128) of a 128-bit mask; 128 if none.
+SA_DEV int mask_next(const uint32_t (&M)[4], int i) {
+    const int q = i >> 5;
+    const uint32_t lc = ~0u << (i & 31);
+    const uint32_t t0 = q == 0 ? (M[0] & lc) : 0u;
+    const uint32_t t1 = q == 1 ? (M[1] & lc) : (q < 1 ? M[1] : 0u);
+    const uint32_t t2 = q == 2 ? (M[2] & lc) : (q < 2 ? M[2] : 0u);
+    const uint32_t t3 = q == 3 ? (M[3] & lc) : (q < 3 ? M[3] : 0u);
+    if (t0) return __ffs(t0) - 1;
+    if (t1) return 31 + __ffs(t1);
+    if (t2) return 63 + __ffs(t2);
+    if (t3) return 95 + __ffs(t3);
+    return 128;
+}
+
+// 32 genome bases at signed position p (bases before 0 or past the padded
+// planes read as N).  nbg = ceil(glen / 32): planes[0 .. nbg + 1] exist.
+SA_DEV void extract32_any(const uint4* planes, uint64_t nbg, int64_t p, uint32_t& lo, uint32_t& hi, uint32_t& n) {
+    if (p < 0) {
+        const int sft = static_cast<int>(-p);  // < 32
+        extract32_ldg(planes, 0, lo, hi, n);
+        lo <<= sft;
+        hi <<= sft;
+        n = (n << sft) | ((1u << sft) - 1u);
+    } else if ((static_cast<uint64_t>(p) >> 5) > nbg) {
+        lo = hi = 0;
+        n = 0xffffffffu;
+    } else {
+        extract32_ldg(planes, static_cast<uint64_t>(p), lo, hi, n);
+    }
+}
+
+// Segment jobs: this lane's segment reads R (m bases) against the genome
+// window starting at `anchor`, w bases long; live = the segment has a job.
+// Returns, in every lane of a live segment, its distance (<= dl) or -1.
+SA_DEV int lv_seg(const uint4* R, int m, const uint4* G, uint64_t nbg, uint64_t anchor, int w, bool live, int dl,
+                  int lane, uint32_t& cells) {
+    const int wd = 2 * dl + 1;
+    const int seg = lane / wd;
+    const int k = lane - seg * wd - dl;
+    const bool in = live && seg < 32 / wd;
+    const int cap = min(m, w - k);
+    uint32_t M[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        M[q] = 0xffffffffu;
+        if (in && 32 * q < m && 32 * q < cap) {
+            const uint4 r = R[q];
+            uint32_t wl, wh, wn;
+            extract32_any(G, nbg, static_cast<int64_t>(anchor) + k + 32 * q, wl, wh, wn);
+            M[q] = (r.x ^ wl) | (r.y ^ wh) | r.z | wn;
+        }
+        const int b0 = 32 * q;
+        if (cap <= b0) M[q] = 0xffffffffu;
+        else if (cap < b0 + 32) M[q] |= ~0u << (cap - b0);
+    }
+    const uint32_t segmask = in ? (((wd >= 32) ? 0xffffffffu : ((1u << wd) - 1u)) << (seg * wd)) : 0u;
+    int fr = kUnreach, res = -1;
+    bool done = !in;
+    for (int e = 0; e <= dl; ++e) {
+        int up = __shfl_down_sync(kLvFull, fr, 1);
+        int dn = __shfl_up_sync(kLvFull, fr, 1);
+        if (k == dl) up = kUnreach;
+        if (k == -dl) dn = kUnreach;
+        const bool active = !done && k >= -e && k <= e;
+        if (active) {
+            if (k > w) {
+                fr = kUnreach;  // whole diagonal outside the window (REF :47)
+            } else {
+                int cand = e == 0 ? 0 : max(max(fr + 1, up + 1), dn);
+                if (cand < max(0, -k)) {
+                    fr = kUnreach;  // (REF :56-59)
+                } else {
+                    cand = min(cand, cap);  // (REF :60)
+                    const int i = min(mask_next(M, cand), cap);
+                    cells += static_cast<uint32_t>(i - cand) + 1;
+                    fr = i;
+                }
+            }
+        }
+        const uint32_t hit = __ballot_sync(kLvFull, active && fr == m);
+        if (!done && (hit & segmask)) {
+            done = true;
+            res = e;
+        }
+        if (__all_sync(kLvFull, done)) break;
+    }
+    return res;
+}
+
 // standalone LV (lv_batch_kernel): any limit
 SA_DEV int lv_warp_any(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, int dl, int* F,
                        int lane, uint32_t& cells) {
