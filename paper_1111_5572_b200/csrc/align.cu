@@ -341,8 +341,11 @@ SA_DEV bool insert_wave(Ctx& x, bool valid, unsigned long long key, int bit) {
     return true;
 }
 
+#ifndef SA_PB_SEG
+#define SA_PB_SEG 0
+#endif
 #ifndef SA_MASK_LV
-#define SA_MASK_LV 1  // reads <= 128 bases: the mask LV (lv.cuh lv_seg) for the warp kernel's scoring
+#define SA_MASK_LV 0  // 1: the mask LV (lv.cuh lv_seg) scores reads <= 128 bases in the warp kernel (measured slower, see DESIGN)
 #endif
 
 SA_DEV unsigned long long shfl64(unsigned long long v, int src) {
@@ -571,10 +574,13 @@ SA_DEV bool select_order(Ctx& x, uint8_t* order) {
         }
     }
     if (!__all_sync(FULL, ok)) return false;
-#pragma unroll
+    // rolled loops: every warp entering the pruning loop runs this, and the
+    // unrolled network's ~1k instructions measured as instruction-fetch
+    // stalls (33% of the warp kernel's samples at C2)
+#pragma unroll 1
     for (int k = 2; k <= 64; k <<= 1) {
         const bool up = ((2 * lane) & k) == 0;
-#pragma unroll
+#pragma unroll 1
         for (int j = k >> 1; j > 0; j >>= 1) {
             if (j == 1) {
                 const unsigned long long lo = min(v[0], v[1]), hi = max(v[0], v[1]);
@@ -606,7 +612,11 @@ SA_DEV bool prune_all(Ctx& x, unsigned char* pb, int B) {
     uint8_t* slot_b = slot_c + 64;          // slot -> anchor bit
     uint8_t* order = slot_b + 64;           // selection order (tables of <= 64)
     int8_t* slot_d = reinterpret_cast<int8_t*>(order + 64);  // slot -> distance (mask LV passes)
+#if SA_PB_SEG
     const bool seg_lv = a.pb_on == 2 && x.len <= kMaskMaxLen;
+#else
+    constexpr bool seg_lv = false;  // SA_PB_SEG=1 builds the mask-LV batch (pb_on == 2; measured slower)
+#endif
     const bool sorted = x.n_cands <= 64 && select_order(x, order);
     const int c = a.c, d_max = x.d_max;
     uint32_t pos = 0;  // next position in the selection order
