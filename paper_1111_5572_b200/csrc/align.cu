@@ -455,6 +455,13 @@ SA_DEV void score_candidate(Ctx& x, uint32_t idx) {
         const int w = static_cast<int>(want < rem ? want : rem);
         const uint32_t wofs = static_cast<uint32_t>(anchor - gb0 * 32);
         const int d = lv_warp<kRegLV>(orient, x.len, Wsrc, wofs, w, d_limit, x.F, lane, x.cells, a.f16 != 0);
+#if SA_DEBUG_COUNTERS
+        if (a.dbg && lane == 0) {  // seed-loop (warp) LV: calls, iterations, d_limit sum
+            atomicAdd(a.dbg + 4, 1u);
+            atomicAdd(a.dbg + 5, static_cast<unsigned>(d >= 0 ? d + 1 : d_limit + 1));
+            atomicAdd(a.dbg + 6, static_cast<unsigned>(d_limit));
+        }
+#endif
         stat_add(x, S_DIST, 1u);
         x.calls++;
         stat_add(x, S_WINDOW, static_cast<uint32_t>(w));
@@ -1109,6 +1116,13 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
             const int cmax = x.d_max + a.c - 1;
             const int B = (a.force || x.tr.d_best > x.d_max) ? cmax : x.tr.d_best + a.c - 1;
             if (B >= 0 && B <= kPbMax) {
+#if SA_DEBUG_COUNTERS
+                if (a.dbg && lane == 0) {  // pruning batches: entries, candidates, B sum
+                    atomicAdd(a.dbg + 7, 1u);
+                    atomicAdd(a.dbg + 8, x.n_unscored);
+                    atomicAdd(a.dbg + 9, static_cast<unsigned>(B));
+                }
+#endif
                 if (prune_all(x, pb, B)) {
                     stat_add(x, S_MULTI, 1u);
                     early_multi = true;
@@ -2352,8 +2366,25 @@ int launch_align_seeded(const AlignLaunch& a, int grid, int block, cudaStream_t 
         b.pre_list = nullptr;
         b.pre_list_count = nullptr;
     }
+#if SA_DEBUG_COUNTERS
+    static unsigned int* d_wdbg = nullptr;
+    if (!d_wdbg) {
+        cudaMalloc(&d_wdbg, 16 * sizeof(unsigned int));
+    }
+    cudaMemsetAsync(d_wdbg, 0, 16 * sizeof(unsigned int), st);
+    b.dbg = d_wdbg;
+#endif
     if (b.dl_max <= 15) launch_variant<false, true, true, false, true>(b, grid, block, st);
     else launch_variant<false, true, false, false, true>(b, grid, block, st);
+#if SA_DEBUG_COUNTERS
+    {
+        unsigned int h[16];
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h, d_wdbg, sizeof(h), cudaMemcpyDeviceToHost);
+        fprintf(stderr, "[warp] reads %u: seed-loop LV calls %u iterations %u d_limit sum %u; pruning entries %u "
+                        "candidates %u B sum %u\n", a.pre_list_count ? 0u : a.n_reads, h[4], h[5], h[6], h[7], h[8], h[9]);
+    }
+#endif
     return n;
 }
 
