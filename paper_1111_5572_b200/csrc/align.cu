@@ -820,6 +820,25 @@ SA_DEV void clear_table(CandTable& t, uint32_t n_cands, bool full, int lane) {
 
 // per-seed flags
 constexpr uint32_t kSeedN = 1, kSeedQflip = 2, kSeedPal = 4, kSeedSingleRc = 8;
+// A seed the seed kernel left unprobed (beyond its eager count): the record
+// holds the canonical key in .y (low) / .z (high) until resolve_lazy probes it.
+constexpr uint32_t kSeedLazy = 16;
+
+// Probe a lazy record's key (REF seed_index.cpp:128-143), giving the record
+// the seed kernel would have written.
+SA_DEV uint4 resolve_lazy(const AlignLaunch& a, uint4 rec) {
+    const uint64_t canon = (static_cast<uint64_t>(rec.z) << 32) | rec.y;
+    uint32_t fl = rec.x & ~kSeedLazy;
+    unsigned pl = 0, m = 0;
+    const bool found = probe_slot(a.table, a.n_slots, canon, pl, m);
+    uint32_t c = 0;
+    if (found) {
+        const uint32_t ntot = m & 0x7fffffffu;
+        c = (fl & kSeedPal) ? 2u * ntot : ntot;
+        if (m & 0x80000000u) fl |= kSeedSingleRc;
+    }
+    return make_uint4(fl, c, found ? pl : 0u, rec.w);
+}
 
 
 // Seed at read offset `off` (planes R): flags (N / query-is-rc-of-canon /
@@ -955,6 +974,11 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
     int tested = 0;
     bool any_lookup = false, any_popular = false, early_multi = false, overflow = false;
 
+    if (grecs && wave0_ready && lane < n_eff) {  // wave 0 staged from the seed kernel: probe its lazy seeds
+        const uint4 rr = recs[lane];
+        if (rr.x & kSeedLazy) recs[lane] = resolve_lazy(a, rr);
+    }
+    __syncwarp();
     // The seed loop (REF :256-316) with the pruning loop (REF :296-315) folded
     // in, so score_best -- and the LV under it -- is inlined once.
     bool pruning = false;
@@ -965,7 +989,11 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
             if ((i & 31) == 0 && (i > 0 || !wave0_ready)) {  // speculative probes, seeds i .. i+31
                 if (grecs) {  // resolved by the seed kernel
                     __syncwarp();
-                    if (i + lane < n_eff) recs[lane] = grecs[i + lane];
+                    if (i + lane < n_eff) {
+                        uint4 rr = grecs[i + lane];
+                        if (rr.x & kSeedLazy) rr = resolve_lazy(a, rr);
+                        recs[lane] = rr;
+                    }
                     __syncwarp();
                 } else {
                     compute_wave_sync(a, x.R, offs, i, n_eff, len, recs, lane);
@@ -1334,7 +1362,8 @@ __global__ void __launch_bounds__(kSoloThreads, SA_SOLO_MIN_BLOCKS) solo_kernel(
                 for (;;) {
                     if (!pruning) {
                         if (i >= n_eff) break;
-                        const uint4 rec = __ldg(recs + i);
+                        uint4 rec = __ldg(recs + i);
+                        if (rec.x & kSeedLazy) rec = resolve_lazy(a, rec);  // probed on demand
                         if (rec.x & kSeedN) {  // REF :259-262
                             c.skip_n++;
                             ++i;
@@ -1765,15 +1794,22 @@ __global__ void __launch_bounds__(256, SA_SEED_MIN_BLOCKS) seed_kernel(const Ali
                         uint32_t fl = 0;
                         if (key != canon) fl |= kSeedQflip;
                         if (key == rck) fl |= kSeedPal;
-                        unsigned pl = 0, m = 0;
-                        const bool found = probe_slot(a.table, a.n_slots, canon, pl, m);
-                        uint32_t c = 0;
-                        if (found) {
-                            const uint32_t ntot = m & 0x7fffffffu;
-                            c = (fl & kSeedPal) ? 2u * ntot : ntot;
-                            if (m & 0x80000000u) fl |= kSeedSingleRc;
+                        if (a.eager > 0 && cnt + g >= a.eager) {
+                            // beyond the eager seeds: probed on demand by the
+                            // aligner (most reads stop after 2-4 lookups, C2 3.5)
+                            rv = make_uint4(fl | kSeedLazy, static_cast<uint32_t>(canon),
+                                            static_cast<uint32_t>(canon >> 32), static_cast<uint32_t>(my_off));
+                        } else {
+                            unsigned pl = 0, m = 0;
+                            const bool found = probe_slot(a.table, a.n_slots, canon, pl, m);
+                            uint32_t c = 0;
+                            if (found) {
+                                const uint32_t ntot = m & 0x7fffffffu;
+                                c = (fl & kSeedPal) ? 2u * ntot : ntot;
+                                if (m & 0x80000000u) fl |= kSeedSingleRc;
+                            }
+                            rv = make_uint4(fl, c, found ? pl : 0u, static_cast<uint32_t>(my_off));
                         }
-                        rv = make_uint4(fl, c, found ? pl : 0u, static_cast<uint32_t>(my_off));
                     }
                     rec[cnt + g] = rv;
                 }
@@ -1792,7 +1828,7 @@ __global__ void __launch_bounds__(256, SA_SEED_MIN_BLOCKS) seed_kernel(const Ali
 SA_DEV void prefetch_windows(const AlignLaunch& a, const uint4* recs, int n, int len, int lane) {
     if (lane < n && lane < 32) {
         const uint4 rr = recs[lane];
-        if (!(rr.x & kSeedN) && rr.y == 1u) {
+        if (!(rr.x & (kSeedN | kSeedLazy)) && rr.y == 1u) {
             const uint32_t dir = ((rr.x & kSeedSingleRc) ? 1u : 0u) ^ ((rr.x & kSeedQflip) ? 1u : 0u);
             const int o = static_cast<int>(rr.w);
             const int64_t anc = static_cast<int64_t>(rr.z) - (dir ? (len - a.s - o) : o);

@@ -99,6 +99,9 @@ struct AlignLaunch {
     // diagnostics (SA_DEBUG_SOLO): solo-kernel hand-over reasons
     // [0] a seed with too many hits, [1] too many candidates, [2] a long LV
     unsigned int* dbg;
+    // seed_kernel probes the first `eager` seeds of each read (0: all); the
+    // rest are left as lazy records for the aligner kernels to probe on demand
+    int eager;
 };
 
 #ifndef SA_FAST_WARPS

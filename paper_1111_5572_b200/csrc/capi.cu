@@ -274,6 +274,12 @@ int make_shape(Replica& rep, const sa_params* p, uint64_t Lmax, LaunchShape& sh,
         return e ? std::max(0, std::min(2, atoi(e))) : 1;
     }();
     a.pb_on = pb_mode;
+    // SA_EAGER_PROBES: seeds the seed kernel probes per read (0: all)
+    static const int eager = [] {
+        const char* e = getenv("SA_EAGER_PROBES");
+        return e ? std::max(0, atoi(e)) : 4;
+    }();
+    a.eager = eager;
     const uint64_t pb_bytes = a.pb_on ? prune_batch_bytes() : 0;
     auto spw_for = [&](int f16, int gw) {
         return round16(common_for(f16, gw) + 8ull * a.sbw + cand_table_bytes(a.cap, a.hcap)) + pb_bytes;
