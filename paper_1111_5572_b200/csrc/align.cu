@@ -1839,9 +1839,6 @@ SA_DEV void prefetch_windows(const AlignLaunch& a, const uint4* recs, int n, int
     }
 }
 
-#ifndef SA_MIN_BLOCKS
-#define SA_MIN_BLOCKS 3  // blocks of SA_FAST_WARPS warps per SM the register budget must allow
-#endif
 
 // kSlow: global candidate tables over a work list; kPipe: static striding with
 // the cp.async read pipeline (short reads); kRegLV: register LV only;

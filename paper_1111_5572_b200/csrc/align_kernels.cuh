@@ -107,6 +107,11 @@ struct AlignLaunch {
 #ifndef SA_FAST_WARPS
 #define SA_FAST_WARPS 8  // warps per block of the align kernels (compile-time: launch bounds)
 #endif
+#ifndef SA_MIN_BLOCKS
+#define SA_MIN_BLOCKS 3  // blocks of SA_FAST_WARPS warps per SM the register budget must allow
+#endif
+// warps per SM the align kernels' register budget allows
+constexpr int kRegWarpsPerSM = SA_FAST_WARPS * SA_MIN_BLOCKS;
 
 // Streamed chunk of read r.  Chunk sizes: 2^first_shift reads for the first
 // two chunks, then 2^shift each (both runtime launch fields): short first

@@ -292,7 +292,7 @@ int make_shape(Replica& rep, const sa_params* p, uint64_t Lmax, LaunchShape& sh,
         warps_sm = 0;
         for (int w = 1; w <= SA_FAST_WARPS; ++w) {
             if (static_cast<uint64_t>(w) * spw > kMaxSmem) break;
-            const int tot = std::min<int>(24 / w, static_cast<int>(kMaxSmem / (w * spw))) * w;
+            const int tot = std::min<int>(kRegWarpsPerSM / w, static_cast<int>(kMaxSmem / (w * spw))) * w;
             if (tot >= warps_sm) {
                 warps_sm = tot;
                 best_w = w;
@@ -342,8 +342,8 @@ int make_shape(Replica& rep, const sa_params* p, uint64_t Lmax, LaunchShape& sh,
     int warps = best_block(a.smem_per_warp, warps_sm);
     // shared-memory-limited layouts run best in small blocks (C3: 2-warp
     // blocks 139 ms, 7-warp 149 ms per 500 k reads)
-    if (warps_sm < 24 && warps > 2 && 2 * a.smem_per_warp <= kMaxSmem) {
-        const int tot2 = std::min<int>(12, static_cast<int>(kMaxSmem / (2 * a.smem_per_warp))) * 2;
+    if (warps_sm < kRegWarpsPerSM && warps > 2 && 2 * a.smem_per_warp <= kMaxSmem) {
+        const int tot2 = std::min<int>(kRegWarpsPerSM / 2, static_cast<int>(kMaxSmem / (2 * a.smem_per_warp))) * 2;
         if (tot2 >= warps_sm - 1) warps = 2;
     }
     if (const char* fw = getenv("SA_FORCE_WARPS")) {  // tuning: warps per block
@@ -375,7 +375,7 @@ int make_shape(Replica& rep, const sa_params* p, uint64_t Lmax, LaunchShape& sh,
         int w2 = 0;
         const int pw = getenv("SA_FORCE_WARPS") ? warps : 2;
         if (pw <= warps && static_cast<uint64_t>(pw) * a.smem_per_warp <= kMaxSmem) {
-            const int tot = std::min<int>(24 / pw, static_cast<int>(kMaxSmem / (pw * a.smem_per_warp))) * pw;
+            const int tot = std::min<int>(kRegWarpsPerSM / pw, static_cast<int>(kMaxSmem / (pw * a.smem_per_warp))) * pw;
             best_block(a.smem_per_warp, w2);
             if (tot >= w2 - 1 &&
                 align_fast_occupancy(a, 32 * pw, a.smem_per_warp * pw, &bps) == cudaSuccess && bps >= 1) {
@@ -395,7 +395,7 @@ int make_shape(Replica& rep, const sa_params* p, uint64_t Lmax, LaunchShape& sh,
     sh.slow_hcap = static_cast<int>(hcap_slow);
     sh.slow_table_bytes = (cand_table_bytes(sh.slow_cap, sh.slow_hcap) + 255) & ~255ull;
     sh.slow_smem_per_warp = round16(common) + pb_bytes;
-    uint64_t slow_warps = std::min<uint64_t>(static_cast<uint64_t>(rep.sm_count) * 24,
+    uint64_t slow_warps = std::min<uint64_t>(static_cast<uint64_t>(rep.sm_count) * kRegWarpsPerSM,
                                              std::max<uint64_t>(32, kSlowScratchBudget / sh.slow_table_bytes));
     // 8-warp blocks where shared memory allows: the device path launches this
     // kernel after every batch, usually with nothing to do, and 3552 one-warp
