@@ -63,7 +63,13 @@ uint64_t chunk_reads_setting(uint64_t n_reads) {
     return std::min<uint64_t>(512u << 10, std::max<uint64_t>(49152, want));
 }
 constexpr uint64_t kChunkBytes = 256ull << 20;
-constexpr int kFastCap = 64, kFastHcap = 128;
+#ifndef SA_FAST_CAP
+#define SA_FAST_CAP 64    // candidates per read in the shared-memory table (more: the global-table pass)
+#endif
+#ifndef SA_FAST_HCAP
+#define SA_FAST_HCAP 128  // its hash slots (power of two)
+#endif
+constexpr int kFastCap = SA_FAST_CAP, kFastHcap = SA_FAST_HCAP;
 constexpr uint64_t kSlowScratchBudget = 6ull << 30;  // global candidate tables of the overflow kernel
 
 struct Stage {  // one of the two pipeline slots of a replica
