@@ -581,6 +581,23 @@ SA_DEV bool select_order(Ctx& x, uint8_t* order) {
         }
     }
     if (!__all_sync(FULL, ok)) return false;
+    if (x.n_cands <= 32) {  // one key per lane: a 32-key network (keys 2 lane and 2 lane + 1 regrouped)
+        // key of candidate `lane`: lane l holds candidates 2l and 2l + 1
+        const unsigned long long a0 = shfl64(v[0], lane >> 1), a1 = shfl64(v[1], lane >> 1);
+        unsigned long long u = (lane & 1) ? a1 : a0;
+#pragma unroll 1
+        for (int k = 2; k <= 32; k <<= 1) {
+            const bool up = (lane & k) == 0;
+#pragma unroll 1
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                const unsigned long long o = shfl64(u, lane ^ j);
+                u = (((lane & j) == 0) == up) ? min(u, o) : max(u, o);
+            }
+        }
+        order[lane] = static_cast<uint8_t>(u & 63u);
+        __syncwarp();
+        return true;
+    }
     // rolled loops: every warp entering the pruning loop runs this, and the
     // unrolled network's ~1k instructions measured as instruction-fetch
     // stalls (33% of the warp kernel's samples at C2)
