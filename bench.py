@@ -430,6 +430,59 @@ def cpu_baseline(cfg, g, packed, nmask, bases, offs, res_dev, args) -> dict:
             "parity_mismatches_vs_gpu": mism, "t1": _t1(ix, cfg, sb, so)}
 
 
+def run_box(args) -> None:
+    """Whole-box e2e through the product's own multi-device API: ONE process,
+    sa_create(devices=[0 .. N-1]) -- a full index replica per GPU, one host
+    worker thread per GPU pulling chunks of the batch from a shared cursor,
+    results in input order (the replacement for the reference's worker pool
+    over reads, REF src/driver.cpp:134-142, src/scheduler.cpp:8-31).  Weak
+    scaling: N x reads_per_gpu reads per step.  `--box-devices 0,0` runs two
+    replicas on one GPU (plumbing check)."""
+    import torch
+
+    from paper_1111_5572_b200 import api, synth
+
+    cfg = synth.CONFIGS[args.config]
+    devs = [int(d) for d in args.box_devices.split(",")] if args.box_devices else list(range(args.gpus))
+    R = (args.reads_per_gpu or cfg.n_reads) * len(devs)
+    g = synth.make_genome(cfg)
+    packed, nmask = synth.pack_genome(g)
+    bases, offs, _, _ = synth.make_reads(cfg, g, n_reads=R, seed=cfg.read_seed)
+    genome = api.PackedGenome(packed, nmask, g.size)
+    t0 = time.perf_counter()
+    idx = api.SeedIndex.build(genome, cfg.params.seed_size, devices=devs)
+    build_s = time.perf_counter() - t0
+    al = api.Aligner(idx, genome, cfg.params)
+    pin_b, pin_r = api.PinnedBuffer(bases.nbytes), api.PinnedBuffer(R * 24)
+    hb = pin_b.array(np.uint8, bases.size)
+    hb[:] = bases
+    hr = pin_r.array(api.RESULT_DTYPE, R)
+    for _ in range(args.warmup):
+        al.align_arrays(hb, offs, hr)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(devs[0])
+    sampler.start()
+    ms = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        al.align_arrays(hb, offs, hr)
+        ms.append(1000.0 * (time.perf_counter() - t0))
+    clocks = sampler.stop()
+    v = R * args.steps / (sum(ms) / 1000.0)
+    line = {"metric": _baseline_metric(), "value": v, "unit": UNIT, "n_gpus": len(set(devs)), "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": sum(ms) / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {**_workload(cfg, R // len(devs)),
+                       "parallelism": f"one process, sa_create(devices={devs}): a replica per device, a host "
+                                      f"worker per replica, chunks from a shared cursor"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": int(bases.nbytes),
+                    "d2h_bytes_per_step": int(R * 24),
+                    "timing": "host wall clock around sa_align_batch (pinned host buffers), whole box"},
+            "gpu_launches": al.last_launches() * args.steps, "clocks": clocks,
+            "setup_s": {"gpu_index_build": round(build_s, 2)}, "mode": "box"}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -440,11 +493,16 @@ def main():
     ap.add_argument("--reads-per-gpu", type=int, default=0)
     ap.add_argument("--cpu-sample", type=int, default=0, help="0: CPU_SAMPLE[config]")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--box", action="store_true",
+                    help="one process driving every GPU through sa_create(devices=[0..N-1]) (whole-box e2e)")
+    ap.add_argument("--box-devices", default="", help="with --box: explicit device list, e.g. 0,0")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.box:
+        run_box(args)
     else:
         run_ours(args)
 

@@ -1603,6 +1603,26 @@ __global__ void __launch_bounds__(kSoloThreads, SA_SOLO_MIN_BLOCKS) solo_kernel(
     if (lane < kNumStats && acc) atomicAdd(a.stats + lane, acc);
 }
 
+// The reads solo_kernel listed for the warp kernel still hold the lazy
+// records it did not reach: one thread per (listed read, seed) probes them
+// here, all at once, instead of each warp kernel read paying a dependent
+// round of probes when it starts.
+__global__ void __launch_bounds__(256) resolve_kernel(const AlignLaunch a) {
+    const uint32_t n = *a.pre_list_count;
+    const uint32_t nr = static_cast<uint32_t>(a.pre_rstride);
+    const uint64_t total = static_cast<uint64_t>(n) * nr;
+    for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t < total;
+         t += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t r = __ldg(a.pre_list + t / nr);
+        const uint32_t sd = static_cast<uint32_t>(t % nr);
+        const uint2 meta = __ldg(a.pre_meta + r);
+        if ((meta.y >> 16) != 0 || sd >= (meta.y & 0xffffu)) continue;
+        uint4* rec = a.pre_recs + static_cast<uint64_t>(r) * a.pre_rstride + sd;
+        const uint4 v = *rec;
+        if (v.x & kSeedLazy) *rec = resolve_lazy(a, v);
+    }
+}
+
 // ------------------------------------------------------------------ seed kernel
 // Stage 1 of the two-kernel path: one thread per read (full lane use, and
 // the probes of a whole warp of reads in flight at once).  Decodes the read
@@ -2347,7 +2367,14 @@ void launch_align_fast(const AlignLaunch& a, int grid, int block, cudaStream_t s
     }
 }
 
-void launch_seed(const AlignLaunch& a, cudaStream_t st) {
+bool solo_eligible(const AlignLaunch& a);
+
+void launch_seed(const AlignLaunch& a0, cudaStream_t st) {
+    // lazy seeds only where the solo kernel runs (it probes them on demand and
+    // resolves the rest of the reads it lists, resolve_kernel); a launch on the
+    // warp kernel alone gets every seed probed here
+    AlignLaunch a = a0;
+    if (!solo_eligible(a)) a.eager = 0;
     // G lanes per read: the smallest power of two covering the blocks
     const int nbmax = (a.pre_pstride >> 1) - 1;
     auto go = [&](auto kernel, int G) {
@@ -2404,6 +2431,10 @@ int launch_align_seeded(const AlignLaunch& a, int grid, int block, cudaStream_t 
         }
         solo_kernel<<<static_cast<int>(std::max<uint64_t>(g, 1)), kSoloThreads, 0, st>>>(sa);
         ++n;
+        if (a.eager > 0 && a.eager < a.n) {  // lazy records of the listed reads
+            resolve_kernel<<<148 * 8, 256, 0, st>>>(a);
+            ++n;
+        }
         if (dbg) {
             unsigned int n = 0, why[4] = {0, 0, 0, 0};
             cudaStreamSynchronize(st);

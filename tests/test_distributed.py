@@ -1,6 +1,7 @@
-"""N>1 path on CPU: world_size-2 gloo process group, reads sharded across
-ranks, results gathered in read order, timings max-reduced.  The per-rank
-aligner is the oracle here (no GPU); on the box it is the CUDA path."""
+"""N>1 path: world_size-2 gloo process group, reads sharded across ranks,
+results gathered in read order, timings max-reduced.  On CPU the per-rank
+aligner is the oracle; the gpu-marked variant runs the CUDA aligner per rank.
+A two-device replica test runs when the box has two GPUs."""
 import os
 import socket
 
@@ -28,7 +29,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, use_gpu=False):
     import sys
 
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -45,8 +46,16 @@ def _worker(rank, world, port, q):
     packed, nmask = synth.pack_genome(g)
     bases, offs, _, _ = synth.make_reads(cfg, g)
     oi = O.OracleIndex(packed, nmask, g.size, 20)
-    res = align_sharded(lambda b, o: oi.align_arrays(cfg.params, b, o)[0], bases, offs, rank, world,
-                        O.RESULT_DTYPE)
+    if use_gpu:  # the CUDA path per rank (every rank on device 0: independent replicas, no waiting)
+        from paper_1111_5572_b200 import api
+
+        genome = api.PackedGenome(packed, nmask, g.size)
+        al = api.Aligner(api.SeedIndex.build(genome, 20, devices=[0]), genome, cfg.params)
+        fn = al.align_arrays
+    else:
+        def fn(b, o):
+            return oi.align_arrays(cfg.params, b, o)[0]
+    res = align_sharded(fn, bases, offs, rank, world, O.RESULT_DTYPE)
     t = max_over_ranks(float(rank + 1))
     if rank == 0:
         whole, _ = oi.align_arrays(cfg.params, bases, offs)
@@ -54,11 +63,11 @@ def _worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-def test_two_rank_gloo_shard_and_gather():
+def _two_ranks(use_gpu):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, use_gpu)) for r in range(2)]
     for p in procs:
         p.start()
     diff, t, n = q.get(timeout=300)
@@ -67,3 +76,36 @@ def test_two_rank_gloo_shard_and_gather():
         assert p.exitcode == 0
     assert diff == [] and n == 3001
     assert t == 2.0
+
+
+def test_two_rank_gloo_shard_and_gather():
+    _two_ranks(False)
+
+
+@pytest.mark.gpu
+def test_two_rank_gloo_cuda_path():
+    """The same sharding with the CUDA aligner per rank."""
+    _two_ranks(True)
+
+
+@pytest.mark.gpu
+def test_replicas_on_distinct_devices():
+    """sa_create over two distinct GPUs (skipped on a one-GPU box): chunks
+    dealt to a host worker per device, results in input order, equal to one
+    device's."""
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    from oracle import oracle as O
+    from paper_1111_5572_b200 import api, synth
+
+    cfg = synth.CONFIGS["C1"].scaled(genome_len=5_000_000, n_reads=400_000)
+    g = synth.make_genome(cfg)
+    packed, nmask = synth.pack_genome(g)
+    bases, offs, _, _ = synth.make_reads(cfg, g)
+    genome = api.PackedGenome(packed, nmask, g.size)
+    one = api.Aligner(api.SeedIndex.build(genome, 20, devices=[0]), genome, cfg.params).align_arrays(bases, offs)
+    al2 = api.Aligner(api.SeedIndex.build(genome, 20, devices=[0, 1]), genome, cfg.params)
+    two = al2.align_arrays(bases, offs)
+    assert O.compare_results(one, two) == []
