@@ -581,23 +581,6 @@ SA_DEV bool select_order(Ctx& x, uint8_t* order) {
         }
     }
     if (!__all_sync(FULL, ok)) return false;
-    if (x.n_cands <= 32) {  // one key per lane: a 32-key network (keys 2 lane and 2 lane + 1 regrouped)
-        // key of candidate `lane`: lane l holds candidates 2l and 2l + 1
-        const unsigned long long a0 = shfl64(v[0], lane >> 1), a1 = shfl64(v[1], lane >> 1);
-        unsigned long long u = (lane & 1) ? a1 : a0;
-#pragma unroll 1
-        for (int k = 2; k <= 32; k <<= 1) {
-            const bool up = (lane & k) == 0;
-#pragma unroll 1
-            for (int j = k >> 1; j > 0; j >>= 1) {
-                const unsigned long long o = shfl64(u, lane ^ j);
-                u = (((lane & j) == 0) == up) ? min(u, o) : max(u, o);
-            }
-        }
-        order[lane] = static_cast<uint8_t>(u & 63u);
-        __syncwarp();
-        return true;
-    }
     // rolled loops: every warp entering the pruning loop runs this, and the
     // unrolled network's ~1k instructions measured as instruction-fetch
     // stalls (33% of the warp kernel's samples at C2)
@@ -991,11 +974,6 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
     int tested = 0;
     bool any_lookup = false, any_popular = false, early_multi = false, overflow = false;
 
-    if (grecs && wave0_ready && lane < n_eff) {  // wave 0 staged from the seed kernel: probe its lazy seeds
-        const uint4 rr = recs[lane];
-        if (rr.x & kSeedLazy) recs[lane] = resolve_lazy(a, rr);
-    }
-    __syncwarp();
     // The seed loop (REF :256-316) with the pruning loop (REF :296-315) folded
     // in, so score_best -- and the LV under it -- is inlined once.
     bool pruning = false;
@@ -1006,11 +984,7 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
             if ((i & 31) == 0 && (i > 0 || !wave0_ready)) {  // speculative probes, seeds i .. i+31
                 if (grecs) {  // resolved by the seed kernel
                     __syncwarp();
-                    if (i + lane < n_eff) {
-                        uint4 rr = grecs[i + lane];
-                        if (rr.x & kSeedLazy) rr = resolve_lazy(a, rr);
-                        recs[lane] = rr;
-                    }
+                    if (i + lane < n_eff) recs[lane] = grecs[i + lane];  // resolved (resolve_kernel)
                     __syncwarp();
                 } else {
                     compute_wave_sync(a, x.R, offs, i, n_eff, len, recs, lane);
