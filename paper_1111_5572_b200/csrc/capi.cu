@@ -279,7 +279,10 @@ int make_shape(Replica& rep, const sa_params* p, uint64_t Lmax, LaunchShape& sh,
         const char* e = getenv("SA_PB_MODE");
         return e ? std::max(0, std::min(2, atoi(e))) : 1;
     }();
-    a.pb_on = pb_mode;
+    // only where the batch can apply (its bound B <= 5 needs small limits):
+    // long-read layouts are shared-memory-limited and keep the space (C3:
+    // 138 vs 199 ms per 500 k reads with the area present)
+    a.pb_on = a.dl_max <= 15 ? pb_mode : 0;
     // SA_EAGER_PROBES: seeds the seed kernel probes per read (0: all)
     static const int eager = [] {
         const char* e = getenv("SA_EAGER_PROBES");
