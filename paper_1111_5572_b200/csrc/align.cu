@@ -946,11 +946,133 @@ SA_DEV void resolve_wave0(const AlignLaunch& a, int n_eff, int len, uint4* recs,
     __syncwarp();
 }
 
+// Classification and result (REF aligner.cpp:318-363) and the read's
+// counters, once the seed and pruning loops are over.
+SA_DEV void finish_read(Ctx& x, uint32_t r, bool early_multi, bool any_popular, bool any_lookup,
+                        unsigned long long& acc) {
+    const AlignLaunch& a = *x.a;
+    const int lane = x.lane;
+    const int len = x.len;
+    // classification, REF :318-363
+    int kind;
+    bool all_pop = false;
+    const int d_max = x.d_max;
+    if (early_multi) {
+        kind = SA_MULTIPLE_HITS;
+    } else {
+        if (x.tr.d_best <= d_max && x.tr.d_second >= x.tr.d_best + a.c) kind = SA_SINGLE_HIT;
+        else if (x.tr.d_best <= d_max) kind = SA_MULTIPLE_HITS;
+        else kind = SA_NOT_FOUND;
+        if (kind == SA_NOT_FOUND && any_popular && !any_lookup) {
+            all_pop = true;
+            kind = SA_MULTIPLE_HITS;
+        }
+    }
+    sa_result res;
+    res.position = 0;
+    res.distance = -1;
+    res.gap = 0;
+    res.kind = static_cast<uint8_t>(kind);
+    res.has_position = 0;
+    res.direction = 0;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) res.reserved[i] = 0;
+    bool first_best = false;
+    if (kind == SA_SINGLE_HIT ||
+        (kind == SA_MULTIPLE_HITS && x.tr.d_best < kInfDistance && x.tr.d_best <= d_max)) {
+        res.has_position = 1;
+        res.position = x.tr.best_pos;
+        res.direction = static_cast<uint8_t>(x.tr.best_dir);
+        res.distance = x.tr.d_best;
+        res.gap = tracker_gap(x.tr);
+    }
+    if (kind == SA_SINGLE_HIT && x.first_valid && x.first_dir == x.tr.best_dir) {
+        const uint64_t delta = x.first_pos > x.tr.best_pos ? x.first_pos - x.tr.best_pos
+                                                           : x.tr.best_pos - x.first_pos;
+        first_best = delta <= static_cast<uint64_t>(a.bs);
+    }
+    {  // sa_result as three 8-byte words, one lane each
+        uint64_t w = 0;
+        if (lane == 0) w = res.position;
+        else if (lane == 1)
+            w = static_cast<uint32_t>(res.distance) | (static_cast<uint64_t>(static_cast<uint32_t>(res.gap)) << 32);
+        else if (lane == 2)
+            w = res.kind | (static_cast<uint64_t>(res.has_position) << 8) | (static_cast<uint64_t>(res.direction) << 16);
+        if (lane < 3) reinterpret_cast<uint64_t*>(a.results + r)[lane] = w;
+    }
+    stat_add(x, S_READS, 1u);
+    stat_add(x, S_ALL_POP, all_pop ? 1u : 0u);
+    stat_add(x, S_FIRST_BEST, first_best ? 1u : 0u);
+    stat_add(x, S_SINGLE + (kind - SA_SINGLE_HIT), 1u);
+    stat_add(x, S_READ_BASES, static_cast<uint32_t>(len));
+    acc += x.rs;
+}
+
+// ------------------------------------------------------------------ pruning hand-off
+// With a prune queue (AlignLaunch::pq_*), a read that enters the pruning loop
+// (REF aligner.cpp:296-315) under a batchable bound is not pruned by the warp
+// kernel: its state -- candidate table, tracker, first-scored locus, call
+// count, flags and the counters so far -- goes to a record in the queue, and
+// prune_kernel finishes it (prune_all, then finish_read).  The warp kernel's
+// hot code then holds only the seed loop, and the pruning code runs in a
+// kernel of its own.  Record layout (16-byte units from the pool base):
+//   u32 r, len; i32 d_best, d_second; u64 best_pos, first_pos;
+//   u32 calls, n_cands, n_unscored, flags; i32 d_max, B; u32 pad[4];
+//   u32 rs[20] (lane-distributed counters); then u64 keys[n], u64 masks[n], u32 cnts[n]
+constexpr uint32_t kPqHeader = 160;
+enum { PQ_ANY_POP = 1, PQ_ANY_LOOKUP = 2, PQ_FIRST_DONE = 4, PQ_FIRST_VALID = 8, PQ_FIRST_DIR = 16, PQ_BEST_DIR = 32 };
+
+SA_DEV uint32_t pq_bytes(uint32_t n) { return (kPqHeader + 20u * n + 15u) & ~15u; }
+
+// Returns false when the pool is full (the caller prunes inline).
+SA_DEV bool pq_defer(Ctx& x, uint32_t r, int B, bool any_popular, bool any_lookup) {
+    const AlignLaunch& a = *x.a;
+    const int lane = x.lane;
+    const uint32_t n = x.n_cands;
+    unsigned long long off = 0;
+    if (lane == 0) off = atomicAdd(a.pq_cursor, static_cast<unsigned long long>(pq_bytes(n)));
+    off = __shfl_sync(FULL, off, 0);
+    if (off + pq_bytes(n) > a.pq_cap) return false;
+    unsigned char* rec = a.pq_pool + off;
+    if (lane == 0) {
+        uint32_t* h = reinterpret_cast<uint32_t*>(rec);
+        h[0] = r;
+        h[1] = static_cast<uint32_t>(x.len);
+        h[2] = static_cast<uint32_t>(x.tr.d_best);
+        h[3] = static_cast<uint32_t>(x.tr.d_second);
+        reinterpret_cast<uint64_t*>(rec)[2] = x.tr.best_pos;
+        reinterpret_cast<uint64_t*>(rec)[3] = x.first_pos;
+        h[8] = x.calls;
+        h[9] = n;
+        h[10] = x.n_unscored;
+        h[11] = (any_popular ? PQ_ANY_POP : 0) | (any_lookup ? PQ_ANY_LOOKUP : 0) | (x.first_done ? PQ_FIRST_DONE : 0) |
+                (x.first_valid ? PQ_FIRST_VALID : 0) | (x.first_dir ? PQ_FIRST_DIR : 0) |
+                (x.tr.best_dir ? PQ_BEST_DIR : 0);
+        h[12] = static_cast<uint32_t>(x.d_max);
+        h[13] = static_cast<uint32_t>(B);
+    }
+    if (lane < kNumStats) reinterpret_cast<uint32_t*>(rec + 64)[lane] = x.rs;
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(rec + kPqHeader);
+    for (uint32_t j = lane; j < n; j += 32) {
+        keys[j] = x.t.ckey[j];
+        keys[n + j] = x.t.cmask[j];
+        reinterpret_cast<uint32_t*>(keys + 2 * n)[j] = x.t.ccnt[j];
+    }
+    __syncwarp();
+    if (lane == 0) {
+        __threadfence();
+        const unsigned slot = atomicAdd(a.pq_count, 1u);
+        a.pq_list[slot] = static_cast<uint32_t>(off >> 4);
+    }
+    return true;
+}
+
 // Align one read whose planes are already in x.R / x.C.  recs holds the seed
-// records of wave 0 when wave0_ready.  Returns false when the candidate
-// table overflowed (nothing committed).
+// records of wave 0 when wave0_ready.  Returns 0 when the candidate table
+// overflowed (nothing committed), 1 when the read is done, 2 when it went to
+// the prune queue.
 template <bool kRegLV>
-SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
+SA_DEV int align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
                       unsigned long long& acc, uint4* recs, bool wave0_ready, const uint4* grecs = nullptr,
                       unsigned char* pb = nullptr) {
     const AlignLaunch& a = *x.a;
@@ -1135,6 +1257,11 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
             const int cmax = x.d_max + a.c - 1;
             const int B = (a.force || x.tr.d_best > x.d_max) ? cmax : x.tr.d_best + a.c - 1;
             if (B >= 0 && B <= kPbMax) {
+                if (a.pq_pool) {  // to prune_kernel; a full pool sends the read to the global-table pass
+                    const bool ok = pq_defer(x, r, B, any_popular, any_lookup);
+                    clear_table(x.t, x.n_cands, !ok, lane);
+                    return ok ? 2 : 0;
+                }
 #if SA_DEBUG_COUNTERS
                 if (a.dbg && lane == 0) {  // pruning batches: entries, candidates, B sum
                     atomicAdd(a.dbg + 7, 1u);
@@ -1167,64 +1294,11 @@ SA_DEV bool align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
 
     if (overflow) {
         clear_table(x.t, x.n_cands, true, lane);
-        return false;
+        return 0;
     }
     clear_table(x.t, x.n_cands, false, lane);
-
-    // classification, REF :318-363
-    int kind;
-    bool all_pop = false;
-    const int d_max = x.d_max;
-    if (early_multi) {
-        kind = SA_MULTIPLE_HITS;
-    } else {
-        if (x.tr.d_best <= d_max && x.tr.d_second >= x.tr.d_best + a.c) kind = SA_SINGLE_HIT;
-        else if (x.tr.d_best <= d_max) kind = SA_MULTIPLE_HITS;
-        else kind = SA_NOT_FOUND;
-        if (kind == SA_NOT_FOUND && any_popular && !any_lookup) {
-            all_pop = true;
-            kind = SA_MULTIPLE_HITS;
-        }
-    }
-    sa_result res;
-    res.position = 0;
-    res.distance = -1;
-    res.gap = 0;
-    res.kind = static_cast<uint8_t>(kind);
-    res.has_position = 0;
-    res.direction = 0;
-#pragma unroll
-    for (int i = 0; i < 5; ++i) res.reserved[i] = 0;
-    bool first_best = false;
-    if (kind == SA_SINGLE_HIT ||
-        (kind == SA_MULTIPLE_HITS && x.tr.d_best < kInfDistance && x.tr.d_best <= d_max)) {
-        res.has_position = 1;
-        res.position = x.tr.best_pos;
-        res.direction = static_cast<uint8_t>(x.tr.best_dir);
-        res.distance = x.tr.d_best;
-        res.gap = tracker_gap(x.tr);
-    }
-    if (kind == SA_SINGLE_HIT && x.first_valid && x.first_dir == x.tr.best_dir) {
-        const uint64_t delta = x.first_pos > x.tr.best_pos ? x.first_pos - x.tr.best_pos
-                                                           : x.tr.best_pos - x.first_pos;
-        first_best = delta <= static_cast<uint64_t>(a.bs);
-    }
-    {  // sa_result as three 8-byte words, one lane each
-        uint64_t w = 0;
-        if (lane == 0) w = res.position;
-        else if (lane == 1)
-            w = static_cast<uint32_t>(res.distance) | (static_cast<uint64_t>(static_cast<uint32_t>(res.gap)) << 32);
-        else if (lane == 2)
-            w = res.kind | (static_cast<uint64_t>(res.has_position) << 8) | (static_cast<uint64_t>(res.direction) << 16);
-        if (lane < 3) reinterpret_cast<uint64_t*>(a.results + r)[lane] = w;
-    }
-    stat_add(x, S_READS, 1u);
-    stat_add(x, S_ALL_POP, all_pop ? 1u : 0u);
-    stat_add(x, S_FIRST_BEST, first_best ? 1u : 0u);
-    stat_add(x, S_SINGLE + (kind - SA_SINGLE_HIT), 1u);
-    stat_add(x, S_READ_BASES, static_cast<uint32_t>(len));
-    acc += x.rs;
-    return true;
+    finish_read(x, r, early_multi, any_popular, any_lookup, acc);
+    return 1;
 }
 
 // ------------------------------------------------------------------ solo kernel
@@ -1616,7 +1690,14 @@ __global__ void __launch_bounds__(256) resolve_kernel(const AlignLaunch a) {
 template <int G>
 __global__ void __launch_bounds__(256, SA_SEED_MIN_BLOCKS) seed_kernel(const AlignLaunch a) {
     const int lane = threadIdx.x & 31;
-    if (a.pre_list_count && blockIdx.x == 0 && threadIdx.x == 0) *a.pre_list_count = 0;  // solo_kernel appends next
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (a.pre_list_count) *a.pre_list_count = 0;  // solo_kernel appends next
+        if (a.pq_cursor) {                             // the warp kernel's prune queue
+            *a.pq_cursor = 0;
+            *a.pq_count = 0;
+            *a.pq_cursor2 = 0;
+        }
+    }
     const int g = lane & (G - 1);
     const int gbase = lane & ~(G - 1);
     const uint32_t groups = (gridDim.x * blockDim.x) / G;
@@ -1968,8 +2049,8 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
             x.len = len;
             x.d_max = a.dmax_param >= 0 ? a.dmax_param : (12 * len + 99) / 100;
             const int ne = ne_pre >= 0 ? ne_pre : (q ? n_eff1 : n_eff0);
-            if (!align_one<kRegLV>(x, r, ne, offs + q * a.n_off_cap, len / a.s, acc, recs + 32 * q, wave0_ready,
-                                   grecs, pb))
+            if (align_one<kRegLV>(x, r, ne, offs + q * a.n_off_cap, len / a.s, acc, recs + 32 * q, wave0_ready,
+                                  grecs, pb) == 0)
                 overflowed(r);
         }
     };
@@ -2179,6 +2260,76 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
         }
     }
 
+    __syncwarp();
+    unsigned long long cells = x.cells;
+    for (int o = 16; o > 0; o >>= 1) cells += __shfl_xor_sync(FULL, cells, o);
+    if (lane == S_CELLS) acc += cells;
+    if (lane < kNumStats && acc) atomicAdd(a.stats + lane, acc);
+}
+
+// The prune queue's reads (pq_defer): warp per read, a persistent grid.
+__global__ void __launch_bounds__(256) prune_kernel(const AlignLaunch a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    constexpr uint32_t kTab = 64 * (8 + 8 + 4);
+    unsigned char* ws = smem + static_cast<size_t>(wib) * (kTab + kPbBytes);
+    Ctx x;
+    x.a = &a;
+    x.lane = lane;
+    x.cells = 0;
+    x.t.cap = 64;
+    x.t.hcap = 0;
+    x.t.ckey = reinterpret_cast<unsigned long long*>(ws);
+    x.t.cmask = x.t.ckey + 64;
+    x.t.ccnt = reinterpret_cast<uint32_t*>(x.t.cmask + 64);
+    x.t.chslot = nullptr;
+    x.t.hkey = nullptr;
+    x.t.hval = nullptr;
+    unsigned char* pb = ws + kTab;
+    const int half = a.pre_pstride >> 1;
+    unsigned long long acc = 0;
+    const uint32_t n = *a.pq_count;
+    for (;;) {
+        uint32_t k = 0;
+        if (lane == 0) k = atomicAdd(a.pq_cursor2, 1u);
+        k = __shfl_sync(FULL, k, 0);
+        if (k >= n) break;
+        const unsigned char* rec = a.pq_pool + (static_cast<uint64_t>(__ldg(a.pq_list + k)) << 4);
+        const uint32_t* h = reinterpret_cast<const uint32_t*>(rec);
+        const uint32_t r = h[0];
+        x.len = static_cast<int>(h[1]);
+        x.tr.d_best = static_cast<int>(h[2]);
+        x.tr.d_second = static_cast<int>(h[3]);
+        x.tr.best_pos = reinterpret_cast<const uint64_t*>(rec)[2];
+        x.first_pos = reinterpret_cast<const uint64_t*>(rec)[3];
+        x.calls = h[8];
+        x.n_cands = h[9];
+        x.n_unscored = h[10];
+        const uint32_t fl = h[11];
+        x.d_max = static_cast<int>(h[12]);
+        const int B = static_cast<int>(h[13]);
+        x.first_done = (fl & PQ_FIRST_DONE) != 0;
+        x.first_valid = (fl & PQ_FIRST_VALID) != 0;
+        x.first_dir = (fl & PQ_FIRST_DIR) ? 1 : 0;
+        x.tr.best_dir = (fl & PQ_BEST_DIR) ? 1 : 0;
+        x.rs = lane < kNumStats ? reinterpret_cast<const uint32_t*>(rec + 64)[lane] : 0u;
+        const unsigned long long* keys = reinterpret_cast<const unsigned long long*>(rec + kPqHeader);
+        for (uint32_t j = lane; j < x.n_cands; j += 32) {
+            x.t.ckey[j] = keys[j];
+            x.t.cmask[j] = keys[x.n_cands + j];
+            x.t.ccnt[j] = reinterpret_cast<const uint32_t*>(keys + 2 * x.n_cands)[j];
+        }
+        x.R = a.pre_planes + static_cast<uint64_t>(r) * a.pre_pstride;  // read planes stay in global memory
+        x.C = x.R + half;
+        __syncwarp();
+        bool early_multi = false;
+        if (prune_all(x, pb, B)) {
+            stat_add(x, S_MULTI, 1u);
+            early_multi = true;
+        }
+        finish_read(x, r, early_multi, (fl & PQ_ANY_POP) != 0, (fl & PQ_ANY_LOOKUP) != 0, acc);
+    }
     __syncwarp();
     unsigned long long cells = x.cells;
     for (int o = 16; o > 0; o >>= 1) cells += __shfl_xor_sync(FULL, cells, o);
@@ -2429,8 +2580,19 @@ int launch_align_seeded(const AlignLaunch& a, int grid, int block, cudaStream_t 
     cudaMemsetAsync(d_wdbg, 0, 16 * sizeof(unsigned int), st);
     b.dbg = d_wdbg;
 #endif
+    if (!b.pb_on) b.pq_pool = nullptr;  // nothing is deferred without the pruning batch
     if (b.dl_max <= 15) launch_variant<false, true, true, false, true>(b, grid, block, st);
     else launch_variant<false, true, false, false, true>(b, grid, block, st);
+    if (b.pq_pool) {  // the reads it handed to the prune queue
+        const uint32_t spw = prune_kernel_smem_per_warp();
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(prune_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * spw);
+            attr = true;
+        }
+        prune_kernel<<<148 * 4, 256, 8 * spw, st>>>(b);
+        ++n;
+    }
 #if SA_DEBUG_COUNTERS
     {
         unsigned int h[16];
@@ -2468,6 +2630,7 @@ void launch_lookup(const LookupLaunch& a, cudaStream_t st) {
 }
 
 uint32_t prune_batch_bytes() { return kPbBytes; }
+uint32_t prune_kernel_smem_per_warp() { return 64 * (8 + 8 + 4) + kPbBytes; }
 
 cudaError_t align_set_smem(uint32_t smem_bytes) {
     const int b = static_cast<int>(smem_bytes);

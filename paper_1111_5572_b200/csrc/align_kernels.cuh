@@ -102,6 +102,15 @@ struct AlignLaunch {
     // seed_kernel probes the first `eager` seeds of each read (0: all); the
     // rest are left as lazy records for the aligner kernels to probe on demand
     int eager;
+    // prune queue (align.cu pq_defer / prune_kernel), kPre warp kernel only:
+    // pool of pq_cap bytes, byte cursor, records listed in pq_list[0 .. *pq_count)
+    // (16-byte units), work cursor for prune_kernel; zeroed by the seed kernel
+    unsigned char* pq_pool;
+    uint64_t pq_cap;
+    unsigned long long* pq_cursor;
+    unsigned int* pq_count;
+    unsigned int* pq_cursor2;
+    unsigned int* pq_list;
 };
 
 #ifndef SA_FAST_WARPS
@@ -171,6 +180,7 @@ void launch_lv_batch(const LvLaunch& a, int grid, int block, cudaStream_t st);
 void launch_lookup(const LookupLaunch& a, cudaStream_t st);
 cudaError_t align_fast_occupancy(const AlignLaunch& a, int block, uint32_t smem_bytes, int* blocks_per_sm);
 cudaError_t align_set_smem(uint32_t smem_bytes);
-uint32_t prune_batch_bytes();  // per warp, appended to the align kernels' shared-memory layout
+uint32_t prune_batch_bytes();
+uint32_t prune_kernel_smem_per_warp();  // per warp, appended to the align kernels' shared-memory layout
 
 }  // namespace sab

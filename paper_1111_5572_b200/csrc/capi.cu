@@ -89,6 +89,11 @@ struct Stage {  // one of the two pipeline slots of a replica
     uint4* pre_recs = nullptr;
     uint2* pre_meta = nullptr;
     unsigned int* pre_list = nullptr;  // solo_kernel's list for the warp kernel; count in the last entry
+    unsigned char* pq_pool = nullptr;  // the warp kernel's prune queue (align.cu pq_defer)
+    uint64_t pq_cap = 0;
+    unsigned int* pq_list = nullptr;
+    uint64_t pq_list_cap = 0;
+    unsigned long long* pq_ctl = nullptr;  // byte cursor; count | work cursor
     uint64_t pre_planes_cap = 0, pre_recs_cap = 0, pre_meta_cap = 0, pre_list_cap = 0;
     // seeded pipeline: input landed / consumed by the seed kernel / aligned /
     // results copied out
@@ -529,6 +534,15 @@ bool use_pre() {
 int pre_pstride(const AlignLaunch& a) { return 2 * (a.wbr - 1); }  // (nb + 1) blocks per orientation
 int pre_rstride(const AlignLaunch& a) { return a.n_off_cap; }
 
+// SA_PRUNE_SPLIT=0 keeps the pruning loop inside the warp kernel
+bool prune_split() {
+    static const bool on = [] {
+        const char* e = getenv("SA_PRUNE_SPLIT");
+        return e ? atoi(e) != 0 : true;
+    }();
+    return on;
+}
+
 int ensure_pre(sa_context* ctx, Stage& s, uint64_t n_reads, const LaunchShape& sh) {
     if (!use_pre() || !sh.proto.prefetch) return SA_OK;
     const uint64_t np = n_reads * static_cast<uint64_t>(pre_pstride(sh.proto));
@@ -546,7 +560,24 @@ int ensure_pre(sa_context* ctx, Stage& s, uint64_t n_reads, const LaunchShape& s
     if (int rc = grow(&s.pre_recs, s.pre_recs_cap, nr, sizeof(uint4))) return rc;
     if (int rc = grow(&s.pre_meta, s.pre_meta_cap, n_reads, sizeof(uint2))) return rc;
     if (int rc = grow(&s.pre_list, s.pre_list_cap, n_reads + 1, sizeof(unsigned int))) return rc;
+    if (prune_split()) {  // ~13% of C2 reads, ~540 B each; a full pool just prunes inline
+        uint64_t cap_b = s.pq_cap;
+        if (int rc = grow(&s.pq_pool, cap_b, n_reads * 256, 1)) return rc;
+        s.pq_cap = cap_b;
+        if (int rc = grow(&s.pq_list, s.pq_list_cap, n_reads, sizeof(unsigned int))) return rc;
+        if (!s.pq_ctl) CUDA_TRY(ctx, cudaMalloc(&s.pq_ctl, 2 * sizeof(unsigned long long)));
+    }
     return SA_OK;
+}
+
+void set_pq(AlignLaunch& a, const Stage& s) {
+    if (!prune_split() || !s.pq_pool) return;
+    a.pq_pool = s.pq_pool;
+    a.pq_cap = s.pq_cap;
+    a.pq_cursor = s.pq_ctl;
+    a.pq_count = reinterpret_cast<unsigned int*>(s.pq_ctl + 1);
+    a.pq_cursor2 = a.pq_count + 1;
+    a.pq_list = s.pq_list;
 }
 
 int ensure_scratch(sa_context* ctx, Replica& rep, const LaunchShape& sh) {
@@ -604,6 +635,7 @@ int enqueue_align(sa_context* ctx, Replica& rep, Stage& stg, const LaunchShape& 
         a.pre_meta = stg.pre_meta;
         a.pre_list = stg.pre_list;
         a.pre_list_count = stg.pre_list + (stg.pre_list_cap - 1);
+        set_pq(a, stg);
         a.pre_pstride = pre_pstride(a);
         a.pre_rstride = pre_rstride(a);
         const uint64_t ch = dev_chunk_reads();
@@ -631,6 +663,7 @@ int enqueue_align(sa_context* ctx, Replica& rep, Stage& stg, const LaunchShape& 
         return SA_OK;
     }
     AlignLaunch b = a;
+    b.pq_pool = nullptr;  // the global-table kernel prunes inline
     b.cursor = stg.d_ctl + 1;
     b.work_list = d_overflow;
     b.work_count = stg.d_ctl + 2;
@@ -1196,6 +1229,7 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
         a.pre_meta = st.pre_meta;
         a.pre_list = st.pre_list;
         a.pre_list_count = st.pre_list + (st.pre_list_cap - 1);
+        set_pq(a, st);
         a.pre_pstride = pre_pstride(a);
         a.pre_rstride = pre_rstride(a);
         a.packed = packed ? st.d_pack : nullptr;
@@ -1436,6 +1470,9 @@ void sa_destroy(sa_context* ctx) {
             if (s.pre_recs) cudaFree(s.pre_recs);
             if (s.pre_meta) cudaFree(s.pre_meta);
             if (s.pre_list) cudaFree(s.pre_list);
+            if (s.pq_pool) cudaFree(s.pq_pool);
+            if (s.pq_list) cudaFree(s.pq_list);
+            if (s.pq_ctl) cudaFree(s.pq_ctl);
             if (s.d_pack) cudaFree(s.d_pack);
             if (s.h_pack) cudaFreeHost(s.h_pack);
             if (s.h_in) cudaFreeHost(s.h_in);
