@@ -1253,7 +1253,9 @@ SA_DEV int align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
             break;
         }
 #if SA_PRUNE_BATCH
-        if (pruning && pb != nullptr) {  // the rest of the pruning loop, a batch at a time
+        // the batch exists only for short-read layouts (d_limit <= 15: the
+        // register-LV kernels); the long-read kernels are compiled without it
+        if (kRegLV && pruning && pb != nullptr) {  // the rest of the pruning loop, a batch at a time
             const int cmax = x.d_max + a.c - 1;
             const int B = (a.force || x.tr.d_best > x.d_max) ? cmax : x.tr.d_best + a.c - 1;
             if (B >= 0 && B <= kPbMax) {
