@@ -2582,7 +2582,9 @@ int launch_align_seeded(const AlignLaunch& a, int grid, int block, cudaStream_t 
     cudaMemsetAsync(d_wdbg, 0, 16 * sizeof(unsigned int), st);
     b.dbg = d_wdbg;
 #endif
-    if (!b.pb_on) b.pq_pool = nullptr;  // nothing is deferred without the pruning batch
+    // nothing is deferred without the pruning batch, nor in launches too small
+    // for the solo kernel (C0, 10 k reads: the extra launch costs more than it saves)
+    if (!b.pb_on || !solo_eligible(a)) b.pq_pool = nullptr;
     if (b.dl_max <= 15) launch_variant<false, true, true, false, true>(b, grid, block, st);
     else launch_variant<false, true, false, false, true>(b, grid, block, st);
     if (b.pq_pool) {  // the reads it handed to the prune queue
