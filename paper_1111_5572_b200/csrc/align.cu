@@ -581,6 +581,22 @@ SA_DEV bool select_order(Ctx& x, uint8_t* order) {
         }
     }
     if (!__all_sync(FULL, ok)) return false;
+    if (x.n_cands <= 32) {  // one key per lane, a 32-key network (candidate l from lane l / 2)
+        const unsigned long long a0 = shfl64(v[0], lane >> 1), a1 = shfl64(v[1], lane >> 1);
+        unsigned long long u = (lane & 1) ? a1 : a0;
+#pragma unroll 1
+        for (int k = 2; k <= 32; k <<= 1) {
+            const bool up = (lane & k) == 0;
+#pragma unroll 1
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                const unsigned long long o = shfl64(u, lane ^ j);
+                u = (((lane & j) == 0) == up) ? min(u, o) : max(u, o);
+            }
+        }
+        order[lane] = static_cast<uint8_t>(u & 63u);
+        __syncwarp();
+        return true;
+    }
     // rolled loops: every warp entering the pruning loop runs this, and the
     // unrolled network's ~1k instructions measured as instruction-fetch
     // stalls (33% of the warp kernel's samples at C2)
@@ -2275,7 +2291,9 @@ __global__ void __launch_bounds__(256) prune_kernel(const AlignLaunch a) {
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     constexpr uint32_t kTab = 64 * (8 + 8 + 4);
-    unsigned char* ws = smem + static_cast<size_t>(wib) * (kTab + kPbBytes);
+    const uint32_t planes_bytes = static_cast<uint32_t>(a.pre_pstride) * 16u;
+    unsigned char* ws = smem + static_cast<size_t>(wib) * (kTab + kPbBytes + planes_bytes);
+    uint4* planes = reinterpret_cast<uint4*>(ws + kTab + kPbBytes);
     Ctx x;
     x.a = &a;
     x.lane = lane;
@@ -2322,8 +2340,12 @@ __global__ void __launch_bounds__(256) prune_kernel(const AlignLaunch a) {
             x.t.cmask[j] = keys[x.n_cands + j];
             x.t.ccnt[j] = reinterpret_cast<const uint32_t*>(keys + 2 * x.n_cands)[j];
         }
-        x.R = a.pre_planes + static_cast<uint64_t>(r) * a.pre_pstride;  // read planes stay in global memory
-        x.C = x.R + half;
+        {  // the read's forward and reverse-complement planes, into shared memory
+            const uint4* gp = a.pre_planes + static_cast<uint64_t>(r) * a.pre_pstride;
+            for (int t = lane; t < a.pre_pstride; t += 32) planes[t] = gp[t];
+        }
+        x.R = planes;
+        x.C = planes + half;
         __syncwarp();
         bool early_multi = false;
         if (prune_all(x, pb, B)) {
@@ -2588,11 +2610,11 @@ int launch_align_seeded(const AlignLaunch& a, int grid, int block, cudaStream_t 
     if (b.dl_max <= 15) launch_variant<false, true, true, false, true>(b, grid, block, st);
     else launch_variant<false, true, false, false, true>(b, grid, block, st);
     if (b.pq_pool) {  // the reads it handed to the prune queue
-        const uint32_t spw = prune_kernel_smem_per_warp();
-        static bool attr = false;
-        if (!attr) {
+        const uint32_t spw = prune_kernel_smem_per_warp() + static_cast<uint32_t>(b.pre_pstride) * 16u;
+        static uint32_t attr = 0;
+        if (attr < 8 * spw) {
             cudaFuncSetAttribute(prune_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * spw);
-            attr = true;
+            attr = 8 * spw;
         }
         prune_kernel<<<148 * 4, 256, 8 * spw, st>>>(b);
         ++n;
