@@ -1,4 +1,4 @@
-"""e2e probe at C1: sa_align_batch wall time per call from pinned buffers,
+"""e2e probe (default C1, --config C2 ...): sa_align_batch wall time per call from pinned buffers,
 beside the plain H2D of the same bytes (the copy floor).  Run with
 SA_DEBUG_PIPE=1 for the pipeline's span lines, SA_CHUNK_READS=n to force
 the chunk size.
@@ -20,12 +20,13 @@ def main():
     ap.add_argument("--reads", type=int, default=1_000_000)
     ap.add_argument("--calls", type=int, default=8)
     ap.add_argument("--copy-floor", action="store_true")
+    ap.add_argument("--config", default="C1")
     args = ap.parse_args()
     import torch
 
     from paper_1111_5572_b200 import api, synth
 
-    cfg = synth.CONFIGS["C1"]
+    cfg = synth.CONFIGS[args.config]
     g = synth.make_genome(cfg)
     packed, nmask = synth.pack_genome(g)
     bases, offs, _, _ = synth.make_reads(cfg, g, n_reads=args.reads)
