@@ -2268,7 +2268,14 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
             // the list holds launch-absolute ids (read_base + r, as overflowed() stores
             // them); no list: every read of the launch
             if (kSlow && a.work_list) r = a.work_list[r] - static_cast<uint32_t>(a.read_base);
-            const uint64_t o0 = a.offsets[r], o1 = a.offsets[r + 1];
+            uint64_t o0, o1;
+            if (a.fixed_len) {  // equal-length chunk: no offsets were copied in
+                o0 = a.base_off + static_cast<uint64_t>(r) * a.fixed_len;
+                o1 = o0 + a.fixed_len;
+            } else {
+                o0 = a.offsets[r];
+                o1 = a.offsets[r + 1];
+            }
             const int len = static_cast<int>(o1 - o0);
             const uintptr_t addr = reinterpret_cast<uintptr_t>(a.bases + (o0 - a.base_off));
             const uintptr_t abase = addr & ~static_cast<uintptr_t>(3);

@@ -98,6 +98,8 @@ struct Stage {  // one of the two pipeline slots of a replica
     // seeded pipeline: input landed / consumed by the seed kernel / aligned /
     // results copied out
     cudaEvent_t e_in = nullptr, e_seeded = nullptr, e_al = nullptr, e_out = nullptr;
+    cudaEvent_t e_ov = nullptr;  // the chunk's global-table pass done (seeded pipeline)
+    bool ov_pending = false;     // the stage's last chunk ran a global-table pass
     // packed input (pack.cpp): pinned host planes and their device copy
     uint32_t* h_pack = nullptr;
     uint32_t* d_pack = nullptr;
@@ -183,6 +185,7 @@ struct Replica {
         uint64_t chunks_cap = 0;
         unsigned int epoch = 0;
         cudaStream_t ci = nullptr, kk = nullptr, co = nullptr;
+        cudaStream_t ov = nullptr;  // seeded pipeline: the chunks' global-table passes, in order (shared scratch)
         cudaEvent_t e_begin = nullptr, e_ready = nullptr, k0 = nullptr, k1 = nullptr, e_end = nullptr;
     } sm;
 };
@@ -443,7 +446,7 @@ int ensure_stage(sa_context* ctx, Stage& s, uint64_t bytes, uint64_t reads) {
         CUDA_TRY(ctx, cudaEventCreate(&s.km));
         CUDA_TRY(ctx, cudaEventCreate(&s.k1));
         CUDA_TRY(ctx, cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
-        for (cudaEvent_t* e : {&s.e_in, &s.e_seeded, &s.e_al, &s.e_out})
+        for (cudaEvent_t* e : {&s.e_in, &s.e_seeded, &s.e_al, &s.e_out, &s.e_ov})
             CUDA_TRY(ctx, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
         CUDA_TRY(ctx, cudaMalloc(&s.d_ctl, kCtlWords * sizeof(unsigned int)));
     }
@@ -1040,6 +1043,7 @@ int align_streamed(sa_context* ctx, Replica& rep, const sa_params* params, const
 struct SeededChunk {
     uint64_t r0 = 0, r1 = 0;
     int stage = 0;
+    bool ov = false;  // its overflowing reads get their own global-table pass
     cudaStream_t cs = nullptr;  // compute stream
     AlignLaunch a{};
     int grid = 0, block = 0;
@@ -1057,6 +1061,16 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
         CUDA_TRY(ctx, cudaStreamCreateWithFlags(&S.co, cudaStreamNonBlocking));
         for (cudaEvent_t* e : {&S.e_begin, &S.e_ready, &S.k0, &S.k1, &S.e_end}) CUDA_TRY(ctx, cudaEventCreate(e));
     }
+    if (!S.ov) CUDA_TRY(ctx, cudaStreamCreateWithFlags(&S.ov, cudaStreamNonBlocking));
+    for (int j = 0; j < kPipeStages; ++j) rep.stage[j].ov_pending = false;
+    // Reads that overflow the shared candidate table are redone chunk by
+    // chunk by the global-table kernel on its own stream, between the
+    // chunk's align kernels and its copy-out (SA_CHUNK_OVERFLOW=0: one pass at
+    // the end of the batch, which measured ~3.5 ms of a 29 ms C2 call).
+    static const bool chunk_overflow = [] {
+        const char* e = getenv("SA_CHUNK_OVERFLOW");
+        return e ? atoi(e) != 0 : true;
+    }();
     const size_t n_chunks = bounds.size() - 1;
     LaunchShape sh;
     uint64_t shape_L = 0;
@@ -1102,7 +1116,30 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
         CUDA_TRY(ctx, cudaGetLastError());
         ++launches;
         CUDA_TRY(ctx, cudaEventRecord(st.e_al, pend.cs));
-        CUDA_TRY(ctx, cudaStreamWaitEvent(S.co, st.e_al, 0));
+        if (pend.ov) {  // the chunk's overflowing reads: global-table kernel, stream S.ov
+            CUDA_TRY(ctx, cudaStreamWaitEvent(S.ov, st.e_al, 0));
+            AlignLaunch b = pend.a;
+            b.cursor = st.d_ctl + 1;
+            b.work_list = st.d_overflow;
+            b.work_count = st.d_ctl + 2;
+            b.overflow_list = nullptr;
+            b.overflow_count = nullptr;
+            b.cap = sh.slow_cap;
+            b.hcap = sh.slow_hcap;
+            b.smem_per_warp = sh.slow_smem_per_warp;
+            b.sbw = 0;
+            b.prefetch = 0;
+            b.pq_pool = nullptr;
+            b.pre_list = nullptr;
+            b.pre_list_count = nullptr;
+            launch_align_slow(b, sh.slow_grid, sh.slow_block, S.ov);
+            CUDA_TRY(ctx, cudaGetLastError());
+            ++launches;
+            CUDA_TRY(ctx, cudaEventRecord(st.e_ov, S.ov));
+            CUDA_TRY(ctx, cudaStreamWaitEvent(S.co, st.e_ov, 0));
+        } else {
+            CUDA_TRY(ctx, cudaStreamWaitEvent(S.co, st.e_al, 0));
+        }
         if (stage_out) {
             if (int rc = drain_results(st)) return rc;  // this stage's previous chunk
             CUDA_TRY(ctx, cudaMemcpyAsync(st.h_res, st.d_results, (pend.r1 - pend.r0) * sizeof(sa_result),
@@ -1136,7 +1173,10 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
         }
         // one length for the whole chunk: the offsets need not be copied
         const uint32_t fixed = (Lmin == Lc && Lc > 0 && Lc < (1u << 30)) ? static_cast<uint32_t>(Lc) : 0u;
-        Lc = std::min<uint64_t>(Lc, 1024);  // longer reads are deferred by the seed kernel
+        // a chunk whose reads all fit the layout redoes its overflows itself;
+        // longer reads (deferred by the seed kernel) go to the end-of-batch pass
+        const bool ov = chunk_overflow && !packed && Lc <= 1024;  // (host-packed chunks keep no ASCII copy)
+        Lc = std::min<uint64_t>(Lc, 1024);
         if (k == 0 || Lc > shape_L) {
             std::string w;
             if ((bad = cached_shape(rep, params, std::max(Lc, shape_L), sh, w))) {
@@ -1200,6 +1240,8 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
             }
         }
         if (k >= kPipeStages) CUDA_TRY(ctx, cudaStreamWaitEvent(S.ci, st.e_seeded, 0));
+        if (st.ov_pending) CUDA_TRY(ctx, cudaStreamWaitEvent(S.ci, st.e_ov, 0));  // its pass reads the bytes too
+        st.ov_pending = ov;
         if (packed)
             CUDA_TRY(ctx, cudaMemcpyAsync(st.d_pack, st.h_pack, 3 * wpp * sizeof(uint32_t), cudaMemcpyHostToDevice,
                                           S.ci));
@@ -1218,8 +1260,8 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
         a.results = st.d_results;
         a.stats = rep.d_stats;
         a.cursor = st.d_ctl;
-        a.overflow_list = rep.d_defer;
-        a.overflow_count = rep.d_defer_count;
+        a.overflow_list = ov ? st.d_overflow : rep.d_defer;
+        a.overflow_count = ov ? st.d_ctl + 2 : rep.d_defer_count;
         a.error_flag = rep.d_err;
         a.error_read = rep.d_err_read;
         a.read_base = r0;
@@ -1238,6 +1280,7 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
         cudaStream_t cs = multi ? st.st : S.kk;
         CUDA_TRY(ctx, cudaStreamWaitEvent(cs, st.e_in, 0));
         if (k == 0) CUDA_TRY(ctx, cudaEventRecord(S.k0, cs));
+        if (ov) CUDA_TRY(ctx, cudaMemsetAsync(st.d_ctl, 0, kCtlWords * sizeof(unsigned int), cs));
         mark('W');
         launch_seed(a, cs);
         mark('s');
@@ -1251,6 +1294,7 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
         pend.a = a;
         pend.grid = sh.pipe_grid;
         pend.block = sh.pipe_block;
+        pend.ov = ov;
         have_pend = true;
         if (multi) {
             if (int rc = align_pending()) return rc;
@@ -1265,6 +1309,10 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
             CUDA_TRY(ctx, cudaEventRecord(rep.stage[j].done, rep.stage[j].st));
             CUDA_TRY(ctx, cudaStreamWaitEvent(S.kk, rep.stage[j].done, 0));
         }
+    if (k > 0) {  // and the global-table passes
+        CUDA_TRY(ctx, cudaEventRecord(rep.stage[0].e_ov, S.ov));
+        CUDA_TRY(ctx, cudaStreamWaitEvent(S.kk, rep.stage[0].e_ov, 0));
+    }
     if (k > 0) {
         CUDA_TRY(ctx, cudaEventRecord(S.k1, S.kk));
         CUDA_TRY(ctx, cudaStreamWaitEvent(S.co, S.k1, 0));
@@ -1489,7 +1537,7 @@ void sa_destroy(sa_context* ctx) {
                         static_cast<void*>(rep.sm.res), static_cast<void*>(rep.sm.flags),
                         static_cast<void*>(rep.sm.done), static_cast<void*>(rep.sm.adj)})
             if (q) cudaFree(q);
-        for (cudaStream_t q : {rep.sm.ci, rep.sm.kk, rep.sm.co})
+        for (cudaStream_t q : {rep.sm.ci, rep.sm.kk, rep.sm.co, rep.sm.ov})
             if (q) cudaStreamDestroy(q);
         for (cudaEvent_t e : {rep.sm.e_begin, rep.sm.e_ready, rep.sm.k0, rep.sm.k1, rep.sm.e_end})
             if (e) cudaEventDestroy(e);
