@@ -1242,7 +1242,19 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
         if (k >= kPipeStages) CUDA_TRY(ctx, cudaStreamWaitEvent(S.ci, st.e_seeded, 0));
         if (st.ov_pending) CUDA_TRY(ctx, cudaStreamWaitEvent(S.ci, st.e_ov, 0));  // its pass reads the bytes too
         st.ov_pending = ov;
-        if (packed)
+        static const bool no_copy = getenv("SA_DEBUG_NOCOPY") != nullptr;  // diagnostics: compute-only pipeline
+        if (no_copy) {  // the batch's bytes from a device-resident copy instead of the H2D (timing only)
+            static char* d_all = nullptr;
+            static uint64_t all_cap = 0;
+            const uint64_t tot = offsets[n_reads] - offsets[0];
+            if (tot > all_cap) {
+                if (d_all) cudaFree(d_all);
+                CUDA_TRY(ctx, cudaMalloc(&d_all, tot));
+                CUDA_TRY(ctx, cudaMemcpy(d_all, bases + offsets[0], tot, cudaMemcpyHostToDevice));
+                all_cap = tot;
+            }
+            CUDA_TRY(ctx, cudaMemcpyAsync(st.d_bases, d_all + (b0 - offsets[0]), b1 - b0, cudaMemcpyDeviceToDevice, S.ci));
+        } else if (packed)
             CUDA_TRY(ctx, cudaMemcpyAsync(st.d_pack, st.h_pack, 3 * wpp * sizeof(uint32_t), cudaMemcpyHostToDevice,
                                           S.ci));
         else
