@@ -626,6 +626,53 @@ SA_DEV bool select_order(Ctx& x, uint8_t* order) {
     return true;
 }
 
+// The same order for larger tables (the global-table kernel: up to 16 k
+// candidates), sorted in place in the table's hash-value area -- free once
+// no more hits are added; hcap >= 2 cap gives room for next_pow2(n) keys --
+// by a warp bitonic network in memory.  keys[p] & 0x3fff = candidate index
+// at position p.  Returns false when a count or the index does not fit.
+SA_DEV bool select_order_large(Ctx& x, unsigned long long* keys) {
+    const AlignLaunch& a = *x.a;
+    const int lane = x.lane;
+    const uint32_t n = x.n_cands;
+    if (n > 0x4000u) return false;
+    uint32_t P = 64;
+    while (P < n) P <<= 1;
+    bool ok = true;
+    for (uint32_t j = lane; j < P; j += 32) {
+        unsigned long long v = ~0ull;
+        if (j < n) {
+            const uint32_t cc = x.t.ccnt[j];
+            if (!(cc & kScored)) {
+                ok &= cc < 0xffffu;
+                const unsigned long long kk = x.t.ckey[j];
+                const unsigned long long amin =
+                    (kk >> 1) * static_cast<unsigned long long>(a.bs) +
+                    static_cast<unsigned long long>(__ffsll(static_cast<long long>(x.t.cmask[j])) - 1);
+                v = (static_cast<unsigned long long>(0xffffu - cc) << 48) | (amin << 15) | ((kk & 1ull) << 14) | j;
+            }
+        }
+        keys[j] = v;
+    }
+    if (!__all_sync(FULL, ok)) return false;
+    __syncwarp();
+    for (uint32_t k = 2; k <= P; k <<= 1) {
+        for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
+            for (uint32_t i = lane; i < P / 2; i += 32) {
+                const uint32_t lo = (i / jj) * 2 * jj + (i % jj), hi = lo + jj;
+                const bool up = (lo & k) == 0;
+                const unsigned long long u = keys[lo], v = keys[hi];
+                if ((u > v) == up) {
+                    keys[lo] = v;
+                    keys[hi] = u;
+                }
+            }
+            __syncwarp();
+        }
+    }
+    return true;
+}
+
 // The whole rest of the pruning loop.  Returns true when the multi exit fired.
 SA_DEV bool prune_all(Ctx& x, unsigned char* pb, int B) {
     const AlignLaunch& a = *x.a;
@@ -641,6 +688,11 @@ SA_DEV bool prune_all(Ctx& x, unsigned char* pb, int B) {
     constexpr bool seg_lv = false;  // SA_PB_SEG=1 builds the mask-LV batch (pb_on == 2; measured slower)
 #endif
     const bool sorted = x.n_cands <= 64 && select_order(x, order);
+    // larger tables (global-table kernel): sorted in the hash-value area
+    unsigned long long* big = (!sorted && x.n_cands > 64 && x.t.hcap >= 2 * x.t.cap)
+                                  ? reinterpret_cast<unsigned long long*>(x.t.hval)
+                                  : nullptr;
+    if (big && !select_order_large(x, big)) big = nullptr;
     const int c = a.c, d_max = x.d_max;
     uint32_t pos = 0;  // next position in the selection order
     while (x.n_unscored > 0) {
@@ -648,11 +700,11 @@ SA_DEV bool prune_all(Ctx& x, unsigned char* pb, int B) {
         //    64 anchors; lane j holds the j-th
         int my_idx = 0, nc = 0;
         uint32_t my_cnt = 0, my_start = 0;
-        if (sorted) {
+        if (sorted || big) {
             const uint32_t p = pos + lane;
             const bool have = p < pos + x.n_unscored;
             if (have) {
-                my_idx = order[p];
+                my_idx = sorted ? order[p] : static_cast<int>(big[p] & 0x3fffu);
                 my_cnt = __popcll(static_cast<long long>(x.t.cmask[my_idx]));
             }
             my_start = my_cnt;
