@@ -1139,7 +1139,7 @@ SA_DEV bool pq_defer(Ctx& x, uint32_t r, int B, bool any_popular, bool any_looku
 // records of wave 0 when wave0_ready.  Returns 0 when the candidate table
 // overflowed (nothing committed), 1 when the read is done, 2 when it went to
 // the prune queue.
-template <bool kRegLV>
+template <bool kRegLV, bool kSlow = false>
 SA_DEV int align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
                       unsigned long long& acc, uint4* recs, bool wave0_ready, const uint4* grecs = nullptr,
                       unsigned char* pb = nullptr) {
@@ -1164,6 +1164,8 @@ SA_DEV int align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
     int tested = 0;
     bool any_lookup = false, any_popular = false, early_multi = false, overflow = false;
 
+    bool big_init = false, big_ok = false;  // kSlow: sorted pruning order
+    uint32_t big_pos = 0;
     // The seed loop (REF :256-316) with the pruning loop (REF :296-315) folded
     // in, so score_best -- and the LV under it -- is inlined once.
     bool pruning = false;
@@ -1347,7 +1349,25 @@ SA_DEV int align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
             }
         }
 #endif
-        score_best<kRegLV>(x);  // REF :288 (and :306 inside the pruning loop)
+        if (kSlow && pruning) {
+            // global-table kernel, pruning loop without the batch (long reads):
+            // the loop's order sorted once (select_order_large), then scored
+            // candidate by candidate, instead of an argmax over the table each time
+            if (!big_init) {
+                big_init = true;
+                big_ok = x.n_cands > 64 && x.t.hcap >= 2 * x.t.cap &&
+                         select_order_large(x, reinterpret_cast<unsigned long long*>(x.t.hval));
+                big_pos = 0;
+            }
+            if (big_ok) {
+                const unsigned long long* big = reinterpret_cast<const unsigned long long*>(x.t.hval);
+                score_candidate<kRegLV>(x, static_cast<uint32_t>(big[big_pos++] & 0x3fffu));
+            } else {
+                score_best<kRegLV>(x);
+            }
+        } else {
+            score_best<kRegLV>(x);  // REF :288 (and :306 inside the pruning loop)
+        }
         if (x.tr.d_best < a.c && x.tr.d_second < x.tr.d_best + a.c) {  // REF :290-295 / :307-312
             stat_add(x, S_MULTI, 1u);
             early_multi = true;
@@ -2119,7 +2139,7 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
             x.len = len;
             x.d_max = a.dmax_param >= 0 ? a.dmax_param : (12 * len + 99) / 100;
             const int ne = ne_pre >= 0 ? ne_pre : (q ? n_eff1 : n_eff0);
-            if (align_one<kRegLV>(x, r, ne, offs + q * a.n_off_cap, len / a.s, acc, recs + 32 * q, wave0_ready,
+            if (align_one<kRegLV, kSlow>(x, r, ne, offs + q * a.n_off_cap, len / a.s, acc, recs + 32 * q, wave0_ready,
                                   grecs, pb) == 0)
                 overflowed(r);
         }
