@@ -1463,9 +1463,18 @@ __global__ void __launch_bounds__(kSoloThreads, SA_SOLO_MIN_BLOCKS) solo_kernel(
     const int half = a.pre_pstride >> 1;
     const int bsh = a.bs_shift;
     unsigned long long acc = 0;  // lane k: stats slot k of the warp
+    // 32 reads per warp at a time from a.solo_cursor (zeroed by the seed
+    // kernel): a read's cost varies widely, and a block-strided loop lasted
+    // as long as its slowest warp; without a cursor, block striding
     const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t base = blockIdx.x * blockDim.x; base < a.n_reads; base += stride) {
-        const uint32_t r = base + tid;
+    uint32_t base = blockIdx.x * blockDim.x + (tid & ~31);
+    if (a.solo_cursor) {
+        uint32_t v = 0;
+        if (lane == 0) v = atomicAdd(a.solo_cursor, 32u);
+        base = __shfl_sync(FULL, v, 0);
+    }
+    for (; base < a.n_reads;) {
+        const uint32_t r = base + lane;
         // per-read outcome: 0 none, 1 committed, 2 complex (warp kernel)
         int outcome = 0;
         SoloRead c;
@@ -1737,6 +1746,13 @@ __global__ void __launch_bounds__(kSoloThreads, SA_SOLO_MIN_BLOCKS) solo_kernel(
             put(S_MULTI, full ? c.multi : 0u);
             put(S_PRUNE, full ? c.prune : 0u);
         }
+        if (a.solo_cursor) {
+            uint32_t v = 0;
+            if (lane == 0) v = atomicAdd(a.solo_cursor, 32u);
+            base = __shfl_sync(FULL, v, 0);
+        } else {
+            base += stride;
+        }
     }
     if (lane < kNumStats && acc) atomicAdd(a.stats + lane, acc);
 }
@@ -1782,6 +1798,8 @@ __global__ void __launch_bounds__(256, SA_SEED_MIN_BLOCKS) seed_kernel(const Ali
     const int lane = threadIdx.x & 31;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (a.pre_list_count) *a.pre_list_count = 0;  // solo_kernel appends next
+        if (a.solo_cursor) *a.solo_cursor = 0;         // the solo and warp kernels' read cursors
+        if (a.work_cursor) *a.work_cursor = 0;
         if (a.pq_cursor) {                             // the warp kernel's prune queue
             *a.pq_cursor = 0;
             *a.pq_count = 0;
@@ -2168,32 +2186,55 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
             const uint4* gr = a.pre_recs + static_cast<uint64_t>(rr) * a.pre_rstride;
             for (int t = lane; t < nrec; t += 32) cp_async16(recs + 32 * q + t, gr + t);
         };
-        uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+        // Reads are fetched dynamically (a.work_cursor, zeroed by the seed
+        // kernel), one read ahead: listed reads vary widely in cost, and with
+        // static striding a launch lasted as long as its unluckiest warp
+        // (chunks of the batch pipeline hold ~20 listed reads per warp).
+        // Without a cursor (never in practice) reads are strided statically.
+        const bool dyn = a.work_cursor != nullptr;
+        uint32_t stat_next = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+        auto grab = [&]() -> uint32_t {
+            uint32_t v;
+            if (dyn) {
+                v = 0;
+                if (lane == 0) v = atomicAdd(a.work_cursor, 1u);
+                v = __shfl_sync(FULL, v, 0);
+            } else {
+                v = stat_next;
+                stat_next += nw;
+            }
+            return v;
+        };
+        uint32_t r = grab();
         if (r < N) {
             uint2 m_c = __ldg(a.pre_meta + rid(r)), m_n = make_uint2(0, 1u << 16);
             issue_copy(r, 0);
             cp_async_commit();
-            if (r + nw < N) {
-                m_n = __ldg(a.pre_meta + rid(r + nw));
-                issue_copy(r + nw, 1);
+            uint32_t r_n = grab();
+            if (r_n < N) {
+                m_n = __ldg(a.pre_meta + rid(r_n));
+                issue_copy(r_n, 1);
             }
             cp_async_commit();
             int p = 0;
-            for (; r < N; r += nw) {
-                cp_async_wait0();  // read r (and r+nw, issued an iteration ago) have landed
+            while (r < N) {
+                cp_async_wait0();  // read r (and r_n, issued an iteration ago) have landed
                 __syncwarp();
-                if (r + nw < N && (m_n.y >> 16) == 0)
+                if (r_n < N && (m_n.y >> 16) == 0)
                     prefetch_windows(a, recs + 32 * (p ^ 1), static_cast<int>(m_n.y & 0xffffu),
                                      static_cast<int>(m_n.x), lane);
+                const uint32_t r_nn = r_n < N ? grab() : N;
                 uint2 m_nn = make_uint2(0, 1u << 16);
-                if (r + 2 * nw < N) m_nn = __ldg(a.pre_meta + rid(r + 2 * nw));
+                if (r_nn < N) m_nn = __ldg(a.pre_meta + rid(r_nn));
                 const uint32_t rr = rid(r);
                 process(rr, p, static_cast<int>(m_c.x), static_cast<int>(m_c.y >> 16), true,
                         static_cast<int>(m_c.y & 0xffffu), a.pre_recs + static_cast<uint64_t>(rr) * a.pre_rstride);
-                if (r + 2 * nw < N) issue_copy(r + 2 * nw, p);
+                if (r_nn < N) issue_copy(r_nn, p);
                 cp_async_commit();
                 m_c = m_n;
                 m_n = m_nn;
+                r = r_n;
+                r_n = r_nn;
                 p ^= 1;
             }
             cp_async_wait0();

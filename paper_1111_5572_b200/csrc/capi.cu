@@ -94,6 +94,7 @@ struct Stage {  // one of the two pipeline slots of a replica
     unsigned int* pq_list = nullptr;
     uint64_t pq_list_cap = 0;
     unsigned long long* pq_ctl = nullptr;  // byte cursor; count | work cursor
+    unsigned int* pre_ctl = nullptr;       // kPre read cursors: solo, warp kernel
     uint64_t pre_planes_cap = 0, pre_recs_cap = 0, pre_meta_cap = 0, pre_list_cap = 0;
     // seeded pipeline: input landed / consumed by the seed kernel / aligned /
     // results copied out
@@ -563,6 +564,7 @@ int ensure_pre(sa_context* ctx, Stage& s, uint64_t n_reads, const LaunchShape& s
     if (int rc = grow(&s.pre_recs, s.pre_recs_cap, nr, sizeof(uint4))) return rc;
     if (int rc = grow(&s.pre_meta, s.pre_meta_cap, n_reads, sizeof(uint2))) return rc;
     if (int rc = grow(&s.pre_list, s.pre_list_cap, n_reads + 1, sizeof(unsigned int))) return rc;
+    if (!s.pre_ctl) CUDA_TRY(ctx, cudaMalloc(&s.pre_ctl, 8 * sizeof(unsigned int)));
     if (prune_split()) {  // ~13% of C2 reads, ~540 B each; a full pool just prunes inline
         uint64_t cap_b = s.pq_cap;
         if (int rc = grow(&s.pq_pool, cap_b, n_reads * 256, 1)) return rc;
@@ -574,6 +576,11 @@ int ensure_pre(sa_context* ctx, Stage& s, uint64_t n_reads, const LaunchShape& s
 }
 
 void set_pq(AlignLaunch& a, const Stage& s) {
+    static const bool stat_stride = getenv("SA_STATIC_STRIDE") != nullptr;  // tuning: no read cursors
+    if (s.pre_ctl && !stat_stride) {
+        a.solo_cursor = s.pre_ctl;
+        a.work_cursor = s.pre_ctl + 1;
+    }
     if (!prune_split() || !s.pq_pool) return;
     a.pq_pool = s.pq_pool;
     a.pq_cap = s.pq_cap;
@@ -1533,6 +1540,7 @@ void sa_destroy(sa_context* ctx) {
             if (s.pq_pool) cudaFree(s.pq_pool);
             if (s.pq_list) cudaFree(s.pq_list);
             if (s.pq_ctl) cudaFree(s.pq_ctl);
+            if (s.pre_ctl) cudaFree(s.pre_ctl);
             if (s.d_pack) cudaFree(s.d_pack);
             if (s.h_pack) cudaFreeHost(s.h_pack);
             if (s.h_in) cudaFreeHost(s.h_in);
