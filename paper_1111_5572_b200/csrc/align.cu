@@ -1463,18 +1463,9 @@ __global__ void __launch_bounds__(kSoloThreads, SA_SOLO_MIN_BLOCKS) solo_kernel(
     const int half = a.pre_pstride >> 1;
     const int bsh = a.bs_shift;
     unsigned long long acc = 0;  // lane k: stats slot k of the warp
-    // 32 reads per warp at a time from a.solo_cursor (zeroed by the seed
-    // kernel): a read's cost varies widely, and a block-strided loop lasted
-    // as long as its slowest warp; without a cursor, block striding
     const uint32_t stride = gridDim.x * blockDim.x;
-    uint32_t base = blockIdx.x * blockDim.x + (tid & ~31);
-    if (a.solo_cursor) {
-        uint32_t v = 0;
-        if (lane == 0) v = atomicAdd(a.solo_cursor, 32u);
-        base = __shfl_sync(FULL, v, 0);
-    }
-    for (; base < a.n_reads;) {
-        const uint32_t r = base + lane;
+    for (uint32_t base = blockIdx.x * blockDim.x; base < a.n_reads; base += stride) {
+        const uint32_t r = base + tid;
         // per-read outcome: 0 none, 1 committed, 2 complex (warp kernel)
         int outcome = 0;
         SoloRead c;
@@ -1746,13 +1737,6 @@ __global__ void __launch_bounds__(kSoloThreads, SA_SOLO_MIN_BLOCKS) solo_kernel(
             put(S_MULTI, full ? c.multi : 0u);
             put(S_PRUNE, full ? c.prune : 0u);
         }
-        if (a.solo_cursor) {
-            uint32_t v = 0;
-            if (lane == 0) v = atomicAdd(a.solo_cursor, 32u);
-            base = __shfl_sync(FULL, v, 0);
-        } else {
-            base += stride;
-        }
     }
     if (lane < kNumStats && acc) atomicAdd(a.stats + lane, acc);
 }
@@ -1798,8 +1782,7 @@ __global__ void __launch_bounds__(256, SA_SEED_MIN_BLOCKS) seed_kernel(const Ali
     const int lane = threadIdx.x & 31;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (a.pre_list_count) *a.pre_list_count = 0;  // solo_kernel appends next
-        if (a.solo_cursor) *a.solo_cursor = 0;         // the solo and warp kernels' read cursors
-        if (a.work_cursor) *a.work_cursor = 0;
+        if (a.work_cursor) *a.work_cursor = 0;         // the warp kernel's read cursor
         if (a.pq_cursor) {                             // the warp kernel's prune queue
             *a.pq_cursor = 0;
             *a.pq_count = 0;

@@ -111,10 +111,8 @@ struct AlignLaunch {
     unsigned int* pq_count;
     unsigned int* pq_cursor2;
     unsigned int* pq_list;
-    // kPre path: dynamic read cursors of the solo kernel (32 reads per warp
-    // grab) and of the warp kernel (one listed read per grab), zeroed by the
-    // seed kernel; null = static striding
-    unsigned int* solo_cursor;
+    // kPre path: the warp kernel's dynamic read cursor (one listed read per
+    // grab), zeroed by the seed kernel; null = static striding
     unsigned int* work_cursor;
 };
 

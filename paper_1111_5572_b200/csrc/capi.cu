@@ -576,14 +576,12 @@ int ensure_pre(sa_context* ctx, Stage& s, uint64_t n_reads, const LaunchShape& s
 }
 
 void set_pq(AlignLaunch& a, const Stage& s) {
-    // dynamic read cursors (tuning switches; static striding measured faster
-    // for the solo kernel: C1 0.94 vs 1.07 ms, C2 22.6 vs 22.9 ms)
-    static const bool solo_dyn = getenv("SA_SOLO_DYN") != nullptr;
-    static const bool warp_dyn = getenv("SA_WARP_DYN") != nullptr;
-    if (s.pre_ctl) {
-        a.solo_cursor = solo_dyn ? s.pre_ctl : nullptr;
-        a.work_cursor = warp_dyn ? s.pre_ctl + 1 : nullptr;
-    }
+    // the warp kernel's dynamic read cursor (SA_WARP_DYN=0: static striding)
+    static const bool warp_dyn = [] {
+        const char* e = getenv("SA_WARP_DYN");
+        return e ? atoi(e) != 0 : true;
+    }();
+    if (s.pre_ctl) a.work_cursor = warp_dyn ? s.pre_ctl + 1 : nullptr;
     if (!prune_split() || !s.pq_pool) return;
     a.pq_pool = s.pq_pool;
     a.pq_cap = s.pq_cap;
