@@ -2663,7 +2663,43 @@ bool solo_eligible(const AlignLaunch& a) {
            a.bs_shift <= 5 && (a.glen >> a.bs_shift) < (1ull << 31);
 }
 
+// Diagnostics (SA_DEBUG_KTIME): per-kernel device time of the kPre launches,
+// accumulated; sab_debug_ktimes prints and resets them (serialises the stream).
+namespace {
+struct KTimer {
+    bool on = getenv("SA_DEBUG_KTIME") != nullptr;
+    double ms[4] = {0, 0, 0, 0};  // solo, resolve, warp, prune
+    cudaEvent_t ev[5] = {};
+    void mark(int i, cudaStream_t st) {
+        if (!on) return;
+        if (!ev[i]) cudaEventCreate(&ev[i]);
+        cudaEventRecord(ev[i], st);
+    }
+    void span(int k, int i0, int i1) {
+        if (!on) return;
+        cudaEventSynchronize(ev[i1]);
+        float t = 0;
+        cudaEventElapsedTime(&t, ev[i0], ev[i1]);
+        ms[k] += t;
+    }
+};
+KTimer& ktimer() {
+    static KTimer t;
+    return t;
+}
+}  // namespace
+
+extern "C" void sab_debug_ktimes(const char* tag) {
+    KTimer& t = ktimer();
+    if (!t.on) return;
+    fprintf(stderr, "[ktime] %s solo %.3f resolve %.3f warp %.3f prune %.3f ms\n", tag, t.ms[0], t.ms[1], t.ms[2],
+            t.ms[3]);
+    for (double& m : t.ms) m = 0;
+}
+
 int launch_align_seeded(const AlignLaunch& a, int grid, int block, cudaStream_t st) {
+    KTimer& kt = ktimer();
+    kt.mark(0, st);
     AlignLaunch b = a;
     int n = 1;
     if (solo_eligible(a)) {
@@ -2683,9 +2719,14 @@ int launch_align_seeded(const AlignLaunch& a, int grid, int block, cudaStream_t 
         }
         solo_kernel<<<static_cast<int>(std::max<uint64_t>(g, 1)), kSoloThreads, 0, st>>>(sa);
         ++n;
+        kt.mark(1, st);
+        kt.span(0, 0, 1);
         if (a.eager > 0 && a.eager < a.n) {  // lazy records of the listed reads
             resolve_kernel<<<148 * 8, 256, 0, st>>>(a);
             ++n;
+            kt.mark(2, st);
+            kt.span(1, 1, 2);
+            kt.mark(1, st);
         }
         if (dbg) {
             unsigned int n = 0, why[4] = {0, 0, 0, 0};
@@ -2710,8 +2751,11 @@ int launch_align_seeded(const AlignLaunch& a, int grid, int block, cudaStream_t 
     // nothing is deferred without the pruning batch, nor in launches too small
     // for the solo kernel (C0, 10 k reads: the extra launch costs more than it saves)
     if (!b.pb_on || !solo_eligible(a)) b.pq_pool = nullptr;
+    kt.mark(2, st);
     if (b.dl_max <= 15) launch_variant<false, true, true, false, true>(b, grid, block, st);
     else launch_variant<false, true, false, false, true>(b, grid, block, st);
+    kt.mark(3, st);
+    kt.span(2, 2, 3);
     if (b.pq_pool) {  // the reads it handed to the prune queue
         const uint32_t spw = prune_kernel_smem_per_warp() + static_cast<uint32_t>(b.pre_pstride) * 16u;
         static uint32_t attr = 0;
@@ -2721,6 +2765,8 @@ int launch_align_seeded(const AlignLaunch& a, int grid, int block, cudaStream_t 
         }
         prune_kernel<<<148 * 4, 256, 8 * spw, st>>>(b);
         ++n;
+        kt.mark(4, st);
+        kt.span(3, 3, 4);
     }
 #if SA_DEBUG_COUNTERS
     {

@@ -116,6 +116,7 @@ struct Stage {  // one of the two pipeline slots of a replica
 };
 
 int ensure_pack(sa_context* ctx, Stage& s, uint64_t words);
+extern "C" void sab_debug_ktimes(const char* tag);
 
 cudaError_t stage_times(Stage& s, float& fast_ms, float& slow_ms) {
     cudaError_t e = cudaEventSynchronize(s.k1);
@@ -1369,6 +1370,7 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
             else wait += d;
         }
         fprintf(stderr, "[pipe] seed %.3f ms, align %.3f ms, between kernels %.3f ms\n", seed, al, wait);
+        sab_debug_ktimes("pipe");
     }
     for (auto& t : trail) cudaEventDestroy(t.second);
     std::memset(out, 0, sizeof(sa_stats));
