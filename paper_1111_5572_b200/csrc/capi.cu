@@ -27,6 +27,8 @@
 
 using namespace sab;
 
+extern "C" void sab_debug_ktimes(const char* tag);  // align.cu diagnostics (SA_DEBUG_KTIME)
+
 namespace {
 
 thread_local std::string g_thread_err;
@@ -116,7 +118,6 @@ struct Stage {  // one of the two pipeline slots of a replica
 };
 
 int ensure_pack(sa_context* ctx, Stage& s, uint64_t words);
-extern "C" void sab_debug_ktimes(const char* tag);
 
 cudaError_t stage_times(Stage& s, float& fast_ms, float& slow_ms) {
     cudaError_t e = cudaEventSynchronize(s.k1);
