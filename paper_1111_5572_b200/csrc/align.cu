@@ -2518,7 +2518,7 @@ __global__ void __launch_bounds__(256) lv_batch_kernel(const LvLaunch a) {
             __syncwarp();
             continue;
         }
-        const int d = lv_warp_any(R, m, W, 0u, w, dl, F, lane, cells);
+        const int d = lv_warp_any(R, m, W, 0u, w, dl, F, lane, cells, a.bitpar_min);
         if (lane == 0) a.out[p] = d;
         __syncwarp();
     }
@@ -2792,8 +2792,13 @@ void launch_align_slow(const AlignLaunch& a, int grid, int block, cudaStream_t s
 
 void launch_lv_batch(const LvLaunch& a, int grid, int block, cudaStream_t st) {
     static const int bitpar = getenv("SA_LV_BITPAR") != nullptr;  // test hook (lv_bitpar for d_limit <= 15)
+    static const int bitpar_min = [] {  // test hook: the warp bit-parallel LV from this limit
+        const char* e = getenv("SA_LV_WARP_BITPAR_MIN");
+        return e ? std::max(16, atoi(e)) : SA_BITPAR_MIN_DL;
+    }();
     LvLaunch b = a;
     b.bitpar = bitpar;
+    b.bitpar_min = bitpar_min;
     lv_batch_kernel<<<grid, block, b.smem_per_warp * (block / 32), st>>>(b);
 }
 

@@ -155,6 +155,7 @@ struct LvLaunch {
     int32_t* out;
     unsigned int* error_flag;
     int bitpar;  // test hook: lv_bitpar for limits <= 15 (set by launch_lv_batch from SA_LV_BITPAR)
+    int bitpar_min;  // lv_bitpar_warp from this limit (SA_LV_WARP_BITPAR_MIN test hook)
 };
 
 struct LookupLaunch {

@@ -111,10 +111,18 @@ SA_DEV int lv_warp_smem(const uint4* R, int m, const uint4* W, uint32_t wofs, in
 // kRegLV: every d_limit of the launch is <= 15 (register wavefront only);
 // otherwise the shared-memory wavefront serves every limit.  One variant per
 // kernel keeps the inlined code small.
+#ifndef SA_BITPAR_MIN_DL
+#define SA_BITPAR_MIN_DL 256  // limits from here use lv_bitpar_warp (long reads; C4's 607)
+#endif
+SA_DEV int lv_bitpar_warp(const uint4* R, int nblk, int m, const uint4* W, uint32_t wofs, int w, int dl, int lane,
+                          uint32_t& cells);
+
 template <bool kRegLV>
 SA_DEV int lv_warp(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, int dl, int* F,
                    int lane, uint32_t& cells, bool f16 = false) {
     if (kRegLV) return lv_warp_reg(R, m, W, wofs, w, dl, lane, cells);
+    if (dl >= SA_BITPAR_MIN_DL && 2 * dl + 1 <= 2048)
+        return lv_bitpar_warp(R, (m + 31) / 32 + 1, m, W, wofs, w, dl, lane, cells);
     if (f16) return lv_warp_smem(R, m, W, wofs, w, dl, reinterpret_cast<short*>(F), lane, cells);
     return lv_warp_smem(R, m, W, wofs, w, dl, F, lane, cells);
 }
@@ -329,10 +337,144 @@ SA_DEV int lv_seg(const uint4* R, int m, const uint4* G, uint64_t nbg, uint64_t 
     return res;
 }
 
-// standalone LV (lv_batch_kernel): any limit
+// ---------------------------------------------------------------- warp bit-parallel LV
+// Banded bit-parallel bounded edit distance for large limits (long reads),
+// warp-cooperative: lv_bitpar's column recurrence (Myers/Hyyro, band of
+// W = 2 dl + 1 rows, boundary cells >= dl + 1 so every value <= dl is exact
+// and every value > dl stays > dl) with the band spread over the warp, lane l
+// holding band bits 64 l .. 64 l + 63 (W <= 2048, dl <= 1023).  Per column:
+// the eq word from the read planes, the band shifted down one row (bit 0 of
+// the next lane), the addition with its carry scanned across lanes
+// (generate/propagate, 5 shuffles), the HP/HN shift up (bit 63 of the previous
+// lane).  Same value as bounded_distance (REF src/edit_distance.cpp:19-75).
+//
+// It also stops early: every 64 columns the band's minimum H (top plus the
+// least prefix of the vertical deltas, scanned across lanes) is taken; once
+// it exceeds dl no later cell -- every path to row m runs through this column's
+// band, and DP values never fall along a path -- can be <= dl.  The
+// wavefront LV must reach iteration dl + 1 to say "more than dl"
+// (sum over e of 2e + 1 steps); for a long diverged read this stops where the
+// band's minimum crosses dl.
+SA_DEV uint64_t shfl64_lv(uint64_t v, int src) {
+    const uint32_t lo = __shfl_sync(kLvFull, static_cast<uint32_t>(v), src);
+    const uint32_t hi = __shfl_sync(kLvFull, static_cast<uint32_t>(v >> 32), src);
+    return (static_cast<uint64_t>(hi) << 32) | lo;
+}
+
+// 64 read bases from position q (may be negative or past the read: N) of
+// planes R (nblk blocks).
+SA_DEV void read64(const uint4* R, int nblk, int q, uint64_t& l, uint64_t& h, uint64_t& n) {
+    auto blk = [&](int b) -> uint4 { return (b < 0 || b >= nblk) ? make_uint4(0u, 0u, 0xffffffffu, 0u) : R[b]; };
+    const int b = q >> 5;  // arithmetic shift: floor
+    const uint32_t sh = static_cast<uint32_t>(q & 31);
+    const uint4 A = blk(b), B = blk(b + 1), C = blk(b + 2);
+    const uint32_t l0 = __funnelshift_r(A.x, B.x, sh), l1 = __funnelshift_r(B.x, C.x, sh);
+    const uint32_t h0 = __funnelshift_r(A.y, B.y, sh), h1 = __funnelshift_r(B.y, C.y, sh);
+    const uint32_t n0 = __funnelshift_r(A.z, B.z, sh), n1 = __funnelshift_r(B.z, C.z, sh);
+    l = (static_cast<uint64_t>(l1) << 32) | l0;
+    h = (static_cast<uint64_t>(h1) << 32) | h0;
+    n = (static_cast<uint64_t>(n1) << 32) | n0;
+}
+
+SA_DEV int lv_bitpar_warp(const uint4* R, int nblk, int m, const uint4* W, uint32_t wofs, int w, int dl, int lane,
+                          uint32_t& cells) {
+    const int width = 2 * dl + 1;
+    const int b0 = 64 * lane;  // this lane's first band bit
+    auto range = [&](int lo, int hi) -> uint64_t {  // bits [lo, hi] of the band in this lane's word
+        const int a = max(lo, b0), b = min(hi, b0 + 63);
+        if (a > b) return 0ull;
+        const int len = b - a + 1;
+        return (len == 64 ? ~0ull : ((1ull << len) - 1ull)) << (a - b0);
+    };
+    const uint64_t wmask = range(0, width - 1);
+    const bool top_lane_has = (width - 1) >= b0 && (width - 1) <= b0 + 63;
+    const uint64_t inject = top_lane_has ? (1ull << ((width - 1) - b0)) : 0ull;
+    uint64_t VP = range(dl + 1, 2 * dl);  // column 0: rows 1..dl rise by 1
+    uint64_t VN = range(0, dl);           // rows -dl..0 fall by 1 (H[-r][0] = r)
+    int top = dl;                          // H[-dl][0]
+    int best = m <= dl ? m : 0x7fffffff;  // H[m][0] = m
+    const int jend = min(w, m + dl);
+    int j = 1;
+    for (; j <= jend; ++j) {
+        const int q = j - 1 - dl + b0;  // read position of this lane's band bit 0
+        uint64_t rl, rh, rn;
+        read64(R, nblk, q, rl, rh, rn);
+        const uint32_t gpos = wofs + static_cast<uint32_t>(j - 1);
+        const uint4 G = W[gpos >> 5];
+        const uint32_t gb = gpos & 31u;
+        const uint64_t tl = 0ull - ((G.x >> gb) & 1u), th = 0ull - ((G.y >> gb) & 1u), tn = 0ull - ((G.z >> gb) & 1u);
+        const uint64_t eq = ~((rl ^ tl) | (rh ^ th) | rn | tn) & wmask;  // N never matches (REF edit_distance.cpp:11-13)
+        // band down one row
+        const uint64_t vp_up = shfl64_lv(VP, (lane + 1) & 31), vn_up = shfl64_lv(VN, (lane + 1) & 31);
+        VP = ((VP >> 1) | (lane < 31 ? (vp_up << 63) : 0ull)) & wmask;
+        VN = ((VN >> 1) | (lane < 31 ? (vn_up << 63) : 0ull)) & wmask;
+        VP |= inject;
+        // (eq & VP) + VP with the carry across lanes
+        const uint64_t xa = eq & VP;
+        uint64_t sum = xa + VP;
+        uint32_t g = sum < xa ? 1u : 0u;              // carry out with no carry in
+        uint32_t pr = sum == ~0ull ? 1u : 0u;         // a carry in would pass through
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {  // inclusive scan of (g, p): carry out of lanes <= this one
+            const uint32_t g2 = __shfl_up_sync(kLvFull, g, o), p2 = __shfl_up_sync(kLvFull, pr, o);
+            if (lane >= o) {
+                g = g | (pr & g2);
+                pr = pr & p2;
+            }
+        }
+        const uint32_t cin = lane > 0 ? __shfl_up_sync(kLvFull, g, 1) : 0u;
+        const uint32_t cin0 = lane > 0 ? cin : 0u;
+        sum += cin0;
+        const uint64_t D0 = ((sum ^ VP) | eq | VN);
+        const uint64_t HP = VN | ~(D0 | VP);
+        const uint64_t HN = VP & D0;
+        top += static_cast<int>((__shfl_sync(kLvFull, static_cast<uint32_t>(D0), 0) & 1u) ^ 1u);
+        const uint64_t hp_lo = shfl64_lv(HP, (lane + 31) & 31), hn_lo = shfl64_lv(HN, (lane + 31) & 31);
+        const uint64_t X = (HP << 1) | (lane > 0 ? (hp_lo >> 63) : 1ull);
+        const uint64_t HNs = (HN << 1) | (lane > 0 ? (hn_lo >> 63) : 0ull);
+        VN = X & D0 & wmask;
+        VP = (HNs | ~(X | D0)) & wmask;
+        const int bm = m - j + dl;  // band bit of row m
+        if (bm < width) {
+            const uint64_t mk = range(1, bm);
+            const int v = __reduce_add_sync(kLvFull, static_cast<uint32_t>(__popcll(VP & mk))) -
+                          __reduce_add_sync(kLvFull, static_cast<uint32_t>(__popcll(VN & mk)));
+            best = min(best, top + v);
+        }
+        if ((j & 63) == 0 && best > dl) {  // the band's minimum: past dl, nothing later can reach row m within dl
+            const uint64_t vp = VP & ~range(0, 0), vn = VN & ~range(0, 0);  // deltas of rows 1..
+            int run = 0, lmin = 0x7fffffff;
+            for (int t = 0; t < 64; ++t) {
+                run += static_cast<int>((vp >> t) & 1ull) - static_cast<int>((vn >> t) & 1ull);
+                lmin = min(lmin, run);
+            }
+            // exclusive prefix of the lanes' sums
+            int pre = run;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t2 = __shfl_up_sync(kLvFull, pre, o);
+                if (lane >= o) pre += t2;
+            }
+            pre -= run;
+            const int mn = static_cast<int>(__reduce_min_sync(kLvFull, static_cast<uint32_t>(min(0, pre + lmin) + (1 << 20))))
+                           - (1 << 20);
+            if (top + mn > dl) {
+                ++j;
+                break;
+            }
+        }
+    }
+    cells += static_cast<uint32_t>(j - 1 > 0 ? j - 1 : 0) * static_cast<uint32_t>(width);
+    return best <= dl ? best : -1;
+}
+
+// standalone LV (lv_batch_kernel): any limit; bitpar_min = the limit from
+// which the warp bit-parallel LV serves (test hook: lower it to cover it)
 SA_DEV int lv_warp_any(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, int dl, int* F,
-                       int lane, uint32_t& cells) {
+                       int lane, uint32_t& cells, int bitpar_min = SA_BITPAR_MIN_DL) {
     if (dl <= 15) return lv_warp_reg(R, m, W, wofs, w, dl, lane, cells);
+    if (dl >= bitpar_min && 2 * dl + 1 <= 2048)
+        return lv_bitpar_warp(R, (m + 31) / 32 + 1, m, W, wofs, w, dl, lane, cells);
     return lv_warp_smem(R, m, W, wofs, w, dl, F, lane, cells);
 }
 

@@ -69,3 +69,19 @@ def test_parity_multichunk_and_grid_stride():
                        cwd=ROOT, env={**os.environ, **env}, capture_output=True, text=True, timeout=1500)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
+
+
+@pytest.mark.gpu
+def test_warp_bitparallel_lv_vs_oracle():
+    """lv_bitpar_warp (the long-read LV: band spread over the warp, carries
+    scanned across lanes, early stop once the band's minimum passes the limit)
+    through the standalone LV entry with its threshold lowered to 16
+    (SA_LV_WARP_BITPAR_MIN): the reference's known answers, the golden LV
+    triples, random pairs and wide limits (16-400 on reads of 200-3000
+    bases) against the oracle."""
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-x", "-q",
+                        "-m", "gpu", "-k", "lv_known or lv_random or lv_wide or lv_golden", "-p", "no:cacheprovider"],
+                       cwd=ROOT, env={**os.environ, "SA_LV_WARP_BITPAR_MIN": "16"}, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
