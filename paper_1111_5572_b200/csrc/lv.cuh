@@ -422,9 +422,8 @@ SA_DEV int lv_bitpar_warp(const uint4* R, int nblk, int m, const uint4* W, uint3
                 pr = pr & p2;
             }
         }
-        const uint32_t cin = lane > 0 ? __shfl_up_sync(kLvFull, g, 1) : 0u;
-        const uint32_t cin0 = lane > 0 ? cin : 0u;
-        sum += cin0;
+        const uint32_t cin = __shfl_up_sync(kLvFull, g, 1);  // every lane takes part
+        sum += lane > 0 ? cin : 0u;
         const uint64_t D0 = ((sum ^ VP) | eq | VN);
         const uint64_t HP = VN | ~(D0 | VP);
         const uint64_t HN = VP & D0;
