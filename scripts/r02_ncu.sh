@@ -1,0 +1,18 @@
+#!/bin/bash
+# ncu evidence on one B200 (run under gpurun from the repo root):
+#   launch lists (C2, C1, C4) and --set full captures of each hot kernel (C2, C4).
+TAG=${1:-r02}
+O=gpurun_out
+mkdir -p $O
+K='regex:seed_kernel|solo_kernel|resolve_kernel|align_kernel|prune_kernel'
+B="python bench.py --steps 1 --warmup 3 --no-cpu-baseline"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k "$K" -c 12 --csv \
+    --log-file $O/launches_${TAG}_C2.csv $B > $O/ncu_l2_$TAG.log 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k "$K" -c 12 --csv \
+    --log-file $O/launches_${TAG}_C1.csv $B --config C1 > $O/ncu_l1_$TAG.log 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k "$K" -c 12 --csv \
+    --log-file $O/launches_${TAG}_C4.csv $B --config C4 > $O/ncu_l4_$TAG.log 2>&1
+timeout 2400 ncu --set full --clock-control none --import-source on -k "$K" -c 6 \
+    -o $O/prof_${TAG}_C2 -f $B > $O/ncu_f2_$TAG.log 2>&1
+timeout 1500 ncu --set full --clock-control none --import-source on -k 'regex:align_kernel' -c 1 \
+    -o $O/prof_${TAG}_C4 -f $B --config C4 > $O/ncu_f4_$TAG.log 2>&1
