@@ -33,6 +33,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "align_kernels.cuh"
 #include "common.cuh"
@@ -2513,12 +2514,12 @@ __global__ void __launch_bounds__(256) lv_batch_kernel(const LvLaunch a) {
             continue;
         }
         uint32_t cells = 0;
-        if (a.bitpar && dl <= 15) {  // test hook: the solo kernel's bit-parallel LV, lane 0 alone
+        if (a.bitpar == 1 && dl <= 15) {  // test hook: the solo kernel's bit-parallel LV, lane 0 alone
             if (lane == 0) a.out[p] = lv_bitpar(R, rb, m, W, 0u, w, dl, cells);
             __syncwarp();
             continue;
         }
-        const int d = lv_warp_any(R, m, W, 0u, w, dl, F, lane, cells, a.bitpar_min);
+        const int d = lv_warp_any(R, m, W, 0u, w, dl, F, lane, cells, a.bitpar_min, a.bitpar == 2);
         if (lane == 0) a.out[p] = d;
         __syncwarp();
     }
@@ -2791,7 +2792,11 @@ void launch_align_slow(const AlignLaunch& a, int grid, int block, cudaStream_t s
 }
 
 void launch_lv_batch(const LvLaunch& a, int grid, int block, cudaStream_t st) {
-    static const int bitpar = getenv("SA_LV_BITPAR") != nullptr;  // test hook (lv_bitpar for d_limit <= 15)
+    // test hooks: SA_LV_BITPAR (lv_bitpar for d_limit <= 15), SA_LV_LONG=bitpar (lv_bitpar_warp
+    // instead of the systolic lv_sys for the long-read limits)
+    static const int bitpar = getenv("SA_LV_BITPAR") != nullptr
+                                  ? 1
+                                  : (getenv("SA_LV_LONG") && !strcmp(getenv("SA_LV_LONG"), "bitpar") ? 2 : 0);
     static const int bitpar_min = [] {  // test hook: the warp bit-parallel LV from this limit
         const char* e = getenv("SA_LV_WARP_BITPAR_MIN");
         return e ? std::max(16, atoi(e)) : SA_BITPAR_MIN_DL;

@@ -116,11 +116,18 @@ SA_DEV int lv_warp_smem(const uint4* R, int m, const uint4* W, uint32_t wofs, in
 #endif
 SA_DEV int lv_bitpar_warp(const uint4* R, int nblk, int m, const uint4* W, uint32_t wofs, int w, int dl, int lane,
                           uint32_t& cells);
+SA_DEV int lv_sys(const uint4* R, int nblk, int m, const uint4* W, uint32_t wofs, int w, int dl, int lane,
+                  uint32_t& cells);
+#ifndef SA_LV_LONG
+#define SA_LV_LONG 1  // limits >= SA_BITPAR_MIN_DL: 1 systolic (lv_sys, dl <= 960), 0 lv_bitpar_warp
+#endif
 
 template <bool kRegLV>
 SA_DEV int lv_warp(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, int dl, int* F,
                    int lane, uint32_t& cells, bool f16 = false) {
     if (kRegLV) return lv_warp_reg(R, m, W, wofs, w, dl, lane, cells);
+    if (SA_LV_LONG && dl >= SA_BITPAR_MIN_DL && dl <= 960)
+        return lv_sys(R, (m + 31) / 32 + 1, m, W, wofs, w, dl, lane, cells);
     if (dl >= SA_BITPAR_MIN_DL && 2 * dl + 1 <= 2048)
         return lv_bitpar_warp(R, (m + 31) / 32 + 1, m, W, wofs, w, dl, lane, cells);
     if (f16) return lv_warp_smem(R, m, W, wofs, w, dl, reinterpret_cast<short*>(F), lane, cells);
@@ -467,11 +474,143 @@ SA_DEV int lv_bitpar_warp(const uint4* R, int nblk, int m, const uint4* W, uint3
     return best <= dl ? best : -1;
 }
 
+// ---------------------------------------------------------------- systolic LV
+// Banded bit-parallel bounded edit distance for large limits (long reads),
+// lane per row block with the blocks skewed in time (a systolic array):
+// the same value as bounded_distance (REF src/edit_distance.cpp:19-75), i.e.
+// min over window prefixes j <= w of the global edit distance D[m][j] when it
+// is <= dl, as lv_bitpar computes it.
+//
+// Rows (read bases) are cut into B = ceil(m / 64) blocks of 64 that END at
+// row m (block b: rows r0(b) = m - 64 (B - b) + 1 .. r0(b) + 63; rows <= 0
+// are virtual never-matching rows with D[-r][j] = j + r, which satisfy the
+// recurrence and feed row 1 as row 0 does -- see lv_bitpar).  Each block
+// keeps Myers/Hyyro vertical deltas (Pv, Mv) and D at its last row (sc);
+// column j advances it with one word step given the horizontal delta
+// entering at its top (hin, from the block above).  Block b runs column j at
+// time t = j + b, on lane b mod 32: the block above finished column j at
+// t - 1, so one shuffle per step carries (hin, sc) down the warp and no carry
+// has to cross lanes inside a step (lv_bitpar_warp's 5-step carry scan).
+//
+// Band: block b runs only the columns [r0 - dl, r0 + 63 + dl] (cells with
+// |row - col| <= dl).  Outside them, values are replaced by upper bounds: the
+// block above a block's first column holds "+1 per row" (Pv = ~0), and a
+// block whose upper neighbour has left the band sees hin = +1.  Computed
+// values are >= the true ones everywhere and equal on every cell whose true
+// value is <= dl (such a cell's optimal path stays in the band), so the
+// minimum over row m is exact whenever it is <= dl.  Every 64 steps the warp
+// stops once every running block's lower bound (sc - popcount(Pv)) exceeds
+// min(dl + 1, best): no later cell can be <= dl or beat the best found (the
+// one-step skew between neighbours costs the + 1).
+// dl <= 960 keeps one running block per lane (block b + 32 starts after b ends).
+constexpr int kSysMaxDl = 960;
+
+SA_DEV int lv_sys(const uint4* R, int nblk, int m, const uint4* W, uint32_t wofs, int w, int dl, int lane,
+                  uint32_t& cells) {
+    const int B = (m + 63) >> 6;
+    const int jend = min(w, m + dl);
+    int best = m <= dl ? m : 0x3fffffff;  // D[m][0] = m
+    if (jend >= 1 && B > 0) {
+        const int tmax = jend + B - 1;  // block B - 1's last column, skewed
+        int b = lane - 32;              // current block (loaded below)
+        int r0 = 0, js = 1, je = 0, above_end = 0;
+        uint64_t Pv = 0, Mv = 0, q0 = 0, q1 = 0, q2 = 0, q3 = 0;
+        int sc = 0;
+        bool fresh = false;
+        uint32_t gp = 0, gx = 0, gy = 0, gz = 0;
+        int pub = 0;  // published each step: (sc << 2) | (hout + 1)
+        uint32_t steps = 0;
+        for (int t = 1; t <= tmax; ++t) {
+            const int rcv = __shfl_sync(kLvFull, pub, (lane + 31) & 31);
+            if (t - b > je && b + 32 < B) {  // this lane's next block
+                b += 32;
+                r0 = m - 64 * (B - b) + 1;
+                js = max(1, r0 - dl);
+                je = min(jend, r0 + 63 + dl);
+                above_end = min(jend, r0 - 1 + dl);  // block b - 1's last column
+                uint64_t l, h, n;
+                read64(R, nblk, r0 - 1, l, h, n);  // rows r0 .. r0 + 63 = read bases r0 - 1 ..
+                q0 = ~(l | h | n);                 // eq masks per genome base (lo, hi) = (0,0) (1,0) (0,1) (1,1)
+                q1 = l & ~h & ~n;
+                q2 = ~l & h & ~n;
+                q3 = l & h & ~n;
+                if (js == 1) {  // exact column 0: D[row][0] = |row|
+                    const int t1 = 1 - r0;  // first real row's bit
+                    Pv = t1 <= 0 ? ~0ull : (t1 >= 64 ? 0ull : (~0ull << t1));
+                    Mv = ~Pv;
+                    sc = abs(r0 + 63);
+                    fresh = false;
+                } else {  // "+1 per row" below the block above (an upper bound, outside the band)
+                    Pv = ~0ull;
+                    Mv = 0ull;
+                    fresh = true;
+                }
+                gp = wofs + static_cast<uint32_t>(js - 1);  // window base of column js
+                const uint4 G = W[gp >> 5];
+                gx = G.x >> (gp & 31u);
+                gy = G.y >> (gp & 31u);
+                gz = G.z >> (gp & 31u);
+            }
+            const int j = t - b;
+            const bool act = b >= 0 && j >= js && j <= je;
+            if (act) {
+                if ((gp & 31u) == 0u) {
+                    const uint4 G = W[gp >> 5];
+                    gx = G.x;
+                    gy = G.y;
+                    gz = G.z;
+                }
+                const uint64_t eqlo = (gx & 1u) ? q1 : q0, eqhi = (gx & 1u) ? q3 : q2;
+                const uint64_t Eq0 = (gz & 1u) ? 0ull : ((gy & 1u) ? eqhi : eqlo);  // N never matches
+                gx >>= 1;
+                gy >>= 1;
+                gz >>= 1;
+                ++gp;
+                int hin = 1, scin = 0;
+                if (b > 0 && j <= above_end) {
+                    hin = (rcv & 3) - 1;
+                    scin = rcv >> 2;
+                }
+                const uint64_t hneg = hin < 0 ? 1ull : 0ull;
+                const uint64_t Xv = Eq0 | Mv;
+                const uint64_t Eq = Eq0 | hneg;
+                const uint64_t Xh = (((Eq & Pv) + Pv) ^ Pv) | Eq;
+                uint64_t Ph = Mv | ~(Xh | Pv);
+                uint64_t Mh = Pv & Xh;
+                const int hout = static_cast<int>(Ph >> 63) - static_cast<int>(Mh >> 63);
+                Ph = (Ph << 1) | (hin > 0 ? 1ull : 0ull);
+                Mh = (Mh << 1) | hneg;
+                Pv = Mh | ~(Xv | Ph);
+                Mv = Ph & Xv;
+                if (fresh) {
+                    sc = scin + __popcll(Pv) - __popcll(Mv);
+                    fresh = false;
+                } else {
+                    sc += hout;
+                }
+                pub = (sc << 2) | (hout + 1);
+                if (b == B - 1) best = min(best, sc);  // D[m][j]
+                ++steps;
+            }
+            if ((t & 63) == 0) {
+                const int bw = static_cast<int>(__reduce_min_sync(kLvFull, static_cast<uint32_t>(best)));
+                const int thr = min(dl + 1, bw);
+                const bool done = !act || sc - __popcll(Pv) > thr;
+                if (__all_sync(kLvFull, done)) break;
+            }
+        }
+        cells += steps * 64u;
+    }
+    best = static_cast<int>(__reduce_min_sync(kLvFull, static_cast<uint32_t>(best)));
+    return best <= dl ? best : -1;
+}
+
 // standalone LV (lv_batch_kernel): any limit; bitpar_min = the limit from
 // which the warp bit-parallel LV serves (test hook: lower it to cover it)
 SA_DEV int lv_warp_any(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, int dl, int* F,
-                       int lane, uint32_t& cells, int bitpar_min = SA_BITPAR_MIN_DL) {
+                       int lane, uint32_t& cells, int bitpar_min = SA_BITPAR_MIN_DL, bool long_bitpar = !SA_LV_LONG) {
     if (dl <= 15) return lv_warp_reg(R, m, W, wofs, w, dl, lane, cells);
+    if (!long_bitpar && dl >= bitpar_min && dl <= kSysMaxDl) return lv_sys(R, (m + 31) / 32 + 1, m, W, wofs, w, dl, lane, cells);
     if (dl >= bitpar_min && 2 * dl + 1 <= 2048)
         return lv_bitpar_warp(R, (m + 31) / 32 + 1, m, W, wofs, w, dl, lane, cells);
     return lv_warp_smem(R, m, W, wofs, w, dl, F, lane, cells);

@@ -123,6 +123,39 @@ def test_lv_wide_limits_vs_oracle():
     assert got == want
 
 
+def test_lv_long_limits_vs_oracle():
+    """Long reads at long-read limits (256-960: the systolic lv_sys serves
+    them, C4's 607 among them): close and diverged windows, windows cut short
+    (genome end), N bases on both sides."""
+    rng = np.random.default_rng(607)
+    triples = []
+    for t in range(48):
+        L = int(rng.integers(1500, 10001))
+        read = list(ACGT[rng.integers(0, 4, L)].tobytes().decode())
+        for _ in range(int(rng.integers(0, 4))):
+            read[int(rng.integers(0, L))] = "N"
+        read = "".join(read)
+        win = list(read)
+        rate = [0.01, 0.05, 0.08, 0.12, 0.3][t % 5]
+        for _ in range(int(L * rate)):
+            i = int(rng.integers(0, len(win)))
+            op = int(rng.integers(0, 3))
+            if op == 0:
+                win[i] = "ACGTN"[int(rng.integers(0, 5))]
+            elif op == 1:
+                win.insert(i, "ACGT"[int(rng.integers(0, 4))])
+            else:
+                del win[i]
+        dl = int(rng.integers(256, 961))
+        win = "".join(win) + ACGT[rng.integers(0, 4, dl)].tobytes().decode()
+        cut = L + dl if t % 3 else int(rng.integers(max(1, L - dl), L + dl))
+        triples.append((read, win[:cut], dl))
+    got = api.bounded_distance_batch(triples)
+    want = [O.or_bounded_distance(r, w, d) for r, w, d in triples]
+    assert got == want
+    assert any(v is None for v in want) and any(v is not None for v in want)
+
+
 # ----------------------------------------------------------------- lookup
 
 @pytest.mark.parametrize("s", [3, 4, 7, 8, 20, 31, 32])

@@ -72,16 +72,19 @@ def test_parity_multichunk_and_grid_stride():
 
 
 @pytest.mark.gpu
-def test_warp_bitparallel_lv_vs_oracle():
-    """lv_bitpar_warp (the long-read LV: band spread over the warp, carries
-    scanned across lanes, early stop once the band's minimum passes the limit)
-    through the standalone LV entry with its threshold lowered to 16
-    (SA_LV_WARP_BITPAR_MIN): the reference's known answers, the golden LV
-    triples, random pairs and wide limits (16-400 on reads of 200-3000
-    bases) against the oracle."""
+@pytest.mark.parametrize("variant", ["sys", "bitpar"])
+def test_warp_bitparallel_lv_vs_oracle(variant):
+    """The long-read LVs through the standalone LV entry with their threshold
+    lowered to 16 (SA_LV_WARP_BITPAR_MIN): lv_sys (systolic: lane per row
+    block, blocks skewed in time, the default) and lv_bitpar_warp (band
+    spread over the warp, carries scanned across lanes; SA_LV_LONG=bitpar).
+    The reference's known answers, the golden LV triples, random pairs and
+    wide limits (16-400 on reads of 200-3000 bases) against the oracle."""
+    env = {**os.environ, "SA_LV_WARP_BITPAR_MIN": "16"}
+    if variant == "bitpar":
+        env["SA_LV_LONG"] = "bitpar"
     r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-x", "-q",
                         "-m", "gpu", "-k", "lv_known or lv_random or lv_wide or lv_golden", "-p", "no:cacheprovider"],
-                       cwd=ROOT, env={**os.environ, "SA_LV_WARP_BITPAR_MIN": "16"}, capture_output=True, text=True,
-                       timeout=900)
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
