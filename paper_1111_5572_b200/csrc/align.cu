@@ -2043,8 +2043,12 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
     x.lane = lane;
     // pruning-batch area at the end of the warp's share (capi.cu make_shape)
     unsigned char* pb = a.pb_on ? ws + a.smem_per_warp - kPbBytes : nullptr;
-    uint4* planes = reinterpret_cast<uint4*>(ws);  // buffer q: R = planes + 2q*wbr, C = R + wbr
-    x.W = planes + (a.prefetch ? 4 : 2) * a.wbr;  // one {R, C} buffer without the read pipeline
+    // buffer q: R = planes + 2q*wbr, C = R + wbr (global slot per warp for the long-read layouts)
+    uint4* planes = a.gplanes ? a.gplanes + static_cast<uint64_t>((blockIdx.x * blockDim.x + threadIdx.x) >> 5) *
+                                                a.gplanes_per_warp
+                              : reinterpret_cast<uint4*>(ws);
+    // one {R, C} buffer without the read pipeline
+    x.W = a.gplanes ? reinterpret_cast<uint4*>(ws) : planes + (a.prefetch ? 4 : 2) * a.wbr;
     uint4* recs = x.W + (a.gw ? 0 : a.wbw);  // 2 x 32; no window area when the LV reads the genome in place
     uint4* pslot = recs + 64;                       // 32
     unsigned long long* pcanon = reinterpret_cast<unsigned long long*>(pslot + 32);  // 32
@@ -2786,7 +2790,9 @@ int launch_align_pre(const AlignLaunch& a, int grid, int block, cudaStream_t st)
     return 1 + launch_align_seeded(a, grid, block, st);
 }
 
-void launch_align_slow(const AlignLaunch& a, int grid, int block, cudaStream_t st) {
+void launch_align_slow(const AlignLaunch& a0, int grid, int block, cudaStream_t st) {
+    AlignLaunch a = a0;
+    a.gplanes = nullptr;  // its own grid: planes in shared memory (slow_smem_per_warp holds them)
     if (a.dl_max <= 15) launch_variant<true, false, true>(a, grid, block, st);
     else launch_variant<true, false, false>(a, grid, block, st);
 }

@@ -65,6 +65,12 @@ struct AlignLaunch {
     int lcap;
     int f16;  // LV frontier as 16-bit entries (reads < 32 k bases)
     int gw;   // shared-memory LV reads the genome window from global memory (no staging area)
+    // long-read layouts with the systolic LV (dl_max >= 256): the read's
+    // planes {R, C} live in a per-warp global slot (gplanes + warp id *
+    // gplanes_per_warp uint4s) instead of shared memory -- lv_sys touches
+    // them once per 64 rows -- so more warps fit per SM (null: shared memory)
+    uint4* gplanes;
+    uint32_t gplanes_per_warp;
     int bs_shift;  // log2(bucket_size) when it is a power of two, else -1
     // Two-kernel path (seed_kernel + align_kernel<.., kPre>): per read, the
     // seed kernel writes forward then reverse-complement planes

@@ -86,6 +86,8 @@ struct Stage {  // one of the two pipeline slots of a replica
     cudaEvent_t k0 = nullptr, km = nullptr, k1 = nullptr;  // fast kernel [k0,km), slow [km,k1)
     cudaEvent_t done = nullptr;                             // after the stage's last D2H
     bool done_pending = false;  // sa_align_device: `done` recorded after the last call's work
+    uint4* d_gplanes = nullptr;  // per-warp global read planes of the long-read layouts (AlignLaunch::gplanes)
+    uint64_t gplanes_bytes = 0;
     // seed-kernel outputs of the two-kernel path (launch_align_pre)
     uint4* pre_planes = nullptr;
     uint4* pre_recs = nullptr;
@@ -139,6 +141,7 @@ struct LaunchShape {
     uint64_t slow_table_bytes;
     uint64_t scratch_bytes;  // global candidate tables of the overflow path
     int slow_cap, slow_hcap;
+    uint64_t gplanes_bytes;  // per-warp global read planes (long-read layouts, AlignLaunch::gplanes)
 };
 
 struct Replica {
@@ -279,8 +282,13 @@ int make_shape(Replica& rep, const sa_params* p, uint64_t Lmax, LaunchShape& sh,
     // gw: the LV reads the genome window from global memory (always for the
     // register LV; for the shared-memory LV only when dropping the staged
     // window fits more warps)
+    // gp: the read planes in a per-warp global slot (long reads with the
+    // systolic LV, which reads them once per 64 rows; SA_NO_GPLANES keeps them
+    // in shared memory).  C4: 10 -> 19 warps per SM.
+    static const bool no_gplanes = getenv("SA_NO_GPLANES") != nullptr;
+    const bool gp = !no_gplanes && !a.prefetch && SA_LV_LONG && a.dl_max >= SA_BITPAR_MIN_DL && a.dl_max <= kSysMaxDl;
     auto common_for = [&](int f16, int gw) {
-        return 16ull * ((a.prefetch ? 4 : 2) * a.wbr + (gw ? 0 : a.wbw) + 64 + 32) + 8ull * 32 +
+        return 16ull * ((gp ? 0 : (a.prefetch ? 4 : 2) * a.wbr) + (gw ? 0 : a.wbw) + 64 + 32) + 8ull * 32 +
                4ull * (2 * a.n_off_cap + f_ints_for(f16)) + 8ull * kNumStats;
     };
     // the pruning batch's area (align.cu prune_batch) closes each warp's share
@@ -414,7 +422,7 @@ int make_shape(Replica& rep, const sa_params* p, uint64_t Lmax, LaunchShape& sh,
     sh.slow_cap = static_cast<int>(cap_slow);
     sh.slow_hcap = static_cast<int>(hcap_slow);
     sh.slow_table_bytes = (cand_table_bytes(sh.slow_cap, sh.slow_hcap) + 255) & ~255ull;
-    sh.slow_smem_per_warp = round16(common) + pb_bytes;
+    sh.slow_smem_per_warp = round16(common + (gp ? 16ull * 2 * a.wbr : 0)) + pb_bytes;  // planes in shared memory there
     uint64_t slow_warps = std::min<uint64_t>(static_cast<uint64_t>(rep.sm_count) * kRegWarpsPerSM,
                                              std::max<uint64_t>(32, kSlowScratchBudget / sh.slow_table_bytes));
     // 8-warp blocks where shared memory allows: the device path launches this
@@ -426,6 +434,12 @@ int make_shape(Replica& rep, const sa_params* p, uint64_t Lmax, LaunchShape& sh,
     sh.slow_grid = static_cast<int>(slow_warps / sw);
     a.gscratch_per_warp = sh.slow_table_bytes;
     sh.scratch_bytes = slow_warps * sh.slow_table_bytes;
+    a.gplanes = nullptr;
+    a.gplanes_per_warp = gp ? static_cast<uint32_t>(2 * a.wbr) : 0u;
+    sh.gplanes_bytes = gp ? 16ull * a.gplanes_per_warp *
+                                static_cast<uint64_t>(std::max(sh.fast_grid * (sh.fast_block / 32),
+                                                               sh.pipe_grid * (sh.pipe_block / 32)))
+                          : 0;
     // the slow launch overrides cap/hcap/smem_per_warp
     return SA_OK;
 }
@@ -593,6 +607,17 @@ void set_pq(AlignLaunch& a, const Stage& s) {
     a.pq_list = s.pq_list;
 }
 
+// a stage's global read-plane slots (kernels of different stages run concurrently)
+int ensure_gplanes(sa_context* ctx, Stage& s, const LaunchShape& sh) {
+    if (sh.gplanes_bytes > s.gplanes_bytes) {
+        if (s.d_gplanes) cudaFree(s.d_gplanes);
+        s.d_gplanes = nullptr;
+        CUDA_TRY(ctx, cudaMalloc(&s.d_gplanes, sh.gplanes_bytes));
+        s.gplanes_bytes = sh.gplanes_bytes;
+    }
+    return SA_OK;
+}
+
 int ensure_scratch(sa_context* ctx, Replica& rep, const LaunchShape& sh) {
     const uint64_t need = sh.scratch_bytes;
     if (need > rep.gscratch_bytes) {
@@ -640,6 +665,8 @@ int enqueue_align(sa_context* ctx, Replica& rep, Stage& stg, const LaunchShape& 
     a.error_read = rep.d_err_read;
     a.read_base = read_base;
     a.gscratch = rep.d_gscratch;
+    if (int rc = ensure_gplanes(ctx, stg, sh)) return rc;
+    a.gplanes = a.gplanes_per_warp ? stg.d_gplanes : nullptr;
     CUDA_TRY(ctx, cudaMemsetAsync(stg.d_ctl, 0, kCtlWords * sizeof(unsigned int), stg.st));
     if (time_it) CUDA_TRY(ctx, cudaEventRecord(stg.k0, stg.st));
     if (use_pre() && a.prefetch && stg.pre_planes) {  // seed kernel + align kernel
@@ -783,6 +810,7 @@ int overflow_pass(sa_context* ctx, Replica& rep, Stage& stg, const sa_params* pa
     b.error_read = rep.d_err_read;
     b.read_base = 0;
     b.gscratch = rep.d_gscratch;
+    b.gplanes = nullptr;
     b.cap = sh.slow_cap;
     b.hcap = sh.slow_hcap;
     b.smem_per_warp = sh.slow_smem_per_warp;
@@ -959,6 +987,8 @@ int align_streamed(sa_context* ctx, Replica& rep, const sa_params* params, const
     a.error_read = rep.d_err_read;
     a.read_base = 0;
     a.gscratch = rep.d_gscratch;
+    if (int rc = ensure_gplanes(ctx, rep.stage[0], sh)) return rc;
+    a.gplanes = a.gplanes_per_warp ? rep.stage[0].d_gplanes : nullptr;
     a.chunk_flag = S.flags;
     a.chunk_done = S.done;
     a.chunk_adj = S.adj;
@@ -1288,6 +1318,7 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
         a.error_read = rep.d_err_read;
         a.read_base = r0;
         a.gscratch = rep.d_gscratch;
+        a.gplanes = nullptr;  // seeded layouts (reads <= 1 kbp) keep their planes in shared memory
         a.pre_planes = st.pre_planes;
         a.pre_recs = st.pre_recs;
         a.pre_meta = st.pre_meta;
@@ -1556,6 +1587,8 @@ void sa_destroy(sa_context* ctx) {
         if (rep.d_err_read) cudaFree(rep.d_err_read);
         if (rep.h_ctl) cudaFreeHost(rep.h_ctl);
         if (rep.d_gscratch) cudaFree(rep.d_gscratch);
+        for (auto& sg : rep.stage)
+            if (sg.d_gplanes) cudaFree(sg.d_gplanes);
         if (rep.d_defer) cudaFree(rep.d_defer);
         for (void* q : {static_cast<void*>(rep.sm.bases), static_cast<void*>(rep.sm.offs),
                         static_cast<void*>(rep.sm.res), static_cast<void*>(rep.sm.flags),
@@ -1824,6 +1857,7 @@ int sa_align_device(sa_context* ctx, const sa_params* params, const char* d_base
     if (int rc = ensure_stage(ctx, stg, 0, n_reads)) return rc;
     const uint64_t pre_n = dev_chunk_reads() ? std::min(n_reads, dev_chunk_reads()) : n_reads;
     if (int rc = ensure_pre(ctx, stg, pre_n, sh)) return rc;
+    if (int rc = ensure_gplanes(ctx, stg, sh)) return rc;  // before the per-call copy below
     // The caller's stream drives; this stage keeps only control words and
     // the seed-kernel scratch, which every call shares.  A call on another
     // stream therefore waits for the previous call's work (event `done`), so

@@ -27,6 +27,17 @@
 
 namespace sab {
 
+// Long-read LV (lv.cuh): limits from SA_BITPAR_MIN_DL up to kSysMaxDl use the
+// systolic bit-parallel lv_sys (SA_LV_LONG 1) or lv_bitpar_warp (0, and above
+// kSysMaxDl up to 1023); below, the LV wavefronts.
+#ifndef SA_BITPAR_MIN_DL
+#define SA_BITPAR_MIN_DL 256
+#endif
+#ifndef SA_LV_LONG
+#define SA_LV_LONG 1
+#endif
+constexpr int kSysMaxDl = 960;
+
 constexpr uint64_t kEmptyKey = ~0ull;
 constexpr int kInfDistance = 0x7fffffff / 4;  // REF include/seedaln/aligner.hpp:15
 constexpr int kGapCap = 1000;                 // REF aligner.hpp:34

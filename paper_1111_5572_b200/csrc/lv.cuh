@@ -111,22 +111,16 @@ SA_DEV int lv_warp_smem(const uint4* R, int m, const uint4* W, uint32_t wofs, in
 // kRegLV: every d_limit of the launch is <= 15 (register wavefront only);
 // otherwise the shared-memory wavefront serves every limit.  One variant per
 // kernel keeps the inlined code small.
-#ifndef SA_BITPAR_MIN_DL
-#define SA_BITPAR_MIN_DL 256  // limits from here use lv_bitpar_warp (long reads; C4's 607)
-#endif
 SA_DEV int lv_bitpar_warp(const uint4* R, int nblk, int m, const uint4* W, uint32_t wofs, int w, int dl, int lane,
                           uint32_t& cells);
 SA_DEV int lv_sys(const uint4* R, int nblk, int m, const uint4* W, uint32_t wofs, int w, int dl, int lane,
                   uint32_t& cells);
-#ifndef SA_LV_LONG
-#define SA_LV_LONG 1  // limits >= SA_BITPAR_MIN_DL: 1 systolic (lv_sys, dl <= 960), 0 lv_bitpar_warp
-#endif
 
 template <bool kRegLV>
 SA_DEV int lv_warp(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, int dl, int* F,
                    int lane, uint32_t& cells, bool f16 = false) {
     if (kRegLV) return lv_warp_reg(R, m, W, wofs, w, dl, lane, cells);
-    if (SA_LV_LONG && dl >= SA_BITPAR_MIN_DL && dl <= 960)
+    if (SA_LV_LONG && dl >= SA_BITPAR_MIN_DL && dl <= kSysMaxDl)
         return lv_sys(R, (m + 31) / 32 + 1, m, W, wofs, w, dl, lane, cells);
     if (dl >= SA_BITPAR_MIN_DL && 2 * dl + 1 <= 2048)
         return lv_bitpar_warp(R, (m + 31) / 32 + 1, m, W, wofs, w, dl, lane, cells);
@@ -502,8 +496,8 @@ SA_DEV int lv_bitpar_warp(const uint4* R, int nblk, int m, const uint4* W, uint3
 // stops once every running block's lower bound (sc - popcount(Pv)) exceeds
 // min(dl + 1, best): no later cell can be <= dl or beat the best found (the
 // one-step skew between neighbours costs the + 1).
-// dl <= 960 keeps one running block per lane (block b + 32 starts after b ends).
-constexpr int kSysMaxDl = 960;
+// dl <= kSysMaxDl (960, common.cuh) keeps one running block per lane (block
+// b + 32 starts after b ends).
 
 SA_DEV int lv_sys(const uint4* R, int nblk, int m, const uint4* W, uint32_t wofs, int w, int dl, int lane,
                   uint32_t& cells) {

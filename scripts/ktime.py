@@ -29,7 +29,10 @@ for i in range(3):
     al.align_device(db.data_ptr(), do.data_ptr(), n, cfg.read_len, dr.data_ptr(), 0, s)
     al.sync(s)
     lib.sab_debug_ktimes(b"device")
-hr = np.zeros(n, api.RESULT_DTYPE)
+pin_b, pin_r = api.PinnedBuffer(bases.nbytes), api.PinnedBuffer(n * 24)
+hb = pin_b.array(np.uint8, bases.size)
+hb[:] = bases
+hr = pin_r.array(api.RESULT_DTYPE, n)
 for i in range(3):
-    al.align_arrays(bases, offs, hr)
+    al.align_arrays(hb, offs, hr)
     lib.sab_debug_ktimes(b"pipeline")
