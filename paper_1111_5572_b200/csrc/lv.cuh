@@ -481,10 +481,11 @@ SA_DEV int lv_bitpar_warp(const uint4* R, int nblk, int m, const uint4* W, uint3
 // recurrence and feed row 1 as row 0 does -- see lv_bitpar).  Each block
 // keeps Myers/Hyyro vertical deltas (Pv, Mv) and D at its last row (sc);
 // column j advances it with one word step given the horizontal delta
-// entering at its top (hin, from the block above).  Block b runs column j at
-// time t = j + b, on lane b mod 32: the block above finished column j at
-// t - 1, so one shuffle per step carries (hin, sc) down the warp and no carry
-// has to cross lanes inside a step (lv_bitpar_warp's 5-step carry scan).
+// entering at its top (hin, from the block above).  Block b runs columns
+// 2p - 1 and 2p at time t = p + b, on lane b mod 32: the block above finished
+// them at t - 1, so one shuffle per step carries (both hin, sc) down the warp
+// and no carry has to cross lanes inside a step (lv_bitpar_warp's 5-step
+// carry scan); two columns per step halve the per-step bookkeeping.
 //
 // Band: block b runs only the columns [r0 - dl, r0 + 63 + dl] (cells with
 // |row - col| <= dl).  Outside them, values are replaced by upper bounds: the
@@ -494,8 +495,8 @@ SA_DEV int lv_bitpar_warp(const uint4* R, int nblk, int m, const uint4* W, uint3
 // value is <= dl (such a cell's optimal path stays in the band), so the
 // minimum over row m is exact whenever it is <= dl.  Every 64 steps the warp
 // stops once every running block's lower bound (sc - popcount(Pv)) exceeds
-// min(dl + 1, best): no later cell can be <= dl or beat the best found (the
-// one-step skew between neighbours costs the + 1).
+// min(dl, best - 1) + 2: no later cell can be <= dl or beat the best found
+// (the two-column skew between neighbours costs the + 2).
 // dl <= kSysMaxDl (960, common.cuh) keeps one running block per lane (block
 // b + 32 starts after b ends).
 
@@ -505,23 +506,60 @@ SA_DEV int lv_sys(const uint4* R, int nblk, int m, const uint4* W, uint32_t wofs
     const int jend = min(w, m + dl);
     int best = m <= dl ? m : 0x3fffffff;  // D[m][0] = m
     if (jend >= 1 && B > 0) {
-        const int tmax = jend + B - 1;  // block B - 1's last column, skewed
-        int b = lane - 32;              // current block (loaded below)
-        int r0 = 0, js = 1, je = 0, above_end = 0;
+        constexpr int kNever = 0x3fffffff;
+        // two columns per step: block b runs columns 2p - 1, 2p at time p + b
+        const int tmax = ((jend + 1) >> 1) + B - 1;
+        int b = lane - 32;                    // current block (loaded at t == tsw)
+        int tsw = lane < B ? 1 : kNever;      // time of the next block switch
+        int ts = kNever, te = -1;             // running steps [ts, te] of the current block
+        int js = 1, je = 0, ae = -kNever;     // its columns, and the block above's last column
         uint64_t Pv = 0, Mv = 0, q0 = 0, q1 = 0, q2 = 0, q3 = 0;
         int sc = 0;
         bool fresh = false;
         uint32_t gp = 0, gx = 0, gy = 0, gz = 0;
-        int pub = 0;  // published each step: (sc << 2) | (hout + 1)
-        uint32_t steps = 0;
+        int pub = 0;  // published each step: (sc << 4) | (hout(2p - 1) + 1) << 2 | (hout(2p) + 1)
+        uint32_t cols = 0;
+        const bool last_lane_block = ((B - 1) & 31) == lane;
+        // one column of this lane's block: Myers/Hyyro word step, hin entering at the top
+        auto column = [&](int hin) -> int {
+            if ((gp & 31u) == 0u) {
+                const uint4 G = W[gp >> 5];
+                gx = G.x;
+                gy = G.y;
+                gz = G.z;
+            }
+            const uint64_t eqlo = (gx & 1u) ? q1 : q0, eqhi = (gx & 1u) ? q3 : q2;
+            const uint64_t Eq0 = (gz & 1u) ? 0ull : ((gy & 1u) ? eqhi : eqlo);  // N never matches
+            gx >>= 1;
+            gy >>= 1;
+            gz >>= 1;
+            ++gp;
+            const uint64_t hneg = hin < 0 ? 1ull : 0ull;
+            const uint64_t Xv = Eq0 | Mv;
+            const uint64_t Eq = Eq0 | hneg;
+            const uint64_t Xh = (((Eq & Pv) + Pv) ^ Pv) | Eq;
+            uint64_t Ph = Mv | ~(Xh | Pv);
+            uint64_t Mh = Pv & Xh;
+            const int hout = static_cast<int>(Ph >> 63) - static_cast<int>(Mh >> 63);
+            Ph = (Ph << 1) | (hin > 0 ? 1ull : 0ull);
+            Mh = (Mh << 1) | hneg;
+            Pv = Mh | ~(Xv | Ph);
+            Mv = Ph & Xv;
+            ++cols;
+            return hout;
+        };
+        bool act = false;
         for (int t = 1; t <= tmax; ++t) {
             const int rcv = __shfl_sync(kLvFull, pub, (lane + 31) & 31);
-            if (t - b > je && b + 32 < B) {  // this lane's next block
+            if (t == tsw) {  // this lane's next block
                 b += 32;
-                r0 = m - 64 * (B - b) + 1;
+                const int r0 = m - 64 * (B - b) + 1;
                 js = max(1, r0 - dl);
                 je = min(jend, r0 + 63 + dl);
-                above_end = min(jend, r0 - 1 + dl);  // block b - 1's last column
+                ts = ((js + 1) >> 1) + b;
+                te = ((je + 1) >> 1) + b;
+                tsw = b + 32 < B ? te + 1 : kNever;
+                ae = b > 0 ? min(jend, r0 - 1 + dl) : -kNever;
                 uint64_t l, h, n;
                 read64(R, nblk, r0 - 1, l, h, n);  // rows r0 .. r0 + 63 = read bases r0 - 1 ..
                 q0 = ~(l | h | n);                 // eq masks per genome base (lo, hi) = (0,0) (1,0) (0,1) (1,1)
@@ -545,55 +583,42 @@ SA_DEV int lv_sys(const uint4* R, int nblk, int m, const uint4* W, uint32_t wofs
                 gy = G.y >> (gp & 31u);
                 gz = G.z >> (gp & 31u);
             }
-            const int j = t - b;
-            const bool act = b >= 0 && j >= js && j <= je;
+            act = t >= ts && t <= te;
             if (act) {
-                if ((gp & 31u) == 0u) {
-                    const uint4 G = W[gp >> 5];
-                    gx = G.x;
-                    gy = G.y;
-                    gz = G.z;
-                }
-                const uint64_t eqlo = (gx & 1u) ? q1 : q0, eqhi = (gx & 1u) ? q3 : q2;
-                const uint64_t Eq0 = (gz & 1u) ? 0ull : ((gy & 1u) ? eqhi : eqlo);  // N never matches
-                gx >>= 1;
-                gy >>= 1;
-                gz >>= 1;
-                ++gp;
-                int hin = 1, scin = 0;
-                if (b > 0 && j <= above_end) {
-                    hin = (rcv & 3) - 1;
-                    scin = rcv >> 2;
-                }
-                const uint64_t hneg = hin < 0 ? 1ull : 0ull;
-                const uint64_t Xv = Eq0 | Mv;
-                const uint64_t Eq = Eq0 | hneg;
-                const uint64_t Xh = (((Eq & Pv) + Pv) ^ Pv) | Eq;
-                uint64_t Ph = Mv | ~(Xh | Pv);
-                uint64_t Mh = Pv & Xh;
-                const int hout = static_cast<int>(Ph >> 63) - static_cast<int>(Mh >> 63);
-                Ph = (Ph << 1) | (hin > 0 ? 1ull : 0ull);
-                Mh = (Mh << 1) | hneg;
-                Pv = Mh | ~(Xv | Ph);
-                Mv = Ph & Xv;
-                if (fresh) {
-                    sc = scin + __popcll(Pv) - __popcll(Mv);
+                const int j2 = 2 * (t - b), j1 = j2 - 1;
+                const int h1a = ((rcv >> 2) & 3) - 1, h2a = (rcv & 3) - 1, sce = rcv >> 4;
+                const int hin1 = j1 <= ae ? h1a : 1;  // the block above left the band: +1
+                const int hin2 = j2 <= ae ? h2a : 1;
+                int ho1 = 0, ho2 = 0;
+                const bool last = last_lane_block && b == B - 1;
+                if (j1 >= js) {
+                    // a new block's bottom before its first column: the block above's D
+                    // there (its D at j1 is its published sc less its hout at j2) + 64
+                    if (fresh) sc = sce - (j2 <= ae ? h2a : 0) - hin1 + 64;
                     fresh = false;
-                } else {
-                    sc += hout;
+                    ho1 = column(hin1);
+                    sc += ho1;
+                    if (last) best = min(best, sc);  // D[m][j1]
                 }
-                pub = (sc << 2) | (hout + 1);
-                if (b == B - 1) best = min(best, sc);  // D[m][j]
-                ++steps;
+                if (j2 <= je) {
+                    if (fresh) sc = sce - hin2 + 64;
+                    fresh = false;
+                    ho2 = column(hin2);
+                    sc += ho2;
+                    if (last) best = min(best, sc);  // D[m][j2]
+                }
+                pub = (sc << 4) | ((ho1 + 1) << 2) | (ho2 + 1);
             }
             if ((t & 63) == 0) {
+                // neighbours are one step (two columns) apart: future cells stay
+                // above min(dl, best - 1) once every running block's bound exceeds it by 2
                 const int bw = static_cast<int>(__reduce_min_sync(kLvFull, static_cast<uint32_t>(best)));
-                const int thr = min(dl + 1, bw);
+                const int thr = min(dl + 2, bw + 1);
                 const bool done = !act || sc - __popcll(Pv) > thr;
                 if (__all_sync(kLvFull, done)) break;
             }
         }
-        cells += steps * 64u;
+        cells += cols * 64u;
     }
     best = static_cast<int>(__reduce_min_sync(kLvFull, static_cast<uint32_t>(best)));
     return best <= dl ? best : -1;

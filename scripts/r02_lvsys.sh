@@ -1,0 +1,7 @@
+#!/bin/bash
+# lv_sys checks on one B200: LV parity suites, every C4 read, C4 bench
+O=gpurun_out; mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -m gpu -k "lv_" > $O/t_lv.log 2>&1; echo rc=$? >> $O/t_lv.log
+timeout 900 python -m pytest tests/test_gpu_solo.py -q -x -m gpu -k "warp_bitparallel" > $O/t_lvw.log 2>&1; echo rc=$? >> $O/t_lvw.log
+timeout 1200 python -m pytest tests/test_gpu_fullsize.py -q -x -m gpu -k "c4" > $O/t_c4.log 2>&1; echo rc=$? >> $O/t_c4.log
+timeout 900 python bench.py --config C4 --steps 3 --no-cpu-baseline > $O/b_c4.json 2> $O/b_c4.err
