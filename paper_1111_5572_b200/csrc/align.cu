@@ -356,7 +356,10 @@ SA_DEV unsigned long long shfl64(unsigned long long v, int src) {
 }
 
 // REF aligner.cpp:169-221 score_candidate
-template <bool kRegLV>
+// kSys: the kernel may run the systolic long-read LV (lv_sys): only the
+// dynamic-fetch kernel of reads > 1 kbp; elsewhere its inlined code only
+// raised register pressure (C3's seeded kernel spilled 40 -> 112 B, 120 -> 140 ms)
+template <bool kRegLV, bool kSys = false>
 SA_DEV void score_candidate(Ctx& x, uint32_t idx) {
     const AlignLaunch& a = *x.a;
     const int lane = x.lane;
@@ -455,7 +458,7 @@ SA_DEV void score_candidate(Ctx& x, uint32_t idx) {
         const uint64_t want = static_cast<uint64_t>(x.len) + static_cast<uint64_t>(d_limit);
         const int w = static_cast<int>(want < rem ? want : rem);
         const uint32_t wofs = static_cast<uint32_t>(anchor - gb0 * 32);
-        const int d = lv_warp<kRegLV>(orient, x.len, Wsrc, wofs, w, d_limit, x.F, lane, x.cells, a.f16 != 0);
+        const int d = lv_warp<kRegLV, kSys>(orient, x.len, Wsrc, wofs, w, d_limit, x.F, lane, x.cells, a.f16 != 0);
 #if SA_DEBUG_COUNTERS
         if (a.dbg && lane == 0) {  // seed-loop (warp) LV: calls, iterations, d_limit sum
             atomicAdd(a.dbg + 4, 1u);
@@ -523,10 +526,10 @@ SA_DEV int pick_best(Ctx& x) {
     return __shfl_sync(FULL, bi, __ffs(win) - 1);
 }
 
-template <bool kRegLV>
+template <bool kRegLV, bool kSys = false>
 SA_DEV void score_best(Ctx& x) {
     const int bi = pick_best(x);
-    if (bi >= 0) score_candidate<kRegLV>(x, static_cast<uint32_t>(bi));
+    if (bi >= 0) score_candidate<kRegLV, kSys>(x, static_cast<uint32_t>(bi));
 }
 
 // ------------------------------------------------------------------ pruning batch
@@ -1140,7 +1143,7 @@ SA_DEV bool pq_defer(Ctx& x, uint32_t r, int B, bool any_popular, bool any_looku
 // records of wave 0 when wave0_ready.  Returns 0 when the candidate table
 // overflowed (nothing committed), 1 when the read is done, 2 when it went to
 // the prune queue.
-template <bool kRegLV, bool kSlow = false>
+template <bool kRegLV, bool kSlow = false, bool kSys = false>
 SA_DEV int align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
                       unsigned long long& acc, uint4* recs, bool wave0_ready, const uint4* grecs = nullptr,
                       unsigned char* pb = nullptr) {
@@ -1362,12 +1365,12 @@ SA_DEV int align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
             }
             if (big_ok) {
                 const unsigned long long* big = reinterpret_cast<const unsigned long long*>(x.t.hval);
-                score_candidate<kRegLV>(x, static_cast<uint32_t>(big[big_pos++] & 0x3fffu));
+                score_candidate<kRegLV, kSys>(x, static_cast<uint32_t>(big[big_pos++] & 0x3fffu));
             } else {
-                score_best<kRegLV>(x);
+                score_best<kRegLV, kSys>(x);
             }
         } else {
-            score_best<kRegLV>(x);  // REF :288 (and :306 inside the pruning loop)
+            score_best<kRegLV, kSys>(x);  // REF :288 (and :306 inside the pruning loop)
         }
         if (x.tr.d_best < a.c && x.tr.d_second < x.tr.d_best + a.c) {  // REF :290-295 / :307-312
             stat_add(x, S_MULTI, 1u);
@@ -2044,11 +2047,13 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
     // pruning-batch area at the end of the warp's share (capi.cu make_shape)
     unsigned char* pb = a.pb_on ? ws + a.smem_per_warp - kPbBytes : nullptr;
     // buffer q: R = planes + 2q*wbr, C = R + wbr (global slot per warp for the long-read layouts)
-    uint4* planes = a.gplanes ? a.gplanes + static_cast<uint64_t>((blockIdx.x * blockDim.x + threadIdx.x) >> 5) *
-                                                a.gplanes_per_warp
-                              : reinterpret_cast<uint4*>(ws);
+    // (only the dynamic-fetch kernel of reads > 1 kbp has global planes)
+    const bool gpl = !kPipe && !kSlow && a.gplanes != nullptr;
+    uint4* planes = gpl ? a.gplanes + static_cast<uint64_t>((blockIdx.x * blockDim.x + threadIdx.x) >> 5) *
+                                          a.gplanes_per_warp
+                        : reinterpret_cast<uint4*>(ws);
     // one {R, C} buffer without the read pipeline
-    x.W = a.gplanes ? reinterpret_cast<uint4*>(ws) : planes + (a.prefetch ? 4 : 2) * a.wbr;
+    x.W = gpl ? reinterpret_cast<uint4*>(ws) : planes + (a.prefetch ? 4 : 2) * a.wbr;
     uint4* recs = x.W + (a.gw ? 0 : a.wbw);  // 2 x 32; no window area when the LV reads the genome in place
     uint4* pslot = recs + 64;                       // 32
     unsigned long long* pcanon = reinterpret_cast<unsigned long long*>(pslot + 32);  // 32
@@ -2145,7 +2150,7 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
             x.len = len;
             x.d_max = a.dmax_param >= 0 ? a.dmax_param : (12 * len + 99) / 100;
             const int ne = ne_pre >= 0 ? ne_pre : (q ? n_eff1 : n_eff0);
-            if (align_one<kRegLV, kSlow>(x, r, ne, offs + q * a.n_off_cap, len / a.s, acc, recs + 32 * q, wave0_ready,
+            if (align_one<kRegLV, kSlow, !kPipe && !kSlow && !kRegLV>(x, r, ne, offs + q * a.n_off_cap, len / a.s, acc, recs + 32 * q, wave0_ready,
                                   grecs, pb) == 0)
                 overflowed(r);
         }

@@ -274,6 +274,15 @@ int make_shape(Replica& rep, const sa_params* p, uint64_t Lmax, LaunchShape& sh,
     a.prefetch = L <= 1024 ? 1 : 0;
     a.cap = kFastCap;
     a.hcap = kFastHcap;
+    if (a.dl_max > 15) {  // long-read layouts: SA_LONG_CAP candidates in the shared table (tuning)
+        static const int long_cap = [] {
+            const char* e = getenv("SA_LONG_CAP");
+            return e ? std::max(16, std::min(1024, atoi(e))) : kFastCap;
+        }();
+        a.cap = long_cap;
+        a.hcap = 1;
+        while (a.hcap < 2 * a.cap) a.hcap <<= 1;
+    }
     a.lcap = L;  // every read of this layout fits
     a.sbw = a.prefetch ? round4((L + 3) / 4 + 2) : 0;
     auto f_ints_for = [&](int f16) {

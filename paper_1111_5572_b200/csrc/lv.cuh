@@ -116,11 +116,11 @@ SA_DEV int lv_bitpar_warp(const uint4* R, int nblk, int m, const uint4* W, uint3
 SA_DEV int lv_sys(const uint4* R, int nblk, int m, const uint4* W, uint32_t wofs, int w, int dl, int lane,
                   uint32_t& cells);
 
-template <bool kRegLV>
+template <bool kRegLV, bool kSys = false>
 SA_DEV int lv_warp(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, int dl, int* F,
                    int lane, uint32_t& cells, bool f16 = false) {
     if (kRegLV) return lv_warp_reg(R, m, W, wofs, w, dl, lane, cells);
-    if (SA_LV_LONG && dl >= SA_BITPAR_MIN_DL && dl <= kSysMaxDl)
+    if (kSys && SA_LV_LONG && dl >= SA_BITPAR_MIN_DL && dl <= kSysMaxDl)
         return lv_sys(R, (m + 31) / 32 + 1, m, W, wofs, w, dl, lane, cells);
     if (dl >= SA_BITPAR_MIN_DL && 2 * dl + 1 <= 2048)
         return lv_bitpar_warp(R, (m + 31) / 32 + 1, m, W, wofs, w, dl, lane, cells);
