@@ -13,7 +13,7 @@ timeout 1200 python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_re
 for c in C0 C1 C3 C4; do
   timeout 900 python bench.py --config $c --steps 5 > $O/bench_${TAG}_$c.json 2> $O/bench_${TAG}_$c.err
 done
-timeout 900 python bench.py --box --box-devices 0,0 --steps 5 > $O/bench_${TAG}_box00.json 2> $O/bench_${TAG}_box00.err
+timeout 900 python bench.py --box --box-devices 0,0 --config C1 --steps 5 > $O/bench_${TAG}_box00.json 2> $O/bench_${TAG}_box00.err
 B="python bench.py --steps 1 --warmup 3 --no-cpu-baseline"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k 'regex:align_kernel' -c 12 --csv \
     --log-file $O/launches_${TAG}_C4.csv $B --config C4 > $O/ncu_l4_$TAG.log 2>&1
