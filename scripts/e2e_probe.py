@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--calls", type=int, default=8)
     ap.add_argument("--copy-floor", action="store_true")
     ap.add_argument("--config", default="C1")
+    ap.add_argument("--pageable", action="store_true", help="time the call from ordinary (pageable) numpy buffers")
     args = ap.parse_args()
     import torch
 
@@ -37,6 +38,8 @@ def main():
     hr = pin_r.array(api.RESULT_DTYPE, args.reads)
     hb[:] = bases
     ho[:] = offs
+    if args.pageable:
+        hb, ho, hr = bases, offs, np.zeros(args.reads, api.RESULT_DTYPE)
     for _ in range(3):
         al.align_arrays(hb, ho, hr)
     ms = []
@@ -45,7 +48,7 @@ def main():
         al.align_arrays(hb, ho, hr)
         ms.append(1000 * (time.perf_counter() - t0))
     ms.sort()
-    print(f"chunk={os.environ.get('SA_CHUNK_READS', 'auto')} e2e ms min {ms[0]:.3f} median {ms[len(ms)//2]:.3f} "
+    print(f"{'pageable ' if args.pageable else ''}chunk={os.environ.get('SA_CHUNK_READS', 'auto')} e2e ms min {ms[0]:.3f} median {ms[len(ms)//2]:.3f} "
           f"-> {args.reads / ms[len(ms)//2] / 1e3:.1f} M reads/s; event span {al.last_timing()[0]:.3f} ms", flush=True)
     if args.copy_floor:
         x = torch.from_numpy(hb)  # pinned
