@@ -15,7 +15,7 @@ launching stream, L2 flushed (256 MiB write) before every timed step, max over
 ranks.  `e2e`: the same batch through the public C-ABI call sa_align_batch from
 pinned host buffers (H2D reads, kernels, D2H results inside the timed region);
 `e2e.pageable` repeats it from ordinary (pageable) host memory, which the
-library stages through its own pinned buffers.  Weak scaling: each rank aligns
+library packs (2+1 bits per base, every host thread) into its own pinned buffers.  Weak scaling: each rank aligns
 its own reads against its own index replica; no collective on the data path.
 `--impl reference`: the reference's own CPU Aligner (oracle/_ref, compiled from
 /root/reference) on all host cores over the SAME reads as rank 0 of our arm,
@@ -365,7 +365,8 @@ def run_ours(args) -> None:
                 "gpu_launches_per_step": e2e_launches,
                 "pageable": {"value": pg_value, "unit": UNIT, "ms_per_step": pg_total / args.steps,
                              "timing": "host wall clock around sa_align_batch with pageable numpy buffers "
-                                       "(library-owned pinned staging)"}},
+                                       "(the library packs them on every host thread into its own pinned "
+                                       "bit-plane buffers)"}},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks,
         "stats_per_step": {k: st[k] for k in ("reads", "seed_lookups", "hits_consumed", "distance_calls",

@@ -1126,7 +1126,7 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
     int k = 0, bad = SA_OK;
     SeededChunk pend;
     bool have_pend = false;
-    const bool packed = pack_enabled();
+    const bool packed = pack_enabled(is_pageable(bases));
     // pageable caller buffers go through pinned staging (SA_NO_STAGING: hand
     // them to cudaMemcpyAsync as they are, which the driver stages synchronously)
     static const bool no_staging = getenv("SA_NO_STAGING") != nullptr;

@@ -41,7 +41,7 @@ int fail_thread(int code, const std::string& msg);
 int char_to_code(char c);
 
 // pack.cpp: ASCII reads -> three bit planes {lo, hi, n} (host thread pool)
-bool pack_enabled();
+bool pack_enabled(bool pageable);  // host packing of this call's reads (pack.cpp)
 uint64_t pack_words_per_plane(uint64_t n_bases);
 void pack_planar(const char* src, uint64_t n, uint32_t* planes, uint64_t wpp);
 // multi-threaded memcpy (host thread pool), for staging pageable input

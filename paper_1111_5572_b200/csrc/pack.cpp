@@ -202,12 +202,17 @@ class PackPool {
     std::atomic<uint64_t> cursor_{0}, done_{0};
 };
 
-// SA_PACK_THREADS=n (n > 0) turns packing on with n threads.  Off by default:
-// on the measured box 8 threads pack ~22 GB/s of ASCII (host memory bound),
-// slower than the 54 GB/s copy engine moves it unpacked.
-int pack_threads_setting() {
+// SA_PACK_THREADS=n (n > 0) turns packing on with n threads (0: never).
+// Unset: pinned callers send ASCII (8 threads pack ~22 GB/s, host memory
+// bound, slower than the 54 GB/s copy engine moves it unpacked), pageable
+// callers are packed by every host thread -- their bytes must cross host
+// memory once anyway, and packing writes 3/8 of what a staging copy writes
+// (C2 pageable e2e 52.4 -> 43.4 ms).
+int pack_threads_for(bool pageable) {
     const char* e = getenv("SA_PACK_THREADS");
-    return e ? std::max(0, std::min(64, atoi(e))) : 0;
+    if (e) return std::max(0, std::min(64, atoi(e)));
+    if (!pageable) return 0;
+    return std::max(4, std::min(64, static_cast<int>(std::thread::hardware_concurrency())));
 }
 
 // Generic persistent worker pool for host copies into pinned staging
@@ -306,7 +311,7 @@ void parallel_copy(void* dst, const void* src, uint64_t n) {
     pool.run(static_cast<char*>(dst), static_cast<const char*>(src), n);
 }
 
-bool pack_enabled() { return pack_threads_setting() > 0; }
+bool pack_enabled(bool pageable) { return pack_threads_for(pageable) > 0; }
 
 uint64_t pack_words_per_plane(uint64_t n_bases) { return (n_bases + 31) / 32 + 2; }
 
@@ -314,7 +319,7 @@ uint64_t pack_words_per_plane(uint64_t n_bases) { return (n_bases + 31) / 32 + 2
 // the two pad words of each plane are zeroed (the kernel's funnel shift reads
 // one word past a read's last block).
 void pack_planar(const char* src, uint64_t n, uint32_t* planes, uint64_t wpp) {
-    static PackPool pool(std::max(1, pack_threads_setting()) - 1);  // sized at first use
+    static PackPool pool(std::max(1, pack_threads_for(true)) - 1);  // sized at first use
     static const PackFn fn = pick(0);
     const uint64_t words = (n + 31) / 32;
     for (int p = 0; p < 3; ++p)

@@ -5,3 +5,4 @@ timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -m gpu -k "lv_" > $O
 timeout 900 python -m pytest tests/test_gpu_solo.py -q -x -m gpu -k "warp_bitparallel" > $O/t_lvw.log 2>&1; echo rc=$? >> $O/t_lvw.log
 timeout 1200 python -m pytest tests/test_gpu_fullsize.py -q -x -m gpu -k "c4" > $O/t_c4.log 2>&1; echo rc=$? >> $O/t_c4.log
 timeout 900 python bench.py --config C4 --steps 3 --no-cpu-baseline > $O/b_c4.json 2> $O/b_c4.err
+bash scripts/variants.sh --steps 3 --config C4 > $O/variants_c4.log 2>&1
