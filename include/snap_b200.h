@@ -126,8 +126,10 @@ const char* sa_last_error(const sa_context* ctx);
  * {A,C,G,T,N}: read i is bases[offsets[i] .. offsets[i+1]).  results[i] is
  * the AlignmentResult of read i (input order).  stats (nullable) receives the
  * AlignStats summed over the batch (REF aligner.cpp:31-48 merge semantics).
- * Blocking.  Host buffers may be pageable or pinned (sa_host_alloc);
- * pinned buffers get the double-buffered asynchronous path.
+ * Blocking.  Host buffers may be pageable or pinned (sa_host_alloc): pinned
+ * reads are copied in chunk by chunk behind the kernels; pageable reads are
+ * packed (2+1 bits per base) by the library's host threads into its own
+ * pinned buffers first.  Either way copies overlap the kernels.
  * Errors: SA_EINVAL on invalid params, a seed-size mismatch with the index
  * (REF aligner.cpp:119-121), or a read of length >= s holding a character
  * outside {A,C,G,T,N} (REF genome.cpp:182-200 throws from align()). */

@@ -126,7 +126,7 @@ public:
     // The run_align worker's batch (REF src/driver.cpp:104-124): any
     // container of Read-like records with a `bases` string (seedaln::Read,
     // REF include/seedaln/read.hpp:9-14).  The bases are gathered into one
-    // host buffer; the library stages it through its own pinned buffers.
+    // host buffer; the library packs it into its own pinned buffers.
     template <class Reads, class = decltype(std::declval<const Reads&>().begin()->bases)>
     std::vector<sa_result> align_reads(const Reads& reads) {
         std::string buf;
