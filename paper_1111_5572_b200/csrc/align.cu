@@ -231,6 +231,7 @@ struct Ctx {
     int first_dir;
     uint64_t first_pos;
     uint32_t cells;  // per lane, LV cells of the launch (dp_cells)
+    uint32_t qf_tries, qf_hits;  // q-gram filter attempts / rejections of this warp
     // Per-read counters, lane-distributed: lane k holds stats slot k (sa_stats
     // order) for the read in flight -- one register for all of them.  Added to
     // the warp totals when the read completes, dropped if it overflows.
@@ -345,6 +346,9 @@ SA_DEV bool insert_wave(Ctx& x, bool valid, unsigned long long key, int bit) {
 #ifndef SA_PB_SEG
 #define SA_PB_SEG 0
 #endif
+#ifndef SA_QGRAM_FILTER
+#define SA_QGRAM_FILTER 1  // long-read LVs: the exact q-gram pre-test (lv.cuh qgram_reject); 0 off
+#endif
 #ifndef SA_MASK_LV
 #define SA_MASK_LV 0  // 1: the mask LV (lv.cuh lv_seg) scores reads <= 128 bases in the warp kernel (measured slower, see DESIGN)
 #endif
@@ -458,7 +462,22 @@ SA_DEV void score_candidate(Ctx& x, uint32_t idx) {
         const uint64_t want = static_cast<uint64_t>(x.len) + static_cast<uint64_t>(d_limit);
         const int w = static_cast<int>(want < rem ? want : rem);
         const uint32_t wofs = static_cast<uint32_t>(anchor - gb0 * 32);
-        const int d = lv_warp<kRegLV, kSys>(orient, x.len, Wsrc, wofs, w, d_limit, x.F, lane, x.cells, a.f16 != 0);
+        int d;
+        // long-read LVs: the q-gram filter first (lv.cuh qgram_reject) where it
+        // has room (the LV frontier area, >= 512 B), where a piece's band is at
+        // most ~2 pieces wide (d_limit <= kQfPiece: its cost per read q-gram is
+        // (piece + 2 d_limit) / piece inserts; C4's 607 measured 77 -> 91 ms
+        // with nothing rejected) and, per warp, while it keeps paying off (no
+        // more tries after 32 attempts with < 1/8 rejected)
+        if (!kRegLV && SA_QGRAM_FILTER && a.f_ints >= 128 && d_limit <= kQfPiece &&
+            (x.qf_tries < 32 || 8 * x.qf_hits >= x.qf_tries) &&
+            (++x.qf_tries, qgram_reject(orient, x.len, Wsrc, wofs, w, d_limit, reinterpret_cast<uint32_t*>(x.F),
+                                        lane))) {
+            ++x.qf_hits;
+            d = -1;
+        } else {
+            d = lv_warp<kRegLV, kSys>(orient, x.len, Wsrc, wofs, w, d_limit, x.F, lane, x.cells, a.f16 != 0);
+        }
 #if SA_DEBUG_COUNTERS
         if (a.dbg && lane == 0) {  // seed-loop (warp) LV: calls, iterations, d_limit sum
             atomicAdd(a.dbg + 4, 1u);
@@ -2063,6 +2082,8 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
     // warp totals, lane-distributed (lane k: sa_stats slot k); LV cells per lane
     unsigned long long acc = 0;
     x.cells = 0;
+    x.qf_tries = 0;
+    x.qf_hits = 0;
     unsigned char* tb;
     if (kSlow) {
         const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -2411,6 +2432,8 @@ __global__ void __launch_bounds__(256) prune_kernel(const AlignLaunch a) {
     x.a = &a;
     x.lane = lane;
     x.cells = 0;
+    x.qf_tries = 0;
+    x.qf_hits = 0;
     x.t.cap = 64;
     x.t.hcap = 0;
     x.t.ckey = reinterpret_cast<unsigned long long*>(ws);
