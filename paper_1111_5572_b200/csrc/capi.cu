@@ -54,17 +54,22 @@ constexpr int kCtlWords = 4;  // cursor_fast, cursor_slow, overflow_count, error
 // 48 k and 512 k reads.  Each chunk costs a kernel ramp and tail (~15 us), so
 // big batches want big chunks (C2, 10 M reads: e2e 152 M reads/s at 48 k,
 // 196 M at 512 k), while a 1 M batch wants enough chunks to overlap copy and
-// compute (C1: 48 k best).  SA_CHUNK_READS overrides (tuning).
-uint64_t chunk_reads_setting(uint64_t n_reads) {
+// compute (C1: 48 k best).  The 48 k floor scales with the mean read length
+// past 128 bases: a long read's kernels cost ~length x d_limit, so a chunk's
+// tail (its slowest reads) grows with the length while its copy shrinks in
+// relative terms (C3, 500 k x 1 kbp: e2e 167 / 137 / 121 / 112 ms at chunks
+// of 48 k / 96 k / 192 k / >= 256 k reads).  SA_CHUNK_READS overrides (tuning).
+uint64_t chunk_reads_setting(uint64_t n_reads, uint64_t mean_len) {
     static const long long forced = [] {
         const char* e = getenv("SA_CHUNK_READS");
         return e ? atoll(e) : 0ll;
     }();
     if (forced >= 1024) return static_cast<uint64_t>(forced);
     const uint64_t want = ((n_reads / 24 + 16383) / 16384) * 16384;
-    return std::min<uint64_t>(512u << 10, std::max<uint64_t>(49152, want));
+    const uint64_t floor = 49152ull * std::max<uint64_t>(1, mean_len / 128);
+    return std::min<uint64_t>(512u << 10, std::max<uint64_t>(floor, want));
 }
-constexpr uint64_t kChunkBytes = 256ull << 20;
+constexpr uint64_t kChunkBytes = 512ull << 20;  // byte cap per chunk (6 stages of device + staging buffers)
 #ifndef SA_FAST_CAP
 #define SA_FAST_CAP 64    // candidates per read in the shared-memory table (more: the global-table pass)
 #endif
@@ -1671,7 +1676,7 @@ int sa_align_batch(sa_context* ctx, const sa_params* params, const char* bases,
     // the previous chunk; a bad chunk stops the batch before it is enqueued.
     // Chunk sizes ramp up (16 k, 32 k, ... reads) so the first kernel starts
     // after a short copy; the GPU is busy with chunk k while chunk k+1 copies.
-    const uint64_t chunk_reads = chunk_reads_setting(n_reads);
+    const uint64_t chunk_reads = chunk_reads_setting(n_reads, (offsets[n_reads] - offsets[0]) / n_reads);
     std::vector<uint64_t> bounds{0};
     {
         // sizes ramp up (16 k, 32 k, ...) so the first kernel starts after a
