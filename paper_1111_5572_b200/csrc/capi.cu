@@ -1229,7 +1229,9 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
         const uint32_t fixed = (Lmin == Lc && Lc > 0 && Lc < (1u << 30)) ? static_cast<uint32_t>(Lc) : 0u;
         // a chunk whose reads all fit the layout redoes its overflows itself;
         // longer reads (deferred by the seed kernel) go to the end-of-batch pass
-        const bool ov = chunk_overflow && !packed && Lc <= 1024;  // (host-packed chunks keep no ASCII copy)
+        // (host-packed chunks keep no ASCII copy; reads > 256 bases: one pass at the end
+        // of the batch -- C3's per-chunk passes cost 112 vs 101 ms of e2e in their tails)
+        const bool ov = chunk_overflow && !packed && Lc <= 256;
         Lc = std::min<uint64_t>(Lc, 1024);
         if (k == 0 || Lc > shape_L) {
             std::string w;
