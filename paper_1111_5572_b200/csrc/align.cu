@@ -232,6 +232,7 @@ struct Ctx {
     uint64_t first_pos;
     uint32_t cells;  // per lane, LV cells of the launch (dp_cells)
     uint32_t qf_tries, qf_hits;  // q-gram filter attempts / rejections of this warp
+    uint32_t* qbm;               // its 4^kQfQ-bit bitmap (shared memory), null: no filter
     // Per-read counters, lane-distributed: lane k holds stats slot k (sa_stats
     // order) for the read in flight -- one register for all of them.  Added to
     // the warp totals when the read completes, dropped if it overflows.
@@ -463,16 +464,18 @@ SA_DEV void score_candidate(Ctx& x, uint32_t idx) {
         const int w = static_cast<int>(want < rem ? want : rem);
         const uint32_t wofs = static_cast<uint32_t>(anchor - gb0 * 32);
         int d;
-        // long-read LVs: the q-gram filter first (lv.cuh qgram_reject) where it
-        // has room (the LV frontier area, >= 512 B), where a piece's band is at
-        // most ~2 pieces wide (d_limit <= kQfPiece: its cost per read q-gram is
-        // (piece + 2 d_limit) / piece inserts; C4's 607 measured 77 -> 91 ms
-        // with nothing rejected) and, per warp, while it keeps paying off (no
-        // more tries after 32 attempts with < 1/8 rejected)
-        if (!kRegLV && SA_QGRAM_FILTER && a.f_ints >= 128 && d_limit <= kQfPiece &&
+        // long-read LVs: the q-gram filter first (lv.cuh qgram_reject) where the
+        // warp has a bitmap (x.qbm: the LV frontier area, >= 512 B), where a
+        // piece's band is at most ~2 pieces wide (d_limit <= kQfPiece: its cost
+        // per read q-gram is (piece + 2 d_limit) / piece inserts; C4's 607
+        // measured 77 -> 91 ms with nothing rejected) and, per warp, while it
+        // keeps paying off (no more tries after 32 attempts with < 1/8
+        // rejected).  Not in the register-LV (short-read) kernels: there it
+        // would reject ~90% of the seed loop's failing LVs, but its code cost
+        // the C2 warp kernel 32 B of spills and C2 432 -> 420 M reads/s.
+        if (!kRegLV && SA_QGRAM_FILTER && x.qbm != nullptr && d_limit <= kQfPiece &&
             (x.qf_tries < 32 || 8 * x.qf_hits >= x.qf_tries) &&
-            (++x.qf_tries, qgram_reject(orient, x.len, Wsrc, wofs, w, d_limit, reinterpret_cast<uint32_t*>(x.F),
-                                        lane))) {
+            (++x.qf_tries, qgram_reject(orient, x.len, Wsrc, wofs, w, d_limit, x.qbm, lane))) {
             ++x.qf_hits;
             d = -1;
         } else {
@@ -2078,6 +2081,7 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
     unsigned long long* pcanon = reinterpret_cast<unsigned long long*>(pslot + 32);  // 32
     int* offs = reinterpret_cast<int*>(pcanon + 32);  // 2 x n_off_cap
     x.F = offs + 2 * a.n_off_cap;
+    x.qbm = !kRegLV && a.f_ints * 32 >= (1 << (2 * kQfQ)) ? reinterpret_cast<uint32_t*>(x.F) : nullptr;
     uint32_t* stage = reinterpret_cast<uint32_t*>(x.F + a.f_ints);  // 2 x sbw words
     // warp totals, lane-distributed (lane k: sa_stats slot k); LV cells per lane
     unsigned long long acc = 0;
@@ -2434,6 +2438,7 @@ __global__ void __launch_bounds__(256) prune_kernel(const AlignLaunch a) {
     x.cells = 0;
     x.qf_tries = 0;
     x.qf_hits = 0;
+    x.qbm = nullptr;  // (the pruning batch holds its own LV)
     x.t.cap = 64;
     x.t.hcap = 0;
     x.t.ckey = reinterpret_cast<unsigned long long*>(ws);

@@ -1,0 +1,5 @@
+#!/bin/bash
+O=gpurun_out; mkdir -p $O
+timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_solo.py -q -x -m gpu > $O/t_par7.log 2>&1; echo rc=$? >> $O/t_par7.log
+bash scripts/variants.sh --steps 10 > $O/variants_c2.log 2>&1
+bash scripts/variants.sh --steps 20 --config C1 > $O/variants_c1.log 2>&1
