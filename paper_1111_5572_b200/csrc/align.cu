@@ -1800,6 +1800,32 @@ __global__ void __launch_bounds__(256) resolve_kernel(const AlignLaunch a) {
 // windows are assembled with shuffles inside the group, and the read's seeds
 // are dealt round-robin to the lanes so their index probes are in flight
 // together.
+// seed_offsets (REF aligner.cpp:50-79) for one length, sequentially: the
+// tier-0 non-overlapping offsets 0, s, 2s, ... first, then the same ladder
+// from each shift (odd * s) >> level of successive binary subdivisions of
+// [0, s), skipping shifts already used, until n_cap offsets or the shifts run
+// out -- the generator the seed kernel's lanes walk (next_off below).
+constexpr int kSeedTab = 64;
+SA_DEV int seed_offsets_list(int len, int s, int n_cap, int* out) {
+    const int max_off = len - s;
+    uint32_t used = 1u;  // shift 0: the tier-0 ladder
+    int cnt = 0;
+    for (int o = 0; o <= max_off && cnt < n_cap; o += s) out[cnt++] = o;
+    for (int level = 1, odd = 1; cnt < n_cap;) {
+        if ((1 << level) > 4 * s) break;
+        const int shift = (odd * s) >> level;
+        odd += 2;
+        if (odd >= (1 << level)) {
+            ++level;
+            odd = 1;
+        }
+        if ((used >> shift) & 1u) continue;
+        used |= 1u << shift;
+        for (int o = shift; o <= max_off && cnt < n_cap; o += s) out[cnt++] = o;
+    }
+    return cnt;
+}
+
 #ifndef SA_SEED_MIN_BLOCKS
 #define SA_SEED_MIN_BLOCKS 6  // 40 registers: 48 warps per SM (measured +2.5% over the unbounded 42-register build)
 #endif
@@ -1819,6 +1845,27 @@ __global__ void __launch_bounds__(256, SA_SEED_MIN_BLOCKS) seed_kernel(const Ali
     const int gbase = lane & ~(G - 1);
     const uint32_t groups = (gridDim.x * blockDim.x) / G;
     const int half = a.pre_pstride >> 1;
+    // The seed offsets (REF aligner.cpp:50-79) depend only on the read length:
+    // the block lists them once for the length of its first read, and every
+    // read of that length takes them from shared memory instead of walking the
+    // generator in each lane (a quarter of this kernel's instructions).
+    __shared__ int s_off[kSeedTab];
+    __shared__ int s_tab_len, s_tab_n;
+    if (threadIdx.x == 0) {
+        s_tab_len = -1;
+        const uint32_t r0 = (blockIdx.x * blockDim.x) / G;
+        const int n_cap = min(a.n, a.n_off_cap);
+        if (r0 < a.n_reads && n_cap <= kSeedTab) {
+            const int len0 = a.fixed_len ? static_cast<int>(a.fixed_len)
+                                         : static_cast<int>(a.offsets[r0 + 1] - a.offsets[r0]);
+            if (len0 >= a.s && len0 <= a.lcap) {
+                s_tab_n = seed_offsets_list(len0, a.s, n_cap, s_off);
+                s_tab_len = len0;
+            }
+        }
+    }
+    __syncthreads();
+    const int tab_len = s_tab_len, tab_n = s_tab_n;
     const uint32_t gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << gbase);
     // all groups of a warp iterate the same number of times (shuffles)
     const uint32_t first = (blockIdx.x * blockDim.x + threadIdx.x) / G;
@@ -1984,10 +2031,16 @@ __global__ void __launch_bounds__(256, SA_SEED_MIN_BLOCKS) seed_kernel(const Ali
             for (;;) {
                 int my_off = -1;
                 int k = 0;
-                for (; k < G; ++k) {
-                    const int ov = cnt + k < n_cap ? next_off() : -1;
-                    if (ov < 0) break;
-                    if (k == g) my_off = ov;
+                if (status == 0 && len == tab_len) {  // the block's table (same list, same rounds)
+                    const int rem = tab_n - cnt;
+                    k = rem < 0 ? 0 : (rem < G ? rem : G);
+                    if (g < k) my_off = s_off[cnt + g];
+                } else {
+                    for (; k < G; ++k) {
+                        const int ov = cnt + k < n_cap ? next_off() : -1;
+                        if (ov < 0) break;
+                        if (k == g) my_off = ov;
+                    }
                 }
                 const int round_n = __shfl_sync(gmask, k, gbase);  // same in every lane
                 uint32_t l, h, n;
