@@ -2780,6 +2780,10 @@ KTimer& ktimer() {
 }
 }  // namespace
 
+// Diagnostics (SA_DEBUG_TIMELINE, capi.cu): called after each kernel of a
+// seeded launch with a tag (o solo, r resolve, w warp, p prune) and its stream.
+void (*g_timeline_hook)(char tag, cudaStream_t st) = nullptr;
+
 extern "C" void sab_debug_ktimes(const char* tag) {
     KTimer& t = ktimer();
     if (!t.on) return;
@@ -2811,11 +2815,13 @@ int launch_align_seeded(const AlignLaunch& a, int grid, int block, cudaStream_t 
         solo_kernel<<<static_cast<int>(std::max<uint64_t>(g, 1)), kSoloThreads, 0, st>>>(sa);
         ++n;
         kt.mark(1, st);
+        if (g_timeline_hook) g_timeline_hook('o', st);
         kt.span(0, 0, 1);
         if (a.eager > 0 && a.eager < a.n) {  // lazy records of the listed reads
             resolve_kernel<<<148 * 8, 256, 0, st>>>(a);
             ++n;
             kt.mark(2, st);
+            if (g_timeline_hook) g_timeline_hook('r', st);
             kt.span(1, 1, 2);
             kt.mark(1, st);
         }
@@ -2846,6 +2852,7 @@ int launch_align_seeded(const AlignLaunch& a, int grid, int block, cudaStream_t 
     if (b.dl_max <= 15) launch_variant<false, true, true, false, true>(b, grid, block, st);
     else launch_variant<false, true, false, false, true>(b, grid, block, st);
     kt.mark(3, st);
+    if (g_timeline_hook) g_timeline_hook('w', st);
     kt.span(2, 2, 3);
     if (b.pq_pool) {  // the reads it handed to the prune queue
         const uint32_t spw = prune_kernel_smem_per_warp() + static_cast<uint32_t>(b.pre_pstride) * 16u;
@@ -2857,6 +2864,7 @@ int launch_align_seeded(const AlignLaunch& a, int grid, int block, cudaStream_t 
         prune_kernel<<<148 * 4, 256, 8 * spw, st>>>(b);
         ++n;
         kt.mark(4, st);
+        if (g_timeline_hook) g_timeline_hook('p', st);
         kt.span(3, 3, 4);
     }
 #if SA_DEBUG_COUNTERS

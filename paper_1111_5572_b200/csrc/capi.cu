@@ -48,7 +48,39 @@ namespace {
 #ifndef SA_PIPE_STAGES
 #define SA_PIPE_STAGES 6
 #endif
-constexpr int kPipeStages = SA_PIPE_STAGES;  // chunk buffers in flight per replica (copies run ahead of compute)
+constexpr int kPipeStages = SA_PIPE_STAGES;
+
+// Diagnostics (SA_DEBUG_TIMELINE=1): per chunk, events after its H2D (C), seed
+// (S), solo (o), resolve (r), warp (w), prune (p), overflow pass (V) and D2H
+// (D) kernels on their own streams; printed relative to the batch start.
+struct TimelineMark {
+    int chunk;
+    char tag;
+    cudaEvent_t ev;
+};
+std::vector<TimelineMark> g_tl;
+int g_tl_chunk = -1;
+bool timeline_on() {
+    static const bool on = getenv("SA_DEBUG_TIMELINE") != nullptr;
+    return on;
+}
+void tl_mark(char tag, cudaStream_t st) {
+    if (!timeline_on()) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    g_tl.push_back({g_tl_chunk, tag, e});
+}
+void tl_dump(cudaEvent_t base) {
+    if (!timeline_on()) return;
+    for (auto& m : g_tl) {
+        float t = 0;
+        cudaEventElapsedTime(&t, base, m.ev);
+        fprintf(stderr, "[tl] %d %c %.3f\n", m.chunk, m.tag, t);
+        cudaEventDestroy(m.ev);
+    }
+    g_tl.clear();
+}  // chunk buffers in flight per replica (copies run ahead of compute)
 constexpr int kCtlWords = 4;  // cursor_fast, cursor_slow, overflow_count, error_flag
 // Chunk size of the batch pipeline: about 1/24 of the batch, between
 // 48 k and 512 k reads.  Each chunk costs a kernel ramp and tail (~15 us), so
@@ -1096,6 +1128,7 @@ int align_streamed(sa_context* ctx, Replica& rep, const sa_params* params, const
 // Reads longer than the layout are deferred (status 3) to the overflow pass.
 struct SeededChunk {
     uint64_t r0 = 0, r1 = 0;
+    int k = 0;  // chunk number (diagnostics)
     int stage = 0;
     bool ov = false;  // its overflowing reads get their own global-table pass
     cudaStream_t cs = nullptr;  // compute stream
@@ -1165,7 +1198,10 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
         Stage& st = rep.stage[pend.stage];
         CUDA_TRY(ctx, cudaStreamWaitEvent(pend.cs, st.e_out, 0));  // results buffer free (no-op first time)
         mark('w');
+        g_tl_chunk = static_cast<int>(pend.k);
+        if (timeline_on()) sab::g_timeline_hook = tl_mark;
         launches += launch_align_seeded(pend.a, pend.grid, pend.block, pend.cs) - 1;
+        sab::g_timeline_hook = nullptr;
         mark('a');
         CUDA_TRY(ctx, cudaGetLastError());
         ++launches;
@@ -1190,6 +1226,7 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
             CUDA_TRY(ctx, cudaGetLastError());
             ++launches;
             CUDA_TRY(ctx, cudaEventRecord(st.e_ov, S.ov));
+            tl_mark('V', S.ov);
             CUDA_TRY(ctx, cudaStreamWaitEvent(S.co, st.e_ov, 0));
         } else {
             CUDA_TRY(ctx, cudaStreamWaitEvent(S.co, st.e_al, 0));
@@ -1206,6 +1243,7 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
                                           cudaMemcpyDeviceToHost, S.co));
         }
         CUDA_TRY(ctx, cudaEventRecord(st.e_out, S.co));
+        tl_mark('D', S.co);
         return SA_OK;
     };
     for (;;) {
@@ -1319,6 +1357,8 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
             CUDA_TRY(ctx, cudaMemcpyAsync(st.d_offsets, src_o, (r1 - r0 + 1) * sizeof(uint64_t),
                                           cudaMemcpyHostToDevice, S.ci));
         CUDA_TRY(ctx, cudaEventRecord(st.e_in, S.ci));
+        g_tl_chunk = k;
+        tl_mark('C', S.ci);
         // compute: seed(k), then align(k - 1)
         AlignLaunch a = sh.proto;
         a.bases = st.d_bases;
@@ -1353,11 +1393,13 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
         mark('W');
         launch_seed(a, cs);
         mark('s');
+        tl_mark('S', cs);
         CUDA_TRY(ctx, cudaGetLastError());
         ++launches;
         CUDA_TRY(ctx, cudaEventRecord(st.e_seeded, cs));
         pend.r0 = r0;
         pend.r1 = r1;
+        pend.k = k;
         pend.stage = si;
         pend.cs = cs;
         pend.a = a;
@@ -1399,6 +1441,7 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
     CUDA_TRY(ctx, cudaStreamSynchronize(S.ci));
     for (int j = 0; j < kPipeStages; ++j)
         if (int rc = drain_results(rep.stage[j])) return rc;
+    if (k > 0) tl_dump(S.e_begin);
     if (dbg_span && k > 0) {
         float ci = 0, kb = 0, ke = 0;
         cudaEventElapsedTime(&ci, S.e_begin, S.e_ready);
