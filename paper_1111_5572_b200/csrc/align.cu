@@ -2782,7 +2782,7 @@ KTimer& ktimer() {
 
 // Diagnostics (SA_DEBUG_TIMELINE, capi.cu): called after each kernel of a
 // seeded launch with a tag (o solo, r resolve, w warp, p prune) and its stream.
-void (*g_timeline_hook)(char tag, cudaStream_t st) = nullptr;
+thread_local void (*g_timeline_hook)(char tag, cudaStream_t st) = nullptr;
 
 extern "C" void sab_debug_ktimes(const char* tag) {
     KTimer& t = ktimer();

@@ -11,7 +11,7 @@
 namespace sab {
 
 // diagnostics: called after each kernel of a seeded launch (align.cu), set by capi.cu
-extern void (*g_timeline_hook)(char tag, cudaStream_t st);
+extern thread_local void (*g_timeline_hook)(char tag, cudaStream_t st);
 
 // counters accumulated on the device; first 20 mirror sa_stats
 constexpr int kNumStats = 20;

@@ -58,8 +58,8 @@ struct TimelineMark {
     char tag;
     cudaEvent_t ev;
 };
-std::vector<TimelineMark> g_tl;
-int g_tl_chunk = -1;
+thread_local std::vector<TimelineMark> g_tl;  // per host worker (one per replica)
+thread_local int g_tl_chunk = -1;
 bool timeline_on() {
     static const bool on = getenv("SA_DEBUG_TIMELINE") != nullptr;
     return on;
