@@ -141,6 +141,8 @@ struct Stage {  // one of the two pipeline slots of a replica
     // results copied out
     cudaEvent_t e_in = nullptr, e_seeded = nullptr, e_al = nullptr, e_out = nullptr;
     cudaEvent_t e_ov = nullptr;  // the chunk's global-table pass done (seeded pipeline)
+    unsigned char* d_gscratch = nullptr;  // that pass's global candidate tables (per stage: passes run concurrently)
+    uint64_t gscratch_bytes = 0;
     bool ov_pending = false;     // the stage's last chunk ran a global-table pass
     // packed input (pack.cpp): pinned host planes and their device copy
     uint32_t* h_pack = nullptr;
@@ -179,6 +181,7 @@ struct LaunchShape {
     uint64_t scratch_bytes;  // global candidate tables of the overflow path
     int slow_cap, slow_hcap;
     uint64_t gplanes_bytes;  // per-warp global read planes (long-read layouts, AlignLaunch::gplanes)
+    int stage_slow_grid;     // blocks of a per-chunk global-table pass (seeded pipeline)
 };
 
 struct Replica {
@@ -478,6 +481,9 @@ int make_shape(Replica& rep, const sa_params* p, uint64_t Lmax, LaunchShape& sh,
     slow_warps = std::max<uint64_t>(sw, slow_warps / sw * sw);
     sh.slow_block = static_cast<int>(32 * sw);
     sh.slow_grid = static_cast<int>(slow_warps / sw);
+    // a chunk's pass has ~0.3% of a chunk's reads: 4 warps per SM are plenty
+    sh.stage_slow_grid = static_cast<int>(std::max<uint64_t>(
+        1, std::min<uint64_t>(sh.slow_grid, static_cast<uint64_t>(rep.sm_count) * 4 / sw)));
     a.gscratch_per_warp = sh.slow_table_bytes;
     sh.scratch_bytes = slow_warps * sh.slow_table_bytes;
     a.gplanes = nullptr;
@@ -1206,9 +1212,22 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
         CUDA_TRY(ctx, cudaGetLastError());
         ++launches;
         CUDA_TRY(ctx, cudaEventRecord(st.e_al, pend.cs));
-        if (pend.ov) {  // the chunk's overflowing reads: global-table kernel, stream S.ov
-            CUDA_TRY(ctx, cudaStreamWaitEvent(S.ov, st.e_al, 0));
+        if (pend.ov) {  // the chunk's overflowing reads: global-table kernel on the chunk's stream
+            // with the stage's own tables, so the passes of different chunks run
+            // concurrently (one shared stream serialised them: each waited for the
+            // previous chunk's slowest overflowing read)
+            const uint64_t need = static_cast<uint64_t>(sh.stage_slow_grid) * (sh.slow_block / 32) *
+                                  sh.slow_table_bytes;
+            if (need > st.gscratch_bytes) {
+                if (st.d_gscratch) cudaFree(st.d_gscratch);
+                st.d_gscratch = nullptr;
+                st.gscratch_bytes = 0;
+                CUDA_TRY(ctx, cudaMalloc(&st.d_gscratch, need));
+                CUDA_TRY(ctx, cudaMemset(st.d_gscratch, 0xff, need));  // hash keys start empty (self-cleaning after)
+                st.gscratch_bytes = need;
+            }
             AlignLaunch b = pend.a;
+            b.gscratch = st.d_gscratch;
             b.cursor = st.d_ctl + 1;
             b.work_list = st.d_overflow;
             b.work_count = st.d_ctl + 2;
@@ -1222,11 +1241,11 @@ int seeded_pipeline(sa_context* ctx, Replica& rep, const sa_params* params, cons
             b.pq_pool = nullptr;
             b.pre_list = nullptr;
             b.pre_list_count = nullptr;
-            launch_align_slow(b, sh.slow_grid, sh.slow_block, S.ov);
+            launch_align_slow(b, sh.stage_slow_grid, sh.slow_block, pend.cs);
             CUDA_TRY(ctx, cudaGetLastError());
             ++launches;
-            CUDA_TRY(ctx, cudaEventRecord(st.e_ov, S.ov));
-            tl_mark('V', S.ov);
+            CUDA_TRY(ctx, cudaEventRecord(st.e_ov, pend.cs));
+            tl_mark('V', pend.cs);
             CUDA_TRY(ctx, cudaStreamWaitEvent(S.co, st.e_ov, 0));
         } else {
             CUDA_TRY(ctx, cudaStreamWaitEvent(S.co, st.e_al, 0));
@@ -1646,8 +1665,10 @@ void sa_destroy(sa_context* ctx) {
         if (rep.d_err_read) cudaFree(rep.d_err_read);
         if (rep.h_ctl) cudaFreeHost(rep.h_ctl);
         if (rep.d_gscratch) cudaFree(rep.d_gscratch);
-        for (auto& sg : rep.stage)
+        for (auto& sg : rep.stage) {
             if (sg.d_gplanes) cudaFree(sg.d_gplanes);
+            if (sg.d_gscratch) cudaFree(sg.d_gscratch);
+        }
         if (rep.d_defer) cudaFree(rep.d_defer);
         for (void* q : {static_cast<void*>(rep.sm.bases), static_cast<void*>(rep.sm.offs),
                         static_cast<void*>(rep.sm.res), static_cast<void*>(rep.sm.flags),
