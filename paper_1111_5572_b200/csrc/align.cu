@@ -685,7 +685,7 @@ SA_DEV bool select_order_large(Ctx& x, unsigned long long* keys) {
     for (uint32_t k = 2; k <= P; k <<= 1) {
         for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
             for (uint32_t i = lane; i < P / 2; i += 32) {
-                const uint32_t lo = (i / jj) * 2 * jj + (i % jj), hi = lo + jj;
+                const uint32_t lo = ((i & ~(jj - 1u)) << 1) | (i & (jj - 1u)), hi = lo + jj;  // jj: power of two
                 const bool up = (lo & k) == 0;
                 const unsigned long long u = keys[lo], v = keys[hi];
                 if ((u > v) == up) {
