@@ -156,6 +156,43 @@ def test_lv_long_limits_vs_oracle():
     assert any(v is None for v in want) and any(v is not None for v in want)
 
 
+def test_lv_long_limits_edges_vs_oracle():
+    """Edges of the long-read LVs (lv_sys from 256; lv_bitpar_warp above 960):
+    reads ending exactly on / one past a 64-row block, windows shorter than
+    m - d_limit (nothing reachable), empty windows, all-N and N-rich reads,
+    limits at 256, 607, 960, 961 and 1023, limits above the read length."""
+    rng = np.random.default_rng(960)
+    triples = []
+    for m in (255, 256, 257, 511, 512, 513, 1023, 1024, 1025, 4096, 4097):
+        read = ACGT[rng.integers(0, 4, m)].tobytes().decode()
+        for dl in (256, 607, 960, 961, 1023):
+            win = list(read)
+            for _ in range(int(rng.integers(0, max(1, m // 10)))):
+                i = int(rng.integers(0, len(win)))
+                op = int(rng.integers(0, 3))
+                if op == 0:
+                    win[i] = "ACGT"[int(rng.integers(0, 4))]
+                elif op == 1:
+                    win.insert(i, "ACGT"[int(rng.integers(0, 4))])
+                else:
+                    del win[i]
+            win = "".join(win) + ACGT[rng.integers(0, 4, dl)].tobytes().decode()
+            triples.append((read, win[:m + dl], dl))
+            triples.append((read, win[:max(0, m - dl - 1)], dl))  # row m out of reach
+            triples.append((read, "", dl))
+    n_read = "N" * 700
+    triples += [(n_read, ACGT[rng.integers(0, 4, 1000)].tobytes().decode(), 700),
+                (n_read, n_read, 700), (n_read, n_read, 699)]
+    nr = list(ACGT[rng.integers(0, 4, 3000)].tobytes().decode())
+    for i in rng.integers(0, 3000, 200):
+        nr[int(i)] = "N"
+    nr = "".join(nr)
+    triples += [(nr, nr + "ACGT" * 100, 300), (nr, nr.replace("N", "A") + "ACGT" * 100, 250)]
+    got = api.bounded_distance_batch(triples)
+    want = [O.or_bounded_distance(r, w, d) for r, w, d in triples]
+    assert got == want
+
+
 # ----------------------------------------------------------------- lookup
 
 @pytest.mark.parametrize("s", [3, 4, 7, 8, 20, 31, 32])
