@@ -6,7 +6,7 @@
 //     registers, the next read's bytes streamed into shared memory with
 //     cp.async while the current read is processed
 //   * read -> 2-bit planes: SWAR decode of 4 ASCII bases per lane
-//     (__vcmpeq4), 32-base plane words assembled with shuffles; the
+//     (decode4: code arithmetic + byte_perm check), 32-base plane words assembled with shuffles; the
 //     reverse complement (REF :241, genome.cpp:182-200) by __brev of planes
 //   * seed offsets (REF :50-79), computed once per distinct read length
 //   * seed keys + canonical probes of the HBM hash index, one lane per seed,
@@ -63,8 +63,26 @@ SA_DEV void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];"
 
 // ------------------------------------------------------------------ read staging
 
-// Gather bit 0 of each byte into a nibble.
-SA_DEV uint32_t byte_bits(uint32_t x) { return (x | (x >> 7) | (x >> 14) | (x >> 21)) & 0xFu; }
+// Decode 4 ASCII bases (byte j = base j) into nibbles: lo/hi = bits 0/1 of
+// the 2-bit code (A=0 C=1 G=2 T=3, N codes as A), nn = the 'N' bytes, and
+// bad != 0 when a byte is outside {A,C,G,T,N} (REF genome.cpp:182-200).
+// ((c >> 1) ^ (c >> 2)) & 3 is the code of A/C/G/T; the expected character is
+// looked up back from the code (byte_perm) and compared byte-wise; bits are
+// gathered by one multiply per plane (no carries: the partial products are
+// distinct powers of two).
+SA_DEV void decode4(uint32_t v, uint32_t& lo, uint32_t& hi, uint32_t& nn, uint32_t& bad) {
+    const uint32_t x = (v >> 1) ^ (v >> 2);
+    lo = ((x & 0x01010101u) * 0x01020408u) >> 24;
+    hi = ((x & 0x02020202u) * 0x08102040u) >> 28;
+    const uint32_t t = x & 0x03030303u;
+    const uint32_t sel = __byte_perm(t | (t >> 4), 0u, 0x0020u);  // nibble j = code of byte j
+    const uint32_t e = __byte_perm(0x54474341u, 0u, sel);          // "ACGT"[code] per byte
+    const uint32_t dn = v ^ 0x4E4E4E4Eu, de = v ^ e;
+    const uint32_t nzN = ((dn & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | dn;  // bit 7 of byte j: byte j != 'N'
+    const uint32_t nzE = ((de & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | de;  // bit 7 of byte j: not its ACGT char
+    bad = nzN & nzE & 0x80808080u;
+    nn = (((~nzN >> 7) & 0x01010101u) * 0x01020408u) >> 24;
+}
 
 // Decode a read of `len` ASCII bases whose first byte is byte `shift` of the
 // 4-byte-aligned word array Wd (nwords words; generic address space: shared
@@ -91,14 +109,13 @@ SA_DEV bool decode_read(const uint32_t* Wd, int shift, int nwords, int len, uint
                 v = (v & keep) | (0x4E4E4E4Eu & ~keep);
             }
         }
-        const uint32_t isC = __vcmpeq4(v, 0x43434343u), isG = __vcmpeq4(v, 0x47474747u);
-        const uint32_t isT = __vcmpeq4(v, 0x54545454u), isN = __vcmpeq4(v, 0x4E4E4E4Eu);
-        const uint32_t isA = __vcmpeq4(v, 0x41414141u);
-        bad |= (isA | isC | isG | isT | isN) != 0xFFFFFFFFu;
+        uint32_t lo, hi, nn, bd;
+        decode4(v, lo, hi, nn, bd);
+        bad |= bd != 0u;
         const int sh = 4 * (lane & 7);
-        uint32_t lo = byte_bits((isC | isT) & 0x01010101u) << sh;
-        uint32_t hi = byte_bits((isG | isT) & 0x01010101u) << sh;
-        uint32_t nn = byte_bits(isN & 0x01010101u) << sh;
+        lo <<= sh;
+        hi <<= sh;
+        nn <<= sh;
 #pragma unroll
         for (int o = 1; o < 8; o <<= 1) {
             lo |= __shfl_xor_sync(FULL, lo, o);
@@ -1930,13 +1947,12 @@ __global__ void __launch_bounds__(256, SA_SEED_MIN_BLOCKS) seed_kernel(const Ali
                         v = (v & keep) | (0x4E4E4E4Eu & ~keep);
                     }
                 }
-                const uint32_t isC = __vcmpeq4(v, 0x43434343u), isG = __vcmpeq4(v, 0x47474747u);
-                const uint32_t isT = __vcmpeq4(v, 0x54545454u), isN = __vcmpeq4(v, 0x4E4E4E4Eu);
-                const uint32_t isA = __vcmpeq4(v, 0x41414141u);
-                bad |= ~(isA | isC | isG | isT | isN);
-                lo |= byte_bits((isC | isT) & 0x01010101u) << (4 * k);
-                hi |= byte_bits((isG | isT) & 0x01010101u) << (4 * k);
-                nn |= byte_bits(isN & 0x01010101u) << (4 * k);
+                uint32_t l4, h4, n4, b4;
+                decode4(v, l4, h4, n4, b4);
+                bad |= b4;
+                lo |= l4 << (4 * k);
+                hi |= h4 << (4 * k);
+                nn |= n4 << (4 * k);
             }
         }
         const bool any_bad = (__ballot_sync(gmask, bad != 0) & gmask) != 0;

@@ -1587,6 +1587,9 @@ int sa_create(const uint64_t* packed_words, uint64_t n_packed, const uint64_t* n
             return;
         }
         cudaDeviceGetAttribute(&rep.sm_count, cudaDevAttrMultiProcessorCount, rep.device);
+        if (const char* e = getenv("SA_L2_FETCH")) {  // tuning: L2 fetch granularity hint (bytes)
+            cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, static_cast<size_t>(atoi(e)));
+        }
         cudaStream_t st;
         cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
         std::string e;
