@@ -139,10 +139,14 @@ SA_DEV int lv_warp(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, 
 SA_DEV int lv_thread(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, int dl, short* F, int fs,
                      uint32_t& cells, int e_cap) {
     constexpr short kU = -32768;  // unreachable: stays negative after +1 (REF edit_distance.cpp:56-59)
-    for (int t = 0; t < 2 * dl + 3; ++t) F[t * fs] = kU;
     const int off = dl + 1;
     for (int e = 0; e <= dl; ++e) {
         if (e > e_cap) return -2;
+        // iteration e reads diagonals -e..e+1; -e, e and e+1 were never
+        // written (iteration e-1 wrote -(e-1)..e-1), so only they are reset
+        F[(off - e) * fs] = kU;
+        F[(off + e) * fs] = kU;
+        F[(off + e + 1) * fs] = kU;
         bool found = false;
         int left = kU;  // old value of diagonal k-1
         int cur = F[(off - e) * fs];

@@ -288,6 +288,29 @@ def test_invalid_character_raises():
     assert al.align_batch(["ACGx"])[0].kind == api.ResultKind.NotFound
 
 
+@pytest.mark.parametrize("read_len", [100, 1500])
+def test_every_byte_outside_acgtn_raises(read_len):
+    """Every byte value other than A/C/G/T/N, at positions spread over the read
+    (word offsets 0-3, every 32-base block, the last base), fails the batch
+    (REF genome.cpp:182-200); reads of A/C/G/T/N only never do. 100 bp reads
+    are decoded by the seed kernel, 1.5 kbp reads by the long-read kernel."""
+    cfg, g, packed, nmask, bases, offs = _case("C0", 200_000, 10)
+    genome = api.PackedGenome(packed, nmask, g.size)
+    al = api.Aligner(api.SeedIndex.build(genome, 20), genome, cfg.params)
+    rng = np.random.default_rng(7)
+    base = bytearray(rng.choice(list(b"ACGTN"), size=read_len).tobytes())
+    ok = al.align_batch([bytes(base).decode()] * 3)
+    assert len(ok) == 3
+    for v in range(256):
+        if v in b"ACGTN":
+            continue
+        r = bytearray(base)
+        r[(v * 37) % read_len] = v
+        buf, offs2 = api.reads_to_buffer([bytes(base), bytes(r), bytes(base)])
+        with pytest.raises(ValueError):
+            al.align_arrays(np.frombuffer(buf, np.uint8).copy(), offs2)
+
+
 # ----------------------------------------------------------------- golden fixtures (reference outputs)
 
 import json  # noqa: E402
