@@ -298,7 +298,7 @@ def test_every_byte_outside_acgtn_raises(read_len):
     genome = api.PackedGenome(packed, nmask, g.size)
     al = api.Aligner(api.SeedIndex.build(genome, 20), genome, cfg.params)
     rng = np.random.default_rng(7)
-    base = bytearray(rng.choice(list(b"ACGTN"), size=read_len).tobytes())
+    base = bytearray(rng.choice(np.frombuffer(b"ACGTN", np.uint8), size=read_len).tobytes())
     ok = al.align_batch([bytes(base).decode()] * 3)
     assert len(ok) == 3
     for v in range(256):
