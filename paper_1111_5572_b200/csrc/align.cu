@@ -1514,11 +1514,38 @@ __global__ void __launch_bounds__(kSoloThreads, SA_SOLO_MIN_BLOCKS) solo_kernel(
         SoloRead c;
         int kind = SA_NOT_FOUND, len = 0;
         bool all_pop = false, first_best = false, too_short = false;
+        // The read's alignment is a small state machine so the warp stays
+        // converged where it matters: every lane first advances its own seed
+        // loop up to its next LV job (kSeed), then all lanes holding a job run
+        // their LVs together (kLv) -- entered one by one from divergent seed-loop
+        // paths the LV code, 70% of this kernel's instructions, ran with 2.8
+        // active lanes per instruction (profiles/r02y_ncu_C2.md).
+        enum { kIdle = 0, kSeed, kLv, kClassify };
+        int phase = kIdle;
+        const uint4* recs = nullptr;
+        const uint4* Rp = nullptr;
+        int n_eff = 0, d_max = 0, tier0 = 0;
+        Tracker tr;
+        tr.d_best = kInfDistance;
+        tr.d_second = kInfDistance;
+        tr.best_pos = 0;
+        tr.best_dir = 0;
+        uint32_t n_cands = 0, n_unscored = 0, calls = 0;
+        bool first_done = false, first_valid = false;
+        int first_dir = 0;
+        uint64_t first_pos = 0;
+        int tested = 0;
+        bool any_lookup = false, any_popular = false, early_multi = false, pruning = false;
+        int i = 0;
+        // the LV job: candidate key, anchors left, limit, best so far
+        uint32_t job_kk = 0, job_mm = 0;
+        int job_dl = 0, job_best_d = kInfDistance;
+        uint64_t job_best_anchor = 0;
         if (r < a.n_reads) {
             const uint2 meta = __ldg(a.pre_meta + r);
             len = static_cast<int>(meta.x);
             const uint32_t st = meta.y >> 16;
-            const int n_eff = static_cast<int>(meta.y & 0xffffu);
+            n_eff = static_cast<int>(meta.y & 0xffffu);
             outcome = 2;
             if (st == 1) {  // REF aligner.cpp:231-235
                 sa_result res;
@@ -1529,13 +1556,13 @@ __global__ void __launch_bounds__(kSoloThreads, SA_SOLO_MIN_BLOCKS) solo_kernel(
                 res.has_position = 0;
                 res.direction = 0;
 #pragma unroll
-                for (int i = 0; i < 5; ++i) res.reserved[i] = 0;
+                for (int q = 0; q < 5; ++q) res.reserved[q] = 0;
                 a.results[r] = res;
                 too_short = true;
                 outcome = 1;
             } else if (st == 0) {
-                const uint4* recs = a.pre_recs + static_cast<uint64_t>(r) * a.pre_rstride;
-                const uint4* Rp = a.pre_planes + static_cast<uint64_t>(r) * a.pre_pstride;
+                recs = a.pre_recs + static_cast<uint64_t>(r) * a.pre_rstride;
+                Rp = a.pre_planes + static_cast<uint64_t>(r) * a.pre_pstride;
 #if SA_SOLO_PF
                 // the seed loop reads the records one by one behind data-dependent
                 // branches, and the LV walks the planes as the wavefront advances:
@@ -1543,207 +1570,232 @@ __global__ void __launch_bounds__(kSoloThreads, SA_SOLO_MIN_BLOCKS) solo_kernel(
                 for (int t = 0; t < n_eff && t < 16; t += 2) solo_prefetch(recs + t);  // 2 records per 32 B sector
                 for (int t = 0; t < a.pre_pstride && t < 16; t += 2) solo_prefetch(Rp + t);
 #endif
-                const int d_max = a.dmax_param >= 0 ? a.dmax_param : (12 * len + 99) / 100;
-                const int tier0 = len / a.s;
-                Tracker tr;
-                tr.d_best = kInfDistance;
-                tr.d_second = kInfDistance;
-                tr.best_pos = 0;
-                tr.best_dir = 0;
-                uint32_t n_cands = 0, n_unscored = 0, calls = 0;
-                bool first_done = false, first_valid = false;
-                int first_dir = 0;
-                uint64_t first_pos = 0;
-                int tested = 0;
-                bool any_lookup = false, any_popular = false, early_multi = false, bail = false, pruning = false;
-                int i = 0;
-                for (;;) {
-                    if (!pruning) {
-                        if (i >= n_eff) break;
-                        uint4 rec = __ldg(recs + i);
-                        if (rec.x & kSeedLazy) rec = resolve_lazy(a, rec);  // probed on demand
-                        if (rec.x & kSeedN) {  // REF :259-262
-                            c.skip_n++;
-                            ++i;
-                            continue;
-                        }
-                        c.lookups++;
-                        if (rec.y > static_cast<uint32_t>(a.hmax)) {  // REF :265-269
-                            any_popular = true;
-                            c.skip_pop++;
-                            ++i;
-                            continue;
-                        }
-                        any_lookup = true;
-                        c.hits += rec.y;
-                        if (i < tier0) ++tested;
-                        // REF :273-286: every hit of the seed votes for (anchor / bucket, dir)
-                        const uint32_t cnt = rec.y;
-                        if (cnt > static_cast<uint32_t>(SA_SOLO_MAX_HITS)) {  // long vote lists: the warp kernel
-                            if (a.dbg) atomicAdd(a.dbg + 0, 1u);
-                            bail = true;
-                            break;
-                        }
-                        const bool pal = (rec.x & kSeedPal) != 0;
-                        const uint32_t ntot = pal ? cnt / 2 : cnt;
-                        const bool inl = ntot == 1;
-                        const uint32_t n_fwd = inl ? 0u : __ldg(a.pool + rec.z);
-                        const uint32_t qflip = (rec.x & kSeedQflip) ? 1u : 0u;
-                        const int o = static_cast<int>(rec.w);
-                        for (uint32_t t = 0; t < cnt; ++t) {
-                            const uint32_t jj = pal ? (t < ntot ? t : t - ntot) : t;
-                            uint32_t pos, eflag;
-                            if (inl) {
-                                pos = rec.z;
-                                eflag = (rec.x & kSeedSingleRc) ? 1u : 0u;
-                            } else {
-                                pos = __ldg(a.pool + rec.z + 1 + jj);
-                                eflag = jj >= n_fwd ? 1u : 0u;
-                            }
-                            const uint32_t dir = pal ? (t >= ntot ? 1u : 0u) : (eflag ^ qflip);
-                            const int64_t anchor = static_cast<int64_t>(pos) - (dir ? (len - a.s - o) : o);
-                            const uint32_t aa = anchor < 0 ? 0u : static_cast<uint32_t>(anchor);
-                            const uint32_t key = ((aa >> bsh) << 1) | dir;
-                            const uint32_t bit = 1u << (aa & ((1u << bsh) - 1u));
-                            uint32_t j = 0;
-                            while (j < n_cands && ckey[j * cs] != key) ++j;
-                            if (j < n_cands) {
-                                ccnt[j * cs] += 1u;
-                                cmask[j * cs] |= bit;
-                            } else if (n_cands == kSoloCands) {
-                                if (a.dbg) atomicAdd(a.dbg + 1, 1u);
-                                bail = true;
-                                break;
-                            } else {
-                                ckey[j * cs] = key;
-                                cmask[j * cs] = bit;
-                                ccnt[j * cs] = 1u;
-                                ++n_cands;
-                                ++n_unscored;
-                            }
-                        }
-                        if (bail) break;
-                    } else if (n_unscored == 0) {
+                d_max = a.dmax_param >= 0 ? a.dmax_param : (12 * len + 99) / 100;
+                tier0 = len / a.s;
+                phase = kSeed;
+            }
+        }
+        // after a seed's scoring step (REF :290-315): multi exit, pruning switch, next seed
+        auto after_step = [&]() {
+            if (tr.d_best < a.c && tr.d_second < tr.d_best + a.c) {  // REF :290-295 / :307-312
+                c.multi++;
+                early_multi = true;
+                phase = kClassify;
+                return;
+            }
+            if (!pruning) {
+                if (tested >= tr.d_best + a.c) {  // REF :296-315
+                    c.prune++;
+                    pruning = true;
+                }
+                ++i;
+            }
+        };
+        for (;;) {
+            // ---- kSeed: this lane's seed loop up to its next LV job
+            while (phase == kSeed) {
+                if (!pruning) {
+                    if (i >= n_eff) {
+                        phase = kClassify;
                         break;
                     }
-                    // score_best_candidate (REF :141-167)
-                    if (n_unscored > 0) {
-                        uint32_t bi = 0, bc = 0;
-                        uint64_t bord = ~0ull;
-                        for (uint32_t j = 0; j < n_cands; ++j) {
-                            const uint32_t cc = ccnt[j * cs];
-                            if (cc & kScored) continue;
-                            const uint32_t kk = ckey[j * cs];
-                            // amin = bucket * bs + lowest bit; order (amin, dir) as (amin << 1 | dir)
-                            const uint64_t amin = (static_cast<uint64_t>(kk >> 1) << bsh) + (__ffs(cmask[j * cs]) - 1);
-                            const uint64_t ord = (amin << 1) | (kk & 1u);
-                            if (cc > bc || (cc == bc && ord < bord)) {
-                                bc = cc;
-                                bord = ord;
-                                bi = j;
-                            }
-                        }
-                        // score_candidate (REF :169-221)
-                        const uint32_t kk = ckey[bi * cs];
-                        const uint32_t mm = cmask[bi * cs];
-                        ccnt[bi * cs] |= kScored;
-                        --n_unscored;
-                        int d_limit;
-                        if (tr.d_best > d_max) d_limit = d_max + a.c - 1;
-                        else if (tr.d_second >= tr.d_best + a.c) d_limit = tr.d_best + a.c - 1;
-                        else d_limit = tr.d_best - 1;
-                        if (a.force) d_limit = d_max + a.c - 1;
-                        if (d_limit >= 0) {  // (:184)
-                            const int dir = static_cast<int>(kk & 1u);
-                            const uint64_t base_pos = static_cast<uint64_t>(kk >> 1) << bsh;
-                            const uint4* orient = Rp + (dir ? half : 0);
-                            int best_d = kInfDistance;
-                            uint64_t best_anchor = 0;
-                            for (uint32_t m = mm; m != 0u; m &= m - 1u) {
-                                const uint64_t anchor = base_pos + static_cast<uint64_t>(__ffs(m) - 1);
-                                if (anchor >= a.glen) continue;
-                                const uint64_t rem = a.glen - anchor;
-                                const uint64_t want = static_cast<uint64_t>(len) + static_cast<uint64_t>(d_limit);
-                                const int w = static_cast<int>(want < rem ? want : rem);
-#if SA_SOLO_LV == 1
-                                const int d = lv_bitpar(orient, half, len, a.planes, static_cast<uint32_t>(anchor), w,
-                                                        d_limit, c.cells);
-#else
-                                const int d = lv_thread(orient, len, a.planes, static_cast<uint32_t>(anchor), w, d_limit,
-                                                        &s_F[0][tid], cs, c.cells, SA_SOLO_MAX_E);
-#endif
-                                if (d == -2) {
-                                    if (a.dbg) atomicAdd(a.dbg + 2, 1u);
-                                    bail = true;
-                                    break;
-                                }
-                                c.dist++;
-                                calls++;
-                                c.window += static_cast<uint32_t>(w);
-                                if (calls > 1) {
-                                    c.dist_after++;
-                                    if (d < 0) c.early_out++;
-                                }
-                                if (d >= 0 && d < best_d) {
-                                    best_d = d;
-                                    best_anchor = anchor;
-                                }
-                            }
-                            if (bail) break;
-                            if (!first_done) {
-                                first_done = true;
-                                if (best_d < kInfDistance) {
-                                    first_valid = true;
-                                    first_pos = best_anchor;
-                                    first_dir = dir;
-                                }
-                            }
-                            if (best_d < kInfDistance) tracker_observe(tr, a.bs, best_d, best_anchor, dir);
-                        }
-                    }
-                    if (tr.d_best < a.c && tr.d_second < tr.d_best + a.c) {  // REF :290-295 / :307-312
-                        c.multi++;
-                        early_multi = true;
-                        break;
-                    }
-                    if (!pruning) {
-                        if (tested >= tr.d_best + a.c) {  // REF :296-315
-                            c.prune++;
-                            pruning = true;
-                        }
+                    uint4 rec = __ldg(recs + i);
+                    if (rec.x & kSeedLazy) rec = resolve_lazy(a, rec);  // probed on demand
+                    if (rec.x & kSeedN) {  // REF :259-262
+                        c.skip_n++;
                         ++i;
+                        continue;
+                    }
+                    c.lookups++;
+                    if (rec.y > static_cast<uint32_t>(a.hmax)) {  // REF :265-269
+                        any_popular = true;
+                        c.skip_pop++;
+                        ++i;
+                        continue;
+                    }
+                    any_lookup = true;
+                    c.hits += rec.y;
+                    if (i < tier0) ++tested;
+                    // REF :273-286: every hit of the seed votes for (anchor / bucket, dir)
+                    const uint32_t cnt = rec.y;
+                    if (cnt > static_cast<uint32_t>(SA_SOLO_MAX_HITS)) {  // long vote lists: the warp kernel
+                        if (a.dbg) atomicAdd(a.dbg + 0, 1u);
+                        phase = kIdle;
+                        break;
+                    }
+                    const bool pal = (rec.x & kSeedPal) != 0;
+                    const uint32_t ntot = pal ? cnt / 2 : cnt;
+                    const bool inl = ntot == 1;
+                    const uint32_t n_fwd = inl ? 0u : __ldg(a.pool + rec.z);
+                    const uint32_t qflip = (rec.x & kSeedQflip) ? 1u : 0u;
+                    const int o = static_cast<int>(rec.w);
+                    bool full = false;
+                    for (uint32_t t = 0; t < cnt; ++t) {
+                        const uint32_t jj = pal ? (t < ntot ? t : t - ntot) : t;
+                        uint32_t pos, eflag;
+                        if (inl) {
+                            pos = rec.z;
+                            eflag = (rec.x & kSeedSingleRc) ? 1u : 0u;
+                        } else {
+                            pos = __ldg(a.pool + rec.z + 1 + jj);
+                            eflag = jj >= n_fwd ? 1u : 0u;
+                        }
+                        const uint32_t dir = pal ? (t >= ntot ? 1u : 0u) : (eflag ^ qflip);
+                        const int64_t anchor = static_cast<int64_t>(pos) - (dir ? (len - a.s - o) : o);
+                        const uint32_t aa = anchor < 0 ? 0u : static_cast<uint32_t>(anchor);
+                        const uint32_t key = ((aa >> bsh) << 1) | dir;
+                        const uint32_t bit = 1u << (aa & ((1u << bsh) - 1u));
+                        uint32_t j = 0;
+                        while (j < n_cands && ckey[j * cs] != key) ++j;
+                        if (j < n_cands) {
+                            ccnt[j * cs] += 1u;
+                            cmask[j * cs] |= bit;
+                        } else if (n_cands == kSoloCands) {
+                            if (a.dbg) atomicAdd(a.dbg + 1, 1u);
+                            full = true;
+                            break;
+                        } else {
+                            ckey[j * cs] = key;
+                            cmask[j * cs] = bit;
+                            ccnt[j * cs] = 1u;
+                            ++n_cands;
+                            ++n_unscored;
+                        }
+                    }
+                    if (full) {  // more candidates than the table holds: the warp kernel
+                        phase = kIdle;
+                        break;
+                    }
+                } else if (n_unscored == 0) {
+                    phase = kClassify;
+                    break;
+                }
+                // score_best_candidate (REF :141-167)
+                if (n_unscored > 0) {
+                    uint32_t bi = 0, bc = 0;
+                    uint64_t bord = ~0ull;
+                    for (uint32_t j = 0; j < n_cands; ++j) {
+                        const uint32_t cc = ccnt[j * cs];
+                        if (cc & kScored) continue;
+                        const uint32_t kk = ckey[j * cs];
+                        // amin = bucket * bs + lowest bit; order (amin, dir) as (amin << 1 | dir)
+                        const uint64_t amin = (static_cast<uint64_t>(kk >> 1) << bsh) + (__ffs(cmask[j * cs]) - 1);
+                        const uint64_t ord = (amin << 1) | (kk & 1u);
+                        if (cc > bc || (cc == bc && ord < bord)) {
+                            bc = cc;
+                            bord = ord;
+                            bi = j;
+                        }
+                    }
+                    // score_candidate (REF :169-221): the LVs run in the kLv phase
+                    ccnt[bi * cs] |= kScored;
+                    --n_unscored;
+                    int d_limit;
+                    if (tr.d_best > d_max) d_limit = d_max + a.c - 1;
+                    else if (tr.d_second >= tr.d_best + a.c) d_limit = tr.d_best + a.c - 1;
+                    else d_limit = tr.d_best - 1;
+                    if (a.force) d_limit = d_max + a.c - 1;
+                    if (d_limit >= 0) {  // (:184)
+                        job_kk = ckey[bi * cs];
+                        job_mm = cmask[bi * cs];
+                        job_dl = d_limit;
+                        job_best_d = kInfDistance;
+                        job_best_anchor = 0;
+                        phase = kLv;
+                        break;
                     }
                 }
-                if (!bail) {  // classification, REF :318-363
-                    if (early_multi) {
-                        kind = SA_MULTIPLE_HITS;
+                after_step();
+            }
+            // ---- kLv: one anchor's LV per lane, all lanes with a job together
+            if (!__any_sync(FULL, phase == kLv)) break;  // no lane is left in kSeed here
+            if (phase == kLv) {
+                const int dir = static_cast<int>(job_kk & 1u);
+                const uint64_t base_pos = static_cast<uint64_t>(job_kk >> 1) << bsh;
+                bool have = false;
+                uint64_t anchor = 0;
+                while (job_mm != 0u) {
+                    anchor = base_pos + static_cast<uint64_t>(__ffs(job_mm) - 1);
+                    job_mm &= job_mm - 1u;
+                    if (anchor < a.glen) {
+                        have = true;
+                        break;
+                    }
+                }
+                bool bail = false;
+                if (have) {
+                    const uint64_t rem = a.glen - anchor;
+                    const uint64_t want = static_cast<uint64_t>(len) + static_cast<uint64_t>(job_dl);
+                    const int w = static_cast<int>(want < rem ? want : rem);
+#if SA_SOLO_LV == 1
+                    const int d = lv_bitpar(Rp + (dir ? half : 0), half, len, a.planes, static_cast<uint32_t>(anchor), w,
+                                            job_dl, c.cells);
+#else
+                    const int d = lv_thread(Rp + (dir ? half : 0), len, a.planes, static_cast<uint32_t>(anchor), w,
+                                            job_dl, &s_F[0][tid], cs, c.cells, SA_SOLO_MAX_E);
+#endif
+                    if (d == -2) {  // a long wavefront: the warp kernel
+                        if (a.dbg) atomicAdd(a.dbg + 2, 1u);
+                        bail = true;
                     } else {
-                        if (tr.d_best <= d_max && tr.d_second >= tr.d_best + a.c) kind = SA_SINGLE_HIT;
-                        else if (tr.d_best <= d_max) kind = SA_MULTIPLE_HITS;
-                        else kind = SA_NOT_FOUND;
-                        if (kind == SA_NOT_FOUND && any_popular && !any_lookup) {
-                            all_pop = true;
-                            kind = SA_MULTIPLE_HITS;
+                        c.dist++;
+                        calls++;
+                        c.window += static_cast<uint32_t>(w);
+                        if (calls > 1) {
+                            c.dist_after++;
+                            if (d < 0) c.early_out++;
+                        }
+                        if (d >= 0 && d < job_best_d) {
+                            job_best_d = d;
+                            job_best_anchor = anchor;
                         }
                     }
-                    uint64_t w0 = 0, w1 = static_cast<uint32_t>(-1), w2 = static_cast<uint64_t>(kind);
-                    if (kind == SA_SINGLE_HIT || (kind == SA_MULTIPLE_HITS && tr.d_best <= d_max)) {
-                        w0 = tr.best_pos;
-                        w1 = static_cast<uint32_t>(tr.d_best) |
-                             (static_cast<uint64_t>(static_cast<uint32_t>(tracker_gap(tr))) << 32);
-                        w2 |= (1ull << 8) | (static_cast<uint64_t>(tr.best_dir) << 16);
+                }
+                if (bail) {
+                    phase = kIdle;
+                } else if (job_mm == 0u) {  // the candidate's anchors are done
+                    if (!first_done) {
+                        first_done = true;
+                        if (job_best_d < kInfDistance) {
+                            first_valid = true;
+                            first_pos = job_best_anchor;
+                            first_dir = dir;
+                        }
                     }
-                    if (kind == SA_SINGLE_HIT && first_valid && first_dir == tr.best_dir) {
-                        const uint64_t delta = first_pos > tr.best_pos ? first_pos - tr.best_pos : tr.best_pos - first_pos;
-                        first_best = delta <= static_cast<uint64_t>(a.bs);
-                    }
-                    uint64_t* out = reinterpret_cast<uint64_t*>(a.results + r);
-                    out[0] = w0;
-                    out[1] = w1;
-                    out[2] = w2;
-                    outcome = 1;
+                    if (job_best_d < kInfDistance) tracker_observe(tr, a.bs, job_best_d, job_best_anchor, dir);
+                    phase = kSeed;
+                    after_step();
                 }
             }
+        }
+        if (phase == kClassify) {  // classification, REF :318-363
+            if (early_multi) {
+                kind = SA_MULTIPLE_HITS;
+            } else {
+                if (tr.d_best <= d_max && tr.d_second >= tr.d_best + a.c) kind = SA_SINGLE_HIT;
+                else if (tr.d_best <= d_max) kind = SA_MULTIPLE_HITS;
+                else kind = SA_NOT_FOUND;
+                if (kind == SA_NOT_FOUND && any_popular && !any_lookup) {
+                    all_pop = true;
+                    kind = SA_MULTIPLE_HITS;
+                }
+            }
+            uint64_t w0 = 0, w1 = static_cast<uint32_t>(-1), w2 = static_cast<uint64_t>(kind);
+            if (kind == SA_SINGLE_HIT || (kind == SA_MULTIPLE_HITS && tr.d_best <= d_max)) {
+                w0 = tr.best_pos;
+                w1 = static_cast<uint32_t>(tr.d_best) |
+                     (static_cast<uint64_t>(static_cast<uint32_t>(tracker_gap(tr))) << 32);
+                w2 |= (1ull << 8) | (static_cast<uint64_t>(tr.best_dir) << 16);
+            }
+            if (kind == SA_SINGLE_HIT && first_valid && first_dir == tr.best_dir) {
+                const uint64_t delta = first_pos > tr.best_pos ? first_pos - tr.best_pos : tr.best_pos - first_pos;
+                first_best = delta <= static_cast<uint64_t>(a.bs);
+            }
+            uint64_t* out = reinterpret_cast<uint64_t*>(a.results + r);
+            out[0] = w0;
+            out[1] = w1;
+            out[2] = w2;
+            outcome = 1;
         }
         // reads for the warp kernel, warp-aggregated
         const uint32_t cm = __ballot_sync(FULL, outcome == 2);
