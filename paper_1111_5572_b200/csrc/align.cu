@@ -1593,119 +1593,116 @@ __global__ void __launch_bounds__(kSoloThreads, SA_SOLO_MIN_BLOCKS) solo_kernel(
         };
         for (;;) {
             // ---- kSeed: this lane's seed loop up to its next LV job
+            // (structured branches only -- no continue/break out of the body --
+            // so the lanes rejoin after every step of the loop)
             while (phase == kSeed) {
-                if (!pruning) {
-                    if (i >= n_eff) {
-                        phase = kClassify;
-                        break;
-                    }
+                bool score = false;  // this step goes on to score_best_candidate
+                if (pruning) {
+                    if (n_unscored == 0) phase = kClassify;
+                    else score = true;
+                } else if (i >= n_eff) {
+                    phase = kClassify;
+                } else {
                     uint4 rec = __ldg(recs + i);
                     if (rec.x & kSeedLazy) rec = resolve_lazy(a, rec);  // probed on demand
                     if (rec.x & kSeedN) {  // REF :259-262
                         c.skip_n++;
                         ++i;
-                        continue;
-                    }
-                    c.lookups++;
-                    if (rec.y > static_cast<uint32_t>(a.hmax)) {  // REF :265-269
+                    } else if (rec.y > static_cast<uint32_t>(a.hmax)) {  // REF :265-269
+                        c.lookups++;
                         any_popular = true;
                         c.skip_pop++;
                         ++i;
-                        continue;
-                    }
-                    any_lookup = true;
-                    c.hits += rec.y;
-                    if (i < tier0) ++tested;
-                    // REF :273-286: every hit of the seed votes for (anchor / bucket, dir)
-                    const uint32_t cnt = rec.y;
-                    if (cnt > static_cast<uint32_t>(SA_SOLO_MAX_HITS)) {  // long vote lists: the warp kernel
+                    } else if (rec.y > static_cast<uint32_t>(SA_SOLO_MAX_HITS)) {  // long vote lists: the warp kernel
                         if (a.dbg) atomicAdd(a.dbg + 0, 1u);
                         phase = kIdle;
-                        break;
-                    }
-                    const bool pal = (rec.x & kSeedPal) != 0;
-                    const uint32_t ntot = pal ? cnt / 2 : cnt;
-                    const bool inl = ntot == 1;
-                    const uint32_t n_fwd = inl ? 0u : __ldg(a.pool + rec.z);
-                    const uint32_t qflip = (rec.x & kSeedQflip) ? 1u : 0u;
-                    const int o = static_cast<int>(rec.w);
-                    bool full = false;
-                    for (uint32_t t = 0; t < cnt; ++t) {
-                        const uint32_t jj = pal ? (t < ntot ? t : t - ntot) : t;
-                        uint32_t pos, eflag;
-                        if (inl) {
-                            pos = rec.z;
-                            eflag = (rec.x & kSeedSingleRc) ? 1u : 0u;
-                        } else {
-                            pos = __ldg(a.pool + rec.z + 1 + jj);
-                            eflag = jj >= n_fwd ? 1u : 0u;
+                    } else {
+                        c.lookups++;
+                        any_lookup = true;
+                        c.hits += rec.y;
+                        if (i < tier0) ++tested;
+                        // REF :273-286: every hit of the seed votes for (anchor / bucket, dir)
+                        const uint32_t cnt = rec.y;
+                        const bool pal = (rec.x & kSeedPal) != 0;
+                        const uint32_t ntot = pal ? cnt / 2 : cnt;
+                        const bool inl = ntot == 1;
+                        const uint32_t n_fwd = inl ? 0u : __ldg(a.pool + rec.z);
+                        const uint32_t qflip = (rec.x & kSeedQflip) ? 1u : 0u;
+                        const int o = static_cast<int>(rec.w);
+                        bool full = false;
+                        for (uint32_t t = 0; t < cnt && !full; ++t) {
+                            const uint32_t jj = pal ? (t < ntot ? t : t - ntot) : t;
+                            uint32_t pos, eflag;
+                            if (inl) {
+                                pos = rec.z;
+                                eflag = (rec.x & kSeedSingleRc) ? 1u : 0u;
+                            } else {
+                                pos = __ldg(a.pool + rec.z + 1 + jj);
+                                eflag = jj >= n_fwd ? 1u : 0u;
+                            }
+                            const uint32_t dir = pal ? (t >= ntot ? 1u : 0u) : (eflag ^ qflip);
+                            const int64_t anchor = static_cast<int64_t>(pos) - (dir ? (len - a.s - o) : o);
+                            const uint32_t aa = anchor < 0 ? 0u : static_cast<uint32_t>(anchor);
+                            const uint32_t key = ((aa >> bsh) << 1) | dir;
+                            const uint32_t bit = 1u << (aa & ((1u << bsh) - 1u));
+                            uint32_t j = 0;
+                            while (j < n_cands && ckey[j * cs] != key) ++j;
+                            if (j < n_cands) {
+                                ccnt[j * cs] += 1u;
+                                cmask[j * cs] |= bit;
+                            } else if (n_cands == kSoloCands) {  // more candidates than the table holds
+                                if (a.dbg) atomicAdd(a.dbg + 1, 1u);
+                                full = true;
+                            } else {
+                                ckey[j * cs] = key;
+                                cmask[j * cs] = bit;
+                                ccnt[j * cs] = 1u;
+                                ++n_cands;
+                                ++n_unscored;
+                            }
                         }
-                        const uint32_t dir = pal ? (t >= ntot ? 1u : 0u) : (eflag ^ qflip);
-                        const int64_t anchor = static_cast<int64_t>(pos) - (dir ? (len - a.s - o) : o);
-                        const uint32_t aa = anchor < 0 ? 0u : static_cast<uint32_t>(anchor);
-                        const uint32_t key = ((aa >> bsh) << 1) | dir;
-                        const uint32_t bit = 1u << (aa & ((1u << bsh) - 1u));
-                        uint32_t j = 0;
-                        while (j < n_cands && ckey[j * cs] != key) ++j;
-                        if (j < n_cands) {
-                            ccnt[j * cs] += 1u;
-                            cmask[j * cs] |= bit;
-                        } else if (n_cands == kSoloCands) {
-                            if (a.dbg) atomicAdd(a.dbg + 1, 1u);
-                            full = true;
-                            break;
-                        } else {
-                            ckey[j * cs] = key;
-                            cmask[j * cs] = bit;
-                            ccnt[j * cs] = 1u;
-                            ++n_cands;
-                            ++n_unscored;
-                        }
-                    }
-                    if (full) {  // more candidates than the table holds: the warp kernel
-                        phase = kIdle;
-                        break;
-                    }
-                } else if (n_unscored == 0) {
-                    phase = kClassify;
-                    break;
-                }
-                // score_best_candidate (REF :141-167)
-                if (n_unscored > 0) {
-                    uint32_t bi = 0, bc = 0;
-                    uint64_t bord = ~0ull;
-                    for (uint32_t j = 0; j < n_cands; ++j) {
-                        const uint32_t cc = ccnt[j * cs];
-                        if (cc & kScored) continue;
-                        const uint32_t kk = ckey[j * cs];
-                        // amin = bucket * bs + lowest bit; order (amin, dir) as (amin << 1 | dir)
-                        const uint64_t amin = (static_cast<uint64_t>(kk >> 1) << bsh) + (__ffs(cmask[j * cs]) - 1);
-                        const uint64_t ord = (amin << 1) | (kk & 1u);
-                        if (cc > bc || (cc == bc && ord < bord)) {
-                            bc = cc;
-                            bord = ord;
-                            bi = j;
-                        }
-                    }
-                    // score_candidate (REF :169-221): the LVs run in the kLv phase
-                    ccnt[bi * cs] |= kScored;
-                    --n_unscored;
-                    int d_limit;
-                    if (tr.d_best > d_max) d_limit = d_max + a.c - 1;
-                    else if (tr.d_second >= tr.d_best + a.c) d_limit = tr.d_best + a.c - 1;
-                    else d_limit = tr.d_best - 1;
-                    if (a.force) d_limit = d_max + a.c - 1;
-                    if (d_limit >= 0) {  // (:184)
-                        job_kk = ckey[bi * cs];
-                        job_mm = cmask[bi * cs];
-                        job_dl = d_limit;
-                        job_best_d = kInfDistance;
-                        job_best_anchor = 0;
-                        phase = kLv;
-                        break;
+                        if (full) phase = kIdle;  // the warp kernel
+                        else score = true;
                     }
                 }
-                after_step();
+                if (score) {
+                    bool job = false;
+                    // score_best_candidate (REF :141-167)
+                    if (n_unscored > 0) {
+                        uint32_t bi = 0, bc = 0;
+                        uint64_t bord = ~0ull;
+                        for (uint32_t j = 0; j < n_cands; ++j) {
+                            const uint32_t cc = ccnt[j * cs];
+                            const uint32_t kk = ckey[j * cs];
+                            // amin = bucket * bs + lowest bit; order (amin, dir) as (amin << 1 | dir)
+                            const uint64_t amin = (static_cast<uint64_t>(kk >> 1) << bsh) + (__ffs(cmask[j * cs]) - 1);
+                            const uint64_t ord = (amin << 1) | (kk & 1u);
+                            if (!(cc & kScored) && (cc > bc || (cc == bc && ord < bord))) {
+                                bc = cc;
+                                bord = ord;
+                                bi = j;
+                            }
+                        }
+                        // score_candidate (REF :169-221): the LVs run in the kLv phase
+                        ccnt[bi * cs] |= kScored;
+                        --n_unscored;
+                        int d_limit;
+                        if (tr.d_best > d_max) d_limit = d_max + a.c - 1;
+                        else if (tr.d_second >= tr.d_best + a.c) d_limit = tr.d_best + a.c - 1;
+                        else d_limit = tr.d_best - 1;
+                        if (a.force) d_limit = d_max + a.c - 1;
+                        if (d_limit >= 0) {  // (:184)
+                            job_kk = ckey[bi * cs];
+                            job_mm = cmask[bi * cs];
+                            job_dl = d_limit;
+                            job_best_d = kInfDistance;
+                            job_best_anchor = 0;
+                            phase = kLv;
+                            job = true;
+                        }
+                    }
+                    if (!job) after_step();
+                }
             }
             // ---- kLv: one anchor's LV per lane, all lanes with a job together
             if (!__any_sync(FULL, phase == kLv)) break;  // no lane is left in kSeed here
