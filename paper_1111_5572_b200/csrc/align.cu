@@ -1488,7 +1488,10 @@ struct SoloRead {
 #define SA_SOLO_MAX_HITS 4  // hits of one seed the thread votes itself (more: the warp kernel; C2 1/4/8/32: 245/244/238/236 M reads/s)
 #endif
 #ifndef SA_SOLO_MAX_E
-#define SA_SOLO_MAX_E 4  // LV iterations a thread runs before handing its read to the warp kernel
+#define SA_SOLO_MAX_E 2  // LV iterations a thread runs serially
+#endif
+#ifndef SA_SOLO_COOP
+#define SA_SOLO_COOP 1  // 1: the warp finishes longer wavefronts lane per diagonal; 0: their reads go to the warp kernel
 #endif
 __global__ void __launch_bounds__(kSoloThreads, SA_SOLO_MIN_BLOCKS) solo_kernel(const AlignLaunch a) {
     __shared__ uint32_t s_key[kSoloCands][kSoloThreads];   // bucket << 1 | dir
@@ -1706,35 +1709,58 @@ __global__ void __launch_bounds__(kSoloThreads, SA_SOLO_MIN_BLOCKS) solo_kernel(
             }
             // ---- kLv: one anchor's LV per lane, all lanes with a job together
             if (!__any_sync(FULL, phase == kLv)) break;  // no lane is left in kSeed here
+            const int dir = static_cast<int>(job_kk & 1u);
+            bool have = false;
+            uint64_t anchor = 0;
+            int w = 0, d = -1;
             if (phase == kLv) {
-                const int dir = static_cast<int>(job_kk & 1u);
                 const uint64_t base_pos = static_cast<uint64_t>(job_kk >> 1) << bsh;
-                bool have = false;
-                uint64_t anchor = 0;
-                while (job_mm != 0u) {
+                while (job_mm != 0u && !have) {
                     anchor = base_pos + static_cast<uint64_t>(__ffs(job_mm) - 1);
                     job_mm &= job_mm - 1u;
-                    if (anchor < a.glen) {
-                        have = true;
-                        break;
-                    }
+                    have = anchor < a.glen;
                 }
-                bool bail = false;
                 if (have) {
                     const uint64_t rem = a.glen - anchor;
                     const uint64_t want = static_cast<uint64_t>(len) + static_cast<uint64_t>(job_dl);
-                    const int w = static_cast<int>(want < rem ? want : rem);
+                    w = static_cast<int>(want < rem ? want : rem);
 #if SA_SOLO_LV == 1
-                    const int d = lv_bitpar(Rp + (dir ? half : 0), half, len, a.planes, static_cast<uint32_t>(anchor), w,
-                                            job_dl, c.cells);
+                    d = lv_bitpar(Rp + (dir ? half : 0), half, len, a.planes, static_cast<uint32_t>(anchor), w, job_dl,
+                                  c.cells);
 #else
-                    const int d = lv_thread(Rp + (dir ? half : 0), len, a.planes, static_cast<uint32_t>(anchor), w,
-                                            job_dl, &s_F[0][tid], cs, c.cells, SA_SOLO_MAX_E);
+                    d = lv_thread(Rp + (dir ? half : 0), len, a.planes, static_cast<uint32_t>(anchor), w, job_dl,
+                                  &s_F[0][tid], cs, c.cells, SA_SOLO_MAX_E);
 #endif
-                    if (d == -2) {  // a long wavefront: the warp kernel
-                        if (a.dbg) atomicAdd(a.dbg + 2, 1u);
-                        bail = true;
-                    } else {
+                }
+            }
+#if SA_SOLO_COOP && SA_SOLO_LV != 1
+            // The wavefronts still open after SA_SOLO_MAX_E serial iterations are
+            // few and wide (2e + 1 diagonals each): the warp finishes them one at a
+            // time, lane per diagonal, from the owner's frontier column.
+            __syncwarp();  // the owners' frontier columns are read by the other lanes
+            for (uint32_t pend = __ballot_sync(FULL, d == -2); pend != 0u; pend &= pend - 1u) {
+                const int src = __ffs(pend) - 1;
+                const uint4* Rb = reinterpret_cast<const uint4*>(
+                    shfl64(reinterpret_cast<unsigned long long>(Rp + (dir ? half : 0)), src));
+                const uint32_t wofs = __shfl_sync(FULL, static_cast<uint32_t>(anchor), src);
+                const int wb = __shfl_sync(FULL, w, src), dlb = __shfl_sync(FULL, job_dl, src);
+                const int mb = __shfl_sync(FULL, len, src);
+                uint32_t cells = 0;  // every lane's steps count for the owner's read
+                const int res = lv_warp_resume(Rb, mb, a.planes, wofs, wb, dlb, &s_F[0][(tid & ~31) + src], cs,
+                                               SA_SOLO_MAX_E, lane, cells);
+                cells = __reduce_add_sync(FULL, cells);
+                if (lane == src) {
+                    d = res;
+                    c.cells += cells;
+                }
+            }
+#endif
+            if (phase == kLv) {
+                if (d == -2) {  // a long wavefront: the warp kernel
+                    if (a.dbg) atomicAdd(a.dbg + 2, 1u);
+                    phase = kIdle;
+                } else {
+                    if (have) {
                         c.dist++;
                         calls++;
                         c.window += static_cast<uint32_t>(w);
@@ -1747,21 +1773,19 @@ __global__ void __launch_bounds__(kSoloThreads, SA_SOLO_MIN_BLOCKS) solo_kernel(
                             job_best_anchor = anchor;
                         }
                     }
-                }
-                if (bail) {
-                    phase = kIdle;
-                } else if (job_mm == 0u) {  // the candidate's anchors are done
-                    if (!first_done) {
-                        first_done = true;
-                        if (job_best_d < kInfDistance) {
-                            first_valid = true;
-                            first_pos = job_best_anchor;
-                            first_dir = dir;
+                    if (job_mm == 0u) {  // the candidate's anchors are done
+                        if (!first_done) {
+                            first_done = true;
+                            if (job_best_d < kInfDistance) {
+                                first_valid = true;
+                                first_pos = job_best_anchor;
+                                first_dir = dir;
+                            }
                         }
+                        if (job_best_d < kInfDistance) tracker_observe(tr, a.bs, job_best_d, job_best_anchor, dir);
+                        phase = kSeed;
+                        after_step();
                     }
-                    if (job_best_d < kInfDistance) tracker_observe(tr, a.bs, job_best_d, job_best_anchor, dir);
-                    phase = kSeed;
-                    after_step();
                 }
             }
         }

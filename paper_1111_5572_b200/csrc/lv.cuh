@@ -60,12 +60,12 @@ SA_DEV int lv_step(int e, int k, int prev_km1, int prev_k, int prev_kp1, int m, 
 }
 
 // Register wavefront for d_limit <= 15: lane l owns diagonal k = l - d_limit.
-SA_DEV int lv_warp_reg(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, int dl,
-                       int lane, uint32_t& cells) {
+// Iterations e_first..dl, from the frontier value `fr` of iteration e_first - 1.
+SA_DEV int lv_warp_reg_from(int fr, int e_first, const uint4* R, int m, const uint4* W, uint32_t wofs, int w,
+                            int dl, int lane, uint32_t& cells) {
     const int k = lane - dl;
     const bool mine = lane <= 2 * dl;
-    int fr = kUnreach;
-    for (int e = 0; e <= dl; ++e) {
+    for (int e = e_first; e <= dl; ++e) {
         int up = __shfl_down_sync(kLvFull, fr, 1);
         int dn = __shfl_up_sync(kLvFull, fr, 1);
         if (lane == 31) up = kUnreach;
@@ -75,6 +75,26 @@ SA_DEV int lv_warp_reg(const uint4* R, int m, const uint4* W, uint32_t wofs, int
         if (__any_sync(kLvFull, active && fr == m)) return e;
     }
     return -1;
+}
+
+SA_DEV int lv_warp_reg(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, int dl,
+                       int lane, uint32_t& cells) {
+    return lv_warp_reg_from(kUnreach, 0, R, m, W, wofs, w, dl, lane, cells);
+}
+
+// The register wavefront resumed from a serial one (lv_thread returned -2
+// after iteration e0 < dl): F holds iteration e0's values of diagonals
+// -e0..e0 in lv_thread's layout (16-bit entries, stride fs); the warp runs
+// iterations e0 + 1..dl, lane per diagonal.  Same steps, same value.
+SA_DEV int lv_warp_resume(const uint4* R, int m, const uint4* W, uint32_t wofs, int w, int dl,
+                          const short* F, int fs, int e0, int lane, uint32_t& cells) {
+    const int k = lane - dl;
+    int fr = kUnreach;
+    if (lane <= 2 * dl && k >= -e0 && k <= e0) {
+        const int v = F[(k + dl + 1) * fs];
+        if (v >= 0) fr = v;
+    }
+    return lv_warp_reg_from(fr, e0 + 1, R, m, W, wofs, w, dl, lane, cells);
 }
 
 // Shared-memory wavefront for any d_limit: F holds 2 * (2*dl + 3) entries of
