@@ -1485,7 +1485,7 @@ struct SoloRead {
 #define SA_SOLO_LV 0
 #endif
 #ifndef SA_SOLO_MAX_HITS
-#define SA_SOLO_MAX_HITS 4  // hits of one seed the thread votes itself (more: the warp kernel; C2 1/4/8/32: 245/244/238/236 M reads/s)
+#define SA_SOLO_MAX_HITS 6  // hits of one seed the thread votes itself (more: the warp kernel; C2 4/6/8 with the phase-synchronous kernel: 485/492/487 M reads/s)
 #endif
 #ifndef SA_SOLO_MAX_E
 #define SA_SOLO_MAX_E 2  // LV iterations a thread runs serially

@@ -82,7 +82,8 @@ void tl_dump(cudaEvent_t base) {
     g_tl.clear();
 }  // chunk buffers in flight per replica (copies run ahead of compute)
 constexpr int kCtlWords = 4;  // cursor_fast, cursor_slow, overflow_count, error_flag
-// Chunk size of the batch pipeline: about 1/24 of the batch, between
+// Chunk size of the batch pipeline: about 1/32 of the batch (1/24 until the
+// solo kernel got faster: C2 e2e 25.9 ms at 426 k reads per chunk, 25.2 at 328 k), between
 // 48 k and 512 k reads.  Each chunk costs a kernel ramp and tail (~15 us), so
 // big batches want big chunks (C2, 10 M reads: e2e 152 M reads/s at 48 k,
 // 196 M at 512 k), while a 1 M batch wants enough chunks to overlap copy and
@@ -97,7 +98,7 @@ uint64_t chunk_reads_setting(uint64_t n_reads, uint64_t mean_len) {
         return e ? atoll(e) : 0ll;
     }();
     if (forced >= 1024) return static_cast<uint64_t>(forced);
-    const uint64_t want = ((n_reads / 24 + 16383) / 16384) * 16384;
+    const uint64_t want = ((n_reads / 32 + 16383) / 16384) * 16384;
     const uint64_t floor = 49152ull * std::max<uint64_t>(1, mean_len / 128);
     return std::min<uint64_t>(512u << 10, std::max<uint64_t>(floor, want));
 }
