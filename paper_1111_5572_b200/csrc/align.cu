@@ -2814,7 +2814,9 @@ void launch_seed(const AlignLaunch& a0, cudaStream_t st) {
         uint64_t g = (static_cast<uint64_t>(a.n_reads) + groups_per_block - 1) / groups_per_block;
         static const uint64_t cap = [] {  // SA_SEED_GRID overrides (tuning)
             const char* e = getenv("SA_SEED_GRID");
-            return e ? static_cast<uint64_t>(atoll(e)) : uint64_t{1} << 23;  // a group per read (C1 1018 -> 1025 M over 148 x 32)
+            // 64 blocks per SM, grid-stride beyond: a block lists the seed offsets once for its reads
+            // (a group per read -- 2^23 blocks -- measured 491 M reads/s at C2 against 497 M)
+            return e ? static_cast<uint64_t>(atoll(e)) : uint64_t{148 * 64};
         }();
         // gridDim.x * blockDim.x is a 32-bit product in the kernel: at most 2^31 threads
         g = std::max<uint64_t>(1, std::min<uint64_t>({g, std::max<uint64_t>(cap, 1), uint64_t{1} << 23}));
