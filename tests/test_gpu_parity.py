@@ -252,6 +252,37 @@ def test_align_parity(name, glen, nreads, runs, nfrac):
     assert st["reads"] == nreads
 
 
+def test_align_heavily_edited_reads():
+    """Reads carrying 0-16 edits each (substitutions, 1-3 base insertions and
+    deletions, N) at d_max 12: every LV length from an exact match to a
+    wavefront that fails at the limit -- the solo kernel's serial iterations,
+    the warp's lane-per-diagonal finish of the longer ones (lv_warp_resume)
+    and the warp kernel's own LV (test_gpu_solo.py forces each)."""
+    cfg, g, packed, nmask, bases, offs = _case("C1", 3_000_000, 20_000)
+    rng = np.random.default_rng(11)
+    reads = []
+    for i in range(20_000):
+        L = int(rng.integers(90, 130))
+        st = int(rng.integers(0, g.size - L - 8))
+        r = bytearray(g[st:st + L].tobytes())
+        for _ in range(int(rng.integers(0, 17))):
+            q = int(rng.integers(0, len(r)))
+            kind = int(rng.integers(0, 10))
+            if kind < 6:
+                r[q] = ACGT[int(rng.integers(0, 4))]
+            elif kind < 8:
+                del r[q:q + int(rng.integers(1, 4))]
+            elif kind < 9:
+                r[q:q] = bytes(ACGT[int(v)] for v in rng.integers(0, 4, int(rng.integers(1, 4))))
+            else:
+                r[q] = ord("N")
+        if i % 2:
+            r = bytearray(bytes(r).translate(bytes.maketrans(b"ACGT", b"TGCA"))[::-1])
+        reads.append(bytes(r))
+    buf, offs2 = api.reads_to_buffer(reads)
+    _gpu_vs_oracle(cfg, g, packed, nmask, np.frombuffer(buf, np.uint8).copy(), offs2)
+
+
 def test_align_force_max_dlimit_parity():
     cfg, g, packed, nmask, bases, offs = _case("C2", 4_000_000, 10_000, 10, 0.01)
     p = synth.CONFIGS["C2"].params

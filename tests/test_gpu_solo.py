@@ -1,8 +1,8 @@
 """The thread-per-read solo kernel (align.cu solo_kernel) against the oracle.
 
-The solo kernel finishes the reads whose seeds have at most one hit and
-hands every other read to the warp kernel, so by default each batch is split
-between the two kernels.  These runs force each side: SA_SOLO_MIN_READS=1
+The solo kernel finishes the reads whose seeds have few hits (at most 6 each,
+8 candidates in all) and hands every other read to the warp kernel, so by
+default each batch is split between the two kernels.  These runs force each side: SA_SOLO_MIN_READS=1
 puts every launch (small batches, ragged and short reads, N seeds, the
 repeat corpora whose reads bail part-way, force_max_dlimit, the golden
 corpora) through the solo kernel first; SA_NO_SOLO=1 runs the warp kernel
@@ -16,7 +16,7 @@ import sys
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SELECT = "align_parity or ragged or force_max or align_golden or overflow_paths or fixed_length or param_sweep"
+SELECT = "align_parity or ragged or heavily_edited or force_max or align_golden or overflow_paths or fixed_length or param_sweep"
 
 
 @pytest.mark.gpu
