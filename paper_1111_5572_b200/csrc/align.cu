@@ -2566,9 +2566,6 @@ __global__ void __launch_bounds__(32 * SA_FAST_WARPS, SA_MIN_BLOCKS) align_kerne
 }
 
 // The prune queue's reads (pq_defer): warp per read, a persistent grid.
-#ifndef SA_PRUNE_WPF
-#define SA_PRUNE_WPF 1  // prefetch the unscored candidates' genome windows when a queue record is loaded
-#endif
 __global__ void __launch_bounds__(256) prune_kernel(const AlignLaunch a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
@@ -2622,24 +2619,9 @@ __global__ void __launch_bounds__(256) prune_kernel(const AlignLaunch a) {
         x.rs = lane < kNumStats ? reinterpret_cast<const uint32_t*>(rec + 64)[lane] : 0u;
         const unsigned long long* keys = reinterpret_cast<const unsigned long long*>(rec + kPqHeader);
         for (uint32_t j = lane; j < x.n_cands; j += 32) {
-            const unsigned long long kk = keys[j], mm = keys[x.n_cands + j];
-            const uint32_t cc = reinterpret_cast<const uint32_t*>(keys + 2 * x.n_cands)[j];
-            x.t.ckey[j] = kk;
-            x.t.cmask[j] = mm;
-            x.t.ccnt[j] = cc;
-#if SA_PRUNE_WPF
-            // every unscored candidate is scored below: its first anchor's window
-            // starts towards L2 now, behind the selection sort
-            if (!(cc & kScored)) {
-                const uint64_t a0 = (kk >> 1) * static_cast<uint64_t>(a.bs) +
-                                    static_cast<uint64_t>(__ffsll(static_cast<long long>(mm)) - 1);
-                if (a0 < a.glen) {
-                    const uint64_t a1 = a0 + static_cast<uint64_t>(x.len);
-                    prefetch_l2(a.planes + (a0 >> 5));
-                    prefetch_l2(a.planes + ((a1 < a.glen ? a1 : a.glen) >> 5));
-                }
-            }
-#endif
+            x.t.ckey[j] = keys[j];
+            x.t.cmask[j] = keys[x.n_cands + j];
+            x.t.ccnt[j] = reinterpret_cast<const uint32_t*>(keys + 2 * x.n_cands)[j];
         }
         {  // the read's forward and reverse-complement planes, into shared memory
             const uint4* gp = a.pre_planes + static_cast<uint64_t>(r) * a.pre_pstride;
