@@ -1442,12 +1442,13 @@ SA_DEV int align_one(Ctx& x, uint32_t r, int n_eff, const int* offs, int tier0,
 // src/aligner.cpp:223-364) for its own read from the seed kernel's records,
 // with the candidate table and the LV frontier in its own shared-memory
 // column, so all 32 lanes do useful work.  A read it cannot finish within its
-// limits -- a seed with several hits (palindromes included), more than
-// kSoloCands candidates, a bad character or a deferred length -- is appended
-// to pre_list untouched and the warp kernel redoes it from scratch, so the
-// result is the same whichever kernel finishes a read.  The steps below are
-// align_one's (same d_limit rule, candidate order, LV steps, tracker, exits,
-// classification and counters), written sequentially.
+// limits -- a seed with more than SA_SOLO_MAX_HITS hits (palindromes
+// included), more than kSoloCands candidates, a bad character or a deferred
+// length -- is appended to pre_list untouched and the warp kernel redoes it
+// from scratch, so the result is the same whichever kernel finishes a read.
+// The steps are align_one's (same d_limit rule, candidate order, LV steps,
+// tracker, exits, classification and counters), written per lane as a state
+// machine the warp walks together (seed phase, LV phase).
 #ifndef SA_SOLO_CANDS
 #define SA_SOLO_CANDS 8
 #endif
