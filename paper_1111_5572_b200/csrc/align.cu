@@ -1476,7 +1476,7 @@ struct SoloRead {
 };
 
 #ifndef SA_SOLO_MIN_BLOCKS
-#define SA_SOLO_MIN_BLOCKS 6  // 80 registers, 24 warps per SM (C1 934 -> 971 M reads/s over the unbounded 109)
+#define SA_SOLO_MIN_BLOCKS 7  // 72 registers, 28 warps per SM (6 blocks / 80 registers: C2 497 -> 499 M, C1 1,485 -> 1,540 M reads/s; 8 blocks / 64 registers: 500 / 1,475 M)
 #endif
 #ifndef SA_SOLO_LV
 // solo LV: 0 serial wavefront (lv_thread); 1 banded bit-parallel (lv_bitpar).
