@@ -113,9 +113,12 @@ def main() -> None:
              "| kernel | launches | total us | mean us |", "|---|---|---|---|"]
     for k, (c, t) in agg.items():
         lines.append(f"| `{k}` | {c} | {t / 1e3:.1f} | {t / 1e3 / c:.1f} |")
-    hot = [t for n, t in lst if "align_kernel" in n or "seed_kernel" in n]
+    hot = [t for n, t in lst if any(k in n for k in ("seed_kernel", "solo_kernel", "resolve_kernel", "align_kernel",
+                                                       "prune_kernel"))]
     if hot:
-        lines += ["", f"Hot-path kernels (seed + align, all launches in the list): {sum(hot) / 1e6:.3f} ms total."]
+        steps = max(c for c, _ in agg.values())
+        lines += ["", f"Hot-path kernels (seed, solo, resolve, warp, prune, global-table; all launches in the list): "
+                      f"{sum(hot) / 1e6:.3f} ms total, {sum(hot) / 1e6 / steps:.3f} ms per step."]
     dram = 0.0
     for d in ds:
         lines += ["", f"## Full capture: `{d.get('Kernel Name', '?')[:80]}`", "", "| metric | value |", "|---|---|"]
